@@ -1,0 +1,249 @@
+"""Seeded synthetic scene generators shared by the oracle tests and the GPU path.
+
+This module holds NO arithmetic of the method (no transform, snapping, binning,
+coverage, depth or shading) -- only the input geometry, a camera matrix and a
+light vector.  It is the one module both sides consume ("Inputs").
+
+Scenes follow SURVEY.md section 8(d) (shapes of the paper's workloads,
+PAPER.md:1241-1246 Fig. rastpics: Fairy Forest 174K tris "many small and large
+triangles", Buddha 1.1M "very small triangles", all at 1024x768):
+
+  c1  64x64, 8x8 bins, 16 triangles on a half-pixel lattice (oracle check)
+  c2  1024x768, 16x16 bins, 100 UV spheres x 1000 tris  (Fairy-Forest scale)
+  c3  1024x768, bins 8/16/32/64, one 1M-tri UV sphere    (Buddha scale)
+  c4  1920x1080, 16x16 bins, 4M-tri random soup in NDC
+  c5  3840x2160, 16x16 / 8x8 bins, 16M-tri jittered grid (micropolygon density)
+
+Layout: verts f32[V][8] = {px,py,pz,0, nx,ny,nz,0},
+idx i32[T][3], mvp f32[16] row-major with clip = M * (x,y,z,1), light f32[3].
+Seeds: config number (c1 -> 1, ...), numpy default_rng.
+"""
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+LIGHT = np.array([1.0, 1.0, 1.0], np.float32)  # Listing 1 lightvec
+
+
+@dataclass
+class Scene:
+    name: str
+    W: int
+    H: int
+    bin_sizes: tuple
+    verts: np.ndarray
+    idx: np.ndarray
+    mvp: np.ndarray
+    light: np.ndarray = field(default_factory=lambda: LIGHT.copy())
+
+    @property
+    def n_tris(self) -> int:
+        return int(self.idx.shape[0])
+
+    def sha256(self) -> str:
+        h = hashlib.sha256()
+        for a in (self.verts, self.idx, self.mvp, self.light):
+            h.update(np.ascontiguousarray(a).tobytes())
+        return h.hexdigest()
+
+
+def pack_verts(pos, nrm) -> np.ndarray:
+    """f32[V][8] from positions [V][3] and normals [V][3]."""
+    V = pos.shape[0]
+    v = np.zeros((V, 8), np.float32)
+    v[:, 0:3] = pos
+    v[:, 4:7] = nrm
+    return v
+
+
+def ortho_pixel_mvp(W: int, H: int) -> np.ndarray:
+    """Ortho matrix mapping object (x, y) in pixels (y down) to NDC.
+
+    For power-of-two W, H the viewport maps back to exactly (x, y)
+    (SURVEY.md 8(c) pin for O1); object z = 2*zw - 1 gives window depth zw."""
+    M = np.array([[2.0 / W, 0, 0, -1.0],
+                  [0, -2.0 / H, 0, 1.0],
+                  [0, 0, 1.0, 0],
+                  [0, 0, 0, 1.0]], np.float64)
+    return M.astype(np.float32).reshape(16)
+
+
+def perspective_mvp(fovy_deg=60.0, aspect=4.0 / 3.0, near=0.1, far=100.0) -> np.ndarray:
+    """OpenGL perspective projection (camera at origin looking down -z), row-major."""
+    f = 1.0 / math.tan(math.radians(fovy_deg) / 2.0)
+    M = np.array([[f / aspect, 0, 0, 0],
+                  [0, f, 0, 0],
+                  [0, 0, (far + near) / (near - far), 2 * far * near / (near - far)],
+                  [0, 0, -1.0, 0]], np.float64)
+    return M.astype(np.float32).reshape(16)
+
+
+def random_unit(rng, n) -> np.ndarray:
+    v = rng.normal(size=(n, 3))
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    return v.astype(np.float32)
+
+
+# --------------------------------------------------------------------------
+# UV sphere: L vertex rings x S slices + 2 poles; T = 2*S*L, V = S*L + 2
+# --------------------------------------------------------------------------
+def uv_sphere(L: int, S: int):
+    """Unit UV sphere (poles on +-y): returns (unit positions f64[V][3], idx i64[T][3])."""
+    theta = np.pi * (np.arange(L) + 1) / (L + 1)
+    phi = 2 * np.pi * np.arange(S) / S
+    st, ct = np.sin(theta)[:, None], np.cos(theta)[:, None]
+    ring = np.stack([st * np.cos(phi)[None, :], np.broadcast_to(ct, (L, S)),
+                     st * np.sin(phi)[None, :]], axis=-1).reshape(-1, 3)
+    pos = np.concatenate([[[0.0, 1.0, 0.0]], ring, [[0.0, -1.0, 0.0]]], axis=0)
+    top, bot = 0, S * L + 1
+    r = lambda i, j: 1 + i * S + (j % S)  # noqa: E731
+    j = np.arange(S)
+    tris = [np.stack([np.full(S, top), r(0, j + 1), r(0, j)], 1)]
+    i = np.arange(L - 1)[:, None]
+    a, b, c, d = r(i, j), r(i + 1, j), r(i + 1, j + 1), r(i, j + 1)
+    tris.append(np.stack([a, b, c], -1).reshape(-1, 3))
+    tris.append(np.stack([a, c, d], -1).reshape(-1, 3))
+    tris.append(np.stack([np.full(S, bot), r(L - 1, j), r(L - 1, j + 1)], 1))
+    return pos, np.concatenate(tris, 0)
+
+
+def scene_c1() -> Scene:
+    """64x64, 8x8 bins, 16 triangles on a half-pixel lattice (oracle check).
+
+    3 quads split on a diagonal (6 tris; quads A and B share an edge), a 6-tri
+    fan around a vertex exactly on the pixel centre (32.5, 32.5), 4 free tris.
+    Window depths from {0.25, 0.5, 0.75} with forced equal-depth overlaps.
+    Random winding, random unit normals.  Object coords are pixel coords."""
+    rng = np.random.default_rng(1)
+    W = H = 64
+    P = []   # positions (x, y, zw)
+    tris = []
+
+    def vert(x, y, zw):
+        P.append((x, y, zw))
+        return len(P) - 1
+
+    # quads A, B (sharing edge x = 20), C; depths 0.5, 0.5, 0.25
+    qa = [vert(4.5, 4.0, 0.5), vert(20.0, 4.0, 0.5), vert(20.0, 20.5, 0.5), vert(4.5, 20.5, 0.5)]
+    qb = [qa[1], vert(36.0, 6.5, 0.5), vert(36.0, 22.0, 0.5), qa[2]]
+    qc = [vert(40.5, 40.0, 0.25), vert(60.0, 41.5, 0.25), vert(58.5, 60.0, 0.25),
+          vert(42.0, 58.5, 0.25)]
+    for q in (qa, qb, qc):
+        tris += [(q[0], q[1], q[2]), (q[0], q[2], q[3])]
+    # fan of 6 around a vertex on the pixel centre (32.5, 32.5), depth 0.75
+    c = vert(32.5, 32.5, 0.75)
+    ring = [vert(32.5 + 6.0 * math.cos(a), 32.5 + 6.0 * math.sin(a), 0.75)
+            for a in np.arange(6) * (2 * math.pi / 6)]
+    # snap fan ring to the half-pixel lattice
+    for k in ring:
+        x, y, z = P[k]
+        P[k] = (round(2 * x) / 2, round(2 * y) / 2, z)
+    for k in range(6):
+        tris.append((c, ring[k], ring[(k + 1) % 6]))
+    # 4 free triangles: two equal-depth (0.5) overlapping quad A/B, one 0.25 over
+    # the fan, one 0.75 spanning tile borders
+    free = [((8.0, 8.5), (30.0, 12.0), (14.5, 26.0), 0.5),
+            ((10.0, 2.5), (24.0, 16.0), (6.0, 18.0), 0.5),
+            ((28.0, 28.0), (40.0, 30.5), (31.5, 42.0), 0.25),
+            ((2.5, 44.0), (30.0, 48.0), (16.0, 63.5), 0.75)]
+    for a, b, cc, z in free:
+        tris.append((vert(*a, z), vert(*b, z), vert(*cc, z)))
+    tris = np.array(tris, np.int64)
+    # random winding per triangle
+    for t in range(tris.shape[0]):
+        if rng.random() < 0.5:
+            tris[t, [1, 2]] = tris[t, [2, 1]]
+    P = np.array(P, np.float64)
+    pos = np.stack([P[:, 0], P[:, 1], 2.0 * P[:, 2] - 1.0], 1)
+    verts = pack_verts(pos.astype(np.float32), random_unit(rng, P.shape[0]))
+    return Scene("c1", W, H, (8,), verts, tris.astype(np.int32), ortho_pixel_mvp(W, H))
+
+
+def scene_c2() -> Scene:
+    """1024x768, 16x16 bins: 100 UV spheres of 20 rings x 25 slices (T=100,000,
+    V=50,200), radii U[0.5,1.5], centres in the frustum at depth U[3,30]."""
+    rng = np.random.default_rng(2)
+    unit, tri = uv_sphere(20, 25)
+    n = 100
+    tanh = math.tan(math.radians(30.0))
+    d = rng.uniform(3.0, 30.0, n)
+    cx = rng.uniform(-0.8, 0.8, n) * d * tanh * (4.0 / 3.0)
+    cy = rng.uniform(-0.8, 0.8, n) * d * tanh
+    rad = rng.uniform(0.5, 1.5, n)
+    pos = (unit[None] * rad[:, None, None] + np.stack([cx, cy, -d], 1)[:, None, :]).reshape(-1, 3)
+    nrm = np.broadcast_to(unit[None], (n,) + unit.shape).reshape(-1, 3)
+    idx = (tri[None] + (np.arange(n) * unit.shape[0])[:, None, None]).reshape(-1, 3)
+    return Scene("c2", 1024, 768, (16,), pack_verts(pos.astype(np.float32), nrm.astype(np.float32)),
+                 idx.astype(np.int32), perspective_mvp())
+
+
+def scene_c3() -> Scene:
+    """1024x768, bins 8/16/32/64: one UV sphere 500 rings x 1000 slices
+    (T=1,000,000, V=500,002), radius 1 at distance 3.2 (~438 px wide)."""
+    unit, tri = uv_sphere(500, 1000)
+    pos = unit + np.array([0.0, 0.0, -3.2])
+    return Scene("c3", 1024, 768, (8, 16, 32, 64),
+                 pack_verts(pos.astype(np.float32), unit.astype(np.float32)),
+                 tri.astype(np.int32), perspective_mvp())
+
+
+def scene_soup(T: int, W: int, H: int, seed: int, name: str, bin_sizes=(16,)) -> Scene:
+    """Random triangle soup in NDC (mvp = I): centres U([-1,1]^2), circumradius
+    log-uniform [1,8] px, random vertex angles, z_ndc U[-0.8,0.8] +- 0.01."""
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-1.0, 1.0, (T, 2))
+    r = np.exp(rng.uniform(math.log(1.0), math.log(8.0), T))
+    ang = rng.uniform(0.0, 2 * math.pi, (T, 3))
+    x = c[:, 0:1] + (r * 2.0 / W)[:, None] * np.cos(ang)
+    y = c[:, 1:2] + (r * 2.0 / H)[:, None] * np.sin(ang)
+    z = rng.uniform(-0.8, 0.8, (T, 1)) + rng.uniform(-0.01, 0.01, (T, 3))
+    pos = np.stack([x, y, z], -1).reshape(-1, 3).astype(np.float32)
+    nrm = random_unit(rng, 3 * T)
+    idx = np.arange(3 * T, dtype=np.int32).reshape(T, 3)
+    return Scene(name, W, H, bin_sizes, pack_verts(pos, nrm), idx, np.eye(4, dtype=np.float32).reshape(16))
+
+
+def scene_c4(T: int = 4_000_000) -> Scene:
+    """1920x1080, 16x16 bins, 4M-triangle random soup (sort-first case)."""
+    return scene_soup(T, 1920, 1080, 4, "c4")
+
+
+def scene_grid(nx: int, ny: int, W: int, H: int, seed: int, name: str, bin_sizes) -> Scene:
+    """Jittered grid mesh over NDC [-1,1]^2: (nx+1)(ny+1) verts, 2*nx*ny tris,
+    interior vertices jittered +-0.25 cell, alternating diagonals (a planar
+    partition of the screen: every pixel centre is covered exactly once)."""
+    rng = np.random.default_rng(seed)
+    gx, gy = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1))  # [ny+1][nx+1]
+    x = -1.0 + 2.0 * gx / nx
+    y = -1.0 + 2.0 * gy / ny
+    interior = (gx > 0) & (gx < nx) & (gy > 0) & (gy < ny)
+    x = x + interior * rng.uniform(-0.25, 0.25, x.shape) * (2.0 / nx)
+    y = y + interior * rng.uniform(-0.25, 0.25, y.shape) * (2.0 / ny)
+    z = 0.5 + 0.1 * np.sin(3 * np.pi * x) * np.cos(2 * np.pi * y)
+    pos = np.stack([x, y, z], -1).reshape(-1, 3).astype(np.float32)
+    nrm = np.stack([-0.3 * np.cos(3 * np.pi * x), 0.2 * np.sin(2 * np.pi * y), np.ones_like(x)], -1)
+    nrm = (nrm / np.linalg.norm(nrm, axis=-1, keepdims=True)).reshape(-1, 3).astype(np.float32)
+    vid = lambda i, j: j * (nx + 1) + i  # noqa: E731
+    i, j = np.meshgrid(np.arange(nx), np.arange(ny))
+    a, b, c, d = vid(i, j), vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1)
+    alt = ((i + j) % 2 == 0)[..., None]
+    t1 = np.where(alt, np.stack([a, b, c], -1), np.stack([a, b, d], -1))
+    t2 = np.where(alt, np.stack([a, c, d], -1), np.stack([b, c, d], -1))
+    idx = np.stack([t1, t2], 2).reshape(-1, 3).astype(np.int32)
+    return Scene(name, W, H, bin_sizes, pack_verts(pos, nrm), idx, np.eye(4, dtype=np.float32).reshape(16))
+
+
+def scene_c5() -> Scene:
+    """3840x2160, 16M-triangle jittered grid (4000x2000 quads; V=8,006,001)."""
+    return scene_grid(4000, 2000, 3840, 2160, 5, "c5", (16, 8))
+
+
+CONFIGS = {"c1": scene_c1, "c2": scene_c2, "c3": scene_c3, "c4": scene_c4, "c5": scene_c5}
+
+
+def make(name: str) -> Scene:
+    return CONFIGS[name]()
