@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark of the binned rasterizer hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl piko|reference]
+                    [--config c3] [--bin 16]
+
+A step is one frame: the whole hot path (vertex transform + setup, AssignBin
+count / scan / stable scatter, Schedule, per-bin raster + depth + shade +
+write-back; for N > 1 also the NCCL tile-key gather and rank-0 resolve) on the
+seeded synthetic scene of BASELINE.json configs[2] (1M-triangle UV sphere,
+1024x768, Buddha scale) with 16x16 bins by default.  Inputs are resident in HBM;
+L2 is flushed (256 MiB write) before every timed step, outside its events.
+Per-step device time comes from CUDA events on the draw stream; per-kernel
+times from piko_set_profiling (events between the kernels on the same stream).
+N > 1: torchrun, one process per GPU, sort-first (every rank transforms all
+triangles, rasterizes its bins b mod N == rank); time = max over ranks.
+--impl reference times the CPU oracle (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mtriangles/s at 1024x768 (binned raster frame, 1M-tri UV sphere)"
+UNIT = "Mtri/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="piko", choices=["piko", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--bin", type=int, default=16)
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle work")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(cfg, s, bw):
+    return {"c2": "c2: 100 UV spheres, 100K tris", "c3": "c3: UV sphere 500x1000, 1M tris",
+            "c4": "c4: random soup, 4M tris", "c5": "c5: jittered grid, 16M tris"}.get(cfg, cfg) + \
+        f", {s.W}x{s.H}, {bw}x{bw} bins"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms in a thread."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.samples = []
+        self.window = None
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                self.samples.append((time.time(), f))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def summary(self):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        inwin = [f for t, f in self.samples if self.window and self.window[0] - 0.15 <= t <= self.window[1] + 0.15]
+        use = inwin or [f for _, f in self.samples]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for f in use for n, v in zip(names, f[4:8]) if v.lower() == "active"})
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [num(f[0]) for f in use if num(f[0]) is not None]
+        mx = [num(f[1]) for f in use if num(f[1]) is not None]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(use), "in_timed_region": bool(inwin)}
+
+
+def cpu_baseline(s, budget):
+    import oracle
+    t0 = time.perf_counter()
+    frames = 0
+    while True:
+        oracle.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
+        frames += 1
+        if time.perf_counter() - t0 >= budget:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": s.n_tris * frames / dt / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{frames} full frame(s) of the same scene, single-threaded C oracle "
+                      f"(gcc -O2), {dt:.1f} s", "ms_per_frame": 1e3 * dt / frames}
+
+
+def algorithmic_bytes(stage, T, V, L, P, NB, npx, ncov, npass):
+    """Bytes the method must move per launch of a stage."""
+    if stage == "setup":      # idx + vertex positions in; records + pairs out
+        return 12 * T + 16 * V + 48 * L + 8 * P
+    if stage == "bin_scan":   # counts in, bin_start out, counts zeroed
+        return 12 * NB
+    if stage == "radix":      # per pass 8 B in + 8 B out (last pass 4 B out)
+        return npass * 16 * P - (4 * P if npass else 0)
+    if stage == "tile":       # CSR + records in; 24 B/px out; winner re-gather
+        return 4 * (NB + 1) + 4 * P + 48 * P + 24 * npx + 108 * ncov
+    if stage == "resolve":
+        return 8 * npx + 24 * npx + 108 * ncov
+    return 0
+
+
+def run_piko(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1404_6293_b200 as piko
+    import scenes
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    s = scenes.make(args.config)
+    bw = args.bin
+    verts = torch.from_numpy(s.verts).to(dev)
+    idx = torch.from_numpy(s.idx).to(dev)
+    r = piko.Renderer(s.W, s.H, bw, device=dev)
+    if world > 1:
+        obj = [piko.piko_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        piko.piko_attach_comm(r.ctx, obj[0], rank, world)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    # warm-up in checked mode (capacity settles), then asynchronous draws
+    for _ in range(max(args.warmup, 3)):
+        r.draw(verts, idx, s.mvp, s.light, stream)
+    piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
+    stats = r.stats()
+    ncov = int((r.primid() >= 0).sum().item()) if rank == 0 else 0
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    piko.piko_set_profiling(r.ctx, 1)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_wall0 = time.time()
+    for k in range(args.steps):
+        flush.fill_(float(k))                       # L2 flush, outside the step's events
+        ev[k][0].record(stream)
+        r.draw(verts, idx, s.mvp, s.light, stream)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t_wall1 = time.time()
+    status = piko.piko_finish(r.ctx)
+    if status != piko.PIKO_OK:
+        raise SystemExit(f"frame status {status}: {piko.piko_last_error(r.ctx)}")
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    prof, nprof = piko.piko_get_profile(r.ctx)
+    piko.piko_set_profiling(r.ctx, 0)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    if sampler:
+        sampler.mark(t_wall0, t_wall1)
+
+    # end-to-end through the public host-buffer call (H2D + frame + D2H per step)
+    e2e = None
+    if not args.no_e2e:
+        piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_CHECKED)
+        hv = torch.from_numpy(s.verts).pin_memory()
+        hi = torch.from_numpy(s.idx).pin_memory()
+        hrgba = torch.empty((s.H, s.W, 4), dtype=torch.float32).pin_memory()
+        hdepth = torch.empty((s.H, s.W), dtype=torch.float32).pin_memory()
+        ke = max(3, min(args.steps, 20))
+        for _ in range(2):
+            piko.piko_draw_host(r.ctx, hv, hi, s.mvp, s.light, hrgba, hdepth, stream)
+        ee = []
+        for _ in range(ke):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            a.record(stream)
+            piko.piko_draw_host(r.ctx, hv, hi, s.mvp, s.light, hrgba, hdepth, stream)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            ee.append(a.elapsed_time(b))
+        e_ms = sum(ee)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": s.n_tris * ke / (e_ms / 1e3) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(hv.numel() * 4 + hi.numel() * 4),
+               "d2h_bytes_per_step": int((hrgba.numel() + hdepth.numel()) * 4) if rank == 0 else 0,
+               "ms_per_step": e_ms / ke, "steps": ke}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        r.close()
+        return
+
+    clocks = sampler.summary()
+    T, V = s.n_tris, s.verts.shape[0]
+    P, L, NB = stats["n_pairs"], stats["n_live"], stats["n_bins"]
+    npx = s.W * s.H
+    per_frame = {k: v / max(nprof, 1) for k, v in prof.items()}
+    cand = {k: per_frame[k] for k in ("setup", "bin_scan", "radix", "tile", "resolve") if per_frame[k] > 0}
+    dom = max(cand, key=cand.get)
+    nb = algorithmic_bytes(dom, T, V, L, P, NB, npx, ncov, stats["radix_passes"])
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = nb / (per_frame[dom] / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}_b{bw}.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": nb,
+                "ms_per_launch": per_frame[dom],
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
+    frame_bytes = sum(algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"])
+                      for k in ("setup", "bin_scan", "radix", "tile"))
+    ms = total_ms / args.steps
+    out = {
+        "metric": METRIC, "value": T * args.steps / (total_ms / 1e3) / 1e6, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f32+int32/int64", "data": "synthetic (seeded scenes/)",
+        "config": {"workload": workload_name(args.config, s, bw), "config": args.config,
+                   "width": s.W, "height": s.H, "bin": bw, "n_tris": T, "n_verts": V,
+                   "n_pairs": P, "n_live": L, "covered_px": ncov, "l2": "flushed (256 MiB) before every step",
+                   "parallelism": f"sort-first x{world}" if world > 1 else "1 GPU"},
+        "fps": 1e3 / ms,
+        "frame_roofline": {"algorithmic_bytes": frame_bytes, "frac": frame_bytes / (ms / 1e3) / 1e9 / peak},
+        "kernel_ms": per_frame,
+        "roofline": roofline,
+        "gpu_launches": stats["kernels_per_frame"] * args.steps,
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(s, args.cpu_budget)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    r.close()
+
+
+def run_reference(args):
+    """Reference arm = the CPU oracle as it stands, on rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import scenes
+    s = scenes.make(args.config)
+    for _ in range(args.warmup):
+        oracle.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
+    t = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
+        t.append(time.perf_counter() - t0)
+    total = sum(t)
+    v = s.n_tris * args.steps / total / 1e6
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32+int32/int64", "data": "synthetic (seeded scenes/)",
+           "config": {"workload": workload_name(args.config, s, args.bin), "config": args.config,
+                      "width": s.W, "height": s.H, "bin": args.bin, "n_tris": s.n_tris},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"{args.steps} full frames, single-threaded C oracle (gcc -O2)"},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_piko(a)

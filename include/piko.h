@@ -1,0 +1,188 @@
+/*
+ * piko.h -- C ABI of the B200-native binned triangle rasterizer (the one
+ * data-parallel hot path of Piko, arXiv 1404.6293).
+ *
+ * The operation (sec. 7.1 "Baseline Rasterizer": Vertex
+ * Shader -> Rasterizer -> Fragment Shader -> Depth Test -> Composite, run as
+ * the binned pipeline of sec. 7.2.2; shading per Listing 1,
+ * P:514-545): draw an indexed triangle list with a model-view-projection
+ * matrix and a directional light into a colour buffer and a depth buffer.
+ * The path inside piko_draw is
+ *   vertex transform + fixed-point setup      ("Vertex Shader")
+ *   AssignBin: bbox -> tiles, count, exclusive scan, stable scatter into per-bin
+ *              lists in primitive order       (Table 3
+ *              AssignToBoundingBox; P:1081-1084 prefix sums "while maintaining
+ *              primitive order")
+ *   Schedule:  one CTA per bin (LoadBalance); across GPUs bin b is
+ *              owned by rank b mod R (DirectMap round robin)
+ *   Process:   per bin, fixed-point edge coverage, depth test with a packed
+ *              64-bit (depth, primID) minimum, Lambert shade, write-back.
+ * The exact result (bit-exact coverage/depth/primID/bin lists) is defined in
+ * DESIGN.md ("Readings of the paper", R1..R18) and by the CPU oracle in
+ * oracle/piko_oracle.c, which this library does not share code with.
+ *
+ * Conventions for every entry point:
+ *  - Pointers marked "device" must be CUDA device memory of the device that
+ *    was current when the context was created (e.g. torch CUDA tensors);
+ *    pointers marked "host" are ordinary (preferably pinned) host memory.
+ *  - Device input buffers must be 16-byte aligned (vectorised loads).
+ *  - The caller owns every buffer it passes; the library keeps no caller
+ *    pointer beyond the stream work enqueued by that call.  The context owns
+ *    its scratch (setup records, pair lists, bin CSR, primID and key buffers).
+ *  - Return codes: PIKO_OK (0) or a negative PIKO_E* code; piko_last_error()
+ *    gives a message.  A context serves one host thread at a time.
+ */
+#ifndef PIKO_H_
+#define PIKO_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct piko_ctx piko_ctx;
+
+enum {
+  PIKO_OK = 0,
+  PIKO_EINVAL = -1,    /* invalid argument                                   */
+  PIKO_ENOMEM = -2,    /* device or host allocation failed                   */
+  PIKO_ECUDA = -3,     /* a CUDA call or kernel failed                       */
+  PIKO_ENCCL = -4,     /* NCCL unavailable or an NCCL call failed            */
+  PIKO_ECAPACITY = -5, /* pair-list capacity exceeded and could not grow     */
+  PIKO_ESTATE = -6     /* call not valid in the context's current state      */
+};
+
+/* piko_set_debug flags */
+#define PIKO_DEBUG_COVERAGE_COUNT 1u /* count covering triangles per pixel   */
+
+/* piko_set_sync modes */
+#define PIKO_SYNC_CHECKED 0 /* default: piko_draw waits for the frame, checks
+                               the pair capacity, regrows and re-issues on
+                               overflow; returns after the frame completed.   */
+#define PIKO_SYNC_ASYNC 1   /* piko_draw only enqueues; an overflow of the
+                               frame is reported by the next piko_draw or by
+                               piko_finish (the frame's outputs are then invalid
+                               and the capacity has been grown).              */
+
+/* Create a context for a width x height framebuffer binned into bin_w x bin_h
+ * pixel tiles (AssignToBoundingBox bins; Listing 1 uses 8x8).
+ *   1 <= width, height <= 16384 (guard band, R2);
+ *   bin_w, bin_h powers of two in [8, 64].
+ * Bins form a ceil(width/bin_w) x ceil(height/bin_h) row-major grid,
+ * bin = ty * binsX + tx; edge bins may be partial (R13).
+ * Uses the CUDA device current on the calling thread.
+ * Returns NULL on error (message via piko_last_error(NULL)).                 */
+piko_ctx *piko_create(int width, int height, int bin_w, int bin_h);
+
+/* Render one frame (asynchronous on `stream` in PIKO_SYNC_ASYNC mode).
+ *   verts     device, f32[n_verts][8] = {px,py,pz,pad, nx,ny,nz,pad}
+ *             (object-space position and normal, R15)
+ *   idx       device, i32[n_tris][3]; caller guarantees 0 <= idx < n_verts
+ *   n_tris    0 <= n_tris; the primitive ID of triangle t is t
+ *   mvp       host, f32[16] row-major, clip = M * (x,y,z,1); copied at call time
+ *   light     host, f32[3], direction toward the light (Listing 1 lightvec,
+ *             normalised inside); copied at call time
+ *   out_rgba  device, f32[height][width][4], row 0 = top; background (0,0,0,0)
+ *   out_depth device, f32[height][width]; window depth in [0,1], 1.0 = clear
+ *   stream    a cudaStream_t (NULL = legacy default stream)
+ * After piko_attach_comm with nranks > 1, only rank 0's out_* receive the frame
+ * (others may pass NULL) and every rank must pass identical scene buffers.
+ * Errors: PIKO_EINVAL for null pointers with n_tris > 0, n_tris < 0, misaligned
+ * buffers, a non-finite or zero light; PIKO_ECAPACITY; PIKO_ECUDA.
+ * n_tris == 0 clears the outputs.                                             */
+int piko_draw(piko_ctx *ctx, const float *verts, const int32_t *idx, int32_t n_tris,
+              const float mvp[16], const float light[3], float *out_rgba, float *out_depth,
+              void *stream);
+
+/* End-to-end variant of piko_draw on HOST buffers: copies verts (n_verts x 8
+ * f32) and idx to context-owned device buffers, draws, copies rgba and depth
+ * back into host buffers, and synchronises `stream` before returning.
+ * Host buffers should be pinned (cudaHostRegister / torch pin_memory) for
+ * full PCIe bandwidth.  Same errors as piko_draw.                            */
+int piko_draw_host(piko_ctx *ctx, const float *h_verts, int64_t n_verts, const int32_t *h_idx,
+                   int32_t n_tris, const float mvp[16], const float light[3], float *h_rgba,
+                   float *h_depth, void *stream);
+
+/* Wait for the last enqueued frame; returns its status (PIKO_ECAPACITY if its
+ * pair lists overflowed -- the capacity has then been grown for the next
+ * frame).                                                                     */
+int piko_finish(piko_ctx *ctx);
+
+/* Select PIKO_SYNC_CHECKED (default) or PIKO_SYNC_ASYNC.                      */
+int piko_set_sync(piko_ctx *ctx, int mode);
+
+/* Destroy; NULL-safe; synchronises internal work first.                       */
+void piko_destroy(piko_ctx *ctx);
+
+/* Last error message of ctx (ctx == NULL: the calling thread's last
+ * piko_create error).  Owned by the library.                                  */
+const char *piko_last_error(const piko_ctx *ctx);
+
+/* Inspection (parity tests).  Device pointers owned by ctx, valid until the
+ * next draw/destroy, readable after the frame's stream work completed.
+ * primID buffer: i32[height][width], -1 = background.                         */
+int piko_get_primid(const piko_ctx *ctx, const int32_t **d_primid);
+
+/* Bin lists of the last frame as CSR: bin_start i32[NB+1], bin_prims i32[P],
+ * ascending primID within each bin.  Bins not owned by this
+ * rank are empty.  *n_pairs = P.  Blocks until the frame completed.           */
+int piko_get_bins(const piko_ctx *ctx, const int32_t **d_bin_start, const int32_t **d_bin_prims,
+                  int64_t *n_pairs);
+
+/* Debug flags (PIKO_DEBUG_COVERAGE_COUNT: u32[height][width] number of
+ * triangles covering each pixel centre, counted before the depth discard).   */
+int piko_set_debug(piko_ctx *ctx, unsigned flags);
+int piko_get_coverage(const piko_ctx *ctx, const uint32_t **d_covcount);
+
+/* Sort-first partition without a communicator ("virtual rank"): rasterize only
+ * bins b with b mod nranks == rank and write only their pixels.  Used to test
+ * the partition on one GPU.  nranks == 1 restores the full frame.            */
+int piko_set_partition(piko_ctx *ctx, int rank, int nranks);
+
+/* Multi-GPU sort-first: attach an NCCL communicator built from a
+ * 128-byte ncclUniqueId that the caller broadcast to all ranks (e.g. through
+ * torch.distributed).  Each rank transforms all triangles, rasterizes the bins
+ * it owns (b mod nranks == rank) into packed 64-bit tile keys, and the keys are
+ * gathered to rank 0 with grouped ncclSend/ncclRecv; rank 0 shades and writes
+ * the frame.  NCCL is loaded at run time (libnccl.so.2).                      */
+int piko_attach_comm(piko_ctx *ctx, const void *nccl_unique_id, int rank, int nranks);
+
+/* Frame statistics of the last frame (blocks until it completed).            */
+typedef struct {
+  int64_t n_tris;       /* triangles submitted                                */
+  int64_t n_live;       /* triangles surviving setup culls (owned bins > 0)   */
+  int64_t n_pairs;      /* (bin, triangle) pairs, P                           */
+  int64_t n_bins;       /* bins in the grid, NB                               */
+  int64_t owned_bins;   /* bins rasterized by this rank                        */
+  int64_t pair_capacity;/* current pair-list capacity                          */
+  int32_t radix_passes; /* LSD passes of the stable scatter                    */
+  int32_t kernels_per_frame; /* kernels launched per frame (this rank)        */
+} piko_stats;
+int piko_get_stats(const piko_ctx *ctx, piko_stats *out);
+
+/* Fill a 128-byte ncclUniqueId (ncclGetUniqueId) for piko_attach_comm; call
+ * on rank 0 and broadcast the bytes.  PIKO_ENCCL if NCCL cannot be loaded.   */
+int piko_nccl_unique_id(void *out_id128);
+
+/* Per-stage device timing with CUDA events recorded on the frame's stream
+ * between the kernels of every frame (no host synchronisation is added).
+ * Stages: */
+#define PIKO_STAGE_CLEAR 0   /* per-frame control/status resets (memsets)   */
+#define PIKO_STAGE_SETUP 1   /* k_setup: transform, setup, count, scan, pairs */
+#define PIKO_STAGE_BINSCAN 2 /* k_bin_scan: CSR bin_start, digit histograms  */
+#define PIKO_STAGE_RADIX 3   /* k_radix_pass x radix_passes: stable scatter   */
+#define PIKO_STAGE_TILE 4    /* k_tile: per-bin raster, depth, shade, store   */
+#define PIKO_STAGE_GATHER 5  /* NCCL tile-key gather (multi-GPU)              */
+#define PIKO_STAGE_RESOLVE 6 /* k_resolve: rank-0 shade of gathered keys      */
+#define PIKO_NUM_STAGES 7
+/* on != 0 enables recording and resets the totals. */
+int piko_set_profiling(piko_ctx *ctx, int on);
+/* Synchronises, then returns per-stage total milliseconds and frame count
+ * since profiling was enabled.                                               */
+int piko_get_profile(piko_ctx *ctx, double ms[PIKO_NUM_STAGES], int64_t *frames);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIKO_H_ */

@@ -1,0 +1,280 @@
+"""B200-native binned triangle rasterizer (Piko, arXiv 1404.6293) -- Python binding.
+
+A thin ctypes binding over ``libpiko.so`` (the C ABI of ``include/piko.h``):
+argument marshalling only -- every step of the path (vertex transform, setup,
+AssignBin count / scan / stable scatter, Schedule, per-bin Process, shading,
+write-back, NCCL tile gather) runs in the CUDA kernels of ``csrc/``.  PyTorch
+is used for device memory, streams and process groups.  There is no CPU
+fallback: importing this package without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpiko.so")
+
+PIKO_OK, PIKO_EINVAL, PIKO_ENOMEM, PIKO_ECUDA, PIKO_ENCCL, PIKO_ECAPACITY, PIKO_ESTATE = 0, -1, -2, -3, -4, -5, -6
+PIKO_DEBUG_COVERAGE_COUNT = 1
+PIKO_SYNC_CHECKED, PIKO_SYNC_ASYNC = 0, 1
+
+# names of every symbol include/piko.h declares (checked by tests)
+EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_set_sync",
+           "piko_destroy", "piko_last_error", "piko_get_primid", "piko_get_bins",
+           "piko_set_debug", "piko_get_coverage", "piko_set_partition", "piko_attach_comm",
+           "piko_get_stats", "piko_nccl_unique_id", "piko_set_profiling", "piko_get_profile")
+STAGES = ("clear", "setup", "bin_scan", "radix", "tile", "gather", "resolve")
+
+
+class PikoError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"piko error {code}: {msg}")
+        self.code = code
+
+
+class piko_stats(ctypes.Structure):
+    _fields_ = [("n_tris", ctypes.c_int64), ("n_live", ctypes.c_int64),
+                ("n_pairs", ctypes.c_int64), ("n_bins", ctypes.c_int64),
+                ("owned_bins", ctypes.c_int64), ("pair_capacity", ctypes.c_int64),
+                ("radix_passes", ctypes.c_int32), ("kernels_per_frame", ctypes.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, I64, U = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint
+    sig = {
+        "piko_create": ([I, I, I, I], P),
+        "piko_draw": ([P, P, P, ctypes.c_int32, P, P, P, P, P], I),
+        "piko_draw_host": ([P, P, I64, P, ctypes.c_int32, P, P, P, P, P], I),
+        "piko_finish": ([P], I),
+        "piko_set_sync": ([P, I], I),
+        "piko_destroy": ([P], None),
+        "piko_last_error": ([P], ctypes.c_char_p),
+        "piko_get_primid": ([P, ctypes.POINTER(P)], I),
+        "piko_get_bins": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(I64)], I),
+        "piko_set_debug": ([P, U], I),
+        "piko_get_coverage": ([P, ctypes.POINTER(P)], I),
+        "piko_set_partition": ([P, I, I], I),
+        "piko_attach_comm": ([P, P, I, I], I),
+        "piko_get_stats": ([P, ctypes.POINTER(piko_stats)], I),
+        "piko_nccl_unique_id": ([P], I),
+        "piko_set_profiling": ([P, I], I),
+        "piko_get_profile": ([P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)], I),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes, f.restype = args, res
+    return lib
+
+
+_lib = _load()
+lib = _lib
+
+
+def _f32x(vals, n):
+    arr = (ctypes.c_float * n)(*[float(v) for v in vals])
+    return arr
+
+
+def _dev_ptr(t, dtype, name):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous {dtype}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(ctx, rc):
+    if rc != PIKO_OK:
+        raise PikoError(rc, piko_last_error(ctx))
+    return rc
+
+
+# ---- the C ABI, one Python function per entry point -------------------------
+def piko_create(width, height, bin_w, bin_h):
+    h = _lib.piko_create(width, height, bin_w, bin_h)
+    if not h:
+        raise PikoError(PIKO_EINVAL, _lib.piko_last_error(None).decode())
+    return ctypes.c_void_p(h)
+
+
+def piko_destroy(ctx):
+    _lib.piko_destroy(ctx)
+
+
+def piko_last_error(ctx):
+    m = _lib.piko_last_error(ctx)
+    return m.decode() if m else ""
+
+
+def piko_draw(ctx, verts, idx, n_tris, mvp, light, out_rgba, out_depth, stream=None, check=True):
+    import torch
+    rc = _lib.piko_draw(ctx, _dev_ptr(verts, torch.float32, "verts"),
+                        _dev_ptr(idx, torch.int32, "idx"), int(n_tris), _f32x(mvp, 16),
+                        _f32x(light, 3), _dev_ptr(out_rgba, torch.float32, "out_rgba"),
+                        _dev_ptr(out_depth, torch.float32, "out_depth"), _stream_ptr(stream))
+    return _check(ctx, rc) if check else rc
+
+
+def piko_draw_host(ctx, verts, idx, mvp, light, out_rgba, out_depth, stream=None):
+    """verts/idx/out_* are CPU torch tensors (pinned for full bandwidth)."""
+    for t in (verts, idx, out_rgba, out_depth):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("piko_draw_host takes contiguous CPU tensors")
+    rc = _lib.piko_draw_host(ctx, ctypes.c_void_p(verts.data_ptr()), verts.shape[0],
+                             ctypes.c_void_p(idx.data_ptr()), idx.shape[0], _f32x(mvp, 16),
+                             _f32x(light, 3), ctypes.c_void_p(out_rgba.data_ptr()),
+                             ctypes.c_void_p(out_depth.data_ptr()), _stream_ptr(stream))
+    return _check(ctx, rc)
+
+
+def piko_finish(ctx):
+    return _lib.piko_finish(ctx)
+
+
+def piko_set_sync(ctx, mode):
+    return _check(ctx, _lib.piko_set_sync(ctx, mode))
+
+
+def piko_get_primid(ctx):
+    p = ctypes.c_void_p()
+    _check(ctx, _lib.piko_get_primid(ctx, ctypes.byref(p)))
+    return p.value
+
+
+def piko_get_bins(ctx):
+    s, q, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+    _check(ctx, _lib.piko_get_bins(ctx, ctypes.byref(s), ctypes.byref(q), ctypes.byref(n)))
+    return s.value, q.value, n.value
+
+
+def piko_set_debug(ctx, flags):
+    return _check(ctx, _lib.piko_set_debug(ctx, flags))
+
+
+def piko_get_coverage(ctx):
+    p = ctypes.c_void_p()
+    _check(ctx, _lib.piko_get_coverage(ctx, ctypes.byref(p)))
+    return p.value
+
+
+def piko_set_partition(ctx, rank, nranks):
+    return _check(ctx, _lib.piko_set_partition(ctx, rank, nranks))
+
+
+def piko_attach_comm(ctx, unique_id: bytes, rank, nranks):
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    return _check(ctx, _lib.piko_attach_comm(ctx, buf, rank, nranks))
+
+
+def piko_get_stats(ctx):
+    st = piko_stats()
+    _check(ctx, _lib.piko_get_stats(ctx, ctypes.byref(st)))
+    return {f: getattr(st, f) for f, _ in piko_stats._fields_}
+
+
+def piko_nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    rc = _lib.piko_nccl_unique_id(buf)
+    if rc != PIKO_OK:
+        raise PikoError(rc, _lib.piko_last_error(None).decode())
+    return buf.raw
+
+
+def piko_set_profiling(ctx, on):
+    return _check(ctx, _lib.piko_set_profiling(ctx, int(bool(on))))
+
+
+def piko_get_profile(ctx):
+    """{stage: total ms} and the number of profiled frames."""
+    ms = (ctypes.c_double * len(STAGES))()
+    n = ctypes.c_int64()
+    _check(ctx, _lib.piko_get_profile(ctx, ms, ctypes.byref(n)))
+    return dict(zip(STAGES, list(ms))), n.value
+
+
+# ---- convenience wrapper ------------------------------------------------------
+class Renderer:
+    """Owns a piko_ctx plus torch output buffers for one framebuffer shape."""
+
+    def __init__(self, width, height, bin_w=16, bin_h=None, device=None):
+        import torch
+        bin_h = bin_w if bin_h is None else bin_h
+        self.device = torch.device(device or "cuda")
+        with torch.cuda.device(self.device):
+            self.ctx = piko_create(width, height, bin_w, bin_h)
+        self.W, self.H, self.bin_w, self.bin_h = width, height, bin_w, bin_h
+        self.rgba = torch.empty((height, width, 4), dtype=torch.float32, device=self.device)
+        self.depth = torch.empty((height, width), dtype=torch.float32, device=self.device)
+
+    @property
+    def n_bins(self):
+        return (-(-self.W // self.bin_w)) * (-(-self.H // self.bin_h))
+
+    def draw(self, verts, idx, mvp, light, stream=None, check=True):
+        return piko_draw(self.ctx, verts, idx, idx.shape[0], mvp, light, self.rgba, self.depth,
+                         stream, check)
+
+    def primid(self):
+        import torch
+        return _wrap_device(piko_get_primid(self.ctx), (self.H, self.W), torch.int32, self.device)
+
+    def coverage(self):
+        import torch
+        return _wrap_device(piko_get_coverage(self.ctx), (self.H, self.W), torch.int32, self.device)
+
+    def bins(self):
+        """(bin_start i32[NB+1], bin_prims i32[P]) as torch tensors (copies)."""
+        import torch
+        s, q, n = piko_get_bins(self.ctx)
+        start = _wrap_device(s, (self.n_bins + 1,), torch.int32, self.device)
+        prims = _wrap_device(q, (n,), torch.int32, self.device) if n else torch.zeros(0, dtype=torch.int32)
+        return start, prims
+
+    def stats(self):
+        return piko_get_stats(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            piko_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _DevView:
+    """Zero-copy __cuda_array_interface__ view of a ctx-owned device buffer."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), True), "version": 2}
+
+
+def _wrap_device(ptr, shape, dtype, device):
+    """Copy a ctx-owned device buffer into a fresh torch tensor (device-to-device)."""
+    import torch
+    typestr = {torch.int32: "<i4", torch.float32: "<f4", torch.int64: "<i8"}[dtype]
+    torch.cuda.synchronize(device)
+    if int(torch.tensor(shape).prod()) == 0:
+        return torch.empty(shape, dtype=dtype, device=device)
+    return torch.as_tensor(_DevView(ptr, shape, typestr), device=device).clone()

@@ -1,0 +1,591 @@
+// piko_api.cu -- host orchestration behind the C ABI of include/piko.h.
+//
+// One piko_ctx = one framebuffer shape + bin grid on one device.  It owns the
+// per-frame scratch (setup records, pair lists, bin CSR, look-back status
+// words, primID / coverage buffers), grows it on demand, enqueues the kernel
+// sequence of a frame on the caller's stream, and (multi-GPU) runs the NCCL
+// tile-key gather to rank 0.  See DESIGN.md "Boundary" and "Host runtime".
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/piko.h"
+#include "piko_internal.h"
+
+using namespace piko;
+
+// ---------------------------------------------------------------------------
+// minimal run-time NCCL binding (dlopen libnccl.so.2; reuses torch's copy if
+// it is already loaded).  Only the calls of the tile gather are bound.
+// ---------------------------------------------------------------------------
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclUint8_ = 1 };  // ncclDataType_t value for ncclUint8
+
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { err = "cannot dlopen libnccl.so.2"; return false; }
+#define PIKO_SYM(n) n = reinterpret_cast<decltype(n)>(dlsym(h, "nccl" #n)); if (!n) { err = "missing nccl" #n; return false; }
+    PIKO_SYM(CommInitRank) PIKO_SYM(CommDestroy) PIKO_SYM(Send) PIKO_SYM(Recv)
+    PIKO_SYM(GroupStart) PIKO_SYM(GroupEnd) PIKO_SYM(GetErrorString) PIKO_SYM(GetUniqueId)
+#undef PIKO_SYM
+    return true;
+  }
+};
+Nccl g_nccl;
+
+thread_local std::string g_create_error;
+
+int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+bool pow2_in(int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1)) == 0; }
+}  // namespace
+
+struct piko_ctx {
+  int device = 0;
+  Grid g{};
+  int bw = 0, bh = 0;
+  int npass = 0;
+  int owned = 0;            // bins owned by this rank
+  unsigned debug = 0;
+  int sync_mode = PIKO_SYNC_CHECKED;
+  bool virt = false;        // virtual rank (partition without communicator)
+  std::string err;
+
+  // scratch
+  int4* rec = nullptr; long long rec_cap = 0;
+  uint32_t* keys[2] = {nullptr, nullptr};
+  int32_t* vals[2] = {nullptr, nullptr};
+  unsigned long long pair_cap = 0;
+  uint32_t* bin_count = nullptr;
+  int32_t* bin_start = nullptr;
+  Control* ctl = nullptr;
+  unsigned long long* st_k1 = nullptr; long long st_k1_cap = 0;
+  unsigned long long* st_scan = nullptr; long long st_scan_n = 0;
+  uint32_t* st_rx = nullptr; long long st_rx_chunks = 0;
+  int32_t* primid = nullptr;
+  uint32_t* cov = nullptr;
+  Control* h_ctl = nullptr;          // pinned mirror of the control block
+  cudaEvent_t done = nullptr;
+  bool pending = false;              // a frame's status not yet checked
+  int last_status = PIKO_OK;
+  long long last_T = 0;
+
+  int grid_k1 = 148, grid_scan = 148, grid_rx = 148;
+
+  // end-to-end staging
+  float* d_verts = nullptr; long long d_verts_cap = 0;
+  int32_t* d_idx = nullptr; long long d_idx_cap = 0;
+  float* d_rgba = nullptr; float* d_depth = nullptr;
+
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  unsigned long long* tile_keys = nullptr;  // [owned_max][bw*bh]
+  unsigned long long* all_keys = nullptr;   // rank 0: [nranks][owned_max][bw*bh]
+  int owned_max = 0;
+
+  // profiling: PIKO_NUM_STAGES + 1 boundary events per frame
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  long long prof_frames = 0;
+  cudaEvent_t* frame_events() {
+    const size_t need = (size_t)(prof_frames + 1) * (PIKO_NUM_STAGES + 1);
+    while (ev_pool.size() < need) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      ev_pool.push_back(e);
+    }
+    return &ev_pool[(size_t)prof_frames * (PIKO_NUM_STAGES + 1)];
+  }
+
+  int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    err = buf;
+    return code;
+  }
+};
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return ctx->fail(PIKO_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                       __FILE__, __LINE__);                                         \
+  } while (0)
+
+static void set_ownership(piko_ctx* ctx, int rank, int nranks) {
+  ctx->g.rank = rank;
+  ctx->g.nranks = nranks;
+  ctx->owned = rank < ctx->g.NB ? (ctx->g.NB - rank + nranks - 1) / nranks : 0;
+  ctx->owned_max = (ctx->g.NB + nranks - 1) / nranks;
+}
+
+extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
+  if (width < 1 || height < 1 || width > 16384 || height > 16384) {
+    g_create_error = "width and height must be in [1, 16384]";
+    return nullptr;
+  }
+  if (!pow2_in(bin_w, 8, 64) || !pow2_in(bin_h, 8, 64)) {
+    g_create_error = "bin_w and bin_h must be powers of two in [8, 64]";
+    return nullptr;
+  }
+  piko_ctx* ctx = new (std::nothrow) piko_ctx();
+  if (!ctx) { g_create_error = "out of host memory"; return nullptr; }
+  cudaGetDevice(&ctx->device);
+  ctx->bw = bin_w; ctx->bh = bin_h;
+  Grid& g = ctx->g;
+  g.W = width; g.H = height;
+  g.bw_log2 = ilog2(bin_w); g.bh_log2 = ilog2(bin_h);
+  g.binsX = (width + bin_w - 1) / bin_w;
+  g.binsY = (height + bin_h - 1) / bin_h;
+  g.NB = g.binsX * g.binsY;
+  set_ownership(ctx, 0, 1);
+  int bits = 0;
+  while ((1ll << bits) < (long long)g.NB) ++bits;
+  ctx->npass = (bits + RX_BITS - 1) / RX_BITS;
+  const long long npx = (long long)width * height;
+  bool ok = cudaMalloc(&ctx->bin_count, sizeof(uint32_t) * g.NB) == cudaSuccess &&
+            cudaMalloc(&ctx->bin_start, sizeof(int32_t) * (g.NB + 1)) == cudaSuccess &&
+            cudaMalloc(&ctx->ctl, sizeof(Control)) == cudaSuccess &&
+            cudaMalloc(&ctx->primid, sizeof(int32_t) * npx) == cudaSuccess &&
+            cudaMallocHost(&ctx->h_ctl, sizeof(Control)) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming) == cudaSuccess;
+  ctx->st_scan_n = (g.NB + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  ok = ok && cudaMalloc(&ctx->st_scan, sizeof(unsigned long long) * ctx->st_scan_n) == cudaSuccess;
+  ok = ok && cudaMemset(ctx->bin_count, 0, sizeof(uint32_t) * g.NB) == cudaSuccess &&
+       cudaMemset(ctx->bin_start, 0, sizeof(int32_t) * (g.NB + 1)) == cudaSuccess &&
+       cudaMemset(ctx->ctl, 0, sizeof(Control)) == cudaSuccess;
+  if (!ok) {
+    g_create_error = std::string("device allocation failed: ") + cudaGetErrorString(cudaGetLastError());
+    piko_destroy(ctx);
+    return nullptr;
+  }
+  memset(ctx->h_ctl, 0, sizeof(Control));
+  ctx->grid_k1 = max_grid_setup();
+  ctx->grid_scan = max_grid_scan();
+  ctx->grid_rx = max_grid_radix();
+  return ctx;
+}
+
+extern "C" void piko_destroy(piko_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+  void* bufs[] = {ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
+                  ctx->bin_start, ctx->ctl, ctx->st_k1, ctx->st_scan, ctx->st_rx, ctx->primid,
+                  ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
+                  ctx->all_keys};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->done) cudaEventDestroy(ctx->done);
+  delete ctx;
+}
+
+extern "C" const char* piko_last_error(const piko_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+// ---- capacity management ----------------------------------------------------
+static int ensure_tris(piko_ctx* ctx, long long T) {
+  if (T > ctx->rec_cap) {
+    long long cap = std::max<long long>(T, 1024);
+    if (ctx->rec) cudaFree(ctx->rec);
+    ctx->rec = nullptr;
+    CK(cudaMalloc(&ctx->rec, sizeof(int4) * 3 * cap));
+    ctx->rec_cap = cap;
+  }
+  const long long chunks = std::max<long long>((T + K1_CHUNK - 1) / K1_CHUNK, 1);
+  if (chunks > ctx->st_k1_cap) {
+    if (ctx->st_k1) cudaFree(ctx->st_k1);
+    ctx->st_k1 = nullptr;
+    CK(cudaMalloc(&ctx->st_k1, sizeof(unsigned long long) * chunks));
+    ctx->st_k1_cap = chunks;
+  }
+  return PIKO_OK;
+}
+
+static int ensure_pairs(piko_ctx* ctx, unsigned long long P) {
+  if (P <= ctx->pair_cap) return PIKO_OK;
+  if (P >= (1ull << 30))
+    return ctx->fail(PIKO_ECAPACITY, "pair count %llu exceeds the 2^30 limit", P);
+  unsigned long long cap = std::min<unsigned long long>(P + P / 4 + 4096, (1ull << 30) - 1);
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->keys[k]) cudaFree(ctx->keys[k]);
+    if (ctx->vals[k]) cudaFree(ctx->vals[k]);
+    ctx->keys[k] = nullptr; ctx->vals[k] = nullptr;
+    CK(cudaMalloc(&ctx->keys[k], sizeof(uint32_t) * cap));
+    CK(cudaMalloc(&ctx->vals[k], sizeof(int32_t) * cap));
+  }
+  const long long chunks = (long long)((cap + RX_CHUNK - 1) / RX_CHUNK);
+  if (ctx->st_rx) cudaFree(ctx->st_rx);
+  ctx->st_rx = nullptr;
+  CK(cudaMalloc(&ctx->st_rx, sizeof(uint32_t) * RX_RADIX * chunks * std::max(ctx->npass, 1)));
+  ctx->st_rx_chunks = chunks;
+  ctx->pair_cap = cap;
+  return PIKO_OK;
+}
+
+static int ensure_cov(piko_ctx* ctx) {
+  if ((ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) && !ctx->cov)
+    CK(cudaMalloc(&ctx->cov, sizeof(uint32_t) * (size_t)ctx->g.W * ctx->g.H));
+  return PIKO_OK;
+}
+
+// ---- one frame ---------------------------------------------------------------
+static int enqueue_frame(piko_ctx* ctx, const float* verts, const int32_t* idx, long long T,
+                         const Mat4& M, const float L[3], float* rgba, float* depth,
+                         cudaStream_t s) {
+  const bool gather = ctx->comm != nullptr && ctx->g.nranks > 1;
+  cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
+  if (ctx->prof && !ev) return ctx->fail(PIKO_ECUDA, "cannot create profiling events");
+  auto mark = [&](int stage) -> cudaError_t { return ev ? cudaEventRecord(ev[stage], s) : cudaSuccess; };
+  CK(mark(0));
+  CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s));
+  const long long k1_chunks = (T + K1_CHUNK - 1) / K1_CHUNK;
+  if (k1_chunks > 0) CK(cudaMemsetAsync(ctx->st_k1, 0, sizeof(unsigned long long) * k1_chunks, s));
+  CK(cudaMemsetAsync(ctx->st_scan, 0, sizeof(unsigned long long) * ctx->st_scan_n, s));
+  if (ctx->npass > 0)
+    CK(cudaMemsetAsync(ctx->st_rx, 0, sizeof(uint32_t) * RX_RADIX * ctx->st_rx_chunks * ctx->npass, s));
+  CK(mark(1 + PIKO_STAGE_CLEAR));
+
+  if (T > 0) {
+    SetupArgs a{};
+    a.verts = verts; a.idx = idx; a.n_tris = T; a.M = M; a.g = ctx->g;
+    a.rec = ctx->rec; a.pair_keys = ctx->keys[0]; a.pair_vals = ctx->vals[0];
+    a.bin_count = ctx->bin_count; a.status = ctx->st_k1; a.ctl = ctx->ctl; a.cap = ctx->pair_cap;
+    CK(launch_setup(a, (int)std::min<long long>(k1_chunks, ctx->grid_k1), s));
+  }
+  CK(mark(1 + PIKO_STAGE_SETUP));
+  {
+    ScanArgs a{};
+    a.bin_count = ctx->bin_count; a.bin_start = ctx->bin_start; a.status = ctx->st_scan;
+    a.ctl = ctx->ctl; a.NB = ctx->g.NB; a.npass = ctx->npass;
+    CK(launch_bin_scan(a, (int)std::min<long long>(ctx->st_scan_n, ctx->grid_scan), s));
+  }
+  CK(mark(1 + PIKO_STAGE_BINSCAN));
+  const int rx_grid = (int)std::min<long long>(ctx->st_rx_chunks, ctx->grid_rx);
+  for (int p = 0; p < ctx->npass; ++p) {
+    RadixArgs a{};
+    a.keys_in = ctx->keys[p & 1]; a.vals_in = ctx->vals[p & 1];
+    a.keys_out = (p + 1 < ctx->npass) ? ctx->keys[(p + 1) & 1] : nullptr;
+    a.vals_out = ctx->vals[(p + 1) & 1];
+    a.status = ctx->st_rx + (size_t)p * RX_RADIX * ctx->st_rx_chunks;
+    a.ctl = ctx->ctl; a.pass = p; a.shift = RX_BITS * p; a.cap = ctx->pair_cap;
+    CK(launch_radix_pass(a, rx_grid, s));
+  }
+  CK(mark(1 + PIKO_STAGE_RADIX));
+  {
+    TileArgs a{};
+    a.verts = verts; a.idx = idx; a.M = M;
+    a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
+    a.g = ctx->g; a.rec = ctx->rec; a.bin_start = ctx->bin_start;
+    a.bin_prims = ctx->vals[ctx->npass & 1]; a.ctl = ctx->ctl;
+    a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
+    a.out_cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
+    a.tile_keys = gather ? ctx->tile_keys : nullptr;
+    CK(launch_tile(a, ctx->bw, ctx->bh, ctx->owned, a.out_cov != nullptr, gather, s));
+  }
+  CK(mark(1 + PIKO_STAGE_TILE));
+  if (gather) {
+    const size_t tile_bytes = sizeof(unsigned long long) * ctx->bw * ctx->bh;
+    const size_t bytes = tile_bytes * ctx->owned_max;
+    if (g_nccl.GroupStart() != 0) return ctx->fail(PIKO_ENCCL, "ncclGroupStart failed");
+    int rc = 0;
+    if (ctx->g.rank == 0) {
+      CK(cudaMemcpyAsync(ctx->all_keys, ctx->tile_keys, tile_bytes * ctx->owned,
+                         cudaMemcpyDeviceToDevice, s));
+      for (int r = 1; r < ctx->g.nranks && rc == 0; ++r) {
+        const int owned_r = r < ctx->g.NB ? (ctx->g.NB - r + ctx->g.nranks - 1) / ctx->g.nranks : 0;
+        if (owned_r > 0)
+          rc = g_nccl.Recv(ctx->all_keys + (size_t)r * ctx->owned_max * ctx->bw * ctx->bh,
+                           tile_bytes * owned_r, ncclUint8_, r, ctx->comm, s);
+      }
+    } else if (ctx->owned > 0) {
+      rc = g_nccl.Send(ctx->tile_keys, tile_bytes * ctx->owned, ncclUint8_, 0, ctx->comm, s);
+    }
+    const int rc2 = g_nccl.GroupEnd();
+    if (rc != 0 || rc2 != 0)
+      return ctx->fail(PIKO_ENCCL, "NCCL gather failed: %s", g_nccl.GetErrorString(rc ? rc : rc2));
+    (void)bytes;
+    CK(mark(1 + PIKO_STAGE_GATHER));
+    if (ctx->g.rank == 0) {
+      ResolveArgs a{};
+      a.verts = verts; a.idx = idx; a.M = M;
+      a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
+      a.g = ctx->g; a.all_keys = ctx->all_keys; a.owned_max = ctx->owned_max;
+      a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
+      CK(launch_resolve(a, s));
+    }
+  } else {
+    CK(mark(1 + PIKO_STAGE_GATHER));
+  }
+  CK(mark(1 + PIKO_STAGE_RESOLVE));
+  if (ev) ++ctx->prof_frames;
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(ctx->done, s));
+  ctx->pending = true;
+  ctx->last_T = T;
+  return PIKO_OK;
+}
+
+// Wait for the pending frame; PIKO_ECAPACITY (and grown capacity) on overflow.
+static int check_frame(piko_ctx* ctx) {
+  if (!ctx->pending) return ctx->last_status;
+  ctx->pending = false;
+  CK(cudaEventSynchronize(ctx->done));
+  if (ctx->h_ctl->overflow) {
+    const int rc = ensure_pairs(ctx, ctx->h_ctl->n_pairs);
+    ctx->last_status = rc != PIKO_OK ? rc : PIKO_ECAPACITY;
+    if (rc == PIKO_OK) ctx->fail(PIKO_ECAPACITY, "pair capacity exceeded (P=%llu); grown", ctx->h_ctl->n_pairs);
+    return ctx->last_status;
+  }
+  ctx->last_status = PIKO_OK;
+  return PIKO_OK;
+}
+
+static int validate_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, int32_t n_tris,
+                         const float* mvp, const float* light, float* rgba, float* depth,
+                         float L[3]) {
+  if (n_tris < 0) return ctx->fail(PIKO_EINVAL, "n_tris < 0");
+  if (!mvp || !light) return ctx->fail(PIKO_EINVAL, "mvp and light must be non-null");
+  const bool need_out = !(ctx->comm && ctx->g.nranks > 1 && ctx->g.rank != 0);
+  if (need_out && (!rgba || !depth)) return ctx->fail(PIKO_EINVAL, "null output buffer");
+  if (n_tris > 0 && (!verts || !idx)) return ctx->fail(PIKO_EINVAL, "null scene buffer");
+  if ((reinterpret_cast<uintptr_t>(verts) | reinterpret_cast<uintptr_t>(idx) |
+       reinterpret_cast<uintptr_t>(rgba)) & 15u)
+    return ctx->fail(PIKO_EINVAL, "verts, idx and out_rgba must be 16-byte aligned");
+  for (int k = 0; k < 3; ++k)
+    if (!std::isfinite(light[k])) return ctx->fail(PIKO_EINVAL, "light must be finite");
+  if (light[0] == 0.0f && light[1] == 0.0f && light[2] == 0.0f)
+    return ctx->fail(PIKO_EINVAL, "light must be non-zero");
+  for (int k = 0; k < 3; ++k) L[k] = light[k];
+  return PIKO_OK;
+}
+
+static int draw_impl(piko_ctx* ctx, const float* verts, const int32_t* idx, int32_t n_tris,
+                     const float mvp[16], const float light[3], float* rgba, float* depth,
+                     cudaStream_t s, bool force_check) {
+  float L[3] = {0.0f, 0.0f, 0.0f};
+  int rc = validate_draw(ctx, verts, idx, n_tris, mvp, light, rgba, depth, L);
+  if (rc != PIKO_OK) return rc;
+  CK(cudaSetDevice(ctx->device));
+  // status of a previous asynchronous frame (grows capacity if it overflowed)
+  int prev = PIKO_OK;
+  if (ctx->pending) prev = check_frame(ctx);
+  if (prev == PIKO_ECUDA) return prev;
+  Mat4 M;
+  memcpy(M.m, mvp, sizeof M.m);
+  if ((rc = ensure_tris(ctx, n_tris)) != PIKO_OK) return rc;
+  if ((rc = ensure_pairs(ctx, std::max<unsigned long long>(ctx->pair_cap, 2ull * n_tris + 4096))) != PIKO_OK)
+    return rc;
+  if ((rc = ensure_cov(ctx)) != PIKO_OK) return rc;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    if ((rc = enqueue_frame(ctx, verts, idx, n_tris, M, L, rgba, depth, s)) != PIKO_OK) return rc;
+    if (ctx->sync_mode == PIKO_SYNC_ASYNC && !force_check) return prev == PIKO_ECAPACITY ? PIKO_OK : prev;
+    rc = check_frame(ctx);
+    if (rc != PIKO_ECAPACITY) return rc;
+    // multi-rank: every rank must re-issue together; a capacity miss is
+    // reported instead of re-issued so ranks cannot diverge.
+    if (ctx->comm && ctx->g.nranks > 1) return rc;
+  }
+  return rc;
+}
+
+extern "C" int piko_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, int32_t n_tris,
+                         const float mvp[16], const float light[3], float* out_rgba,
+                         float* out_depth, void* stream) {
+  if (!ctx) return PIKO_EINVAL;
+  return draw_impl(ctx, verts, idx, n_tris, mvp, light, out_rgba, out_depth,
+                   static_cast<cudaStream_t>(stream), false);
+}
+
+extern "C" int piko_draw_host(piko_ctx* ctx, const float* h_verts, int64_t n_verts,
+                              const int32_t* h_idx, int32_t n_tris, const float mvp[16],
+                              const float light[3], float* h_rgba, float* h_depth, void* stream) {
+  if (!ctx) return PIKO_EINVAL;
+  if (n_verts < 0 || n_tris < 0) return ctx->fail(PIKO_EINVAL, "negative size");
+  if (n_tris > 0 && (!h_verts || !h_idx)) return ctx->fail(PIKO_EINVAL, "null host scene buffer");
+  if (!h_rgba || !h_depth) return ctx->fail(PIKO_EINVAL, "null host output buffer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  const size_t npx = (size_t)ctx->g.W * ctx->g.H;
+  if (n_verts > ctx->d_verts_cap) {
+    if (ctx->d_verts) cudaFree(ctx->d_verts);
+    ctx->d_verts = nullptr;
+    CK(cudaMalloc(&ctx->d_verts, sizeof(float) * 8 * std::max<int64_t>(n_verts, 1)));
+    ctx->d_verts_cap = n_verts;
+  }
+  if (n_tris > ctx->d_idx_cap) {
+    if (ctx->d_idx) cudaFree(ctx->d_idx);
+    ctx->d_idx = nullptr;
+    CK(cudaMalloc(&ctx->d_idx, sizeof(int32_t) * 3 * std::max<int32_t>(n_tris, 1)));
+    ctx->d_idx_cap = n_tris;
+  }
+  if (!ctx->d_rgba) {
+    CK(cudaMalloc(&ctx->d_rgba, sizeof(float) * 4 * npx));
+    CK(cudaMalloc(&ctx->d_depth, sizeof(float) * npx));
+  }
+  if (n_verts > 0)
+    CK(cudaMemcpyAsync(ctx->d_verts, h_verts, sizeof(float) * 8 * n_verts, cudaMemcpyHostToDevice, s));
+  if (n_tris > 0)
+    CK(cudaMemcpyAsync(ctx->d_idx, h_idx, sizeof(int32_t) * 3 * (size_t)n_tris, cudaMemcpyHostToDevice, s));
+  int rc = draw_impl(ctx, ctx->d_verts, ctx->d_idx, n_tris, mvp, light, ctx->d_rgba, ctx->d_depth, s, true);
+  if (rc != PIKO_OK) return rc;
+  const bool has_out = !(ctx->comm && ctx->g.nranks > 1 && ctx->g.rank != 0);
+  if (has_out) {
+    CK(cudaMemcpyAsync(h_rgba, ctx->d_rgba, sizeof(float) * 4 * npx, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_depth, ctx->d_depth, sizeof(float) * npx, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  return PIKO_OK;
+}
+
+extern "C" int piko_finish(piko_ctx* ctx) {
+  if (!ctx) return PIKO_EINVAL;
+  return check_frame(ctx);
+}
+
+extern "C" int piko_set_sync(piko_ctx* ctx, int mode) {
+  if (!ctx) return PIKO_EINVAL;
+  if (mode != PIKO_SYNC_CHECKED && mode != PIKO_SYNC_ASYNC) return ctx->fail(PIKO_EINVAL, "bad sync mode");
+  ctx->sync_mode = mode;
+  return PIKO_OK;
+}
+
+extern "C" int piko_get_primid(const piko_ctx* ctx, const int32_t** d_primid) {
+  if (!ctx || !d_primid) return PIKO_EINVAL;
+  *d_primid = ctx->primid;
+  return PIKO_OK;
+}
+
+extern "C" int piko_get_bins(const piko_ctx* cctx, const int32_t** d_bin_start,
+                             const int32_t** d_bin_prims, int64_t* n_pairs) {
+  piko_ctx* ctx = const_cast<piko_ctx*>(cctx);
+  if (!ctx || !d_bin_start || !d_bin_prims || !n_pairs) return PIKO_EINVAL;
+  int rc = check_frame(ctx);
+  if (rc != PIKO_OK) return rc;
+  *d_bin_start = ctx->bin_start;
+  *d_bin_prims = ctx->vals[ctx->npass & 1];
+  *n_pairs = (int64_t)ctx->h_ctl->n_pairs;
+  return PIKO_OK;
+}
+
+extern "C" int piko_set_debug(piko_ctx* ctx, unsigned flags) {
+  if (!ctx) return PIKO_EINVAL;
+  if (flags & ~PIKO_DEBUG_COVERAGE_COUNT) return ctx->fail(PIKO_EINVAL, "unknown debug flag");
+  ctx->debug = flags;
+  return PIKO_OK;
+}
+
+extern "C" int piko_get_coverage(const piko_ctx* ctx, const uint32_t** d_cov) {
+  if (!ctx || !d_cov) return PIKO_EINVAL;
+  if (!ctx->cov) return PIKO_ESTATE;
+  *d_cov = ctx->cov;
+  return PIKO_OK;
+}
+
+extern "C" int piko_set_partition(piko_ctx* ctx, int rank, int nranks) {
+  if (!ctx) return PIKO_EINVAL;
+  if (ctx->comm) return ctx->fail(PIKO_ESTATE, "communicator attached");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return ctx->fail(PIKO_EINVAL, "bad rank/nranks");
+  set_ownership(ctx, rank, nranks);
+  ctx->virt = nranks > 1;
+  return PIKO_OK;
+}
+
+extern "C" int piko_attach_comm(piko_ctx* ctx, const void* uid, int rank, int nranks) {
+  if (!ctx || !uid) return PIKO_EINVAL;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return ctx->fail(PIKO_EINVAL, "bad rank/nranks");
+  if (ctx->comm) return ctx->fail(PIKO_ESTATE, "communicator already attached");
+  std::string e;
+  if (!g_nccl.load(e)) return ctx->fail(PIKO_ENCCL, "%s", e.c_str());
+  CK(cudaSetDevice(ctx->device));
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof id);
+  const int rc = g_nccl.CommInitRank(&ctx->comm, nranks, id, rank);
+  if (rc != 0) { ctx->comm = nullptr; return ctx->fail(PIKO_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(rc)); }
+  set_ownership(ctx, rank, nranks);
+  const size_t tile_bytes = sizeof(unsigned long long) * ctx->bw * ctx->bh;
+  CK(cudaMalloc(&ctx->tile_keys, tile_bytes * std::max(ctx->owned_max, 1)));
+  if (rank == 0) CK(cudaMalloc(&ctx->all_keys, tile_bytes * ctx->owned_max * (size_t)nranks));
+  return PIKO_OK;
+}
+
+extern "C" int piko_get_stats(const piko_ctx* cctx, piko_stats* out) {
+  piko_ctx* ctx = const_cast<piko_ctx*>(cctx);
+  if (!ctx || !out) return PIKO_EINVAL;
+  int rc = check_frame(ctx);
+  if (rc == PIKO_ECUDA) return rc;
+  out->n_tris = ctx->last_T;
+  out->n_live = (int64_t)ctx->h_ctl->n_live;
+  out->n_pairs = (int64_t)ctx->h_ctl->n_pairs;
+  out->n_bins = ctx->g.NB;
+  out->owned_bins = ctx->owned;
+  out->pair_capacity = (int64_t)ctx->pair_cap;
+  out->radix_passes = ctx->npass;
+  const bool gather = ctx->comm && ctx->g.nranks > 1;
+  out->kernels_per_frame = (ctx->last_T > 0 ? 1 : 0) + 1 + ctx->npass + (ctx->owned > 0 ? 1 : 0) +
+                           (gather && ctx->g.rank == 0 ? 1 : 0);
+  return PIKO_OK;
+}
+
+extern "C" int piko_nccl_unique_id(void* out) {
+  if (!out) return PIKO_EINVAL;
+  std::string e;
+  if (!g_nccl.load(e)) { g_create_error = e; return PIKO_ENCCL; }
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != 0) return PIKO_ENCCL;
+  memcpy(out, &id, sizeof id);
+  return PIKO_OK;
+}
+
+extern "C" int piko_set_profiling(piko_ctx* ctx, int on) {
+  if (!ctx) return PIKO_EINVAL;
+  if (ctx->pending) check_frame(ctx);
+  ctx->prof = on != 0;
+  ctx->prof_frames = 0;
+  return PIKO_OK;
+}
+
+extern "C" int piko_get_profile(piko_ctx* ctx, double ms[PIKO_NUM_STAGES], int64_t* frames) {
+  if (!ctx || !ms || !frames) return PIKO_EINVAL;
+  for (int k = 0; k < PIKO_NUM_STAGES; ++k) ms[k] = 0.0;
+  for (long long f = 0; f < ctx->prof_frames; ++f) {
+    cudaEvent_t* e = &ctx->ev_pool[(size_t)f * (PIKO_NUM_STAGES + 1)];
+    CK(cudaEventSynchronize(e[PIKO_NUM_STAGES]));
+    for (int k = 0; k < PIKO_NUM_STAGES; ++k) {
+      float t = 0.0f;
+      CK(cudaEventElapsedTime(&t, e[k], e[k + 1]));
+      ms[k] += t;
+    }
+  }
+  *frames = ctx->prof_frames;
+  return PIKO_OK;
+}

@@ -1,0 +1,242 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): bin lists, coverage, depth and primID
+bit-exact; RGB within 1e-5 absolute.  Every input is a seeded synthetic scene
+(scenes/), the oracle (oracle/) is independent of the CUDA path.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import scenes
+
+pytestmark = pytest.mark.gpu
+
+RGB_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def env(oracle_lib):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1404_6293_b200 as piko
+    return piko, oracle_lib, torch
+
+
+def gpu_render(env, s, bw, bh=None, cov=True, partition=None, sync=None):
+    piko, _, torch = env
+    bh = bw if bh is None else bh
+    dev = torch.device("cuda:0")
+    verts = torch.from_numpy(np.ascontiguousarray(s.verts)).to(dev)
+    idx = torch.from_numpy(np.ascontiguousarray(s.idx)).to(dev)
+    r = piko.Renderer(s.W, s.H, bw, bh, device=dev)
+    if cov:
+        piko.piko_set_debug(r.ctx, piko.PIKO_DEBUG_COVERAGE_COUNT)
+    if partition is not None:
+        piko.piko_set_partition(r.ctx, *partition)
+        r.rgba.fill_(float("nan"))
+        r.depth.fill_(float("nan"))
+    if sync is not None:
+        piko.piko_set_sync(r.ctx, sync)
+    r.draw(verts, idx, s.mvp, s.light)
+    torch.cuda.synchronize()
+    out = {"rgba": r.rgba.cpu().numpy(), "depth": r.depth.cpu().numpy(),
+           "primid": r.primid().cpu().numpy()}
+    if cov:
+        out["covcount"] = r.coverage().cpu().numpy().view(np.uint32)
+    st, pr = r.bins()
+    out["bin_start"], out["bin_prims"] = st.cpu().numpy(), pr.cpu().numpy()
+    out["stats"] = r.stats()
+    r.close()
+    return out
+
+
+def assert_frame_equal(got, ref, cov=True):
+    assert np.array_equal(got["primid"], ref["primid"]), \
+        f"primID mismatch at {np.argwhere(got['primid'] != ref['primid'])[:5].tolist()}"
+    gd, rd = got["depth"].view(np.uint32), ref["depth"].view(np.uint32)
+    assert np.array_equal(gd, rd), f"depth mismatch at {np.argwhere(gd != rd)[:5].tolist()}"
+    if cov:
+        assert np.array_equal(got["covcount"], ref["covcount"]), "coverage mismatch"
+    err = np.abs(got["rgba"] - ref["rgba"]).max()
+    assert err <= RGB_TOL, err
+
+
+def assert_bins_equal(got, env, s, bw, bh=None, rank=0, nranks=1):
+    bh = bw if bh is None else bh
+    start, prims = env[1].bins(s.verts, s.idx, s.mvp, s.W, s.H, bw, bh, rank, nranks)
+    assert np.array_equal(got["bin_start"], start), "bin_start mismatch"
+    assert np.array_equal(got["bin_prims"], prims), "bin_prims mismatch"
+
+
+def oracle_frame(env, s, cov=True):
+    return env[1].render(s.verts, s.idx, s.mvp, s.light, s.W, s.H, want_covcount=cov)
+
+
+# ------------------------------------------------------------------------------
+@pytest.mark.parametrize("bw,bh", [(8, 8), (16, 16), (32, 32), (64, 64), (8, 32), (64, 16)])
+def test_c1_all_bin_sizes(env, bw, bh):
+    s = scenes.scene_c1()
+    got = gpu_render(env, s, bw, bh)
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, bw, bh)
+
+
+@pytest.mark.parametrize("bw", [8, 16, 32, 64])
+def test_soup_ragged_screen(env, bw):
+    """Random soup on a 200x120 screen (partial edge bins in x and y), incl.
+    triangles straddling the screen edge and the guard band."""
+    s = scenes.scene_soup(20000, 200, 120, seed=21, name="soup", bin_sizes=(bw,))
+    got = gpu_render(env, s, bw)
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, bw)
+
+
+def test_large_triangles_int64_path(env):
+    """Triangles far larger than 128 px (int64 edge path), some covering the
+    whole screen, mixed with tiny ones; perspective camera."""
+    rng = np.random.default_rng(31)
+    W, H = 640, 480
+    T = 400
+    big = rng.uniform(-3, 3, (T, 3, 3))
+    big[:, :, 2] = rng.uniform(-20, -1.5, (T, 3))
+    small = big.mean(1, keepdims=True) + 0.01 * rng.normal(size=(T, 3, 3))
+    pos = np.concatenate([big, small], 0).reshape(-1, 3).astype(np.float32)
+    verts = scenes.pack_verts(pos, scenes.random_unit(rng, pos.shape[0]))
+    idx = np.arange(pos.shape[0], dtype=np.int32).reshape(-1, 3)
+    s = scenes.Scene("big", W, H, (16,), verts, idx, scenes.perspective_mvp())
+    for bw in (8, 16, 64):
+        got = gpu_render(env, s, bw)
+        assert_frame_equal(got, oracle_frame(env, s))
+        assert_bins_equal(got, env, s, bw)
+
+
+def test_capacity_overflow_regrows(env):
+    """Few full-screen triangles -> P far above the initial pair capacity: the
+    checked draw regrows and re-issues, the frame is still exact."""
+    tris = [[(-10.0, -10.0), (3000.0, -10.0), (-10.0, 3000.0)]] * 6 + \
+           [[(1024.0, 768.0), (-1000.0, 768.0), (1024.0, -1000.0)]] * 6
+    from tests.helpers import pixel_scene
+    zs = np.linspace(0.1, 0.9, 12)[:, None].repeat(3, 1)
+    v, i, m = pixel_scene(tris, zs, 1024, 768)
+    s = scenes.Scene("cap", 1024, 768, (8,), v, i, m)
+    got = gpu_render(env, s, 8)
+    assert got["stats"]["n_pairs"] == 12 * 128 * 96
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, 8)
+
+
+def test_empty_and_all_culled(env):
+    piko, _, torch = env
+    s = scenes.scene_c1()
+    e = scenes.Scene("empty", 64, 64, (8,), s.verts, s.idx[:0], s.mvp)
+    got = gpu_render(env, e, 8)
+    assert (got["primid"] == -1).all() and (got["depth"] == 1.0).all() and (got["rgba"] == 0).all()
+    assert got["stats"]["n_pairs"] == 0 and (got["bin_start"] == 0).all()
+    # everything behind the camera
+    c = scenes.Scene("culled", 64, 64, (8,), s.verts, s.idx, scenes.perspective_mvp(aspect=1.0))
+    got = gpu_render(env, c, 8)
+    assert_frame_equal(got, oracle_frame(env, c))
+
+
+def test_c2_full(env):
+    s = scenes.scene_c2()
+    got = gpu_render(env, s, 16)
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, 16)
+
+
+@pytest.mark.parametrize("bw", [8, 16, 32, 64])
+def test_c3_full_bin_sweep(env, bw):
+    s = scenes.scene_c3()
+    got = gpu_render(env, s, bw)
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, bw)
+
+
+def test_c4_full(env):
+    s = scenes.scene_c4()
+    got = gpu_render(env, s, 16, cov=False)
+    assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
+    assert_bins_equal(got, env, s, 16)
+
+
+@pytest.mark.parametrize("bw", [16, 8])
+def test_c5_full_planar_partition(env, bw):
+    s = scenes.scene_c5()
+    got = gpu_render(env, s, bw)
+    # planar partition: every pixel covered exactly once (property at full size)
+    assert got["covcount"].min() == 1 and got["covcount"].max() == 1
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, bw)
+
+
+def test_determinism_byte_identical(env):
+    s = scenes.scene_soup(50000, 320, 240, seed=41, name="soup")
+    a = gpu_render(env, s, 16)
+    b = gpu_render(env, s, 16)
+    for k in ("rgba", "depth", "primid", "covcount", "bin_start", "bin_prims"):
+        assert a[k].tobytes() == b[k].tobytes(), k
+
+
+@pytest.mark.parametrize("R", [2, 3, 4])
+def test_virtual_rank_partition(env, R):
+    """Sort-first partition on one GPU: rank r writes exactly its bins
+    (b mod R == r); the union over ranks is the full frame; per-rank bin lists
+    equal the oracle's rank-filtered lists."""
+    s = scenes.scene_soup(30000, 256, 200, seed=51, name="soup")
+    full = oracle_frame(env, s)
+    bw = 16
+    binsX = -(-s.W // bw)
+    ys, xs = np.mgrid[0:s.H, 0:s.W]
+    owner = ((ys // bw) * binsX + xs // bw) % R
+    merged = {k: np.zeros_like(full[k]) for k in ("rgba", "depth", "primid", "covcount")}
+    for r in range(R):
+        got = gpu_render(env, s, bw, partition=(r, R))
+        mine = owner == r
+        assert np.isnan(got["depth"][~mine]).all(), "rank wrote pixels it does not own"
+        for k in merged:
+            merged[k][mine] = got[k][mine]
+        assert_bins_equal(got, env, s, bw, rank=r, nranks=R)
+    assert_frame_equal(merged, full)
+
+
+def test_async_mode_and_finish(env):
+    piko, _, torch = env
+    s = scenes.scene_c2()
+    got = gpu_render(env, s, 16, sync=piko.PIKO_SYNC_ASYNC)
+    assert_frame_equal(got, oracle_frame(env, s))
+
+
+def test_draw_host_e2e_matches_device_path(env):
+    piko, _, torch = env
+    s = scenes.scene_c2()
+    r = piko.Renderer(s.W, s.H, 16)
+    hv = torch.from_numpy(s.verts).pin_memory()
+    hi = torch.from_numpy(s.idx).pin_memory()
+    rgba = torch.empty((s.H, s.W, 4), dtype=torch.float32).pin_memory()
+    depth = torch.empty((s.H, s.W), dtype=torch.float32).pin_memory()
+    piko.piko_draw_host(r.ctx, hv, hi, s.mvp, s.light, rgba, depth)
+    ref = oracle_frame(env, s, cov=False)
+    assert np.array_equal(depth.numpy().view(np.uint32), ref["depth"].view(np.uint32))
+    assert np.abs(rgba.numpy() - ref["rgba"]).max() <= RGB_TOL
+    r.close()
+
+
+def test_argument_validation(env):
+    piko, _, torch = env
+    s = scenes.scene_c1()
+    r = piko.Renderer(64, 64, 8)
+    v = torch.from_numpy(s.verts).cuda()
+    i = torch.from_numpy(s.idx).cuda()
+    assert piko.piko_draw(r.ctx, v, i, -1, s.mvp, s.light, r.rgba, r.depth, check=False) == piko.PIKO_EINVAL
+    assert piko.piko_draw(r.ctx, v, i, 16, s.mvp, [0, 0, 0], r.rgba, r.depth, check=False) == piko.PIKO_EINVAL
+    assert piko.piko_draw(r.ctx, v, i, 16, s.mvp, [np.nan, 0, 1], r.rgba, r.depth, check=False) == piko.PIKO_EINVAL
+    vv = torch.empty(s.verts.size + 1, dtype=torch.float32, device="cuda")[1:].view(-1, 8)
+    assert piko.piko_draw(r.ctx, vv, i, 16, s.mvp, s.light, r.rgba, r.depth, check=False) == piko.PIKO_EINVAL
+    assert piko.piko_draw(r.ctx, None, None, 16, s.mvp, s.light, r.rgba, r.depth, check=False) == piko.PIKO_EINVAL
+    r.close()
