@@ -267,7 +267,7 @@ class _DevView:
 
     def __init__(self, ptr, shape, typestr):
         self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
-                                         "data": (int(ptr), True), "version": 2}
+                                         "data": (int(ptr), False), "version": 2}
 
 
 def _wrap_device(ptr, shape, dtype, device):

@@ -1,21 +1,25 @@
 // kernels.cu -- the hot path of the binned rasterizer, hand-written for sm_100a.
 //
-//   k_setup      vertex transform + fixed-point setup + AssignBin count, fused
-//                with a decoupled-look-back exclusive scan of the per-triangle
-//                pair counts and the expansion of (bin, primID) pairs in
-//                primitive order.
-//   k_bin_scan   exclusive scan of the per-bin pair counts -> CSR bin_start, plus
-//                the digit histograms of the stable LSD radix passes.
-//   k_radix_pass one stable LSD pass (8-bit digit) of the pairs by bin id:
-//                warp match-any ranking, per-digit decoupled look-back,
-//                shared-memory staged scatter.  After the last pass the values
-//                are the CSR bin_prims, ascending primID within each bin.
+//   k_setup      Vertex transform + fixed-point triangle setup + AssignBin count,
+//                fused with a decoupled-look-back exclusive scan of the per-
+//                triangle pair counts and a cooperative, coalesced expansion of
+//                the (bin, primID) pairs in primitive order, the per-bin counts
+//                (warp-aggregated) and the digit histograms of the radix passes.
+//                ("Vertex Shader"; P:684 AssignToBoundingBox;
+//                 P:1081-1084 prefix sums "while maintaining primitive order")
+//   k_radix_pass One stable LSD pass (8-bit digit) of the pairs by bin id: warp
+//                match-any ranking, per-digit decoupled look-back (8 chunks per
+//                probe), shared-memory staged scatter.  Pass 0 also runs the
+//                exclusive scan of the per-bin counts (CSR bin_start) in extra
+//                CTAs.  After the last pass the values are the CSR bin_prims,
+//                ascending primID within each bin.
 //   k_tile       Process, one CTA per owned bin (LoadBalance):
-//                tile z-buffer of packed 64-bit (depth, primID) keys in shared
-//                memory, triangle-parallel raster for small triangles and
+//                a shared-memory tile z-buffer of packed 64-bit (depth, primID)
+//                keys, setup records double-buffered into shared memory with
+//                cp.async, triangle-parallel raster for small triangles and
 //                pixel-parallel raster for large ones, then per-pixel Lambert
 //                shade (Listing 1) and a vectorised write-back.
-//   k_resolve    multi-GPU rank 0: shade gathered tile keys into the frame.
+//   k_resolve    multi-GPU rank 0: shade the gathered tile keys into the frame.
 //
 // Arithmetic follows DESIGN.md R1..R18 with a pinned float op order (IEEE
 // round-to-nearest intrinsics, explicit fma); this TU is compiled with
@@ -26,65 +30,85 @@
 
 namespace piko {
 
-constexpr unsigned long long CLEAR_KEY = 0xFFFFFFFFFFFFFFFFull;
+typedef unsigned long long u64;
+
+constexpr u64 CLEAR_KEY = 0xFFFFFFFFFFFFFFFFull;
 constexpr float W_EPS = 1e-6f;
 constexpr float GUARD = 4194304.0f;  // 2^22 subpixels
 
 // ---------------------------------------------------------------------------
-// memory-model helpers for the look-back scans
+// synchronisation helpers
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void st_release64(u64* p, u64 v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
-  unsigned long long v;
+__device__ __forceinline__ u64 ld_acquire64(const u64* p) {
+  u64 v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_relaxed32(unsigned* p, unsigned v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed64(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned ld_relaxed32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ u64 ld_relaxed64(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
-constexpr unsigned long long LB_AGG = 1ull << 62;   // aggregate published
-constexpr unsigned long long LB_INC = 2ull << 62;   // inclusive prefix published
-constexpr unsigned long long LB_VAL = (1ull << 62) - 1;
+// Look-back status word: tag (frame+1, 20 bits) | flag (2 bits) | value (42 bits)
+constexpr unsigned LB_AGG = 1u, LB_INC = 2u;
+__device__ __forceinline__ u64 lb_pack(unsigned tag, unsigned flag, u64 v) {
+  return ((u64)tag << 44) | ((u64)flag << 42) | v;
+}
+__device__ __forceinline__ unsigned lb_tag(u64 s) { return (unsigned)(s >> 44); }
+__device__ __forceinline__ unsigned lb_flag(u64 s) { return (unsigned)(s >> 42) & 3u; }
+__device__ __forceinline__ u64 lb_val(u64 s) { return s & ((1ull << 42) - 1); }
+__device__ __forceinline__ unsigned frame_tag(u64 frame) { return (unsigned)((frame + 1) & 0xFFFFFu); }
 
 // Decoupled look-back (one full warp): publish this chunk's aggregate, sum the
-// predecessors' values back to the nearest inclusive prefix (32 at a time),
-// publish the inclusive prefix.  Returns the exclusive prefix.
-__device__ unsigned long long lookback_warp(unsigned long long* status, unsigned chunk,
-                                            unsigned long long agg, int lane) {
-  if (lane == 0) st_release64(&status[chunk], (chunk == 0 ? LB_INC : LB_AGG) | agg);
+// predecessors back to the nearest inclusive prefix, 32 per probe; publish the
+// inclusive prefix.  Returns the exclusive prefix.
+__device__ u64 lookback_warp(u64* status, long long chunk, u64 agg, unsigned tag, int lane) {
+  if (lane == 0) st_release64(&status[chunk], lb_pack(tag, chunk == 0 ? LB_INC : LB_AGG, agg));
   if (chunk == 0) return 0;
-  unsigned long long excl = 0;
-  long long hi = (long long)chunk - 1;
+  u64 excl = 0;
+  long long hi = chunk - 1;
   for (;;) {
-    long long i = hi - lane;
-    unsigned long long s = (i >= 0) ? ld_acquire64(&status[i]) : LB_INC;
-    unsigned flag = (unsigned)(s >> 62);
-    unsigned inc = __ballot_sync(0xffffffffu, flag == 2u);
-    unsigned notready = __ballot_sync(0xffffffffu, flag == 0u);
-    int k = inc ? (__ffs(inc) - 1) : 32;
-    unsigned need = (k >= 31) ? 0xffffffffu : ((2u << k) - 1u);
+    const long long i = hi - lane;
+    const u64 s = (i >= 0) ? ld_acquire64(&status[i]) : lb_pack(tag, LB_INC, 0);
+    const bool ready = lb_tag(s) == tag;
+    const unsigned inc = __ballot_sync(0xffffffffu, ready && lb_flag(s) == LB_INC);
+    const unsigned notready = __ballot_sync(0xffffffffu, !ready);
+    const int k = inc ? (__ffs(inc) - 1) : 32;
+    const unsigned need = (k >= 31) ? 0xffffffffu : ((2u << k) - 1u);
     if (notready & need) continue;  // a predecessor has not published yet
-    unsigned long long v = (lane <= k) ? (s & LB_VAL) : 0ull;
+    u64 v = (lane <= k) ? lb_val(s) : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     excl += v;
     if (k < 32) break;
     hi -= 32;
   }
-  if (lane == 0) st_release64(&status[chunk], LB_INC | (excl + agg));
+  if (lane == 0) st_release64(&status[chunk], lb_pack(tag, LB_INC, excl + agg));
   return excl;
 }
 
 // ---------------------------------------------------------------------------
-// vertex transform and triangle setup (DESIGN.md R2-R4, R7, R11; SURVEY O1-O4)
+// vertex transform and triangle setup (DESIGN.md R2-R4, R7, R11)
 // ---------------------------------------------------------------------------
 struct Tri {
   int X0, Y0, X1, Y1, X2, Y2;
@@ -96,10 +120,8 @@ struct Tri {
   int small;
 };
 
-__device__ __forceinline__ bool xform_corner(const float* __restrict__ verts, int vid,
-                                             const Mat4& M, float hw, float hh, int& X,
-                                             int& Y, float& zw, float& rw) {
-  const float4 p = __ldg(reinterpret_cast<const float4*>(verts + 8ll * vid));
+__device__ __forceinline__ bool xform_corner(const float4 p, const Mat4& M, float hw, float hh,
+                                             int& X, int& Y, float& zw, float& rw) {
   const float cx = __fmaf_rn(M.m[0], p.x, __fmaf_rn(M.m[1], p.y, __fmaf_rn(M.m[2], p.z, M.m[3])));
   const float cy = __fmaf_rn(M.m[4], p.x, __fmaf_rn(M.m[5], p.y, __fmaf_rn(M.m[6], p.z, M.m[7])));
   const float cz = __fmaf_rn(M.m[8], p.x, __fmaf_rn(M.m[9], p.y, __fmaf_rn(M.m[10], p.z, M.m[11])));
@@ -120,14 +142,18 @@ __device__ __forceinline__ bool xform_corner(const float* __restrict__ verts, in
   return true;
 }
 
-// Full setup of triangle with corner vertex ids (i0,i1,i2); false = culled.
-__device__ __forceinline__ bool setup_tri(const float* __restrict__ verts, int i0, int i1, int i2,
+__device__ __forceinline__ float4 load_pos(const float* __restrict__ verts, int vid) {
+  return __ldg(reinterpret_cast<const float4*>(verts + 8ll * vid));
+}
+
+// Full setup from the three corner positions; false = culled.
+__device__ __forceinline__ bool setup_tri(float4 p0, float4 p1, float4 p2, int i0, int i1, int i2,
                                           const Mat4& M, int W, int H, Tri& o) {
   const float hw = __fmul_rn(0.5f, __int2float_rn(W));
   const float hh = __fmul_rn(0.5f, __int2float_rn(H));
-  bool ok = xform_corner(verts, i0, M, hw, hh, o.X0, o.Y0, o.zw0, o.rw0);
-  ok = ok && xform_corner(verts, i1, M, hw, hh, o.X1, o.Y1, o.zw1, o.rw1);
-  ok = ok && xform_corner(verts, i2, M, hw, hh, o.X2, o.Y2, o.zw2, o.rw2);
+  bool ok = xform_corner(p0, M, hw, hh, o.X0, o.Y0, o.zw0, o.rw0);
+  ok &= xform_corner(p1, M, hw, hh, o.X1, o.Y1, o.zw1, o.rw1);
+  ok &= xform_corner(p2, M, hw, hh, o.X2, o.Y2, o.zw2, o.rw2);
   if (!ok) return false;
   o.v0 = i0; o.v1 = i1; o.v2 = i2;
   long long area2 = (long long)(o.X1 - o.X0) * (long long)(o.Y2 - o.Y0) -
@@ -160,223 +186,261 @@ __device__ __forceinline__ bool setup_tri(const float* __restrict__ verts, int i
 __device__ __forceinline__ unsigned owned_in_rect(int tx0, int ty0, int tx1, int ty1, const Grid& g) {
   if (g.nranks == 1) return (unsigned)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
   unsigned n = 0;
+  const int w = tx1 - tx0 + 1;
   for (int ty = ty0; ty <= ty1; ++ty) {
-    const int base = ty * g.binsX + tx0;  // bin of tx0 in this row
-    int first = (g.rank - base % g.nranks + g.nranks) % g.nranks;  // offset of 1st owned
-    const int w = tx1 - tx0 + 1;
+    const int base = ty * g.binsX + tx0;
+    const int first = (g.rank - base % g.nranks + g.nranks) % g.nranks;
     if (first < w) n += (unsigned)((w - 1 - first) / g.nranks + 1);
   }
   return n;
 }
 
+// r-th owned bin of the rect, row-major (inverse of owned_in_rect's order)
+__device__ __forceinline__ int owned_bin_at(int tx0, int ty0, int tx1, int ty1, unsigned r, const Grid& g) {
+  const int w = tx1 - tx0 + 1;
+  if (g.nranks == 1) return (ty0 + (int)(r / w)) * g.binsX + tx0 + (int)(r % w);
+  for (int ty = ty0; ty <= ty1; ++ty) {
+    const int base = ty * g.binsX + tx0;
+    const int first = (g.rank - base % g.nranks + g.nranks) % g.nranks;
+    const unsigned n = first < w ? (unsigned)((w - 1 - first) / g.nranks + 1) : 0u;
+    if (r < n) return base + first + (int)r * g.nranks;
+    r -= n;
+  }
+  return -1;  // unreachable for r < owned_in_rect
+}
+
 // ---------------------------------------------------------------------------
-// K1: vertex + setup + count + chunk scan + pair expansion (persistent CTAs)
+// K1: vertex + setup + count + chunk scan + pair expansion
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
-  __shared__ unsigned s_chunk;
-  __shared__ unsigned long long s_warp[K1_THREADS / 32];
-  __shared__ unsigned long long s_base;
+  __shared__ unsigned s_off[K1_CHUNK];   // exclusive local pair offset per triangle
+  __shared__ unsigned s_r0[K1_CHUNK];    // tile rect tx0 | ty0 << 16
+  __shared__ unsigned s_r1[K1_CHUNK];    // tile rect tx1 | ty1 << 16
+  __shared__ unsigned s_hist[MAX_PASSES][RX_RADIX];
+  __shared__ unsigned s_wsum[K1_THREADS / 32];
+  __shared__ u64 s_tk, s_base;
   __shared__ unsigned s_live;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Grid g = a.g;
 
-  for (;;) {
-    if (tid == 0) { s_chunk = atomicAdd(&a.ctl->ticket_k1, 1u); s_live = 0; }
-    __syncthreads();
-    const unsigned chunk = s_chunk;
-    const long long t0 = (long long)chunk * K1_CHUNK;
-    if (t0 >= a.n_tris) break;  // uniform across the CTA
+  pdl_wait();   // the previous frame's tile kernel still reads rec / pairs
+  pdl_trigger();
+  if (tid == 0) { s_tk = atomicAdd(&a.ctl->k1_ticket, 1ull); s_live = 0; }
+  for (int i = tid; i < MAX_PASSES * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const u64 frame = s_tk / gridDim.x;
+  const long long chunk = (long long)(s_tk % gridDim.x);
+  const unsigned tag = frame_tag(frame);
+  const long long t0 = chunk * K1_CHUNK;
+  if (chunk == 0 && tid == 0) a.ctl->frame = frame;
 
-    // ---- setup of this thread's 4 consecutive triangles -------------------
-    const long long tb = t0 + (long long)tid * K1_TPT;
-    int vi[12];
-    if (tb + K1_TPT <= a.n_tris) {
-      const int4* p = reinterpret_cast<const int4*>(a.idx + 3 * tb);
-      const int4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
-      vi[0] = q0.x; vi[1] = q0.y; vi[2] = q0.z; vi[3] = q0.w;
-      vi[4] = q1.x; vi[5] = q1.y; vi[6] = q1.z; vi[7] = q1.w;
-      vi[8] = q2.x; vi[9] = q2.y; vi[10] = q2.z; vi[11] = q2.w;
-    } else {
+  // ---- loads first (all independent): indices, then corner positions ------
+  int vi[K1_TPT][3];
 #pragma unroll
-      for (int k = 0; k < 12; ++k)
-        vi[k] = (tb + k / 3 < a.n_tris) ? __ldg(a.idx + 3 * tb + k) : 0;
-    }
-    unsigned cnt[K1_TPT];
-    int rect[K1_TPT];  // packed tile rect: tx0 | ty0<<8 ... stored as 4 x 8 bit? use 2 ints
-    int rect2[K1_TPT];
-    unsigned live = 0;
+  for (int k = 0; k < K1_TPT; ++k) {
+    const long long t = t0 + tid + k * K1_THREADS;
+    const bool in = t < a.n_tris;
 #pragma unroll
-    for (int k = 0; k < K1_TPT; ++k) {
-      cnt[k] = 0; rect[k] = 0; rect2[k] = 0;
-      const long long t = tb + k;
-      if (t >= a.n_tris) continue;
-      Tri o;
-      if (!setup_tri(a.verts, vi[3 * k], vi[3 * k + 1], vi[3 * k + 2], a.M, g.W, g.H, o)) continue;
-      const int tx0 = o.px0 >> g.bw_log2, tx1 = o.px1 >> g.bw_log2;
-      const int ty0 = o.py0 >> g.bh_log2, ty1 = o.py1 >> g.bh_log2;
-      const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
-      if (c == 0) continue;
-      cnt[k] = c;
-      rect[k] = tx0 | (ty0 << 16);
-      rect2[k] = tx1 | (ty1 << 16);
-      ++live;
-      // depth plane (O6) through the snapped corners
-      const float dx1 = __int2float_rn(o.X1 - o.X0), dy1 = __int2float_rn(o.Y1 - o.Y0);
-      const float dx2 = __int2float_rn(o.X2 - o.X0), dy2 = __int2float_rn(o.Y2 - o.Y0);
-      const float dz1 = __fsub_rn(o.zw1, o.zw0), dz2 = __fsub_rn(o.zw2, o.zw0);
-      const float inv = __fdiv_rn(1.0f, __ll2float_rn(o.area2));
-      const float za = __fmul_rn(__fmaf_rn(dz1, dy2, -__fmul_rn(dz2, dy1)), inv);
-      const float zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
-      int4* r = a.rec + 3 * t;
-      r[0] = make_int4(o.X0, o.Y0, o.X1, o.Y1);
-      r[1] = make_int4(o.X2, o.Y2, __float_as_int(o.zw0), __float_as_int(za));
-      r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
-                       o.small ? REC_SMALL : 0);
-    }
+    for (int c = 0; c < 3; ++c) vi[k][c] = in ? __ldg(a.idx + 3 * t + c) : -1;
+  }
+  float4 pos[K1_TPT][3];
+#pragma unroll
+  for (int k = 0; k < K1_TPT; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      pos[k][c] = vi[k][c] >= 0 ? load_pos(a.verts, vi[k][c]) : make_float4(0.f, 0.f, 0.f, 0.f);
 
-    // ---- CTA exclusive scan of the pair counts ----------------------------
-    const unsigned long long mine = (unsigned long long)cnt[0] + cnt[1] + cnt[2] + cnt[3];
-    unsigned long long inc = mine;
+  // ---- setup, record write (coalesced: consecutive threads, consecutive t) -
+  unsigned cnt[K1_TPT];
+  unsigned live = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += v;
-    }
-    if (lane == 31) s_warp[warp] = inc;
-    if (live) atomicAdd(&s_live, live);
-    __syncthreads();
-    unsigned long long wbase = 0, total = 0;
+  for (int k = 0; k < K1_TPT; ++k) {
+    const int l = tid + k * K1_THREADS;
+    const long long t = t0 + l;
+    cnt[k] = 0;
+    s_r0[l] = 0; s_r1[l] = 0;
+    Tri o;
+    if (vi[k][0] < 0 ||
+        !setup_tri(pos[k][0], pos[k][1], pos[k][2], vi[k][0], vi[k][1], vi[k][2], a.M, g.W, g.H, o))
+      continue;
+    const int tx0 = o.px0 >> g.bw_log2, tx1 = o.px1 >> g.bw_log2;
+    const int ty0 = o.py0 >> g.bh_log2, ty1 = o.py1 >> g.bh_log2;
+    const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
+    if (c == 0) continue;
+    cnt[k] = c;
+    s_r0[l] = (unsigned)tx0 | ((unsigned)ty0 << 16);
+    s_r1[l] = (unsigned)tx1 | ((unsigned)ty1 << 16);
+    ++live;
+    // depth plane (O6) through the snapped corners
+    const float dx1 = __int2float_rn(o.X1 - o.X0), dy1 = __int2float_rn(o.Y1 - o.Y0);
+    const float dx2 = __int2float_rn(o.X2 - o.X0), dy2 = __int2float_rn(o.Y2 - o.Y0);
+    const float dz1 = __fsub_rn(o.zw1, o.zw0), dz2 = __fsub_rn(o.zw2, o.zw0);
+    const float inv = __fdiv_rn(1.0f, __ll2float_rn(o.area2));
+    const float za = __fmul_rn(__fmaf_rn(dz1, dy2, -__fmul_rn(dz2, dy1)), inv);
+    const float zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
+    int4* r = a.rec + 3 * t;
+    r[0] = make_int4(o.X0, o.Y0, o.X1, o.Y1);
+    r[1] = make_int4(o.X2, o.Y2, __float_as_int(o.zw0), __float_as_int(za));
+    r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
+                     o.small ? REC_SMALL : 0);
+  }
+  if (live) atomicAdd(&s_live, live);
 #pragma unroll
-    for (int w = 0; w < K1_THREADS / 32; ++w) {
-      const unsigned long long v = s_warp[w];
-      wbase += (w < warp) ? v : 0ull;
-      total += v;
+  for (int k = 0; k < K1_TPT; ++k) s_off[tid + k * K1_THREADS] = cnt[k];
+  __syncthreads();
+
+  // ---- CTA exclusive scan in triangle order (thread owns 4 consecutive) ----
+  unsigned c4[4], sum = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) { c4[j] = s_off[4 * tid + j]; sum += c4[j]; }
+  unsigned inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) s_wsum[warp] = inc;
+  __syncthreads();
+  unsigned wbase = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < K1_THREADS / 32; ++w) {
+    const unsigned v = s_wsum[w];
+    wbase += (w < warp) ? v : 0u;
+    total += v;
+  }
+  {
+    unsigned run = wbase + inc - sum;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { s_off[4 * tid + j] = run; run += c4[j]; }
+  }
+  if (warp == 0) {
+    const u64 ex = lookback_warp(a.status, chunk, total, tag, lane);
+    if (lane == 0) {
+      s_base = ex;
+      if (s_live) atomicAdd(&a.ctl->n_live[frame & 1], (u64)s_live);
+      if (chunk == (long long)gridDim.x - 1) a.ctl->n_pairs = ex + total;
     }
-    if (warp == 0) {
-      const unsigned long long ex = lookback_warp(a.status, chunk, total, lane);
-      if (lane == 0) {
-        s_base = ex;
-        if (s_live) atomicAdd(&a.ctl->n_live, (unsigned long long)s_live);
-        if (t0 + K1_CHUNK >= a.n_tris) a.ctl->n_pairs = ex + total;  // last chunk
+  }
+  __syncthreads();
+
+  // ---- cooperative expansion: pair j of the chunk -> (bin, t), coalesced ----
+  const u64 base = s_base;
+  if (base + total > a.cap) {
+    if (tid == 0 && total) atomicMax(&a.ctl->overflow_tag, frame + 1);
+    return;
+  }
+  const unsigned nround = (total + K1_THREADS - 1) / K1_THREADS;
+  for (unsigned it = 0; it < nround; ++it) {
+    const unsigned j = it * K1_THREADS + tid;
+    const bool valid = j < total;
+    int b = -1, t = 0;
+    if (valid) {
+      // largest l with s_off[l] <= j (that triangle owns pair j)
+      int lo = 0, hi = K1_CHUNK - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_off[mid] <= j) lo = mid; else hi = mid - 1;
       }
+      const unsigned r0 = s_r0[lo], r1 = s_r1[lo];
+      b = owned_bin_at((int)(r0 & 0xffff), (int)(r0 >> 16), (int)(r1 & 0xffff), (int)(r1 >> 16),
+                       j - s_off[lo], g);
+      t = (int)(t0 + lo);
+      a.pair_keys[base + j] = (uint32_t)b;
+      a.pair_vals[base + j] = t;
     }
-    __syncthreads();
-
-    // ---- expansion: pairs (bin, t) in primitive order ----------------------
-    unsigned long long off = s_base + wbase + (inc - mine);
-    if (off + mine > a.cap) {
-      if (mine) atomicOr(&a.ctl->overflow, 1u);
-    } else {
-#pragma unroll
-      for (int k = 0; k < K1_TPT; ++k) {
-        if (!cnt[k]) continue;
-        const int t = (int)(tb + k);
-        const int tx0 = rect[k] & 0xffff, ty0 = rect[k] >> 16;
-        const int tx1 = rect2[k] & 0xffff, ty1 = rect2[k] >> 16;
-        for (int ty = ty0; ty <= ty1; ++ty) {
-          for (int tx = tx0; tx <= tx1; ++tx) {
-            const int b = ty * g.binsX + tx;
-            if (g.nranks > 1 && (b % g.nranks) != g.rank) continue;
-            a.pair_keys[off] = (uint32_t)b;
-            a.pair_vals[off] = t;
-            atomicAdd(&a.bin_count[b], 1u);
-            ++off;
-          }
-        }
-      }
+    // warp-aggregated per-bin counts and digit histograms
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    if (valid && lane == __ffs(peers) - 1) {
+      const unsigned n = __popc(peers);
+      if (a.npass > 0) atomicAdd(&a.bin_count[b], n);
+      for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], n);
     }
-    __syncthreads();  // s_chunk / s_base reuse
+  }
+  __syncthreads();
+  for (int i = tid; i < a.npass * RX_RADIX; i += K1_THREADS) {
+    const unsigned v = (&s_hist[0][0])[i];
+    if (v) atomicAdd(&a.ctl->digit_hist[frame & 1][0][0] + i, v);
   }
 }
 
 // ---------------------------------------------------------------------------
-// K2: bin counts -> CSR bin_start (decoupled look-back), digit histograms
+// Bin scan (run by extra CTAs of radix pass 0): bin_count -> bin_start
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(SCAN_THREADS) k_bin_scan(ScanArgs a) {
-  __shared__ unsigned s_chunk;
-  __shared__ unsigned long long s_warp[SCAN_THREADS / 32];
-  __shared__ unsigned long long s_base;
-  __shared__ unsigned s_hist[MAX_PASSES][RX_RADIX];
+__device__ void bin_scan_tile(const RadixArgs& a, long long tile, unsigned tag) {
+  __shared__ unsigned s_wsum[SCAN_THREADS / 32];
+  __shared__ u64 s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < MAX_PASSES * RX_RADIX; i += SCAN_THREADS) (&s_hist[0][0])[i] = 0;
-  const bool ovf = a.ctl->overflow != 0;
-  for (;;) {
-    if (tid == 0) s_chunk = atomicAdd(&a.ctl->ticket_scan, 1u);
-    __syncthreads();
-    const unsigned chunk = s_chunk;
-    const long long b0 = (long long)chunk * SCAN_CHUNK;
-    if (b0 >= a.NB) break;
-    const long long bt = b0 + (long long)tid * SCAN_ITEMS;
-    unsigned c[SCAN_ITEMS];
-    unsigned long long mine = 0;
+  const long long b0 = tile * SCAN_CHUNK + (long long)tid * SCAN_ITEMS;
+  unsigned c[SCAN_ITEMS], sum = 0;
 #pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; ++k) {
-      const long long b = bt + k;
-      c[k] = (b < a.NB && !ovf) ? a.bin_count[b] : 0u;
-      mine += c[k];
-      if (c[k]) {
-        for (int p = 0; p < a.npass; ++p)
-          atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], c[k]);
-      }
-    }
-    unsigned long long inc = mine;
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    c[k] = (b0 + k < a.NB) ? a.bin_count[b0 + k] : 0u;
+    sum += c[k];
+  }
+  unsigned inc = sum;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += v;
-    }
-    if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
-    unsigned long long wbase = 0, total = 0;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) s_wsum[warp] = inc;
+  __syncthreads();
+  unsigned wbase = 0, total = 0;
 #pragma unroll
-    for (int w = 0; w < SCAN_THREADS / 32; ++w) {
-      const unsigned long long v = s_warp[w];
-      wbase += (w < warp) ? v : 0ull;
-      total += v;
-    }
-    if (warp == 0) {
-      const unsigned long long ex = lookback_warp(a.status, chunk, total, lane);
-      if (lane == 0) s_base = ex;
-    }
-    __syncthreads();
-    unsigned long long run = s_base + wbase + (inc - mine);
-#pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; ++k) {
-      const long long b = bt + k;
-      if (b < a.NB) {
-        a.bin_start[b] = (int32_t)run;
-        a.bin_count[b] = 0u;  // ready for the next frame
-      }
-      run += c[k];
-    }
-    if (b0 + SCAN_CHUNK >= a.NB && tid == SCAN_THREADS - 1) a.bin_start[a.NB] = (int32_t)run;
-    __syncthreads();
+  for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+    const unsigned v = s_wsum[w];
+    wbase += (w < warp) ? v : 0u;
+    total += v;
+  }
+  if (warp == 0) {
+    const u64 ex = lookback_warp(a.scan_status, tile, total, tag, lane);
+    if (lane == 0) s_base = ex;
   }
   __syncthreads();
-  for (int i = tid; i < a.npass * RX_RADIX; i += SCAN_THREADS) {
-    const unsigned v = (&s_hist[0][0])[i];
-    if (v) atomicAdd(&a.ctl->digit_hist[0][0] + i, v);
+  u64 run = s_base + wbase + inc - sum;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    if (b0 + k < a.NB) {
+      a.bin_start[b0 + k] = (int32_t)run;
+      a.bin_count[b0 + k] = 0u;  // ready for the next frame
+    }
+    run += c[k];
   }
+  if (b0 < a.NB && b0 + SCAN_ITEMS >= a.NB) a.bin_start[a.NB] = (int32_t)run;
 }
 
 // ---------------------------------------------------------------------------
 // K3: one stable LSD radix pass over the (bin, primID) pairs
 // ---------------------------------------------------------------------------
-constexpr unsigned RX_AGG = 1u << 30, RX_INC = 2u << 30, RX_VAL = (1u << 30) - 1;
-
 __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
   __shared__ unsigned s_whist[RX_WARPS][RX_RADIX];
   __shared__ unsigned s_keys[RX_CHUNK];
   __shared__ int s_vals[RX_CHUNK];
-  __shared__ unsigned s_prefix[RX_RADIX];
   __shared__ unsigned s_lstart[RX_RADIX];
   __shared__ unsigned s_gstart[RX_RADIX];
   __shared__ unsigned s_wsum[RX_WARPS];
-  __shared__ unsigned s_chunk;
+  __shared__ u64 s_tk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lanemask_lt = (1u << lane) - 1u;
-  if (a.ctl->overflow) return;
-  const unsigned long long P = a.ctl->n_pairs;
+
+  pdl_wait();
+  pdl_trigger();
+  if (tid == 0) s_tk = atomicAdd(&a.ctl->rx_ticket[a.pass], 1ull);
+#pragma unroll
+  for (int w = 0; w < RX_WARPS; ++w) s_whist[w][tid] = 0;
+  __syncthreads();
+  const u64 frame = s_tk / gridDim.x;
+  const long long chunk = (long long)(s_tk % gridDim.x);
+  const unsigned tag = frame_tag(frame);
+  // on overflow sort nothing, but pass 0 still runs the bin scan (it zeroes
+  // the per-bin counts for the next frame)
+  const u64 P = (a.ctl->overflow_tag == frame + 1) ? 0ull : a.ctl->n_pairs;
+  const long long nchunks = (long long)((P + RX_CHUNK - 1) / RX_CHUNK);
+  if (chunk >= nchunks) {
+    const long long tile = chunk - nchunks;
+    if (a.pass == 0 && tile < (a.NB + SCAN_CHUNK - 1) / SCAN_CHUNK) bin_scan_tile(a, tile, tag);
+    return;
+  }
 
   // block exclusive scan of 256 values (one per thread)
   auto block_excl = [&](unsigned v) -> unsigned {
@@ -393,92 +457,93 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     __syncthreads();
     return base + inc - v;
   };
-  s_prefix[tid] = block_excl(a.ctl->digit_hist[a.pass][tid]);
 
-  for (;;) {
-    if (tid == 0) s_chunk = atomicAdd(&a.ctl->ticket_rx[a.pass], 1u);
+  const u64 c0 = (u64)chunk * RX_CHUNK;
+  unsigned key[RX_ITEMS];
+  int val[RX_ITEMS];
+  unsigned rank[RX_ITEMS];
+  const u64 wb = c0 + (u64)warp * (RX_ITEMS * 32) + lane;
 #pragma unroll
-    for (int w = 0; w < RX_WARPS; ++w) s_whist[w][tid] = 0;
-    __syncthreads();
-    const unsigned chunk = s_chunk;
-    const unsigned long long c0 = (unsigned long long)chunk * RX_CHUNK;
-    if (c0 >= P) break;
-
-    unsigned key[RX_ITEMS];
-    int val[RX_ITEMS];
-    unsigned rank[RX_ITEMS];
-    const unsigned long long wb = c0 + (unsigned long long)warp * (RX_ITEMS * 32) + lane;
+  for (int j = 0; j < RX_ITEMS; ++j) {
+    const u64 pos = wb + j * 32;
+    const bool valid = pos < P;
+    key[j] = valid ? a.keys_in[pos] : 0u;
+    val[j] = valid ? a.vals_in[pos] : 0;
+  }
+  const unsigned gprefix = block_excl(a.ctl->digit_hist[frame & 1][a.pass][tid]);
 #pragma unroll
-    for (int j = 0; j < RX_ITEMS; ++j) {
-      const unsigned long long pos = wb + j * 32;
-      const bool valid = pos < P;
-      key[j] = valid ? a.keys_in[pos] : 0u;
-      val[j] = valid ? a.vals_in[pos] : 0;
-    }
+  for (int j = 0; j < RX_ITEMS; ++j) {
+    const u64 pos = wb + j * 32;
+    const bool valid = pos < P;
+    const unsigned d = valid ? ((key[j] >> a.shift) & (RX_RADIX - 1)) : RX_RADIX;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    unsigned prev = 0;
+    if (valid) prev = s_whist[warp][d];
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) s_whist[warp][d] = prev + __popc(peers);
+    __syncwarp();
+    rank[j] = prev + __popc(peers & lanemask_lt);
+  }
+  __syncthreads();
+  // per digit d = tid: exclusive offsets over warps, chunk total
+  unsigned tot = 0;
 #pragma unroll
-    for (int j = 0; j < RX_ITEMS; ++j) {
-      const unsigned long long pos = wb + j * 32;
-      const bool valid = pos < P;
-      const unsigned d = valid ? ((key[j] >> a.shift) & (RX_RADIX - 1)) : RX_RADIX;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      unsigned prev = 0;
-      if (valid) prev = s_whist[warp][d];
-      __syncwarp();
-      if (valid && lane == __ffs(peers) - 1) s_whist[warp][d] = prev + __popc(peers);
-      __syncwarp();
-      rank[j] = prev + __popc(peers & lanemask_lt);
-    }
-    __syncthreads();
-    // per digit d = tid: exclusive offsets over warps, chunk total
-    unsigned tot = 0;
+  for (int w = 0; w < RX_WARPS; ++w) {
+    const unsigned c = s_whist[w][tid];
+    s_whist[w][tid] = tot;
+    tot += c;
+  }
+  // decoupled look-back per digit (thread tid owns digit tid), 8 chunks per probe
+  u64* st = a.status + (size_t)chunk * RX_RADIX + tid;
+  u64 excl = 0;
+  if (chunk == 0) {
+    st_relaxed64(st, lb_pack(tag, LB_INC, tot));
+  } else {
+    st_relaxed64(st, lb_pack(tag, LB_AGG, tot));
+    long long c = chunk - 1;
+    bool done = false;
+    while (!done) {
+      u64 s[8];
 #pragma unroll
-    for (int w = 0; w < RX_WARPS; ++w) {
-      const unsigned c = s_whist[w][tid];
-      s_whist[w][tid] = tot;
-      tot += c;
-    }
-    const unsigned lstart = block_excl(tot);
-    s_lstart[tid] = lstart;
-    // decoupled look-back per digit (thread tid owns digit tid)
-    unsigned* st = a.status + (size_t)chunk * RX_RADIX + tid;
-    unsigned excl = 0;
-    if (chunk == 0) {
-      st_relaxed32(st, RX_INC | tot);
-    } else {
-      st_relaxed32(st, RX_AGG | tot);
-      const unsigned* q = st - RX_RADIX;
-      for (;;) {
-        unsigned s;
-        do { s = ld_relaxed32(q); } while ((s >> 30) == 0u);
-        excl += s & RX_VAL;
-        if ((s >> 30) == 2u) break;
-        q -= RX_RADIX;
+      for (int j = 0; j < 8; ++j)
+        s[j] = (c - j >= 0) ? ld_relaxed64(a.status + (size_t)(c - j) * RX_RADIX + tid)
+                            : lb_pack(tag, LB_INC, 0);
+      int j = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (done || j != q) continue;  // stop at the first unready entry
+        if (lb_tag(s[q]) != tag) continue;
+        excl += lb_val(s[q]);
+        if (lb_flag(s[q]) == LB_INC) done = true;
+        ++j;
       }
-      st_relaxed32(st, RX_INC | (excl + tot));
+      c -= j;
     }
-    s_gstart[tid] = s_prefix[tid] + excl;
-    __syncthreads();
-    // stage the chunk sorted by digit in shared memory
+    st_relaxed64(st, lb_pack(tag, LB_INC, excl + tot));
+  }
+  const unsigned lstart = block_excl(tot);
+  s_lstart[tid] = lstart;
+  s_gstart[tid] = gprefix + (unsigned)excl;
+  __syncthreads();
+  // stage the chunk sorted by digit in shared memory
 #pragma unroll
-    for (int j = 0; j < RX_ITEMS; ++j) {
-      const unsigned long long pos = wb + j * 32;
-      if (pos < P) {
-        const unsigned d = (key[j] >> a.shift) & (RX_RADIX - 1);
-        const unsigned lp = s_lstart[d] + s_whist[warp][d] + rank[j];
-        s_keys[lp] = key[j];
-        s_vals[lp] = val[j];
-      }
+  for (int j = 0; j < RX_ITEMS; ++j) {
+    const u64 pos = wb + j * 32;
+    if (pos < P) {
+      const unsigned d = (key[j] >> a.shift) & (RX_RADIX - 1);
+      const unsigned lp = s_lstart[d] + s_whist[warp][d] + rank[j];
+      s_keys[lp] = key[j];
+      s_vals[lp] = val[j];
     }
-    __syncthreads();
-    const unsigned n = (unsigned)min((unsigned long long)RX_CHUNK, P - c0);
-    for (unsigned i = tid; i < n; i += RX_THREADS) {
-      const unsigned k = s_keys[i];
-      const unsigned d = (k >> a.shift) & (RX_RADIX - 1);
-      const unsigned g = s_gstart[d] + (i - s_lstart[d]);
-      if (a.keys_out) a.keys_out[g] = k;
-      a.vals_out[g] = s_vals[i];
-    }
-    __syncthreads();
+  }
+  __syncthreads();
+  const unsigned n = (unsigned)min((u64)RX_CHUNK, P - c0);
+  for (unsigned i = tid; i < n; i += RX_THREADS) {
+    const unsigned k = s_keys[i];
+    const unsigned d = (k >> a.shift) & (RX_RADIX - 1);
+    const unsigned gpos = s_gstart[d] + (i - s_lstart[d]);
+    if (a.keys_out) a.keys_out[gpos] = k;
+    a.vals_out[gpos] = s_vals[i];
   }
 }
 
@@ -508,9 +573,8 @@ __device__ __forceinline__ int tl_thr(int Xa, int Ya, int Xb, int Yb) {
 }
 
 // Coverage + depth at sample (Px, Py) (must lie inside the triangle's sample
-// bbox when r.small).  Returns the packed key or CLEAR_KEY; *covered for stats.
-__device__ __forceinline__ unsigned long long eval_key(const RecView& r, int Px, int Py, int t,
-                                                       bool& covered) {
+// bbox when r.small).  Returns the packed key or CLEAR_KEY.
+__device__ __forceinline__ u64 eval_key(const RecView& r, int Px, int Py, int t, bool& covered) {
   bool in;
   if (r.small) {
     const int e01 = (r.X1 - r.X0) * (Py - r.Y0) - (r.Y1 - r.Y0) * (Px - r.X0);
@@ -530,7 +594,7 @@ __device__ __forceinline__ unsigned long long eval_key(const RecView& r, int Px,
   const float z = __fmaf_rn(r.za, __int2float_rn(Px - r.X0),
                             __fmaf_rn(r.zb, __int2float_rn(Py - r.Y0), r.zw0));
   if (!(z >= 0.0f && z <= 1.0f)) return CLEAR_KEY;
-  return ((unsigned long long)(__float_as_uint(z) & 0x7FFFFFFFu) << 32) | (unsigned)t;
+  return ((u64)(__float_as_uint(z) & 0x7FFFFFFFu) << 32) | (unsigned)t;
 }
 
 // O7 shade of pixel sample (Px, Py) by triangle t (recomputes setup).
@@ -539,7 +603,14 @@ __device__ __forceinline__ float4 shade(const float* __restrict__ verts, const i
                                         int Px, int Py) {
   Tri o;
   const int i0 = __ldg(idx + 3ll * t), i1 = __ldg(idx + 3ll * t + 1), i2 = __ldg(idx + 3ll * t + 2);
-  setup_tri(verts, i0, i1, i2, M, W, H, o);  // live: t won a pixel
+  const float4 p0 = load_pos(verts, i0), p1 = load_pos(verts, i1), p2 = load_pos(verts, i2);
+  const float4 m0 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i0 + 4));
+  const float4 m1 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i1 + 4));
+  const float4 m2 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i2 + 4));
+  setup_tri(p0, p1, p2, i0, i1, i2, M, W, H, o);  // live: t won a pixel
+  const float4 n0 = m0;
+  const float4 n1 = (o.v1 == i1) ? m1 : m2;        // corners 1,2 swapped by O2?
+  const float4 n2 = (o.v1 == i1) ? m2 : m1;
   const long long w0 = (long long)(o.X2 - o.X1) * (Py - o.Y1) - (long long)(o.Y2 - o.Y1) * (Px - o.X1);
   const long long w1 = (long long)(o.X0 - o.X2) * (Py - o.Y2) - (long long)(o.Y0 - o.Y2) * (Px - o.X2);
   const long long w2 = (long long)(o.X1 - o.X0) * (Py - o.Y0) - (long long)(o.Y1 - o.Y0) * (Px - o.X0);
@@ -547,9 +618,6 @@ __device__ __forceinline__ float4 shade(const float* __restrict__ verts, const i
   const float l0 = __fmul_rn(__fmul_rn(__ll2float_rn(w0), inv), o.rw0);
   const float l1 = __fmul_rn(__fmul_rn(__ll2float_rn(w1), inv), o.rw1);
   const float l2 = __fmul_rn(__fmul_rn(__ll2float_rn(w2), inv), o.rw2);
-  const float4 n0 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * o.v0 + 4));
-  const float4 n1 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * o.v1 + 4));
-  const float4 n2 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * o.v2 + 4));
   const float vx = __fmaf_rn(l2, n2.x, __fmaf_rn(l1, n1.x, __fmul_rn(l0, n0.x)));
   const float vy = __fmaf_rn(l2, n2.y, __fmaf_rn(l1, n1.y, __fmul_rn(l0, n0.y)));
   const float vz = __fmaf_rn(l2, n2.z, __fmaf_rn(l1, n1.z, __fmul_rn(l0, n0.z)));
@@ -572,45 +640,83 @@ __device__ __forceinline__ void normalise_light(const float in[3], float L[3]) {
 
 constexpr int SMALL_AREA = 16;  // clipped pixel-rect area handled by one thread
 
+template <int BW, int BH, int THREADS>
+struct TileSmem {
+  static constexpr int NPX = BW * BH;
+  u64 key[NPX];
+  int4 rec[2][THREADS][3];
+  unsigned short big[THREADS];
+  int bigt[THREADS];
+};
+
 template <int BW, int BH, int THREADS, bool COV, bool KEYS_ONLY>
 __global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
   constexpr int NPX = BW * BH;
   constexpr int PPT = (NPX + THREADS - 1) / THREADS;
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(smem);   // [NPX]
-  int4* s_q = reinterpret_cast<int4*>(s_key + NPX);                          // [THREADS][3]
-  int* s_qt = reinterpret_cast<int*>(s_q + 3 * THREADS);                     // [THREADS]
-  unsigned* s_cov = reinterpret_cast<unsigned*>(s_qt + THREADS);             // [NPX] (COV)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem<BW, BH, THREADS>& sm = *reinterpret_cast<TileSmem<BW, BH, THREADS>*>(smem_raw);
+  unsigned* s_cov = reinterpret_cast<unsigned*>(smem_raw + sizeof(TileSmem<BW, BH, THREADS>));
   __shared__ int s_qn;
 
   const int tid = threadIdx.x;
   const Grid g = a.g;
-  const int b = g.rank + blockIdx.x * g.nranks;  // owned bin (DirectMap across ranks)
-  const int bx = b % g.binsX, by = b / g.binsX;
-  const int x0 = bx * BW, y0 = by * BH;
-  const int x1 = min(x0 + BW, g.W) - 1, y1 = min(y0 + BH, g.H) - 1;
-  const bool ovf = a.ctl->overflow != 0;
-
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int p = tid + k * THREADS;
     if (p < NPX) {
-      s_key[p] = CLEAR_KEY;
+      sm.key[p] = CLEAR_KEY;
       if (COV) s_cov[p] = 0;
     }
   }
   if (tid == 0) s_qn = 0;
-  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  const u64 frame = a.ctl->frame;
+  if (blockIdx.x == 0) {  // reset the next frame's double-buffered accumulators
+    unsigned* h = &a.ctl->digit_hist[(frame + 1) & 1][0][0];
+    for (int i = tid; i < MAX_PASSES * RX_RADIX; i += THREADS) h[i] = 0;
+    if (tid == 0) a.ctl->n_live[(frame + 1) & 1] = 0;
+    if (a.npass == 0 && tid == 0 && g.NB == 1) {  // single bin: CSR is [0, P]
+      a.bin_start[0] = 0;
+      a.bin_start[1] = (int32_t)a.ctl->n_pairs;
+    }
+  }
+  if ((int)blockIdx.x >= a.owned) return;
+  const int b = g.rank + blockIdx.x * g.nranks;  // owned bin (DirectMap across ranks)
+  const int bx = b % g.binsX, by = b / g.binsX;
+  const int x0 = bx * BW, y0 = by * BH;
+  const int x1 = min(x0 + BW, g.W) - 1, y1 = min(y0 + BH, g.H) - 1;
+  const bool ovf = a.ctl->overflow_tag == frame + 1;
 
-  const int s = ovf ? 0 : a.bin_start[b];
-  const int e = ovf ? 0 : a.bin_start[b + 1];
-  for (int base = s; base < e; base += THREADS) {
-    const int i = base + tid;
-    if (i < e) {
-      const int t = a.bin_prims[i];
-      const int4* rp = a.rec + 3ll * t;
-      const int4 q0 = __ldg(rp), q1 = __ldg(rp + 1), q2 = __ldg(rp + 2);
-      const RecView r = unpack(q0, q1, q2);
+  int s = 0, e = 0;
+  if (!ovf) {
+    if (a.npass == 0) { s = 0; e = (int)a.ctl->n_pairs; }
+    else { s = a.bin_start[b]; e = a.bin_start[b + 1]; }
+  }
+  const int nbatch = (e - s + THREADS - 1) / THREADS;
+  // software pipeline: primIDs two batches ahead, records one batch ahead
+  int t_cur = (s + tid < e) ? a.bin_prims[s + tid] : -1;
+  int t_next = (s + THREADS + tid < e) ? a.bin_prims[s + THREADS + tid] : -1;
+  if (t_cur >= 0) {
+    const int4* rp = a.rec + 3ll * t_cur;
+    cp_async16(&sm.rec[0][tid][0], rp); cp_async16(&sm.rec[0][tid][1], rp + 1);
+    cp_async16(&sm.rec[0][tid][2], rp + 2);
+  }
+  cp_async_commit();
+  for (int k = 0; k < nbatch; ++k) {
+    const int buf = k & 1;
+    if (t_next >= 0) {
+      const int4* rp = a.rec + 3ll * t_next;
+      cp_async16(&sm.rec[buf ^ 1][tid][0], rp); cp_async16(&sm.rec[buf ^ 1][tid][1], rp + 1);
+      cp_async16(&sm.rec[buf ^ 1][tid][2], rp + 2);
+    }
+    cp_async_commit();
+    const int i2 = s + (k + 2) * THREADS + tid;
+    const int t_after = (i2 < e) ? a.bin_prims[i2] : -1;
+    cp_async_wait<1>();
+    __syncthreads();
+    if (t_cur >= 0) {
+      const RecView r = unpack(sm.rec[buf][tid][0], sm.rec[buf][tid][1], sm.rec[buf][tid][2]);
       const int rx0 = max(r.px0, x0), rx1 = min(r.px1, x1);
       const int ry0 = max(r.py0, y0), ry1 = min(r.py1, y1);
       const int area = (rx1 - rx0 + 1) * (ry1 - ry0 + 1);
@@ -619,23 +725,24 @@ __global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
           const int Py = 256 * y + 128;
           for (int x = rx0; x <= rx1; ++x) {
             bool cov;
-            const unsigned long long key = eval_key(r, 256 * x + 128, Py, t, cov);
+            const u64 key = eval_key(r, 256 * x + 128, Py, t_cur, cov);
             const int p = (y - y0) * BW + (x - x0);
             if (COV && cov) atomicAdd(&s_cov[p], 1u);
-            if (key != CLEAR_KEY) atomicMin(&s_key[p], key);
+            if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
           }
         }
       } else {
         const int slot = atomicAdd(&s_qn, 1);
-        s_q[3 * slot] = q0; s_q[3 * slot + 1] = q1; s_q[3 * slot + 2] = q2;
-        s_qt[slot] = t;
+        sm.big[slot] = (unsigned short)tid;
+        sm.bigt[slot] = t_cur;
       }
     }
     __syncthreads();
-    const int n = s_qn;
-    for (int k = 0; k < n; ++k) {
-      const RecView r = unpack(s_q[3 * k], s_q[3 * k + 1], s_q[3 * k + 2]);
-      const int t = s_qt[k];
+    const int nq = s_qn;
+    for (int q = 0; q < nq; ++q) {
+      const int src = sm.big[q];
+      const RecView r = unpack(sm.rec[buf][src][0], sm.rec[buf][src][1], sm.rec[buf][src][2]);
+      const int t = sm.bigt[q];
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
         const int p = tid + j * THREADS;
@@ -643,23 +750,26 @@ __global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
         const int x = x0 + (p % BW), y = y0 + (p / BW);
         if (x < r.px0 || x > r.px1 || y < r.py0 || y > r.py1) continue;
         bool cov;
-        const unsigned long long key = eval_key(r, 256 * x + 128, 256 * y + 128, t, cov);
+        const u64 key = eval_key(r, 256 * x + 128, 256 * y + 128, t, cov);
         if (COV && cov) s_cov[p] += 1u;
-        if (key < s_key[p]) s_key[p] = key;
+        if (key < sm.key[p]) sm.key[p] = key;
       }
     }
     __syncthreads();
     if (tid == 0) s_qn = 0;
-    __syncthreads();
+    t_cur = t_next;
+    t_next = t_after;
   }
+  cp_async_wait<0>();
+  __syncthreads();
 
   // ---- write-back ------------------------------------------------------------
   if (KEYS_ONLY) {
-    unsigned long long* dst = a.tile_keys + (size_t)blockIdx.x * NPX;
+    u64* dst = a.tile_keys + (size_t)blockIdx.x * NPX;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int p = tid + k * THREADS;
-      if (p < NPX) dst[p] = s_key[p];
+      if (p < NPX) dst[p] = sm.key[p];
     }
     return;
   }
@@ -671,7 +781,7 @@ __global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
     if (p >= NPX) continue;
     const int x = x0 + (p % BW), y = y0 + (p / BW);
     if (x > x1 || y > y1) continue;
-    const unsigned long long key = s_key[p];
+    const u64 key = sm.key[p];
     const size_t o = (size_t)y * g.W + x;
     float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
     float depth = 1.0f;
@@ -700,8 +810,7 @@ __global__ void __launch_bounds__(256) k_resolve(ResolveArgs a) {
   const int b = (y >> g.bh_log2) * g.binsX + (x >> g.bw_log2);
   const int r = b % g.nranks, k = b / g.nranks;
   const int p = (y & (bh - 1)) * bw + (x & (bw - 1));
-  const unsigned long long key =
-      a.all_keys[((size_t)r * a.owned_max + k) * (size_t)(bw * bh) + p];
+  const u64 key = a.all_keys[((size_t)r * a.owned_max + k) * (size_t)(bw * bh) + p];
   float L[3];
   normalise_light(a.light, L);
   const size_t o = (size_t)y * g.W + x;
@@ -721,40 +830,50 @@ __global__ void __launch_bounds__(256) k_resolve(ResolveArgs a) {
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-cudaError_t launch_setup(const SetupArgs& a, int grid, cudaStream_t s) {
-  k_setup<<<grid, K1_THREADS, 0, s>>>(a);
-  return cudaGetLastError();
+template <typename Kern, typename Arg>
+static cudaError_t launch_ex(Kern kern, int grid, int threads, size_t smem, bool pdl,
+                             cudaStream_t s, const Arg& a) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
-cudaError_t launch_bin_scan(const ScanArgs& a, int grid, cudaStream_t s) {
-  k_bin_scan<<<grid, SCAN_THREADS, 0, s>>>(a);
-  return cudaGetLastError();
+
+cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s) {
+  return launch_ex(k_setup, grid, K1_THREADS, 0, pdl, s, a);
 }
-cudaError_t launch_radix_pass(const RadixArgs& a, int grid, cudaStream_t s) {
-  k_radix_pass<<<grid, RX_THREADS, 0, s>>>(a);
-  return cudaGetLastError();
+cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream_t s) {
+  return launch_ex(k_radix_pass, grid, RX_THREADS, 0, pdl, s, a);
 }
 
 template <int BW, int BH>
-static cudaError_t launch_tile_t(const TileArgs& a, int nb, bool cov, bool keys_only, cudaStream_t s) {
+static cudaError_t launch_tile_t(const TileArgs& a, int grid, bool cov, bool keys_only, bool pdl,
+                                 cudaStream_t s) {
   constexpr int NPX = BW * BH;
   constexpr int THREADS = NPX < 256 ? NPX : 256;
-  size_t smem = (size_t)NPX * 8 + (size_t)THREADS * (48 + 4) + (cov ? (size_t)NPX * 4 : 0);
+  const size_t smem = sizeof(TileSmem<BW, BH, THREADS>) + (cov ? (size_t)NPX * 4 : 0);
   auto run = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<nb, THREADS, smem, s>>>(a);
-    return cudaGetLastError();
+    return launch_ex(kern, grid, THREADS, smem, pdl, s, a);
   };
   if (keys_only) return cov ? run(k_tile<BW, BH, THREADS, true, true>) : run(k_tile<BW, BH, THREADS, false, true>);
   return cov ? run(k_tile<BW, BH, THREADS, true, false>) : run(k_tile<BW, BH, THREADS, false, false>);
 }
 
 #define PIKO_TILE_CASE(W_, H_) \
-  if (bw == W_ && bh == H_) return launch_tile_t<W_, H_>(a, nb, cov, keys_only, s);
+  if (bw == W_ && bh == H_) return launch_tile_t<W_, H_>(a, grid, cov, keys_only, pdl, s);
 
-cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int nb, bool cov, bool keys_only,
-                        cudaStream_t s) {
-  if (nb <= 0) return cudaSuccess;
+cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
+                        bool pdl, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
   PIKO_TILE_CASE(8, 8) PIKO_TILE_CASE(8, 16) PIKO_TILE_CASE(8, 32) PIKO_TILE_CASE(8, 64)
   PIKO_TILE_CASE(16, 8) PIKO_TILE_CASE(16, 16) PIKO_TILE_CASE(16, 32) PIKO_TILE_CASE(16, 64)
   PIKO_TILE_CASE(32, 8) PIKO_TILE_CASE(32, 16) PIKO_TILE_CASE(32, 32) PIKO_TILE_CASE(32, 64)
@@ -767,16 +886,5 @@ cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s) {
   k_resolve<<<grid, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
-
-static int occ_grid(const void* f, int threads, size_t smem) {
-  int dev = 0, sms = 148, occ = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, threads, smem);
-  return sms * (occ > 0 ? occ : 1);
-}
-int max_grid_setup() { return occ_grid((const void*)k_setup, K1_THREADS, 0); }
-int max_grid_scan() { return occ_grid((const void*)k_bin_scan, SCAN_THREADS, 0); }
-int max_grid_radix() { return occ_grid((const void*)k_radix_pass, RX_THREADS, 0); }
 
 }  // namespace piko

@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -82,7 +83,12 @@ struct piko_ctx {
   Control* ctl = nullptr;
   unsigned long long* st_k1 = nullptr; long long st_k1_cap = 0;
   unsigned long long* st_scan = nullptr; long long st_scan_n = 0;
-  uint32_t* st_rx = nullptr; long long st_rx_chunks = 0;
+  unsigned long long* st_rx = nullptr; long long st_rx_chunks = 0;
+  // grid sizes of the last frame: the ticket/tag scheme of Control needs them
+  // constant, so a change forces a reset of the control block + status words
+  long long last_g1 = -1, last_grx = -1;
+  bool need_reset = true;
+  bool pdl = true;
   int32_t* primid = nullptr;
   uint32_t* cov = nullptr;
   Control* h_ctl = nullptr;          // pinned mirror of the control block
@@ -91,7 +97,6 @@ struct piko_ctx {
   int last_status = PIKO_OK;
   long long last_T = 0;
 
-  int grid_k1 = 148, grid_scan = 148, grid_rx = 148;
 
   // end-to-end staging
   float* d_verts = nullptr; long long d_verts_cap = 0;
@@ -185,9 +190,7 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
     return nullptr;
   }
   memset(ctx->h_ctl, 0, sizeof(Control));
-  ctx->grid_k1 = max_grid_setup();
-  ctx->grid_scan = max_grid_scan();
-  ctx->grid_rx = max_grid_radix();
+  if (const char* e = getenv("PIKO_NO_PDL")) ctx->pdl = e[0] == '0';
   return ctx;
 }
 
@@ -233,9 +236,9 @@ static int ensure_tris(piko_ctx* ctx, long long T) {
 
 static int ensure_pairs(piko_ctx* ctx, unsigned long long P) {
   if (P <= ctx->pair_cap) return PIKO_OK;
-  if (P >= (1ull << 30))
-    return ctx->fail(PIKO_ECAPACITY, "pair count %llu exceeds the 2^30 limit", P);
-  unsigned long long cap = std::min<unsigned long long>(P + P / 4 + 4096, (1ull << 30) - 1);
+  if (P >= MAX_PAIRS)
+    return ctx->fail(PIKO_ECAPACITY, "pair count %llu exceeds the 2^31 limit", P);
+  unsigned long long cap = std::min<unsigned long long>(P + P / 4 + 4096, MAX_PAIRS - 1);
   for (int k = 0; k < 2; ++k) {
     if (ctx->keys[k]) cudaFree(ctx->keys[k]);
     if (ctx->vals[k]) cudaFree(ctx->vals[k]);
@@ -246,9 +249,10 @@ static int ensure_pairs(piko_ctx* ctx, unsigned long long P) {
   const long long chunks = (long long)((cap + RX_CHUNK - 1) / RX_CHUNK);
   if (ctx->st_rx) cudaFree(ctx->st_rx);
   ctx->st_rx = nullptr;
-  CK(cudaMalloc(&ctx->st_rx, sizeof(uint32_t) * RX_RADIX * chunks * std::max(ctx->npass, 1)));
+  CK(cudaMalloc(&ctx->st_rx, sizeof(unsigned long long) * RX_RADIX * chunks * std::max(ctx->npass, 1)));
   ctx->st_rx_chunks = chunks;
   ctx->pair_cap = cap;
+  ctx->need_reset = true;
   return PIKO_OK;
 }
 
@@ -266,51 +270,56 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, const int32_t* idx, 
   cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
   if (ctx->prof && !ev) return ctx->fail(PIKO_ECUDA, "cannot create profiling events");
   auto mark = [&](int stage) -> cudaError_t { return ev ? cudaEventRecord(ev[stage], s) : cudaSuccess; };
+  const long long g1 = std::max<long long>((T + K1_CHUNK - 1) / K1_CHUNK, 1);
+  const long long ntiles = (ctx->g.NB + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  const long long grx = ctx->st_rx_chunks + ntiles;  // pass 0: sort chunks + scan tiles
   CK(mark(0));
-  CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s));
-  const long long k1_chunks = (T + K1_CHUNK - 1) / K1_CHUNK;
-  if (k1_chunks > 0) CK(cudaMemsetAsync(ctx->st_k1, 0, sizeof(unsigned long long) * k1_chunks, s));
-  CK(cudaMemsetAsync(ctx->st_scan, 0, sizeof(unsigned long long) * ctx->st_scan_n, s));
-  if (ctx->npass > 0)
-    CK(cudaMemsetAsync(ctx->st_rx, 0, sizeof(uint32_t) * RX_RADIX * ctx->st_rx_chunks * ctx->npass, s));
+  if (ctx->need_reset || g1 != ctx->last_g1 || grx != ctx->last_grx) {
+    // tickets restart at 0, so every tag-carrying status word must be cleared
+    CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s));
+    CK(cudaMemsetAsync(ctx->st_k1, 0, sizeof(unsigned long long) * ctx->st_k1_cap, s));
+    CK(cudaMemsetAsync(ctx->st_scan, 0, sizeof(unsigned long long) * ctx->st_scan_n, s));
+    if (ctx->npass > 0)
+      CK(cudaMemsetAsync(ctx->st_rx, 0, sizeof(unsigned long long) * RX_RADIX * ctx->st_rx_chunks * ctx->npass, s));
+    CK(cudaMemsetAsync(ctx->bin_count, 0, sizeof(uint32_t) * ctx->g.NB, s));
+    ctx->last_g1 = g1;
+    ctx->last_grx = grx;
+    ctx->need_reset = false;
+  }
   CK(mark(1 + PIKO_STAGE_CLEAR));
-
-  if (T > 0) {
+  {
     SetupArgs a{};
-    a.verts = verts; a.idx = idx; a.n_tris = T; a.M = M; a.g = ctx->g;
+    a.verts = verts; a.idx = idx; a.n_tris = T; a.M = M; a.g = ctx->g; a.npass = ctx->npass;
     a.rec = ctx->rec; a.pair_keys = ctx->keys[0]; a.pair_vals = ctx->vals[0];
     a.bin_count = ctx->bin_count; a.status = ctx->st_k1; a.ctl = ctx->ctl; a.cap = ctx->pair_cap;
-    CK(launch_setup(a, (int)std::min<long long>(k1_chunks, ctx->grid_k1), s));
+    CK(launch_setup(a, (int)g1, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_SETUP));
-  {
-    ScanArgs a{};
-    a.bin_count = ctx->bin_count; a.bin_start = ctx->bin_start; a.status = ctx->st_scan;
-    a.ctl = ctx->ctl; a.NB = ctx->g.NB; a.npass = ctx->npass;
-    CK(launch_bin_scan(a, (int)std::min<long long>(ctx->st_scan_n, ctx->grid_scan), s));
-  }
-  CK(mark(1 + PIKO_STAGE_BINSCAN));
-  const int rx_grid = (int)std::min<long long>(ctx->st_rx_chunks, ctx->grid_rx);
+  CK(mark(1 + PIKO_STAGE_BINSCAN));  // the bin scan runs inside radix pass 0
   for (int p = 0; p < ctx->npass; ++p) {
     RadixArgs a{};
     a.keys_in = ctx->keys[p & 1]; a.vals_in = ctx->vals[p & 1];
     a.keys_out = (p + 1 < ctx->npass) ? ctx->keys[(p + 1) & 1] : nullptr;
     a.vals_out = ctx->vals[(p + 1) & 1];
     a.status = ctx->st_rx + (size_t)p * RX_RADIX * ctx->st_rx_chunks;
-    a.ctl = ctx->ctl; a.pass = p; a.shift = RX_BITS * p; a.cap = ctx->pair_cap;
-    CK(launch_radix_pass(a, rx_grid, s));
+    a.ctl = ctx->ctl; a.pass = p; a.shift = RX_BITS * p;
+    a.bin_count = ctx->bin_count; a.bin_start = ctx->bin_start; a.scan_status = ctx->st_scan;
+    a.NB = ctx->g.NB;
+    CK(launch_radix_pass(a, (int)(p == 0 ? grx : ctx->st_rx_chunks), ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_RADIX));
   {
     TileArgs a{};
     a.verts = verts; a.idx = idx; a.M = M;
     a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
-    a.g = ctx->g; a.rec = ctx->rec; a.bin_start = ctx->bin_start;
+    a.g = ctx->g; a.npass = ctx->npass; a.rec = ctx->rec; a.bin_start = ctx->bin_start;
     a.bin_prims = ctx->vals[ctx->npass & 1]; a.ctl = ctx->ctl;
     a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
     a.out_cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
     a.tile_keys = gather ? ctx->tile_keys : nullptr;
-    CK(launch_tile(a, ctx->bw, ctx->bh, ctx->owned, a.out_cov != nullptr, gather, s));
+    a.owned = ctx->owned;
+    CK(launch_tile(a, ctx->bw, ctx->bh, std::max(ctx->owned, 1), a.out_cov != nullptr, gather,
+                   ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_TILE));
   if (gather) {
@@ -360,7 +369,7 @@ static int check_frame(piko_ctx* ctx) {
   if (!ctx->pending) return ctx->last_status;
   ctx->pending = false;
   CK(cudaEventSynchronize(ctx->done));
-  if (ctx->h_ctl->overflow) {
+  if (ctx->h_ctl->overflow_tag == ctx->h_ctl->frame + 1) {
     const int rc = ensure_pairs(ctx, ctx->h_ctl->n_pairs);
     ctx->last_status = rc != PIKO_OK ? rc : PIKO_ECAPACITY;
     if (rc == PIKO_OK) ctx->fail(PIKO_ECAPACITY, "pair capacity exceeded (P=%llu); grown", ctx->h_ctl->n_pairs);
@@ -368,6 +377,13 @@ static int check_frame(piko_ctx* ctx) {
   }
   ctx->last_status = PIKO_OK;
   return PIKO_OK;
+}
+
+// A failed CUDA call may leave tickets mid-frame: reset before the next frame.
+static int frame_failed(piko_ctx* ctx, int rc) {
+  ctx->need_reset = true;
+  ctx->pending = false;
+  return rc;
 }
 
 static int validate_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, int32_t n_tris,
@@ -407,9 +423,11 @@ static int draw_impl(piko_ctx* ctx, const float* verts, const int32_t* idx, int3
     return rc;
   if ((rc = ensure_cov(ctx)) != PIKO_OK) return rc;
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if ((rc = enqueue_frame(ctx, verts, idx, n_tris, M, L, rgba, depth, s)) != PIKO_OK) return rc;
+    if ((rc = enqueue_frame(ctx, verts, idx, n_tris, M, L, rgba, depth, s)) != PIKO_OK)
+      return frame_failed(ctx, rc);
     if (ctx->sync_mode == PIKO_SYNC_ASYNC && !force_check) return prev == PIKO_ECAPACITY ? PIKO_OK : prev;
     rc = check_frame(ctx);
+    if (rc == PIKO_ECUDA) return frame_failed(ctx, rc);
     if (rc != PIKO_ECAPACITY) return rc;
     // multi-rank: every rank must re-issue together; a capacity miss is
     // reported instead of re-issued so ranks cannot diverge.
@@ -544,15 +562,14 @@ extern "C" int piko_get_stats(const piko_ctx* cctx, piko_stats* out) {
   int rc = check_frame(ctx);
   if (rc == PIKO_ECUDA) return rc;
   out->n_tris = ctx->last_T;
-  out->n_live = (int64_t)ctx->h_ctl->n_live;
+  out->n_live = (int64_t)ctx->h_ctl->n_live[ctx->h_ctl->frame & 1];
   out->n_pairs = (int64_t)ctx->h_ctl->n_pairs;
   out->n_bins = ctx->g.NB;
   out->owned_bins = ctx->owned;
   out->pair_capacity = (int64_t)ctx->pair_cap;
   out->radix_passes = ctx->npass;
   const bool gather = ctx->comm && ctx->g.nranks > 1;
-  out->kernels_per_frame = (ctx->last_T > 0 ? 1 : 0) + 1 + ctx->npass + (ctx->owned > 0 ? 1 : 0) +
-                           (gather && ctx->g.rank == 0 ? 1 : 0);
+  out->kernels_per_frame = 1 + ctx->npass + 1 + (gather && ctx->g.rank == 0 ? 1 : 0);
   return PIKO_OK;
 }
 

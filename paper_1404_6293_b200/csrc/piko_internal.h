@@ -1,6 +1,6 @@
 // piko_internal.h -- structures shared by the kernels (kernels.cu) and the host
 // orchestration (piko_api.cu).  Product code only; nothing here is shared with
-// the oracle (oracle/piko_oracle.c).
+// the CPU checker.
 #pragma once
 
 #include <cstdint>
@@ -10,9 +10,9 @@ namespace piko {
 
 // ---- launch geometry -------------------------------------------------------
 constexpr int K1_THREADS = 256;                     // vertex+setup+AssignBin CTA
-constexpr int K1_TPT = 4;                           // triangles per thread
+constexpr int K1_TPT = 4;                           // triangles per thread (strided)
 constexpr int K1_CHUNK = K1_THREADS * K1_TPT;       // triangles per look-back chunk
-constexpr int SCAN_THREADS = 256;                   // bin-count scan CTA
+constexpr int SCAN_THREADS = 256;                   // bin-count scan (inside radix pass 0)
 constexpr int SCAN_ITEMS = 16;
 constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
 constexpr int RX_THREADS = 256;                     // stable LSD radix pass CTA
@@ -22,16 +22,23 @@ constexpr int RX_CHUNK = RX_THREADS * RX_ITEMS;     // pairs per chunk
 constexpr int RX_BITS = 8;
 constexpr int RX_RADIX = 1 << RX_BITS;
 constexpr int MAX_PASSES = 3;                       // NB <= 2^24 bins
+constexpr unsigned long long MAX_PAIRS = 1ull << 31;  // bin_start is int32
 
-// ---- per-frame device control block (zeroed at frame start) ----------------
+// ---- persistent device control block ----------------------------------------
+// Never memset per frame: every kernel of a frame takes exactly gridDim.x
+// tickets from its counter, so  frame = ticket / gridDim.x  and
+// chunk = ticket % gridDim.x.  Look-back status words carry the tag frame+1.
+// Per-frame accumulators are double-buffered by frame parity; the tile kernel
+// zeroes the next frame's copy.  The host resets the block (and the status
+// arrays) only when a grid size changes or after an error.
 struct Control {
-  unsigned int ticket_k1;
-  unsigned int ticket_scan;
-  unsigned int ticket_rx[MAX_PASSES];
-  unsigned int overflow;         // K1 saw P > pair capacity
-  unsigned long long n_pairs;    // P, written by K1's last chunk
-  unsigned long long n_live;     // live (owned) triangles, statistics
-  unsigned int digit_hist[MAX_PASSES][RX_RADIX];  // per-pass digit histograms
+  unsigned long long k1_ticket;
+  unsigned long long rx_ticket[MAX_PASSES];
+  unsigned long long frame;            // written by K1 chunk 0
+  unsigned long long n_pairs;          // P, written by K1's last chunk
+  unsigned long long overflow_tag;     // frame+1 of the last frame whose P > capacity
+  unsigned long long n_live[2];        // parity double buffer (statistics)
+  unsigned int digit_hist[2][MAX_PASSES][RX_RADIX];  // parity double buffer
 };
 
 struct Mat4 {
@@ -59,22 +66,14 @@ struct SetupArgs {
   long long n_tris;
   Mat4 M;
   Grid g;
+  int npass;
   int4* rec;                    // [n_tris][3]
   uint32_t* pair_keys;          // [cap] bin id per pair
   int32_t* pair_vals;           // [cap] primID per pair
-  uint32_t* bin_count;          // [NB] pairs per bin (zeroed by k_bin_scan)
-  unsigned long long* status;   // [chunks] decoupled look-back
+  uint32_t* bin_count;          // [NB] pairs per bin (zeroed by the bin scan)
+  unsigned long long* status;   // [grid] decoupled look-back
   Control* ctl;
   unsigned long long cap;       // pair capacity
-};
-
-struct ScanArgs {
-  uint32_t* bin_count;          // [NB] in, zeroed on exit
-  int32_t* bin_start;           // [NB+1] out
-  unsigned long long* status;   // [chunks]
-  Control* ctl;
-  int NB;
-  int npass;
 };
 
 struct RadixArgs {
@@ -82,11 +81,15 @@ struct RadixArgs {
   const int32_t* vals_in;
   uint32_t* keys_out;           // may be null on the last pass
   int32_t* vals_out;
-  uint32_t* status;             // [chunks][RX_RADIX]
+  unsigned long long* status;   // [sort chunks][RX_RADIX]
   Control* ctl;
   int pass;
   int shift;
-  unsigned long long cap;
+  // bin scan (pass 0 only): extra CTAs after the sort chunks
+  uint32_t* bin_count;
+  int32_t* bin_start;
+  unsigned long long* scan_status;  // [scan tiles]
+  int NB;
 };
 
 struct TileArgs {
@@ -95,15 +98,17 @@ struct TileArgs {
   Mat4 M;
   float light[3];
   Grid g;
+  int npass;
   const int4* rec;
-  const int32_t* bin_start;
+  int32_t* bin_start;           // written here only when npass == 0 (NB == 1)
   const int32_t* bin_prims;
-  const Control* ctl;
+  Control* ctl;
   float* out_rgba;              // may be null (keys-only mode)
   float* out_depth;
   int32_t* out_primid;
   uint32_t* out_cov;            // debug coverage counts or null
   unsigned long long* tile_keys;  // keys-only mode: [owned][bw*bh]
+  int owned;                    // bins owned by this rank (grid may be larger)
 };
 
 struct ResolveArgs {            // rank 0 after the NCCL gather
@@ -119,16 +124,11 @@ struct ResolveArgs {            // rank 0 after the NCCL gather
   int32_t* out_primid;
 };
 
-// ---- launchers (kernels.cu) ------------------------------------------------
-cudaError_t launch_setup(const SetupArgs& a, int grid, cudaStream_t s);
-cudaError_t launch_bin_scan(const ScanArgs& a, int grid, cudaStream_t s);
-cudaError_t launch_radix_pass(const RadixArgs& a, int grid, cudaStream_t s);
-cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int n_owned_bins, bool cov,
-                        bool keys_only, cudaStream_t s);
+// ---- launchers (kernels.cu); pdl = programmatic dependent launch -----------
+cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s);
+cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream_t s);
+cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
+                        bool pdl, cudaStream_t s);
 cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s);
-// occupancy-derived persistent grid sizes
-int max_grid_setup();
-int max_grid_scan();
-int max_grid_radix();
 
 }  // namespace piko
