@@ -95,6 +95,14 @@ int piko_draw(piko_ctx *ctx, const float *verts, const int32_t *idx, int32_t n_t
               const float mvp[16], const float light[3], float *out_rgba, float *out_depth,
               void *stream);
 
+/* piko_draw with the vertex count given: 0 <= idx < n_verts (n_verts >= 1 when
+ * n_tris > 0).  piko_draw, which has no vertex count, first derives
+ * n_verts = max(idx) + 1 with a device reduction over idx (one extra kernel
+ * reading 12 bytes per triangle); otherwise the two calls are identical.    */
+int piko_draw_indexed(piko_ctx *ctx, const float *verts, int64_t n_verts, const int32_t *idx,
+                      int32_t n_tris, const float mvp[16], const float light[3], float *out_rgba,
+                      float *out_depth, void *stream);
+
 /* End-to-end variant of piko_draw on HOST buffers: copies verts (n_verts x 8
  * f32) and idx to context-owned device buffers, draws, copies rgba and depth
  * back into host buffers, and synchronises `stream` before returning.
@@ -168,10 +176,10 @@ int piko_nccl_unique_id(void *out_id128);
 /* Per-stage device timing with CUDA events recorded on the frame's stream
  * between the kernels of every frame (no host synchronisation is added).
  * Stages: */
-#define PIKO_STAGE_CLEAR 0   /* per-frame control/status resets (memsets)   */
-#define PIKO_STAGE_SETUP 1   /* k_setup: transform, setup, count, scan, pairs */
-#define PIKO_STAGE_BINSCAN 2 /* k_bin_scan: CSR bin_start, digit histograms  */
-#define PIKO_STAGE_RADIX 3   /* k_radix_pass x radix_passes: stable scatter   */
+#define PIKO_STAGE_CLEAR 0   /* resets (only when a grid size changed)        */
+#define PIKO_STAGE_VERTEX 1  /* k_index_max (piko_draw only) + k_vertex      */
+#define PIKO_STAGE_SETUP 2   /* k_setup: setup, count, scan, pairs           */
+#define PIKO_STAGE_RADIX 3   /* k_radix_pass x radix_passes (+ CSR bin scan)  */
 #define PIKO_STAGE_TILE 4    /* k_tile: per-bin raster, depth, shade, store   */
 #define PIKO_STAGE_GATHER 5  /* NCCL tile-key gather (multi-GPU)              */
 #define PIKO_STAGE_RESOLVE 6 /* k_resolve: rank-0 shade of gathered keys      */

@@ -23,8 +23,8 @@ PIKO_SYNC_CHECKED, PIKO_SYNC_ASYNC = 0, 1
 EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_set_sync",
            "piko_destroy", "piko_last_error", "piko_get_primid", "piko_get_bins",
            "piko_set_debug", "piko_get_coverage", "piko_set_partition", "piko_attach_comm",
-           "piko_get_stats", "piko_nccl_unique_id", "piko_set_profiling", "piko_get_profile")
-STAGES = ("clear", "setup", "bin_scan", "radix", "tile", "gather", "resolve")
+           "piko_get_stats", "piko_nccl_unique_id", "piko_draw_indexed", "piko_set_profiling", "piko_get_profile")
+STAGES = ("clear", "vertex", "setup", "radix", "tile", "gather", "resolve")
 
 
 class PikoError(RuntimeError):
@@ -50,6 +50,7 @@ def _load():
         "piko_create": ([I, I, I, I], P),
         "piko_draw": ([P, P, P, ctypes.c_int32, P, P, P, P, P], I),
         "piko_draw_host": ([P, P, I64, P, ctypes.c_int32, P, P, P, P, P], I),
+        "piko_draw_indexed": ([P, P, I64, P, ctypes.c_int32, P, P, P, P, P], I),
         "piko_finish": ([P], I),
         "piko_set_sync": ([P, I], I),
         "piko_destroy": ([P], None),
@@ -129,6 +130,16 @@ def piko_draw(ctx, verts, idx, n_tris, mvp, light, out_rgba, out_depth, stream=N
                         _dev_ptr(idx, torch.int32, "idx"), int(n_tris), _f32x(mvp, 16),
                         _f32x(light, 3), _dev_ptr(out_rgba, torch.float32, "out_rgba"),
                         _dev_ptr(out_depth, torch.float32, "out_depth"), _stream_ptr(stream))
+    return _check(ctx, rc) if check else rc
+
+
+def piko_draw_indexed(ctx, verts, n_verts, idx, n_tris, mvp, light, out_rgba, out_depth,
+                      stream=None, check=True):
+    import torch
+    rc = _lib.piko_draw_indexed(ctx, _dev_ptr(verts, torch.float32, "verts"), int(n_verts),
+                                _dev_ptr(idx, torch.int32, "idx"), int(n_tris), _f32x(mvp, 16),
+                                _f32x(light, 3), _dev_ptr(out_rgba, torch.float32, "out_rgba"),
+                                _dev_ptr(out_depth, torch.float32, "out_depth"), _stream_ptr(stream))
     return _check(ctx, rc) if check else rc
 
 
@@ -227,7 +238,12 @@ class Renderer:
     def n_bins(self):
         return (-(-self.W // self.bin_w)) * (-(-self.H // self.bin_h))
 
-    def draw(self, verts, idx, mvp, light, stream=None, check=True):
+    def draw(self, verts, idx, mvp, light, stream=None, check=True, indexed=True):
+        """indexed=True passes n_verts = verts.shape[0] (piko_draw_indexed);
+        False uses the north-star piko_draw (vertex count derived on device)."""
+        if indexed:
+            return piko_draw_indexed(self.ctx, verts, verts.shape[0], idx, idx.shape[0], mvp, light,
+                                     self.rgba, self.depth, stream, check)
         return piko_draw(self.ctx, verts, idx, idx.shape[0], mvp, light, self.rgba, self.depth,
                          stream, check)
 

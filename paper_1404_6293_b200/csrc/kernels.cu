@@ -24,6 +24,7 @@
 // Arithmetic follows DESIGN.md R1..R18 with a pinned float op order (IEEE
 // round-to-nearest intrinsics, explicit fma); this TU is compiled with
 // --fmad=false so no other contraction can happen.
+#include <algorithm>
 #include <cstdint>
 
 #include "piko_internal.h"
@@ -146,15 +147,23 @@ __device__ __forceinline__ float4 load_pos(const float* __restrict__ verts, int 
   return __ldg(reinterpret_cast<const float4*>(verts + 8ll * vid));
 }
 
-// Full setup from the three corner positions; false = culled.
-__device__ __forceinline__ bool setup_tri(float4 p0, float4 p1, float4 p2, int i0, int i1, int i2,
-                                          const Mat4& M, int W, int H, Tri& o) {
+// Vertex stage record (O1 output): {X, Y, bits(zw), bits(rw)} or X = VX_CULLED.
+__device__ __forceinline__ int4 transform_vertex(float4 p, const Mat4& M, int W, int H) {
   const float hw = __fmul_rn(0.5f, __int2float_rn(W));
   const float hh = __fmul_rn(0.5f, __int2float_rn(H));
-  bool ok = xform_corner(p0, M, hw, hh, o.X0, o.Y0, o.zw0, o.rw0);
-  ok &= xform_corner(p1, M, hw, hh, o.X1, o.Y1, o.zw1, o.rw1);
-  ok &= xform_corner(p2, M, hw, hh, o.X2, o.Y2, o.zw2, o.rw2);
-  if (!ok) return false;
+  int X, Y;
+  float zw, rw;
+  if (!xform_corner(p, M, hw, hh, X, Y, zw, rw)) return make_int4(VX_CULLED, 0, 0, 0);
+  return make_int4(X, Y, __float_as_int(zw), __float_as_int(rw));
+}
+
+// Triangle setup (O2-O4) from the three transformed corners; false = culled.
+__device__ __forceinline__ bool setup_tri(int4 c0, int4 c1, int4 c2, int i0, int i1, int i2, int W,
+                                          int H, Tri& o) {
+  if (c0.x == VX_CULLED || c1.x == VX_CULLED || c2.x == VX_CULLED) return false;
+  o.X0 = c0.x; o.Y0 = c0.y; o.zw0 = __int_as_float(c0.z); o.rw0 = __int_as_float(c0.w);
+  o.X1 = c1.x; o.Y1 = c1.y; o.zw1 = __int_as_float(c1.z); o.rw1 = __int_as_float(c1.w);
+  o.X2 = c2.x; o.Y2 = c2.y; o.zw2 = __int_as_float(c2.z); o.rw2 = __int_as_float(c2.w);
   o.v0 = i0; o.v1 = i1; o.v2 = i2;
   long long area2 = (long long)(o.X1 - o.X0) * (long long)(o.Y2 - o.Y0) -
                     (long long)(o.Y1 - o.Y0) * (long long)(o.X2 - o.X0);
@@ -210,7 +219,43 @@ __device__ __forceinline__ int owned_bin_at(int tx0, int ty0, int tx1, int ty1, 
 }
 
 // ---------------------------------------------------------------------------
-// K1: vertex + setup + count + chunk scan + pair expansion
+// K0: vertex stage -- each vertex transformed and snapped exactly once
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(VX_THREADS) k_vertex(VertexArgs a) {
+  pdl_wait();   // the previous frame's kernels still read xv
+  pdl_trigger();
+  long long V = a.n_verts >= 0 ? a.n_verts : (long long)a.ctl->vmax;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.ctl->vx_need = (unsigned long long)V;
+    if (V > a.cap) a.ctl->vx_overflow = 1;
+  }
+  V = V < a.cap ? V : a.cap;
+  for (long long v = (long long)blockIdx.x * VX_THREADS + threadIdx.x; v < V;
+       v += (long long)gridDim.x * VX_THREADS)
+    a.xv[v] = transform_vertex(load_pos(a.verts, (int)v), a.M, a.W, a.H);
+}
+
+// n_verts for piko_draw (no vertex count in its signature): max(idx) + 1
+__global__ void __launch_bounds__(256) k_index_max(const int32_t* __restrict__ idx, long long n,
+                                                   Control* ctl) {
+  pdl_wait();
+  pdl_trigger();
+  int m = -1;
+  const long long n4 = n / 4;
+  const int4* p = reinterpret_cast<const int4*>(idx);
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n4; i += (long long)gridDim.x * 256) {
+    const int4 q = __ldg(p + i);
+    m = max(m, max(max(q.x, q.y), max(q.z, q.w)));
+  }
+  for (long long i = n4 * 4 + (long long)blockIdx.x * 256 + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+    m = max(m, __ldg(idx + i));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m >= 0) atomicMax(&ctl->vmax, (unsigned)m + 1u);
+}
+
+// ---------------------------------------------------------------------------
+// K1: triangle setup + count + chunk scan + pair expansion
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
   __shared__ unsigned s_off[K1_CHUNK];   // exclusive local pair offset per triangle
@@ -223,7 +268,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Grid g = a.g;
 
-  pdl_wait();   // the previous frame's tile kernel still reads rec / pairs
+  pdl_wait();   // k_vertex output; the previous frame's tile kernel read rec / pairs
   pdl_trigger();
   if (tid == 0) { s_tk = atomicAdd(&a.ctl->k1_ticket, 1ull); s_live = 0; }
   for (int i = tid; i < MAX_PASSES * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
@@ -232,7 +277,10 @@ __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
   const long long chunk = (long long)(s_tk % gridDim.x);
   const unsigned tag = frame_tag(frame);
   const long long t0 = chunk * K1_CHUNK;
-  if (chunk == 0 && tid == 0) a.ctl->frame = frame;
+  if (chunk == 0 && tid == 0) {
+    a.ctl->frame = frame; a.ctl->tile_next = 0; a.ctl->vmax = 0;
+    if (a.ctl->vx_overflow) { a.ctl->vx_overflow = 0; atomicMax(&a.ctl->overflow_tag, frame + 1); }
+  }
 
   // ---- loads first (all independent): indices, then corner positions ------
   int vi[K1_TPT][3];
@@ -241,14 +289,18 @@ __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
     const long long t = t0 + tid + k * K1_THREADS;
     const bool in = t < a.n_tris;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) vi[k][c] = in ? __ldg(a.idx + 3 * t + c) : -1;
+    for (int c = 0; c < 3; ++c) {
+      vi[k][c] = in ? __ldg(a.idx + 3 * t + c) : -1;
+      if (vi[k][c] >= a.xv_cap) vi[k][c] = -1;  // overflowed frame: stay in bounds
+    }
   }
-  float4 pos[K1_TPT][3];
+  int4 cv[K1_TPT][3];
 #pragma unroll
   for (int k = 0; k < K1_TPT; ++k)
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      pos[k][c] = vi[k][c] >= 0 ? load_pos(a.verts, vi[k][c]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      cv[k][c] = vi[k][c] >= 0 ? __ldg(a.xv + vi[k][c]) : make_int4(VX_CULLED, 0, 0, 0);
+  // (a corner index of -1 reads as culled: out-of-range or past n_tris)
 
   // ---- setup, record write (coalesced: consecutive threads, consecutive t) -
   unsigned cnt[K1_TPT];
@@ -260,8 +312,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
     cnt[k] = 0;
     s_r0[l] = 0; s_r1[l] = 0;
     Tri o;
-    if (vi[k][0] < 0 ||
-        !setup_tri(pos[k][0], pos[k][1], pos[k][2], vi[k][0], vi[k][1], vi[k][2], a.M, g.W, g.H, o))
+    if (!setup_tri(cv[k][0], cv[k][1], cv[k][2], vi[k][0], vi[k][1], vi[k][2], g.W, g.H, o))
       continue;
     const int tx0 = o.px0 >> g.bw_log2, tx1 = o.px1 >> g.bw_log2;
     const int ty0 = o.py0 >> g.bh_log2, ty1 = o.py1 >> g.bh_log2;
@@ -597,20 +648,22 @@ __device__ __forceinline__ u64 eval_key(const RecView& r, int Px, int Py, int t,
   return ((u64)(__float_as_uint(z) & 0x7FFFFFFFu) << 32) | (unsigned)t;
 }
 
-// O7 shade of pixel sample (Px, Py) by triangle t (recomputes setup).
-__device__ __forceinline__ float4 shade(const float* __restrict__ verts, const int32_t* __restrict__ idx,
-                                        const Mat4& M, int W, int H, const float L[3], int t,
-                                        int Px, int Py) {
+// O7 shade of pixel sample (Px, Py) by triangle t (recomputes O2 from the
+// vertex-stage records; normals from the caller's vertex buffer).
+__device__ __forceinline__ float4 shade(const float* __restrict__ verts, const int4* __restrict__ xv,
+                                        const int32_t* __restrict__ idx, int W, int H,
+                                        const float L[3], int t, int Px, int Py) {
   Tri o;
   const int i0 = __ldg(idx + 3ll * t), i1 = __ldg(idx + 3ll * t + 1), i2 = __ldg(idx + 3ll * t + 2);
-  const float4 p0 = load_pos(verts, i0), p1 = load_pos(verts, i1), p2 = load_pos(verts, i2);
+  const int4 c0 = __ldg(xv + i0), c1 = __ldg(xv + i1), c2 = __ldg(xv + i2);
   const float4 m0 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i0 + 4));
   const float4 m1 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i1 + 4));
   const float4 m2 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i2 + 4));
-  setup_tri(p0, p1, p2, i0, i1, i2, M, W, H, o);  // live: t won a pixel
+  setup_tri(c0, c1, c2, i0, i1, i2, W, H, o);      // live: t won a pixel
+  const bool swapped = o.X1 != c1.x || o.Y1 != c1.y;  // O2 swapped corners 1 and 2?
   const float4 n0 = m0;
-  const float4 n1 = (o.v1 == i1) ? m1 : m2;        // corners 1,2 swapped by O2?
-  const float4 n2 = (o.v1 == i1) ? m2 : m1;
+  const float4 n1 = swapped ? m2 : m1;
+  const float4 n2 = swapped ? m1 : m2;
   const long long w0 = (long long)(o.X2 - o.X1) * (Py - o.Y1) - (long long)(o.Y2 - o.Y1) * (Px - o.X1);
   const long long w1 = (long long)(o.X0 - o.X2) * (Py - o.Y2) - (long long)(o.Y0 - o.Y2) * (Px - o.X2);
   const long long w2 = (long long)(o.X1 - o.X0) * (Py - o.Y0) - (long long)(o.Y1 - o.Y0) * (Px - o.X0);
@@ -657,18 +710,12 @@ __global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
   TileSmem<BW, BH, THREADS>& sm = *reinterpret_cast<TileSmem<BW, BH, THREADS>*>(smem_raw);
   unsigned* s_cov = reinterpret_cast<unsigned*>(smem_raw + sizeof(TileSmem<BW, BH, THREADS>));
   __shared__ int s_qn;
+  __shared__ int s_job[2];  // [0] = current bin index in the owned list, [1] = prefetched next
 
   const int tid = threadIdx.x;
   const Grid g = a.g;
-#pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    const int p = tid + k * THREADS;
-    if (p < NPX) {
-      sm.key[p] = CLEAR_KEY;
-      if (COV) s_cov[p] = 0;
-    }
-  }
-  if (tid == 0) s_qn = 0;
+  float L[3];
+  normalise_light(a.light, L);
   pdl_wait();
   pdl_trigger();
   const u64 frame = a.ctl->frame;
@@ -681,120 +728,142 @@ __global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
       a.bin_start[1] = (int32_t)a.ctl->n_pairs;
     }
   }
-  if ((int)blockIdx.x >= a.owned) return;
-  const int b = g.rank + blockIdx.x * g.nranks;  // owned bin (DirectMap across ranks)
-  const int bx = b % g.binsX, by = b / g.binsX;
-  const int x0 = bx * BW, y0 = by * BH;
-  const int x1 = min(x0 + BW, g.W) - 1, y1 = min(y0 + BH, g.H) - 1;
   const bool ovf = a.ctl->overflow_tag == frame + 1;
-
-  int s = 0, e = 0;
-  if (!ovf) {
-    if (a.npass == 0) { s = 0; e = (int)a.ctl->n_pairs; }
-    else { s = a.bin_start[b]; e = a.bin_start[b + 1]; }
+  if (tid == 0) {
+    s_job[0] = (int)atomicAdd(&a.ctl->tile_next, 1u);
+    s_job[1] = (int)atomicAdd(&a.ctl->tile_next, 1u);
   }
-  const int nbatch = (e - s + THREADS - 1) / THREADS;
-  // software pipeline: primIDs two batches ahead, records one batch ahead
-  int t_cur = (s + tid < e) ? a.bin_prims[s + tid] : -1;
-  int t_next = (s + THREADS + tid < e) ? a.bin_prims[s + THREADS + tid] : -1;
-  if (t_cur >= 0) {
-    const int4* rp = a.rec + 3ll * t_cur;
-    cp_async16(&sm.rec[0][tid][0], rp); cp_async16(&sm.rec[0][tid][1], rp + 1);
-    cp_async16(&sm.rec[0][tid][2], rp + 2);
-  }
-  cp_async_commit();
-  for (int k = 0; k < nbatch; ++k) {
-    const int buf = k & 1;
-    if (t_next >= 0) {
-      const int4* rp = a.rec + 3ll * t_next;
-      cp_async16(&sm.rec[buf ^ 1][tid][0], rp); cp_async16(&sm.rec[buf ^ 1][tid][1], rp + 1);
-      cp_async16(&sm.rec[buf ^ 1][tid][2], rp + 2);
-    }
-    cp_async_commit();
-    const int i2 = s + (k + 2) * THREADS + tid;
-    const int t_after = (i2 < e) ? a.bin_prims[i2] : -1;
-    cp_async_wait<1>();
-    __syncthreads();
-    if (t_cur >= 0) {
-      const RecView r = unpack(sm.rec[buf][tid][0], sm.rec[buf][tid][1], sm.rec[buf][tid][2]);
-      const int rx0 = max(r.px0, x0), rx1 = min(r.px1, x1);
-      const int ry0 = max(r.py0, y0), ry1 = min(r.py1, y1);
-      const int area = (rx1 - rx0 + 1) * (ry1 - ry0 + 1);
-      if (area <= SMALL_AREA) {
-        for (int y = ry0; y <= ry1; ++y) {
-          const int Py = 256 * y + 128;
-          for (int x = rx0; x <= rx1; ++x) {
-            bool cov;
-            const u64 key = eval_key(r, 256 * x + 128, Py, t_cur, cov);
-            const int p = (y - y0) * BW + (x - x0);
-            if (COV && cov) atomicAdd(&s_cov[p], 1u);
-            if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
-          }
-        }
-      } else {
-        const int slot = atomicAdd(&s_qn, 1);
-        sm.big[slot] = (unsigned short)tid;
-        sm.bigt[slot] = t_cur;
-      }
-    }
-    __syncthreads();
-    const int nq = s_qn;
-    for (int q = 0; q < nq; ++q) {
-      const int src = sm.big[q];
-      const RecView r = unpack(sm.rec[buf][src][0], sm.rec[buf][src][1], sm.rec[buf][src][2]);
-      const int t = sm.bigt[q];
-#pragma unroll
-      for (int j = 0; j < PPT; ++j) {
-        const int p = tid + j * THREADS;
-        if (p >= NPX) continue;
-        const int x = x0 + (p % BW), y = y0 + (p / BW);
-        if (x < r.px0 || x > r.px1 || y < r.py0 || y > r.py1) continue;
-        bool cov;
-        const u64 key = eval_key(r, 256 * x + 128, 256 * y + 128, t, cov);
-        if (COV && cov) s_cov[p] += 1u;
-        if (key < sm.key[p]) sm.key[p] = key;
-      }
-    }
-    __syncthreads();
-    if (tid == 0) s_qn = 0;
-    t_cur = t_next;
-    t_next = t_after;
-  }
-  cp_async_wait<0>();
+  if (tid == 0) s_qn = 0;
   __syncthreads();
 
-  // ---- write-back ------------------------------------------------------------
-  if (KEYS_ONLY) {
-    u64* dst = a.tile_keys + (size_t)blockIdx.x * NPX;
+  // LoadBalance schedule: CTAs pull owned bins from a queue
+  for (;;) {
+    const int job = s_job[0];
+    if (job >= a.owned) break;
+    const int b = g.rank + job * g.nranks;  // owned bin (DirectMap across ranks)
+    const int bx = b % g.binsX, by = b / g.binsX;
+    const int x0 = bx * BW, y0 = by * BH;
+    const int x1 = min(x0 + BW, g.W) - 1, y1 = min(y0 + BH, g.H) - 1;
+    int s = 0, e = 0;
+    if (!ovf) {
+      if (a.npass == 0) { s = 0; e = (int)a.ctl->n_pairs; }
+      else { s = a.bin_start[b]; e = a.bin_start[b + 1]; }
+    }
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int p = tid + k * THREADS;
-      if (p < NPX) dst[p] = sm.key[p];
+      if (p < NPX) {
+        sm.key[p] = CLEAR_KEY;
+        if (COV) s_cov[p] = 0;
+      }
     }
-    return;
-  }
-  float L[3];
-  normalise_light(a.light, L);
+    const int nbatch = (e - s + THREADS - 1) / THREADS;
+    // software pipeline: primIDs two batches ahead, records one batch ahead
+    int t_cur = (s + tid < e) ? a.bin_prims[s + tid] : -1;
+    int t_next = (s + THREADS + tid < e) ? a.bin_prims[s + THREADS + tid] : -1;
+    if (t_cur >= 0) {
+      const int4* rp = a.rec + 3ll * t_cur;
+      cp_async16(&sm.rec[0][tid][0], rp); cp_async16(&sm.rec[0][tid][1], rp + 1);
+      cp_async16(&sm.rec[0][tid][2], rp + 2);
+    }
+    cp_async_commit();
+    for (int k = 0; k < nbatch; ++k) {
+      const int buf = k & 1;
+      if (t_next >= 0) {
+        const int4* rp = a.rec + 3ll * t_next;
+        cp_async16(&sm.rec[buf ^ 1][tid][0], rp); cp_async16(&sm.rec[buf ^ 1][tid][1], rp + 1);
+        cp_async16(&sm.rec[buf ^ 1][tid][2], rp + 2);
+      }
+      cp_async_commit();
+      const int i2 = s + (k + 2) * THREADS + tid;
+      const int t_after = (i2 < e) ? a.bin_prims[i2] : -1;
+      cp_async_wait<1>();
+      __syncthreads();
+      if (t_cur >= 0) {
+        const RecView r = unpack(sm.rec[buf][tid][0], sm.rec[buf][tid][1], sm.rec[buf][tid][2]);
+        const int rx0 = max(r.px0, x0), rx1 = min(r.px1, x1);
+        const int ry0 = max(r.py0, y0), ry1 = min(r.py1, y1);
+        const int area = (rx1 - rx0 + 1) * (ry1 - ry0 + 1);
+        if (area <= SMALL_AREA) {
+          for (int y = ry0; y <= ry1; ++y) {
+            const int Py = 256 * y + 128;
+            for (int x = rx0; x <= rx1; ++x) {
+              bool cov;
+              const u64 key = eval_key(r, 256 * x + 128, Py, t_cur, cov);
+              const int p = (y - y0) * BW + (x - x0);
+              if (COV && cov) atomicAdd(&s_cov[p], 1u);
+              if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
+            }
+          }
+        } else {
+          const int slot = atomicAdd(&s_qn, 1);
+          sm.big[slot] = (unsigned short)tid;
+          sm.bigt[slot] = t_cur;
+        }
+      }
+      __syncthreads();
+      const int nq = s_qn;
+      for (int q = 0; q < nq; ++q) {
+        const int src = sm.big[q];
+        const RecView r = unpack(sm.rec[buf][src][0], sm.rec[buf][src][1], sm.rec[buf][src][2]);
+        const int t = sm.bigt[q];
 #pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    const int p = tid + k * THREADS;
-    if (p >= NPX) continue;
-    const int x = x0 + (p % BW), y = y0 + (p / BW);
-    if (x > x1 || y > y1) continue;
-    const u64 key = sm.key[p];
-    const size_t o = (size_t)y * g.W + x;
-    float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-    float depth = 1.0f;
-    int prim = -1;
-    if (key != CLEAR_KEY) {
-      prim = (int)(unsigned)(key & 0xFFFFFFFFu);
-      depth = __uint_as_float((unsigned)(key >> 32));
-      c = shade(a.verts, a.idx, a.M, g.W, g.H, L, prim, 256 * x + 128, 256 * y + 128);
+        for (int j = 0; j < PPT; ++j) {
+          const int p = tid + j * THREADS;
+          if (p >= NPX) continue;
+          const int x = x0 + (p % BW), y = y0 + (p / BW);
+          if (x < r.px0 || x > r.px1 || y < r.py0 || y > r.py1) continue;
+          bool cov;
+          const u64 key = eval_key(r, 256 * x + 128, 256 * y + 128, t, cov);
+          if (COV && cov) s_cov[p] += 1u;
+          if (key < sm.key[p]) sm.key[p] = key;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) s_qn = 0;
+      t_cur = t_next;
+      t_next = t_after;
     }
-    reinterpret_cast<float4*>(a.out_rgba)[o] = c;
-    a.out_depth[o] = depth;
-    a.out_primid[o] = prim;
-    if (COV) a.out_cov[o] = s_cov[p];
+    cp_async_wait<0>();
+    __syncthreads();
+    // next job (prefetched one bin ahead)
+    if (tid == 0) {
+      s_job[0] = s_job[1];
+      s_job[1] = (int)atomicAdd(&a.ctl->tile_next, 1u);
+    }
+
+    // ---- write-back ----------------------------------------------------------
+    if (KEYS_ONLY) {
+      u64* dst = a.tile_keys + (size_t)job * NPX;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int p = tid + k * THREADS;
+        if (p < NPX) dst[p] = sm.key[p];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int p = tid + k * THREADS;
+        if (p >= NPX) continue;
+        const int x = x0 + (p % BW), y = y0 + (p / BW);
+        if (x > x1 || y > y1) continue;
+        const u64 key = sm.key[p];
+        const size_t o = (size_t)y * g.W + x;
+        float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+        float depth = 1.0f;
+        int prim = -1;
+        if (key != CLEAR_KEY) {
+          prim = (int)(unsigned)(key & 0xFFFFFFFFu);
+          depth = __uint_as_float((unsigned)(key >> 32));
+          c = shade(a.verts, a.xv, a.idx, g.W, g.H, L, prim, 256 * x + 128, 256 * y + 128);
+        }
+        reinterpret_cast<float4*>(a.out_rgba)[o] = c;
+        a.out_depth[o] = depth;
+        a.out_primid[o] = prim;
+        if (COV) a.out_cov[o] = s_cov[p];
+      }
+    }
+    __syncthreads();  // keys / s_job consumed before the next bin reinitialises them
   }
 }
 
@@ -820,7 +889,7 @@ __global__ void __launch_bounds__(256) k_resolve(ResolveArgs a) {
   if (key != CLEAR_KEY) {
     prim = (int)(unsigned)(key & 0xFFFFFFFFu);
     depth = __uint_as_float((unsigned)(key >> 32));
-    c = shade(a.verts, a.idx, a.M, g.W, g.H, L, prim, 256 * x + 128, 256 * y + 128);
+    c = shade(a.verts, a.xv, a.idx, g.W, g.H, L, prim, 256 * x + 128, 256 * y + 128);
   }
   reinterpret_cast<float4*>(a.out_rgba)[o] = c;
   a.out_depth[o] = depth;
@@ -830,9 +899,9 @@ __global__ void __launch_bounds__(256) k_resolve(ResolveArgs a) {
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-template <typename Kern, typename Arg>
+template <typename Kern, typename... Args>
 static cudaError_t launch_ex(Kern kern, int grid, int threads, size_t smem, bool pdl,
-                             cudaStream_t s, const Arg& a) {
+                             cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
@@ -843,9 +912,30 @@ static cudaError_t launch_ex(Kern kern, int grid, int threads, size_t smem, bool
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, a);
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s) {
+  // known count: one thread per vertex; unknown (device-side count): persistent
+  const long long want = a.n_verts >= 0 ? (a.n_verts + VX_THREADS - 1) / VX_THREADS : 8ll * sm_count();
+  return launch_ex(k_vertex, (int)(want > 0 ? want : 1), VX_THREADS, 0, pdl, s, a);
+}
+
+cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool pdl, cudaStream_t s) {
+  const long long want = std::min<long long>((n / 4 + 255) / 256, 8ll * sm_count());
+  return launch_ex(k_index_max, (int)(want > 0 ? want : 1), 256, 0, pdl, s, idx, n, ctl);
+}
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s) {
   return launch_ex(k_setup, grid, K1_THREADS, 0, pdl, s, a);
 }
@@ -853,32 +943,55 @@ cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream
   return launch_ex(k_radix_pass, grid, RX_THREADS, 0, pdl, s, a);
 }
 
+struct TileKernel {
+  void (*fn)(TileArgs) = nullptr;
+  int threads = 0;
+  size_t smem = 0;
+};
+
 template <int BW, int BH>
-static cudaError_t launch_tile_t(const TileArgs& a, int grid, bool cov, bool keys_only, bool pdl,
-                                 cudaStream_t s) {
+static TileKernel tile_kernel_t(bool cov, bool keys_only) {
   constexpr int NPX = BW * BH;
   constexpr int THREADS = NPX < 256 ? NPX : 256;
-  const size_t smem = sizeof(TileSmem<BW, BH, THREADS>) + (cov ? (size_t)NPX * 4 : 0);
-  auto run = [&](auto kern) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return launch_ex(kern, grid, THREADS, smem, pdl, s, a);
-  };
-  if (keys_only) return cov ? run(k_tile<BW, BH, THREADS, true, true>) : run(k_tile<BW, BH, THREADS, false, true>);
-  return cov ? run(k_tile<BW, BH, THREADS, true, false>) : run(k_tile<BW, BH, THREADS, false, false>);
+  TileKernel k;
+  k.threads = THREADS;
+  k.smem = sizeof(TileSmem<BW, BH, THREADS>) + (cov ? (size_t)NPX * 4 : 0);
+  if (keys_only) k.fn = cov ? k_tile<BW, BH, THREADS, true, true> : k_tile<BW, BH, THREADS, false, true>;
+  else k.fn = cov ? k_tile<BW, BH, THREADS, true, false> : k_tile<BW, BH, THREADS, false, false>;
+  return k;
 }
 
 #define PIKO_TILE_CASE(W_, H_) \
-  if (bw == W_ && bh == H_) return launch_tile_t<W_, H_>(a, grid, cov, keys_only, pdl, s);
+  if (bw == W_ && bh == H_) return tile_kernel_t<W_, H_>(cov, keys_only);
 
-cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
-                        bool pdl, cudaStream_t s) {
-  if (grid <= 0) return cudaSuccess;
+static TileKernel tile_kernel(int bw, int bh, bool cov, bool keys_only) {
   PIKO_TILE_CASE(8, 8) PIKO_TILE_CASE(8, 16) PIKO_TILE_CASE(8, 32) PIKO_TILE_CASE(8, 64)
   PIKO_TILE_CASE(16, 8) PIKO_TILE_CASE(16, 16) PIKO_TILE_CASE(16, 32) PIKO_TILE_CASE(16, 64)
   PIKO_TILE_CASE(32, 8) PIKO_TILE_CASE(32, 16) PIKO_TILE_CASE(32, 32) PIKO_TILE_CASE(32, 64)
   PIKO_TILE_CASE(64, 8) PIKO_TILE_CASE(64, 16) PIKO_TILE_CASE(64, 32) PIKO_TILE_CASE(64, 64)
-  return cudaErrorInvalidValue;
+  return TileKernel{};
+}
+
+cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
+                        bool pdl, cudaStream_t s) {
+  const TileKernel k = tile_kernel(bw, bh, cov, keys_only);
+  if (!k.fn) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem);
+  if (e != cudaSuccess) return e;
+  return launch_ex(k.fn, grid, k.threads, k.smem, pdl, s, a);
+}
+
+// persistent grid: all CTAs resident at once (the queue needs no more)
+int tile_grid(int bw, int bh, bool cov, bool keys_only) {
+  const TileKernel k = tile_kernel(bw, bh, cov, keys_only);
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (k.fn) {
+    cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.threads, k.smem);
+  }
+  return sms * (occ > 0 ? occ : 1);
 }
 
 cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s) {

@@ -75,6 +75,7 @@ struct piko_ctx {
 
   // scratch
   int4* rec = nullptr; long long rec_cap = 0;
+  int4* xv = nullptr; long long xv_cap = 0;   // vertex-stage records
   uint32_t* keys[2] = {nullptr, nullptr};
   int32_t* vals[2] = {nullptr, nullptr};
   unsigned long long pair_cap = 0;
@@ -199,7 +200,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
-  void* bufs[] = {ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
+  void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
                   ctx->bin_start, ctx->ctl, ctx->st_k1, ctx->st_scan, ctx->st_rx, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
                   ctx->all_keys};
@@ -256,6 +257,17 @@ static int ensure_pairs(piko_ctx* ctx, unsigned long long P) {
   return PIKO_OK;
 }
 
+// xv capacity for V vertices (V < 0: unknown; sized from an upper bound)
+static int ensure_verts(piko_ctx* ctx, long long V) {
+  if (V > ctx->xv_cap) {
+    if (ctx->xv) cudaFree(ctx->xv);
+    ctx->xv = nullptr;
+    CK(cudaMalloc(&ctx->xv, sizeof(int4) * std::max<long long>(V, 1024)));
+    ctx->xv_cap = std::max<long long>(V, 1024);
+  }
+  return PIKO_OK;
+}
+
 static int ensure_cov(piko_ctx* ctx) {
   if ((ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) && !ctx->cov)
     CK(cudaMalloc(&ctx->cov, sizeof(uint32_t) * (size_t)ctx->g.W * ctx->g.H));
@@ -263,8 +275,8 @@ static int ensure_cov(piko_ctx* ctx) {
 }
 
 // ---- one frame ---------------------------------------------------------------
-static int enqueue_frame(piko_ctx* ctx, const float* verts, const int32_t* idx, long long T,
-                         const Mat4& M, const float L[3], float* rgba, float* depth,
+static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
+                         long long T, const Mat4& M, const float L[3], float* rgba, float* depth,
                          cudaStream_t s) {
   const bool gather = ctx->comm != nullptr && ctx->g.nranks > 1;
   cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
@@ -287,15 +299,23 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, const int32_t* idx, 
     ctx->need_reset = false;
   }
   CK(mark(1 + PIKO_STAGE_CLEAR));
+  if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
+  {
+    VertexArgs a{};
+    a.verts = verts; a.n_verts = T > 0 ? V : 0; a.cap = ctx->xv_cap; a.ctl = ctx->ctl; a.M = M;
+    a.W = ctx->g.W; a.H = ctx->g.H; a.xv = ctx->xv;
+    CK(launch_vertex(a, ctx->pdl, s));
+  }
+  CK(mark(1 + PIKO_STAGE_VERTEX));
   {
     SetupArgs a{};
-    a.verts = verts; a.idx = idx; a.n_tris = T; a.M = M; a.g = ctx->g; a.npass = ctx->npass;
+    a.xv = ctx->xv; a.xv_cap = ctx->xv_cap; a.idx = idx; a.n_tris = T; a.g = ctx->g;
+    a.npass = ctx->npass;
     a.rec = ctx->rec; a.pair_keys = ctx->keys[0]; a.pair_vals = ctx->vals[0];
     a.bin_count = ctx->bin_count; a.status = ctx->st_k1; a.ctl = ctx->ctl; a.cap = ctx->pair_cap;
     CK(launch_setup(a, (int)g1, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_SETUP));
-  CK(mark(1 + PIKO_STAGE_BINSCAN));  // the bin scan runs inside radix pass 0
   for (int p = 0; p < ctx->npass; ++p) {
     RadixArgs a{};
     a.keys_in = ctx->keys[p & 1]; a.vals_in = ctx->vals[p & 1];
@@ -310,7 +330,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, const int32_t* idx, 
   CK(mark(1 + PIKO_STAGE_RADIX));
   {
     TileArgs a{};
-    a.verts = verts; a.idx = idx; a.M = M;
+    a.verts = verts; a.xv = ctx->xv; a.idx = idx;
     a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
     a.g = ctx->g; a.npass = ctx->npass; a.rec = ctx->rec; a.bin_start = ctx->bin_start;
     a.bin_prims = ctx->vals[ctx->npass & 1]; a.ctl = ctx->ctl;
@@ -318,8 +338,8 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, const int32_t* idx, 
     a.out_cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
     a.tile_keys = gather ? ctx->tile_keys : nullptr;
     a.owned = ctx->owned;
-    CK(launch_tile(a, ctx->bw, ctx->bh, std::max(ctx->owned, 1), a.out_cov != nullptr, gather,
-                   ctx->pdl, s));
+    const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, gather)));
+    CK(launch_tile(a, ctx->bw, ctx->bh, grid, a.out_cov != nullptr, gather, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_TILE));
   if (gather) {
@@ -346,7 +366,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, const int32_t* idx, 
     CK(mark(1 + PIKO_STAGE_GATHER));
     if (ctx->g.rank == 0) {
       ResolveArgs a{};
-      a.verts = verts; a.idx = idx; a.M = M;
+      a.verts = verts; a.xv = ctx->xv; a.idx = idx;
       a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
       a.g = ctx->g; a.all_keys = ctx->all_keys; a.owned_max = ctx->owned_max;
       a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
@@ -370,7 +390,8 @@ static int check_frame(piko_ctx* ctx) {
   ctx->pending = false;
   CK(cudaEventSynchronize(ctx->done));
   if (ctx->h_ctl->overflow_tag == ctx->h_ctl->frame + 1) {
-    const int rc = ensure_pairs(ctx, ctx->h_ctl->n_pairs);
+    int rc = ensure_pairs(ctx, ctx->h_ctl->n_pairs);
+    if (rc == PIKO_OK) rc = ensure_verts(ctx, (long long)ctx->h_ctl->vx_need);
     ctx->last_status = rc != PIKO_OK ? rc : PIKO_ECAPACITY;
     if (rc == PIKO_OK) ctx->fail(PIKO_ECAPACITY, "pair capacity exceeded (P=%llu); grown", ctx->h_ctl->n_pairs);
     return ctx->last_status;
@@ -405,9 +426,9 @@ static int validate_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, 
   return PIKO_OK;
 }
 
-static int draw_impl(piko_ctx* ctx, const float* verts, const int32_t* idx, int32_t n_tris,
-                     const float mvp[16], const float light[3], float* rgba, float* depth,
-                     cudaStream_t s, bool force_check) {
+static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
+                     int32_t n_tris, const float mvp[16], const float light[3], float* rgba,
+                     float* depth, cudaStream_t s, bool force_check) {
   float L[3] = {0.0f, 0.0f, 0.0f};
   int rc = validate_draw(ctx, verts, idx, n_tris, mvp, light, rgba, depth, L);
   if (rc != PIKO_OK) return rc;
@@ -419,11 +440,14 @@ static int draw_impl(piko_ctx* ctx, const float* verts, const int32_t* idx, int3
   Mat4 M;
   memcpy(M.m, mvp, sizeof M.m);
   if ((rc = ensure_tris(ctx, n_tris)) != PIKO_OK) return rc;
+  // without a vertex count the device derives max(idx)+1; start at 3 n_tris
+  // (every corner distinct) and grow on a reported vertex overflow
+  if ((rc = ensure_verts(ctx, V >= 0 ? V : 3ll * n_tris)) != PIKO_OK) return rc;
   if ((rc = ensure_pairs(ctx, std::max<unsigned long long>(ctx->pair_cap, 2ull * n_tris + 4096))) != PIKO_OK)
     return rc;
   if ((rc = ensure_cov(ctx)) != PIKO_OK) return rc;
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if ((rc = enqueue_frame(ctx, verts, idx, n_tris, M, L, rgba, depth, s)) != PIKO_OK)
+    if ((rc = enqueue_frame(ctx, verts, V, idx, n_tris, M, L, rgba, depth, s)) != PIKO_OK)
       return frame_failed(ctx, rc);
     if (ctx->sync_mode == PIKO_SYNC_ASYNC && !force_check) return prev == PIKO_ECAPACITY ? PIKO_OK : prev;
     rc = check_frame(ctx);
@@ -440,7 +464,17 @@ extern "C" int piko_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, 
                          const float mvp[16], const float light[3], float* out_rgba,
                          float* out_depth, void* stream) {
   if (!ctx) return PIKO_EINVAL;
-  return draw_impl(ctx, verts, idx, n_tris, mvp, light, out_rgba, out_depth,
+  return draw_impl(ctx, verts, -1, idx, n_tris, mvp, light, out_rgba, out_depth,
+                   static_cast<cudaStream_t>(stream), false);
+}
+
+extern "C" int piko_draw_indexed(piko_ctx* ctx, const float* verts, int64_t n_verts,
+                                 const int32_t* idx, int32_t n_tris, const float mvp[16],
+                                 const float light[3], float* out_rgba, float* out_depth,
+                                 void* stream) {
+  if (!ctx) return PIKO_EINVAL;
+  if (n_verts < 0 || (n_tris > 0 && n_verts < 1)) return ctx->fail(PIKO_EINVAL, "bad n_verts");
+  return draw_impl(ctx, verts, n_verts, idx, n_tris, mvp, light, out_rgba, out_depth,
                    static_cast<cudaStream_t>(stream), false);
 }
 
@@ -474,7 +508,8 @@ extern "C" int piko_draw_host(piko_ctx* ctx, const float* h_verts, int64_t n_ver
     CK(cudaMemcpyAsync(ctx->d_verts, h_verts, sizeof(float) * 8 * n_verts, cudaMemcpyHostToDevice, s));
   if (n_tris > 0)
     CK(cudaMemcpyAsync(ctx->d_idx, h_idx, sizeof(int32_t) * 3 * (size_t)n_tris, cudaMemcpyHostToDevice, s));
-  int rc = draw_impl(ctx, ctx->d_verts, ctx->d_idx, n_tris, mvp, light, ctx->d_rgba, ctx->d_depth, s, true);
+  int rc = draw_impl(ctx, ctx->d_verts, n_verts, ctx->d_idx, n_tris, mvp, light, ctx->d_rgba,
+                     ctx->d_depth, s, true);
   if (rc != PIKO_OK) return rc;
   const bool has_out = !(ctx->comm && ctx->g.nranks > 1 && ctx->g.rank != 0);
   if (has_out) {

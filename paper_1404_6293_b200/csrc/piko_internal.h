@@ -35,6 +35,10 @@ struct Control {
   unsigned long long k1_ticket;
   unsigned long long rx_ticket[MAX_PASSES];
   unsigned long long frame;            // written by K1 chunk 0
+  unsigned int tile_next;              // dynamic bin queue of k_tile (reset by K1 chunk 0)
+  unsigned int vmax;                   // max(idx)+1 from k_index_max (zeroed by K1 chunk 0)
+  unsigned int vx_overflow;            // k_vertex: vmax > xv capacity (K1 turns it into overflow_tag)
+  unsigned long long vx_need;          // vertex count the last frame needed
   unsigned long long n_pairs;          // P, written by K1's last chunk
   unsigned long long overflow_tag;     // frame+1 of the last frame whose P > capacity
   unsigned long long n_live[2];        // parity double buffer (statistics)
@@ -60,11 +64,26 @@ struct Grid {
 // flags bit 0: bbox extent < 2^15 subpixels in x and y -> int32 edge path.
 constexpr int REC_SMALL = 1;
 
-struct SetupArgs {
+// Vertex stage output, one per vertex (16 B): snapped X, Y (subpixels),
+// bits(zw), bits(rw); X == VX_CULLED marks a corner that culls its triangles.
+constexpr int VX_CULLED = (int)0x80000000;
+constexpr int VX_THREADS = 256;
+
+struct VertexArgs {
   const float* verts;
+  long long n_verts;            // < 0: read ctl->vmax (piko_draw without a count)
+  long long cap;                // xv capacity
+  Control* ctl;
+  Mat4 M;
+  int W, H;
+  int4* xv;                     // [n_verts] transformed vertices
+};
+
+struct SetupArgs {
+  const int4* xv;               // transformed vertices
+  long long xv_cap;             // corners with idx >= xv_cap are culled (overflowed frame)
   const int32_t* idx;
   long long n_tris;
-  Mat4 M;
   Grid g;
   int npass;
   int4* rec;                    // [n_tris][3]
@@ -94,8 +113,8 @@ struct RadixArgs {
 
 struct TileArgs {
   const float* verts;
+  const int4* xv;
   const int32_t* idx;
-  Mat4 M;
   float light[3];
   Grid g;
   int npass;
@@ -113,8 +132,8 @@ struct TileArgs {
 
 struct ResolveArgs {            // rank 0 after the NCCL gather
   const float* verts;
+  const int4* xv;
   const int32_t* idx;
-  Mat4 M;
   float light[3];
   Grid g;
   const unsigned long long* all_keys;  // [nranks][owned_max][bw*bh]
@@ -125,10 +144,13 @@ struct ResolveArgs {            // rank 0 after the NCCL gather
 };
 
 // ---- launchers (kernels.cu); pdl = programmatic dependent launch -----------
+cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool pdl, cudaStream_t s);
+cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s);
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s);
 cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream_t s);
 cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
                         bool pdl, cudaStream_t s);
+int tile_grid(int bw, int bh, bool cov, bool keys_only);  // persistent grid size
 cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s);
 
 }  // namespace piko

@@ -27,7 +27,7 @@ def env(oracle_lib):
     return piko, oracle_lib, torch
 
 
-def gpu_render(env, s, bw, bh=None, cov=True, partition=None, sync=None):
+def gpu_render(env, s, bw, bh=None, cov=True, partition=None, sync=None, indexed=True):
     piko, _, torch = env
     bh = bw if bh is None else bh
     dev = torch.device("cuda:0")
@@ -42,7 +42,7 @@ def gpu_render(env, s, bw, bh=None, cov=True, partition=None, sync=None):
         r.depth.fill_(float("nan"))
     if sync is not None:
         piko.piko_set_sync(r.ctx, sync)
-    r.draw(verts, idx, s.mvp, s.light)
+    r.draw(verts, idx, s.mvp, s.light, indexed=indexed)
     torch.cuda.synchronize()
     out = {"rgba": r.rgba.cpu().numpy(), "depth": r.depth.cpu().numpy(),
            "primid": r.primid().cpu().numpy()}
@@ -128,6 +128,30 @@ def test_capacity_overflow_regrows(env):
     assert got["stats"]["n_pairs"] == 12 * 128 * 96
     assert_frame_equal(got, oracle_frame(env, s))
     assert_bins_equal(got, env, s, 8)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_north_star_piko_draw_without_vertex_count(env, name):
+    """piko_draw (no n_verts; derived on device as max(idx)+1) == oracle."""
+    s = scenes.make(name)
+    got = gpu_render(env, s, 16, indexed=False)
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, 16)
+
+
+def test_sparse_indices_vertex_overflow_regrows(env):
+    """piko_draw with indices far beyond 3*n_tris: the vertex-stage capacity
+    overflows, grows and the frame is re-issued; still exact."""
+    s = scenes.scene_soup(50, 128, 96, seed=61, name="sparse")
+    V = 200000
+    verts = np.zeros((V, 8), np.float32)
+    rng = np.random.default_rng(62)
+    far = rng.choice(np.arange(1000, V), size=s.verts.shape[0], replace=False)
+    verts[far] = s.verts
+    sp = scenes.Scene("sparse", s.W, s.H, (16,), verts, far[s.idx].astype(np.int32), s.mvp)
+    got = gpu_render(env, sp, 16, indexed=False)
+    assert_frame_equal(got, oracle_frame(env, sp))
+    assert_bins_equal(got, env, sp, 16)
 
 
 def test_empty_and_all_culled(env):
