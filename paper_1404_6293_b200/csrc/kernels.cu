@@ -8,7 +8,7 @@
 //                ("Vertex Shader"; P:684 AssignToBoundingBox;
 //                 P:1081-1084 prefix sums "while maintaining primitive order")
 //   k_radix_pass One stable LSD pass (8-bit digit) of the pairs by bin id: warp
-//                match-any ranking, per-digit decoupled look-back (8 chunks per
+//                match-any ranking, per-digit decoupled look-back (16 chunks per
 //                probe), shared-memory staged scatter.  Pass 0 also runs the
 //                exclusive scan of the per-bin counts (CSR bin_start) in extra
 //                CTAs.  After the last pass the values are the CSR bin_prims,
@@ -81,28 +81,42 @@ __device__ __forceinline__ u64 lb_val(u64 s) { return s & ((1ull << 42) - 1); }
 __device__ __forceinline__ unsigned frame_tag(u64 frame) { return (unsigned)((frame + 1) & 0xFFFFFu); }
 
 // Decoupled look-back (one full warp): publish this chunk's aggregate, sum the
-// predecessors back to the nearest inclusive prefix, 32 per probe; publish the
-// inclusive prefix.  Returns the exclusive prefix.
+// predecessors back to the nearest inclusive prefix, 128 per probe (4 per lane,
+// lane-major: entry q = hi - 32*j - lane); publish the inclusive prefix.
+// Returns the exclusive prefix.
 __device__ u64 lookback_warp(u64* status, long long chunk, u64 agg, unsigned tag, int lane) {
   if (lane == 0) st_release64(&status[chunk], lb_pack(tag, chunk == 0 ? LB_INC : LB_AGG, agg));
   if (chunk == 0) return 0;
   u64 excl = 0;
   long long hi = chunk - 1;
   for (;;) {
-    const long long i = hi - lane;
-    const u64 s = (i >= 0) ? ld_acquire64(&status[i]) : lb_pack(tag, LB_INC, 0);
-    const bool ready = lb_tag(s) == tag;
-    const unsigned inc = __ballot_sync(0xffffffffu, ready && lb_flag(s) == LB_INC);
-    const unsigned notready = __ballot_sync(0xffffffffu, !ready);
-    const int k = inc ? (__ffs(inc) - 1) : 32;
-    const unsigned need = (k >= 31) ? 0xffffffffu : ((2u << k) - 1u);
-    if (notready & need) continue;  // a predecessor has not published yet
-    u64 v = (lane <= k) ? lb_val(s) : 0ull;
+    u64 sv[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    excl += v;
-    if (k < 32) break;
-    hi -= 32;
+    for (int j = 0; j < 4; ++j) {
+      const long long i = hi - 32 * j - lane;
+      sv[j] = (i >= 0) ? ld_acquire64(&status[i]) : lb_pack(tag, LB_INC, 0);
+    }
+    // walk the 4 groups of 32 in order (nearest predecessors first)
+    bool retry = false, done = false;
+    u64 add = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (retry || done) continue;
+      const bool ready = lb_tag(sv[j]) == tag;
+      const unsigned inc = __ballot_sync(0xffffffffu, ready && lb_flag(sv[j]) == LB_INC);
+      const unsigned notready = __ballot_sync(0xffffffffu, !ready);
+      const int k = inc ? (__ffs(inc) - 1) : 32;
+      const unsigned need = (k >= 31) ? 0xffffffffu : ((2u << k) - 1u);
+      if (notready & need) { retry = true; continue; }  // unpublished predecessor
+      u64 v = (lane <= k) ? lb_val(sv[j]) : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      add += v;
+      hi -= 32;
+      if (k < 32) done = true;
+    }
+    excl += add;   // groups consumed before a retry stay consumed (hi advanced)
+    if (done) break;
   }
   if (lane == 0) st_release64(&status[chunk], lb_pack(tag, LB_INC, excl + agg));
   return excl;
@@ -230,9 +244,21 @@ __global__ void __launch_bounds__(VX_THREADS) k_vertex(VertexArgs a) {
     if (V > a.cap) a.ctl->vx_overflow = 1;
   }
   V = V < a.cap ? V : a.cap;
-  for (long long v = (long long)blockIdx.x * VX_THREADS + threadIdx.x; v < V;
-       v += (long long)gridDim.x * VX_THREADS)
-    a.xv[v] = transform_vertex(load_pos(a.verts, (int)v), a.M, a.W, a.H);
+  constexpr int VPT = 4;  // vertices per thread, loads issued together
+  for (long long v0 = (long long)blockIdx.x * VX_THREADS * VPT + threadIdx.x; v0 < V;
+       v0 += (long long)gridDim.x * VX_THREADS * VPT) {
+    float4 p[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const long long v = v0 + k * VX_THREADS;
+      p[k] = v < V ? load_pos(a.verts, (int)v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const long long v = v0 + k * VX_THREADS;
+      if (v < V) a.xv[v] = transform_vertex(p[k], a.M, a.W, a.H);
+    }
+  }
 }
 
 // n_verts for piko_draw (no vertex count in its signature): max(idx) + 1
@@ -257,7 +283,7 @@ __global__ void __launch_bounds__(256) k_index_max(const int32_t* __restrict__ i
 // ---------------------------------------------------------------------------
 // K1: triangle setup + count + chunk scan + pair expansion
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
+__global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
   __shared__ unsigned s_off[K1_CHUNK];   // exclusive local pair offset per triangle
   __shared__ unsigned s_r0[K1_CHUNK];    // tile rect tx0 | ty0 << 16
   __shared__ unsigned s_r1[K1_CHUNK];    // tile rect tx1 | ty1 << 16
@@ -364,50 +390,56 @@ __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) { s_off[4 * tid + j] = run; run += c4[j]; }
   }
+  __syncthreads();  // every triangle's offset is read by other warps below
+  // pair j of the chunk -> (bin, t): the triangle with the largest s_off <= j
+  auto pair_at = [&](unsigned j, int& b, int& t) {
+    int lo = 0, hi = K1_CHUNK - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= j) lo = mid; else hi = mid - 1;
+    }
+    const unsigned r0 = s_r0[lo], r1 = s_r1[lo];
+    b = owned_bin_at((int)(r0 & 0xffff), (int)(r0 >> 16), (int)(r1 & 0xffff), (int)(r1 >> 16),
+                     j - s_off[lo], g);
+    t = (int)(t0 + lo);
+  };
   if (warp == 0) {
+    // look-back (its latency is hidden behind the counting done by warps 1..7)
     const u64 ex = lookback_warp(a.status, chunk, total, tag, lane);
     if (lane == 0) {
       s_base = ex;
       if (s_live) atomicAdd(&a.ctl->n_live[frame & 1], (u64)s_live);
       if (chunk == (long long)gridDim.x - 1) a.ctl->n_pairs = ex + total;
     }
+  } else {
+    // warp-aggregated per-bin counts and radix digit histograms
+    constexpr int CW = K1_THREADS - 32;
+    for (unsigned j0 = (unsigned)(warp - 1) * 32; j0 < total; j0 += CW) {
+      const unsigned j = j0 + lane;
+      int b = -1, t = 0;
+      if (j < total) pair_at(j, b, t);
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      if (j < total && lane == __ffs(peers) - 1) {
+        const unsigned n = __popc(peers);
+        if (a.npass > 0) atomicAdd(&a.bin_count[b], n);
+        for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], n);
+      }
+    }
   }
   __syncthreads();
 
-  // ---- cooperative expansion: pair j of the chunk -> (bin, t), coalesced ----
+  // ---- expansion: coalesced writes of the pairs at the chunk's global base --
   const u64 base = s_base;
   if (base + total > a.cap) {
     if (tid == 0 && total) atomicMax(&a.ctl->overflow_tag, frame + 1);
-    return;
-  }
-  const unsigned nround = (total + K1_THREADS - 1) / K1_THREADS;
-  for (unsigned it = 0; it < nround; ++it) {
-    const unsigned j = it * K1_THREADS + tid;
-    const bool valid = j < total;
-    int b = -1, t = 0;
-    if (valid) {
-      // largest l with s_off[l] <= j (that triangle owns pair j)
-      int lo = 0, hi = K1_CHUNK - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_off[mid] <= j) lo = mid; else hi = mid - 1;
-      }
-      const unsigned r0 = s_r0[lo], r1 = s_r1[lo];
-      b = owned_bin_at((int)(r0 & 0xffff), (int)(r0 >> 16), (int)(r1 & 0xffff), (int)(r1 >> 16),
-                       j - s_off[lo], g);
-      t = (int)(t0 + lo);
+  } else {
+    for (unsigned j = tid; j < total; j += K1_THREADS) {
+      int b, t;
+      pair_at(j, b, t);
       a.pair_keys[base + j] = (uint32_t)b;
       a.pair_vals[base + j] = t;
     }
-    // warp-aggregated per-bin counts and digit histograms
-    const unsigned peers = __match_any_sync(0xffffffffu, b);
-    if (valid && lane == __ffs(peers) - 1) {
-      const unsigned n = __popc(peers);
-      if (a.npass > 0) atomicAdd(&a.bin_count[b], n);
-      for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], n);
-    }
   }
-  __syncthreads();
   for (int i = tid; i < a.npass * RX_RADIX; i += K1_THREADS) {
     const unsigned v = (&s_hist[0][0])[i];
     if (v) atomicAdd(&a.ctl->digit_hist[frame & 1][0][0] + i, v);
@@ -554,14 +586,15 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     long long c = chunk - 1;
     bool done = false;
     while (!done) {
-      u64 s[8];
+      constexpr int PROBE = 16;
+      u64 s[PROBE];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < PROBE; ++j)
         s[j] = (c - j >= 0) ? ld_relaxed64(a.status + (size_t)(c - j) * RX_RADIX + tid)
                             : lb_pack(tag, LB_INC, 0);
       int j = 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < PROBE; ++q) {
         if (done || j != q) continue;  // stop at the first unready entry
         if (lb_tag(s[q]) != tag) continue;
         excl += lb_val(s[q]);
@@ -703,14 +736,15 @@ struct TileSmem {
 };
 
 template <int BW, int BH, int THREADS, bool COV, bool KEYS_ONLY>
-__global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
+__global__ void __launch_bounds__(THREADS, THREADS >= 256 ? 3 : 8) k_tile(TileArgs a) {
   constexpr int NPX = BW * BH;
   constexpr int PPT = (NPX + THREADS - 1) / THREADS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem<BW, BH, THREADS>& sm = *reinterpret_cast<TileSmem<BW, BH, THREADS>*>(smem_raw);
   unsigned* s_cov = reinterpret_cast<unsigned*>(smem_raw + sizeof(TileSmem<BW, BH, THREADS>));
   __shared__ int s_qn;
-  __shared__ int s_job[2];  // [0] = current bin index in the owned list, [1] = prefetched next
+  __shared__ int s_job;     // current index into the owned-bin list
+  __shared__ int s_rng[2];  // its CSR range [s, e)
 
   const int tid = threadIdx.x;
   const Grid g = a.g;
@@ -729,25 +763,39 @@ __global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
     }
   }
   const bool ovf = a.ctl->overflow_tag == frame + 1;
+  // thread 0 runs a 2-deep software pipeline of queue tickets and CSR ranges,
+  // so a bin's ticket and range are in registers before the bin starts
+  auto range_of = [&](int job, int& rs, int& re) {
+    rs = re = 0;
+    if (ovf || job >= a.owned) return;
+    if (a.npass == 0) { re = (int)a.ctl->n_pairs; return; }
+    const int bb = g.rank + job * g.nranks;
+    rs = a.bin_start[bb];
+    re = a.bin_start[bb + 1];
+  };
+  int q_job = 0, q_s = 0, q_e = 0, q_next = 0;
   if (tid == 0) {
-    s_job[0] = (int)atomicAdd(&a.ctl->tile_next, 1u);
-    s_job[1] = (int)atomicAdd(&a.ctl->tile_next, 1u);
+    q_job = (int)atomicAdd(&a.ctl->tile_next, 1u);
+    q_next = (int)atomicAdd(&a.ctl->tile_next, 1u);
+    range_of(q_job, q_s, q_e);
+    s_job = q_job; s_rng[0] = q_s; s_rng[1] = q_e;
+    s_qn = 0;
   }
-  if (tid == 0) s_qn = 0;
   __syncthreads();
 
   // LoadBalance schedule: CTAs pull owned bins from a queue
   for (;;) {
-    const int job = s_job[0];
+    const int job = s_job;
     if (job >= a.owned) break;
     const int b = g.rank + job * g.nranks;  // owned bin (DirectMap across ranks)
     const int bx = b % g.binsX, by = b / g.binsX;
     const int x0 = bx * BW, y0 = by * BH;
     const int x1 = min(x0 + BW, g.W) - 1, y1 = min(y0 + BH, g.H) - 1;
-    int s = 0, e = 0;
-    if (!ovf) {
-      if (a.npass == 0) { s = 0; e = (int)a.ctl->n_pairs; }
-      else { s = a.bin_start[b]; e = a.bin_start[b + 1]; }
+    const int s = s_rng[0], e = s_rng[1];
+    if (tid == 0) {  // prefetch: next bin's ticket is q_next; fetch its range and a new ticket
+      q_job = q_next;
+      q_next = (int)atomicAdd(&a.ctl->tile_next, 1u);
+      range_of(q_job, q_s, q_e);
     }
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
@@ -826,11 +874,6 @@ __global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
     }
     cp_async_wait<0>();
     __syncthreads();
-    // next job (prefetched one bin ahead)
-    if (tid == 0) {
-      s_job[0] = s_job[1];
-      s_job[1] = (int)atomicAdd(&a.ctl->tile_next, 1u);
-    }
 
     // ---- write-back ----------------------------------------------------------
     if (KEYS_ONLY) {
@@ -863,7 +906,9 @@ __global__ void __launch_bounds__(THREADS) k_tile(TileArgs a) {
         if (COV) a.out_cov[o] = s_cov[p];
       }
     }
-    __syncthreads();  // keys / s_job consumed before the next bin reinitialises them
+    __syncthreads();  // keys consumed before the next bin reinitialises them
+    if (tid == 0) { s_job = q_job; s_rng[0] = q_s; s_rng[1] = q_e; }
+    __syncthreads();
   }
 }
 
@@ -928,7 +973,7 @@ static int sm_count() {
 
 cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s) {
   // known count: one thread per vertex; unknown (device-side count): persistent
-  const long long want = a.n_verts >= 0 ? (a.n_verts + VX_THREADS - 1) / VX_THREADS : 8ll * sm_count();
+  const long long want = a.n_verts >= 0 ? (a.n_verts + 4 * VX_THREADS - 1) / (4 * VX_THREADS) : 8ll * sm_count();
   return launch_ex(k_vertex, (int)(want > 0 ? want : 1), VX_THREADS, 0, pdl, s, a);
 }
 

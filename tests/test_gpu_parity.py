@@ -207,6 +207,33 @@ def test_determinism_byte_identical(env):
         assert a[k].tobytes() == b[k].tobytes(), k
 
 
+@pytest.mark.parametrize("bw", [8, 32])
+def test_many_frames_same_context(env, bw):
+    """Races show up as frame-to-frame differences: 12 back-to-back frames in
+    one context (async mode, no host sync between them) are all exact."""
+    piko, _, torch = env
+    s = scenes.scene_c3()
+    ref = oracle_frame(env, s, cov=False)
+    ostart, oprims = env[1].bins(s.verts, s.idx, s.mvp, s.W, s.H, bw, bw)
+    dev = torch.device("cuda:0")
+    verts = torch.from_numpy(s.verts).to(dev)
+    idx = torch.from_numpy(s.idx).to(dev)
+    r = piko.Renderer(s.W, s.H, bw, device=dev)
+    r.draw(verts, idx, s.mvp, s.light)            # checked: capacity settles
+    piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
+    outs = []
+    for k in range(12):
+        r.draw(verts, idx, s.mvp, s.light)
+        outs.append((r.rgba.clone(), r.depth.clone(), r.primid()))
+    assert piko.piko_finish(r.ctx) == piko.PIKO_OK
+    st, pr = r.bins()
+    assert np.array_equal(st.cpu().numpy(), ostart) and np.array_equal(pr.cpu().numpy(), oprims)
+    for rgba, depth, prim in outs:
+        got = {"rgba": rgba.cpu().numpy(), "depth": depth.cpu().numpy(), "primid": prim.cpu().numpy()}
+        assert_frame_equal(got, ref, cov=False)
+    r.close()
+
+
 @pytest.mark.parametrize("R", [2, 3, 4])
 def test_virtual_rank_partition(env, R):
     """Sort-first partition on one GPU: rank r writes exactly its bins
