@@ -70,6 +70,33 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// optional per-CTA phase timestamps (debug builds: -DPIKO_K1_TIMING)
+__device__ __forceinline__ u64 gtimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef PIKO_K1_TIMING
+// [kernel: 0 setup, 1 radix pass 0, 2 radix pass 1, 3 tile][slot][phase]
+__device__ u64 g_k1_times[4][8192][8];
+#define K1_MARK(i) do { if (threadIdx.x == 0 && chunk < 8192) g_k1_times[0][chunk][i] = gtimer(); } while (0)
+#define RX_MARK(i) do { if (threadIdx.x == 0 && chunk < 8192 && a.pass < 2) g_k1_times[1 + a.pass][chunk][i] = gtimer(); } while (0)
+#define TL_MARK(slot, i) do { if (threadIdx.x == 0 && (slot) < 8192) g_k1_times[3][slot][i] = gtimer(); } while (0)
+__device__ __forceinline__ void g_tl_extra(int job, int n, int cta) { g_k1_times[3][job][3] = n; g_k1_times[3][job][4] = cta; }
+#define TL_CTA(i) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_k1_times[0][7000 + blockIdx.x][i] = gtimer(); } while (0)
+}  // namespace piko
+extern "C" int piko_dbg_k1_times(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, piko::g_k1_times, bytes);
+}
+namespace piko {
+#else
+#define K1_MARK(i) do { } while (0)
+#define RX_MARK(i) do { } while (0)
+#define TL_MARK(slot, i) do { } while (0)
+#define g_tl_extra(a, b, c) do { } while (0)
+#define TL_CTA(i) do { } while (0)
+#endif
+
 // Look-back status word: tag (frame+1, 20 bits) | flag (2 bits) | value (42 bits)
 constexpr unsigned LB_AGG = 1u, LB_INC = 2u;
 __device__ __forceinline__ u64 lb_pack(unsigned tag, unsigned flag, u64 v) {
@@ -303,8 +330,11 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
   const long long chunk = (long long)(s_tk % gridDim.x);
   const unsigned tag = frame_tag(frame);
   const long long t0 = chunk * K1_CHUNK;
+  K1_MARK(0);
   if (chunk == 0 && tid == 0) {
     a.ctl->frame = frame; a.ctl->tile_next = 0; a.ctl->vmax = 0;
+    for (int k = 0; k < NLIST; ++k) a.ctl->list_n[k] = 0;
+    a.ctl->empty_next = 0;
     if (a.ctl->vx_overflow) { a.ctl->vx_overflow = 0; atomicMax(&a.ctl->overflow_tag, frame + 1); }
   }
 
@@ -328,6 +358,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
       cv[k][c] = vi[k][c] >= 0 ? __ldg(a.xv + vi[k][c]) : make_int4(VX_CULLED, 0, 0, 0);
   // (a corner index of -1 reads as culled: out-of-range or past n_tris)
 
+  K1_MARK(1);
   // ---- setup, record write (coalesced: consecutive threads, consecutive t) -
   unsigned cnt[K1_TPT];
   unsigned live = 0;
@@ -361,6 +392,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
     r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
                      o.small ? REC_SMALL : 0);
   }
+  K1_MARK(2);
   if (live) atomicAdd(&s_live, live);
 #pragma unroll
   for (int k = 0; k < K1_TPT; ++k) s_off[tid + k * K1_THREADS] = cnt[k];
@@ -391,6 +423,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
     for (int j = 0; j < 4; ++j) { s_off[4 * tid + j] = run; run += c4[j]; }
   }
   __syncthreads();  // every triangle's offset is read by other warps below
+  K1_MARK(3);
   // pair j of the chunk -> (bin, t): the triangle with the largest s_off <= j
   auto pair_at = [&](unsigned j, int& b, int& t) {
     int lo = 0, hi = K1_CHUNK - 1;
@@ -428,6 +461,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
   }
   __syncthreads();
 
+  K1_MARK(4);
   // ---- expansion: coalesced writes of the pairs at the chunk's global base --
   const u64 base = s_base;
   if (base + total > a.cap) {
@@ -444,6 +478,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
     const unsigned v = (&s_hist[0][0])[i];
     if (v) atomicAdd(&a.ctl->digit_hist[frame & 1][0][0] + i, v);
   }
+  K1_MARK(5);
 }
 
 // ---------------------------------------------------------------------------
@@ -490,6 +525,43 @@ __device__ void bin_scan_tile(const RadixArgs& a, long long tile, unsigned tag) 
     run += c[k];
   }
   if (b0 < a.NB && b0 + SCAN_ITEMS >= a.NB) a.bin_start[a.NB] = (int32_t)run;
+  // Schedule: owned bins into k_tile's work lists (warp-aggregated appends;
+  // the order inside a list does not affect the result).  Bins with more than
+  // a.frag pairs become fragments (their global key tiles are CLEAR: k_tile's
+  // last fragment resets a tile after reading it).
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+#pragma unroll 1
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    const long long b = b0 + k;
+    const bool own = b < a.NB && (a.nranks == 1 || (int)(b % a.nranks) == a.rank);
+    const unsigned cnt = own ? c[k] : 0u;
+    const unsigned nf = (own && cnt > (unsigned)a.frag) ? (cnt + a.frag - 1) / a.frag : 0u;
+    // fragments of split bins: variable-length append
+    unsigned incl = nf;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (tot) {
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(&a.ctl->list_n[0], tot);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      for (unsigned j = 0; j < nf; ++j)
+        a.frag_list[base + incl - nf + j] = make_int2((int)b, (int)j);
+    }
+    // single-fragment and empty bins
+    const int kind = !own ? 3 : (nf > 0 ? 4 : (cnt > 0 ? 1 : 2));
+    const unsigned peers = __match_any_sync(0xffffffffu, kind);
+    const int leader = __ffs(peers) - 1;
+    unsigned pos = 0;
+    if ((kind == 1 || kind == 2) && lane == leader)
+      pos = atomicAdd(&a.ctl->list_n[kind], (unsigned)__popc(peers));
+    pos = __shfl_sync(0xffffffffu, pos, leader);
+    if (kind == 1 || kind == 2)
+      a.bin_list[(size_t)(kind - 1) * a.NB + pos + __popc(peers & lanemask_lt)] = (int32_t)b;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -541,6 +613,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     return base + inc - v;
   };
 
+  RX_MARK(0);
   const u64 c0 = (u64)chunk * RX_CHUNK;
   unsigned key[RX_ITEMS];
   int val[RX_ITEMS];
@@ -554,6 +627,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     val[j] = valid ? a.vals_in[pos] : 0;
   }
   const unsigned gprefix = block_excl(a.ctl->digit_hist[frame & 1][a.pass][tid]);
+  RX_MARK(1);
 #pragma unroll
   for (int j = 0; j < RX_ITEMS; ++j) {
     const u64 pos = wb + j * 32;
@@ -605,6 +679,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     }
     st_relaxed64(st, lb_pack(tag, LB_INC, excl + tot));
   }
+  RX_MARK(3);
   const unsigned lstart = block_excl(tot);
   s_lstart[tid] = lstart;
   s_gstart[tid] = gprefix + (unsigned)excl;
@@ -629,6 +704,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     if (a.keys_out) a.keys_out[gpos] = k;
     a.vals_out[gpos] = s_vals[i];
   }
+  RX_MARK(4);
 }
 
 // ---------------------------------------------------------------------------
@@ -724,16 +800,41 @@ __device__ __forceinline__ void normalise_light(const float in[3], float L[3]) {
   L[2] = __fdiv_rn(in[2], s);
 }
 
-constexpr int SMALL_AREA = 16;  // clipped pixel-rect area handled by one thread
+constexpr int TINY_AREA = 4;    // clipped rect area a thread rasterizes alone
+constexpr int NSTAGE = 4;       // setup-record pipeline depth (rounds in flight per warp)
+constexpr int TQ = NSTAGE + 2;  // primIDs are fetched two rounds before their records
 
 template <int BW, int BH, int THREADS>
 struct TileSmem {
   static constexpr int NPX = BW * BH;
   u64 key[NPX];
-  int4 rec[2][THREADS][3];
-  unsigned short big[THREADS];
-  int bigt[THREADS];
+  int4 rec[NSTAGE][THREADS][3];
 };
+
+// Write one pixel of the frame (or the keys-only tile) from its resolved key.
+template <bool COV, bool KEYS_ONLY>
+__device__ __forceinline__ void store_pixel(const TileArgs& a, const float L[3], int job, int p,
+                                            int npx, int x, int y, u64 key, unsigned cov) {
+  if (KEYS_ONLY) {
+    a.tile_keys[(size_t)job * npx + p] = key;
+    return;
+  }
+  const size_t o = (size_t)y * a.g.W + x;
+  float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+  float depth = 1.0f;
+  int prim = -1;
+  if (key != CLEAR_KEY) {
+    prim = (int)(unsigned)(key & 0xFFFFFFFFu);
+    depth = __uint_as_float((unsigned)(key >> 32));
+#ifndef PIKO_EXP_NOSHADE
+    c = shade(a.verts, a.xv, a.idx, a.g.W, a.g.H, L, prim, 256 * x + 128, 256 * y + 128);
+#endif
+  }
+  reinterpret_cast<float4*>(a.out_rgba)[o] = c;
+  a.out_depth[o] = depth;
+  a.out_primid[o] = prim;
+  if (COV) a.out_cov[o] = cov;
+}
 
 template <int BW, int BH, int THREADS, bool COV, bool KEYS_ONLY>
 __global__ void __launch_bounds__(THREADS, THREADS >= 256 ? 3 : 8) k_tile(TileArgs a) {
@@ -742,61 +843,95 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 256 ? 3 : 8) k_tile(TileAr
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem<BW, BH, THREADS>& sm = *reinterpret_cast<TileSmem<BW, BH, THREADS>*>(smem_raw);
   unsigned* s_cov = reinterpret_cast<unsigned*>(smem_raw + sizeof(TileSmem<BW, BH, THREADS>));
-  __shared__ int s_qn;
-  __shared__ int s_job;     // current index into the owned-bin list
-  __shared__ int s_rng[2];  // its CSR range [s, e)
+  __shared__ int s_bin;     // current bin (-1: work list exhausted)
+  __shared__ int s_rng[3];  // its CSR sub-range [s, e) and fragment count (0: whole bin)
+  __shared__ unsigned s_ln[NLIST];
+  __shared__ int s_last;
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Grid g = a.g;
   float L[3];
   normalise_light(a.light, L);
   pdl_wait();
   pdl_trigger();
   const u64 frame = a.ctl->frame;
+  const bool ovf = a.ctl->overflow_tag == frame + 1;
+  TL_CTA(0);
   if (blockIdx.x == 0) {  // reset the next frame's double-buffered accumulators
     unsigned* h = &a.ctl->digit_hist[(frame + 1) & 1][0][0];
     for (int i = tid; i < MAX_PASSES * RX_RADIX; i += THREADS) h[i] = 0;
     if (tid == 0) a.ctl->n_live[(frame + 1) & 1] = 0;
     if (a.npass == 0 && tid == 0 && g.NB == 1) {  // single bin: CSR is [0, P]
       a.bin_start[0] = 0;
-      a.bin_start[1] = (int32_t)a.ctl->n_pairs;
+      a.bin_start[1] = ovf ? 0 : (int32_t)a.ctl->n_pairs;
     }
   }
-  const bool ovf = a.ctl->overflow_tag == frame + 1;
-  // thread 0 runs a 2-deep software pipeline of queue tickets and CSR ranges,
-  // so a bin's ticket and range are in registers before the bin starts
-  auto range_of = [&](int job, int& rs, int& re) {
-    rs = re = 0;
-    if (ovf || job >= a.owned) return;
-    if (a.npass == 0) { re = (int)a.ctl->n_pairs; return; }
-    const int bb = g.rank + job * g.nranks;
-    rs = a.bin_start[bb];
-    re = a.bin_start[bb + 1];
-  };
-  int q_job = 0, q_s = 0, q_e = 0, q_next = 0;
-  if (tid == 0) {
-    q_job = (int)atomicAdd(&a.ctl->tile_next, 1u);
-    q_next = (int)atomicAdd(&a.ctl->tile_next, 1u);
-    range_of(q_job, q_s, q_e);
-    s_job = q_job; s_rng[0] = q_s; s_rng[1] = q_e;
-    s_qn = 0;
+  // work-list sizes (single-bin grids have no bin scan: one job, bin 0)
+  if (tid < NLIST) {
+    unsigned n;
+    if (a.npass > 0 && !ovf) n = a.ctl->list_n[tid];
+    else if (ovf) n = (tid == 2) ? (unsigned)a.owned : 0u;
+    else {
+      const bool one = a.owned > 0, any = a.ctl->n_pairs > 0;
+      n = (tid == 1) ? (one && any) : (tid == 2) ? (one && !any) : 0u;
+    }
+    s_ln[tid] = n;
   }
   __syncthreads();
+  const unsigned n_frag = s_ln[0], n_work = s_ln[0] + s_ln[1], n_empty = s_ln[2];
+  auto bin_range = [&](int b, int& rs, int& re) {
+    if (a.npass == 0) { rs = 0; re = (int)a.ctl->n_pairs; return; }
+    rs = a.bin_start[b];
+    re = a.bin_start[b + 1];
+  };
+  // work item w -> bin, CSR sub-range, number of fragments of the bin (0: unsplit)
+  auto work_item = [&](unsigned w, int& b, int& rs, int& re, int& nf) {
+    if (w < n_frag) {
+      const int2 it = a.frag_list[w];
+      b = it.x;
+      int s0, e0;
+      bin_range(b, s0, e0);
+      nf = (e0 - s0 + a.frag - 1) / a.frag;
+      rs = s0 + it.y * a.frag;
+      re = min(rs + a.frag, e0);
+    } else if (w < n_work) {
+      b = (a.npass == 0) ? 0 : a.bin_list[w - n_frag];
+      bin_range(b, rs, re);
+      nf = 0;
+    } else {
+      b = -1;
+    }
+  };
+  auto empty_bin = [&](unsigned e) -> int {  // e < n_empty
+    if (ovf) return g.rank + (int)e * g.nranks;
+    if (a.npass == 0) return 0;
+    return a.bin_list[(size_t)g.NB + e];
+  };
 
-  // LoadBalance schedule: CTAs pull owned bins from a queue
+  // ---- LoadBalance schedule over the work list ----------------
+  // thread 0 keeps the next item in registers one item ahead
+  int q_bin = -1, q_s = 0, q_e = 0, q_nf = 0;
+  unsigned q_tk = 0;
+  if (tid == 0) {
+    const unsigned t0 = atomicAdd(&a.ctl->tile_next, 1u);
+    q_tk = atomicAdd(&a.ctl->tile_next, 1u);
+    int b0 = -1, s0 = 0, e0 = 0, nf0 = 0;
+    work_item(t0, b0, s0, e0, nf0);
+    s_bin = b0; s_rng[0] = s0; s_rng[1] = e0; s_rng[2] = nf0;
+  }
+  __syncthreads();
   for (;;) {
-    const int job = s_job;
-    if (job >= a.owned) break;
-    const int b = g.rank + job * g.nranks;  // owned bin (DirectMap across ranks)
+    const int b = s_bin;
+    if (b < 0) break;
+    const int s = s_rng[0], e = s_rng[1], nfrag = s_rng[2];
+    TL_MARK(b, 0);
+    if (tid == 0) {  // prefetch the next item
+      work_item(q_tk, q_bin, q_s, q_e, q_nf);
+      if (q_bin >= 0) q_tk = atomicAdd(&a.ctl->tile_next, 1u);
+    }
     const int bx = b % g.binsX, by = b / g.binsX;
     const int x0 = bx * BW, y0 = by * BH;
     const int x1 = min(x0 + BW, g.W) - 1, y1 = min(y0 + BH, g.H) - 1;
-    const int s = s_rng[0], e = s_rng[1];
-    if (tid == 0) {  // prefetch: next bin's ticket is q_next; fetch its range and a new ticket
-      q_job = q_next;
-      q_next = (int)atomicAdd(&a.ctl->tile_next, 1u);
-      range_of(q_job, q_s, q_e);
-    }
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int p = tid + k * THREADS;
@@ -805,111 +940,193 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 256 ? 3 : 8) k_tile(TileAr
         if (COV) s_cov[p] = 0;
       }
     }
-    const int nbatch = (e - s + THREADS - 1) / THREADS;
-    // software pipeline: primIDs two batches ahead, records one batch ahead
-    int t_cur = (s + tid < e) ? a.bin_prims[s + tid] : -1;
-    int t_next = (s + THREADS + tid < e) ? a.bin_prims[s + THREADS + tid] : -1;
-    if (t_cur >= 0) {
-      const int4* rp = a.rec + 3ll * t_cur;
-      cp_async16(&sm.rec[0][tid][0], rp); cp_async16(&sm.rec[0][tid][1], rp + 1);
-      cp_async16(&sm.rec[0][tid][2], rp + 2);
+    __syncthreads();  // tile cleared before any warp rasterizes into it
+    // Each warp streams its share of the bin's list (items s + k*THREADS +
+    // warp*32 + lane) through its own cp.async pipeline: no CTA barrier until
+    // the bin is done.  Tiny triangles: one thread loops over its pixels;
+    // larger ones: warp-cooperative (triangle, pixel) expansion.
+    const int nround = (e - s + THREADS - 1) / THREADS;
+    int tq[TQ];
+#pragma unroll
+    for (int j = 0; j < TQ; ++j) {
+      const int i = s + j * THREADS + tid;
+      tq[j] = i < e ? a.bin_prims[i] : -1;
     }
-    cp_async_commit();
-    for (int k = 0; k < nbatch; ++k) {
-      const int buf = k & 1;
-      if (t_next >= 0) {
-        const int4* rp = a.rec + 3ll * t_next;
-        cp_async16(&sm.rec[buf ^ 1][tid][0], rp); cp_async16(&sm.rec[buf ^ 1][tid][1], rp + 1);
-        cp_async16(&sm.rec[buf ^ 1][tid][2], rp + 2);
+#pragma unroll
+    for (int j = 0; j < NSTAGE - 1; ++j) {
+      if (tq[j] >= 0) {
+        const int4* rp = a.rec + 3ll * tq[j];
+        cp_async16(&sm.rec[j][tid][0], rp); cp_async16(&sm.rec[j][tid][1], rp + 1);
+        cp_async16(&sm.rec[j][tid][2], rp + 2);
       }
       cp_async_commit();
-      const int i2 = s + (k + 2) * THREADS + tid;
-      const int t_after = (i2 < e) ? a.bin_prims[i2] : -1;
-      cp_async_wait<1>();
-      __syncthreads();
+    }
+    for (int k = 0; k < nround; ++k) {
+      const int buf = k % NSTAGE;
+      const int t_cur = tq[0];
+      {  // issue round k + NSTAGE - 1, fetch the primIDs of round k + TQ
+        const int tn = tq[NSTAGE - 1];
+        if (tn >= 0) {
+          const int nb = (k + NSTAGE - 1) % NSTAGE;
+          const int4* rp = a.rec + 3ll * tn;
+          cp_async16(&sm.rec[nb][tid][0], rp); cp_async16(&sm.rec[nb][tid][1], rp + 1);
+          cp_async16(&sm.rec[nb][tid][2], rp + 2);
+        }
+        cp_async_commit();
+#pragma unroll
+        for (int j = 0; j < TQ - 1; ++j) tq[j] = tq[j + 1];
+        const int i = s + (k + TQ) * THREADS + tid;
+        tq[TQ - 1] = i < e ? a.bin_prims[i] : -1;
+      }
+      cp_async_wait<NSTAGE - 1>();
+      __syncwarp();  // warp-mates' records of round k are visible
+      int rx0 = 0, ry0 = 0, w = 1, area = 0;
       if (t_cur >= 0) {
         const RecView r = unpack(sm.rec[buf][tid][0], sm.rec[buf][tid][1], sm.rec[buf][tid][2]);
-        const int rx0 = max(r.px0, x0), rx1 = min(r.px1, x1);
-        const int ry0 = max(r.py0, y0), ry1 = min(r.py1, y1);
-        const int area = (rx1 - rx0 + 1) * (ry1 - ry0 + 1);
-        if (area <= SMALL_AREA) {
-          for (int y = ry0; y <= ry1; ++y) {
-            const int Py = 256 * y + 128;
-            for (int x = rx0; x <= rx1; ++x) {
+        rx0 = max(r.px0, x0); ry0 = max(r.py0, y0);
+        w = min(r.px1, x1) - rx0 + 1;
+        const int h = min(r.py1, y1) - ry0 + 1;
+        area = w * h;
+#ifdef PIKO_EXP_NORASTER
+        area = 0;
+#endif
+        if (area <= TINY_AREA) {
+#ifdef PIKO_EXP_NORASTER
+          if (r.X0 == 123456789) sm.key[0] = t_cur;
+#else
+          for (int y = ry0; y < ry0 + h; ++y)
+            for (int x = rx0; x < rx0 + w; ++x) {
               bool cov;
-              const u64 key = eval_key(r, 256 * x + 128, Py, t_cur, cov);
+              const u64 key = eval_key(r, 256 * x + 128, 256 * y + 128, t_cur, cov);
               const int p = (y - y0) * BW + (x - x0);
               if (COV && cov) atomicAdd(&s_cov[p], 1u);
+#ifndef PIKO_EXP_NOATOM
               if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
+#else
+              if (key == 12345) sm.key[p] = key;
+#endif
             }
-          }
-        } else {
-          const int slot = atomicAdd(&s_qn, 1);
-          sm.big[slot] = (unsigned short)tid;
-          sm.bigt[slot] = t_cur;
+#endif
+          area = 0;
         }
       }
-      __syncthreads();
-      const int nq = s_qn;
-      for (int q = 0; q < nq; ++q) {
-        const int src = sm.big[q];
-        const RecView r = unpack(sm.rec[buf][src][0], sm.rec[buf][src][1], sm.rec[buf][src][2]);
-        const int t = sm.bigt[q];
+      if (__any_sync(0xffffffffu, area > 0)) {
+        unsigned incl = (unsigned)area;
 #pragma unroll
-        for (int j = 0; j < PPT; ++j) {
-          const int p = tid + j * THREADS;
-          if (p >= NPX) continue;
-          const int x = x0 + (p % BW), y = y0 + (p / BW);
-          if (x < r.px0 || x > r.px1 || y < r.py0 || y > r.py1) continue;
-          bool cov;
-          const u64 key = eval_key(r, 256 * x + 128, 256 * y + 128, t, cov);
-          if (COV && cov) s_cov[p] += 1u;
-          if (key < sm.key[p]) sm.key[p] = key;
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        for (unsigned base = 0; base < total; base += 32) {
+          const unsigned item = base + lane;
+          int src = 0;  // first lane whose inclusive prefix exceeds item
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const unsigned v = __shfl_sync(0xffffffffu, incl, src + st - 1);
+            if (v <= item) src += st;
+          }
+          src = min(src, 31);
+          const unsigned incl_s = __shfl_sync(0xffffffffu, incl, src);
+          const int area_s = __shfl_sync(0xffffffffu, area, src);
+          const int rx0_s = __shfl_sync(0xffffffffu, rx0, src);
+          const int ry0_s = __shfl_sync(0xffffffffu, ry0, src);
+          const int w_s = __shfl_sync(0xffffffffu, w, src);
+          const int t_s = __shfl_sync(0xffffffffu, t_cur, src);
+          if (item < total) {
+            const int off = (int)(item - (incl_s - (unsigned)area_s));
+            const int y = ry0_s + off / w_s, x = rx0_s + off % w_s;
+            const int sl = warp * 32 + src;
+            const RecView rs = unpack(sm.rec[buf][sl][0], sm.rec[buf][sl][1], sm.rec[buf][sl][2]);
+            bool cov;
+            const u64 key = eval_key(rs, 256 * x + 128, 256 * y + 128, t_s, cov);
+            const int p = (y - y0) * BW + (x - x0);
+            if (COV && cov) atomicAdd(&s_cov[p], 1u);
+            if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
+          }
         }
       }
-      __syncthreads();
-      if (tid == 0) s_qn = 0;
-      t_cur = t_next;
-      t_next = t_after;
+      __syncwarp();  // round k's slots are free for round k + NSTAGE
     }
     cp_async_wait<0>();
     __syncthreads();
+    TL_MARK(b, 1);
 
     // ---- write-back ----------------------------------------------------------
-    if (KEYS_ONLY) {
-      u64* dst = a.tile_keys + (size_t)job * NPX;
-#pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        const int p = tid + k * THREADS;
-        if (p < NPX) dst[p] = sm.key[p];
-      }
-    } else {
+    const int job = (b - g.rank) / g.nranks;
+    if (nfrag == 0) {
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         const int p = tid + k * THREADS;
         if (p >= NPX) continue;
         const int x = x0 + (p % BW), y = y0 + (p / BW);
-        if (x > x1 || y > y1) continue;
-        const u64 key = sm.key[p];
-        const size_t o = (size_t)y * g.W + x;
-        float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-        float depth = 1.0f;
-        int prim = -1;
-        if (key != CLEAR_KEY) {
-          prim = (int)(unsigned)(key & 0xFFFFFFFFu);
-          depth = __uint_as_float((unsigned)(key >> 32));
-          c = shade(a.verts, a.xv, a.idx, g.W, g.H, L, prim, 256 * x + 128, 256 * y + 128);
+        if (!KEYS_ONLY && (x > x1 || y > y1)) continue;
+        store_pixel<COV, KEYS_ONLY>(a, L, job, p, NPX, x, y, sm.key[p], COV ? s_cov[p] : 0u);
+      }
+    } else {
+      // fragment of a split bin: merge into the bin's global key tile; the
+      // last fragment to arrive writes the bin
+      u64* gk = a.gkey + (size_t)b * NPX;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int p = tid + k * THREADS;
+        if (p >= NPX) continue;
+        if (sm.key[p] != CLEAR_KEY) atomicMin(&gk[p], sm.key[p]);
+        if (COV && s_cov[p]) atomicAdd(&a.gcov[(size_t)b * NPX + p], s_cov[p]);
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned done = atomicAdd(&a.arrive[b], 1u) + 1u;
+        s_last = done == (unsigned)nfrag;
+        if (s_last) a.arrive[b] = 0u;  // ready for the next frame
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const int p = tid + k * THREADS;
+          if (p >= NPX) continue;
+          const int x = x0 + (p % BW), y = y0 + (p / BW);
+          if (!KEYS_ONLY && (x > x1 || y > y1)) continue;
+          const u64 key = __ldcg(&gk[p]);
+          const unsigned cv = COV ? __ldcg(&a.gcov[(size_t)b * NPX + p]) : 0u;
+          gk[p] = CLEAR_KEY;  // ready for the next frame
+          if (COV) a.gcov[(size_t)b * NPX + p] = 0u;
+          store_pixel<COV, KEYS_ONLY>(a, L, job, p, NPX, x, y, key, cv);
         }
-        reinterpret_cast<float4*>(a.out_rgba)[o] = c;
-        a.out_depth[o] = depth;
-        a.out_primid[o] = prim;
-        if (COV) a.out_cov[o] = s_cov[p];
       }
     }
+    TL_MARK(b, 2);
+    if (tid == 0 && b < 8192) { g_tl_extra(b, e - s, blockIdx.x); }
     __syncthreads();  // keys consumed before the next bin reinitialises them
-    if (tid == 0) { s_job = q_job; s_rng[0] = q_s; s_rng[1] = q_e; }
+    if (tid == 0) { s_bin = q_bin; s_rng[0] = q_s; s_rng[1] = q_e; s_rng[2] = q_nf; }
     __syncthreads();
   }
+
+  TL_CTA(1);
+  // ---- empty bins: background only, no shared memory, no barriers ------------
+  // every warp pulls groups of EMPTY_GROUP bins from a second queue
+  for (;;) {
+    unsigned tk = 0;
+    if (lane == 0) tk = atomicAdd(&a.ctl->empty_next, 1u);
+    tk = __shfl_sync(0xffffffffu, tk, 0);
+    const unsigned e0 = tk * EMPTY_GROUP;
+    if (e0 >= n_empty) break;
+    for (unsigned e = e0; e < min(e0 + EMPTY_GROUP, n_empty); ++e) {
+      const int b = empty_bin(e);
+      const int x0 = (b % g.binsX) * BW, y0 = (b / g.binsX) * BH;
+      const int x1 = min(x0 + BW, g.W) - 1, y1 = min(y0 + BH, g.H) - 1;
+      const int job = (b - g.rank) / g.nranks;
+      for (int p = lane; p < NPX; p += 32) {
+        const int x = x0 + (p % BW), y = y0 + (p / BW);
+        if (!KEYS_ONLY && (x > x1 || y > y1)) continue;
+        store_pixel<COV, KEYS_ONLY>(a, L, job, p, NPX, x, y, CLEAR_KEY, 0u);
+      }
+    }
+  }
+  TL_CTA(2);
 }
 
 // ---------------------------------------------------------------------------

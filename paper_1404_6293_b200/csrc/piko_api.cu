@@ -81,6 +81,11 @@ struct piko_ctx {
   unsigned long long pair_cap = 0;
   uint32_t* bin_count = nullptr;
   int32_t* bin_start = nullptr;
+  int2* frag_list = nullptr; long long frag_cap = 0;  // split-bin fragments
+  int32_t* bin_list = nullptr;       // [2][NB] single-fragment and empty bins
+  unsigned long long* gkey = nullptr;  // [NB][bw*bh] key tiles of split bins
+  uint32_t* gcov = nullptr;          // [NB][bw*bh] coverage tiles (debug)
+  uint32_t* arrive = nullptr;        // [NB] fragment arrival counters
   Control* ctl = nullptr;
   unsigned long long* st_k1 = nullptr; long long st_k1_cap = 0;
   unsigned long long* st_scan = nullptr; long long st_scan_n = 0;
@@ -176,6 +181,9 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   const long long npx = (long long)width * height;
   bool ok = cudaMalloc(&ctx->bin_count, sizeof(uint32_t) * g.NB) == cudaSuccess &&
             cudaMalloc(&ctx->bin_start, sizeof(int32_t) * (g.NB + 1)) == cudaSuccess &&
+            cudaMalloc(&ctx->bin_list, sizeof(int32_t) * 2 * (size_t)g.NB) == cudaSuccess &&
+            cudaMalloc(&ctx->gkey, sizeof(unsigned long long) * (size_t)g.NB * bin_w * bin_h) == cudaSuccess &&
+            cudaMalloc(&ctx->arrive, sizeof(uint32_t) * (size_t)g.NB) == cudaSuccess &&
             cudaMalloc(&ctx->ctl, sizeof(Control)) == cudaSuccess &&
             cudaMalloc(&ctx->primid, sizeof(int32_t) * npx) == cudaSuccess &&
             cudaMallocHost(&ctx->h_ctl, sizeof(Control)) == cudaSuccess &&
@@ -201,7 +209,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   cudaDeviceSynchronize();
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
-                  ctx->bin_start, ctx->ctl, ctx->st_k1, ctx->st_scan, ctx->st_rx, ctx->primid,
+                  ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->st_k1, ctx->st_scan, ctx->st_rx, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
                   ctx->all_keys};
   for (void* p : bufs)
@@ -253,6 +261,11 @@ static int ensure_pairs(piko_ctx* ctx, unsigned long long P) {
   CK(cudaMalloc(&ctx->st_rx, sizeof(unsigned long long) * RX_RADIX * chunks * std::max(ctx->npass, 1)));
   ctx->st_rx_chunks = chunks;
   ctx->pair_cap = cap;
+  const long long fcap = (long long)(cap / (unsigned long long)tile_frag(ctx->bw, ctx->bh)) + ctx->g.NB + 1;
+  if (ctx->frag_list) cudaFree(ctx->frag_list);
+  ctx->frag_list = nullptr;
+  CK(cudaMalloc(&ctx->frag_list, sizeof(int2) * fcap));
+  ctx->frag_cap = fcap;
   ctx->need_reset = true;
   return PIKO_OK;
 }
@@ -269,8 +282,11 @@ static int ensure_verts(piko_ctx* ctx, long long V) {
 }
 
 static int ensure_cov(piko_ctx* ctx) {
-  if ((ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) && !ctx->cov)
+  if ((ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) && !ctx->cov) {
     CK(cudaMalloc(&ctx->cov, sizeof(uint32_t) * (size_t)ctx->g.W * ctx->g.H));
+    CK(cudaMalloc(&ctx->gcov, sizeof(uint32_t) * (size_t)ctx->g.NB * ctx->bw * ctx->bh));
+    ctx->need_reset = true;
+  }
   return PIKO_OK;
 }
 
@@ -294,6 +310,9 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     if (ctx->npass > 0)
       CK(cudaMemsetAsync(ctx->st_rx, 0, sizeof(unsigned long long) * RX_RADIX * ctx->st_rx_chunks * ctx->npass, s));
     CK(cudaMemsetAsync(ctx->bin_count, 0, sizeof(uint32_t) * ctx->g.NB, s));
+    CK(cudaMemsetAsync(ctx->arrive, 0, sizeof(uint32_t) * ctx->g.NB, s));
+    CK(cudaMemsetAsync(ctx->gkey, 0xFF, sizeof(unsigned long long) * ctx->g.NB * ctx->bw * ctx->bh, s));
+    if (ctx->gcov) CK(cudaMemsetAsync(ctx->gcov, 0, sizeof(uint32_t) * ctx->g.NB * ctx->bw * ctx->bh, s));
     ctx->last_g1 = g1;
     ctx->last_grx = grx;
     ctx->need_reset = false;
@@ -324,7 +343,10 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.status = ctx->st_rx + (size_t)p * RX_RADIX * ctx->st_rx_chunks;
     a.ctl = ctx->ctl; a.pass = p; a.shift = RX_BITS * p;
     a.bin_count = ctx->bin_count; a.bin_start = ctx->bin_start; a.scan_status = ctx->st_scan;
-    a.NB = ctx->g.NB;
+    a.NB = ctx->g.NB; a.rank = ctx->g.rank; a.nranks = ctx->g.nranks;
+    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
+    a.gcov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->gcov : nullptr;
+    a.frag = tile_frag(ctx->bw, ctx->bh); a.npx = ctx->bw * ctx->bh;
     CK(launch_radix_pass(a, (int)(p == 0 ? grx : ctx->st_rx_chunks), ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_RADIX));
@@ -338,6 +360,8 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.out_cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
     a.tile_keys = gather ? ctx->tile_keys : nullptr;
     a.owned = ctx->owned;
+    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
+    a.gcov = ctx->gcov; a.arrive = ctx->arrive; a.frag = tile_frag(ctx->bw, ctx->bh);
     const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, gather)));
     CK(launch_tile(a, ctx->bw, ctx->bh, grid, a.out_cov != nullptr, gather, ctx->pdl, s));
   }

@@ -13,7 +13,7 @@ constexpr int K1_THREADS = 256;                     // vertex+setup+AssignBin CT
 constexpr int K1_TPT = 4;                           // triangles per thread (strided)
 constexpr int K1_CHUNK = K1_THREADS * K1_TPT;       // triangles per look-back chunk
 constexpr int SCAN_THREADS = 256;                   // bin-count scan (inside radix pass 0)
-constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
 constexpr int RX_THREADS = 256;                     // stable LSD radix pass CTA
 constexpr int RX_WARPS = RX_THREADS / 32;
@@ -23,6 +23,15 @@ constexpr int RX_BITS = 8;
 constexpr int RX_RADIX = 1 << RX_BITS;
 constexpr int MAX_PASSES = 3;                       // NB <= 2^24 bins
 constexpr unsigned long long MAX_PAIRS = 1ull << 31;  // bin_start is int32
+// Schedule: the bin scan builds k_tile's work lists.  A bin with more than
+// `frag` pairs is split into fragments of `frag` consecutive CSR entries that
+// different CTAs rasterize and merge into a global key tile (64-bit atomicMin);
+// the last fragment to arrive shades the bin.  Lists: [0] fragments of split
+// bins (processed first: longest bins first, LPT), [1] single-fragment bins,
+// [2] empty bins.
+constexpr int NLIST = 3;
+constexpr int FRAG_ROUNDS = 4;   // fragment = FRAG_ROUNDS * threads-per-CTA pairs
+constexpr int EMPTY_GROUP = 8;   // empty bins per k_tile queue ticket
 
 // ---- persistent device control block ----------------------------------------
 // Never memset per frame: every kernel of a frame takes exactly gridDim.x
@@ -36,6 +45,8 @@ struct Control {
   unsigned long long rx_ticket[MAX_PASSES];
   unsigned long long frame;            // written by K1 chunk 0
   unsigned int tile_next;              // dynamic bin queue of k_tile (reset by K1 chunk 0)
+  unsigned int list_n[NLIST];          // work-list sizes (reset by K1 chunk 0)
+  unsigned int empty_next;             // k_tile queue of empty-bin groups (reset by K1 chunk 0)
   unsigned int vmax;                   // max(idx)+1 from k_index_max (zeroed by K1 chunk 0)
   unsigned int vx_overflow;            // k_vertex: vmax > xv capacity (K1 turns it into overflow_tag)
   unsigned long long vx_need;          // vertex count the last frame needed
@@ -109,6 +120,13 @@ struct RadixArgs {
   int32_t* bin_start;
   unsigned long long* scan_status;  // [scan tiles]
   int NB;
+  int rank, nranks;             // only owned bins enter the work lists
+  int2* frag_list;              // [frag_cap] {bin, fragment}
+  int32_t* bin_list;            // [2][NB] single-fragment bins, empty bins
+  unsigned long long* gkey;     // [NB][bw*bh] key tiles of split bins
+  uint32_t* gcov;               // [NB][bw*bh] coverage tiles (debug) or null
+  int frag;                     // pairs per fragment
+  int npx;                      // pixels per bin
 };
 
 struct TileArgs {
@@ -128,6 +146,12 @@ struct TileArgs {
   uint32_t* out_cov;            // debug coverage counts or null
   unsigned long long* tile_keys;  // keys-only mode: [owned][bw*bh]
   int owned;                    // bins owned by this rank (grid may be larger)
+  const int2* frag_list;
+  const int32_t* bin_list;
+  unsigned long long* gkey;
+  uint32_t* gcov;
+  uint32_t* arrive;             // [NB] fragments merged so far (self-resetting)
+  int frag;
 };
 
 struct ResolveArgs {            // rank 0 after the NCCL gather
@@ -151,6 +175,8 @@ cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream
 cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
                         bool pdl, cudaStream_t s);
 int tile_grid(int bw, int bh, bool cov, bool keys_only);  // persistent grid size
+inline int tile_threads(int bw, int bh) { return bw * bh < 256 ? bw * bh : 256; }
+inline int tile_frag(int bw, int bh) { return FRAG_ROUNDS * tile_threads(bw, bh); }
 cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s);
 
 }  // namespace piko

@@ -1,0 +1,93 @@
+#!/usr/bin/env python
+"""Build a -DPIKO_K1_TIMING variant of libpiko, render frames and print the
+per-CTA phase timelines (globaltimer ns) of k_setup, the radix passes and k_tile."""
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import __graft_entry__ as ge
+
+extra = [f for f in os.environ.get("PIKO_EXP", "").split() if f]
+lib = f"/tmp/libpiko_timing{os.getpid()}.so"
+objs = []
+for src in ge.SOURCES:
+    o = f"/tmp/{src}.timing.o"
+    subprocess.check_call([ge._nvcc(), *ge.NVCC_FLAGS, "-DPIKO_K1_TIMING", *extra, "-c",
+                           os.path.join(ge.CSRC, src), "-o", o])
+    objs.append(o)
+subprocess.check_call([ge._nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
+                       "-o", lib, "-ldl", "-lcudart"])
+import paper_1404_6293_b200 as piko  # noqa: E402
+piko.LIB_PATH = lib
+piko._lib = piko.lib = piko._load()
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import scenes  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
+bw = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+s = scenes.make(cfg)
+v = torch.from_numpy(s.verts).cuda()
+i = torch.from_numpy(s.idx).cuda()
+r = piko.Renderer(s.W, s.H, bw)
+for _ in range(3):
+    r.draw(v, i, s.mvp, s.light)
+torch.cuda.synchronize()
+st = r.stats()
+buf = np.zeros((4, 8192, 8), np.uint64)
+h = ctypes.CDLL(lib)
+rc = h.piko_dbg_k1_times(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
+assert rc == 0, rc
+T0 = int(buf[0, 0, 0])
+
+
+def show(name, t, phases, n):
+    t = t[:n].astype(np.int64)
+    ok = t[:, 0] > 0
+    t = t[ok]
+    base = t[:, 0].min()
+    print(f"== {name}: {len(t)} units, start {base - T0} ns after k_setup chunk 0, span {t[:, len(phases)-1].max() - base} ns")
+    for k in range(1, len(phases)):
+        d = t[:, k] - t[:, k - 1]
+        print(f"   {phases[k]:16s} median {np.median(d):8.0f}  p90 {np.percentile(d, 90):8.0f}  max {d.max():8.0f}")
+    srt = np.sort(t[:, 0] - base)
+    print(f"   unit start: p50 {srt[len(srt)//2]}  last {srt[-1]};  unit end p50 {np.median(t[:, len(phases)-1]-base):.0f}")
+
+
+n1 = (s.n_tris + 1023) // 1024
+show("k_setup", buf[0], ["start", "loads", "setup", "scan", "lookback+count", "expand"], n1)
+nrx = (st["n_pairs"] + 4095) // 4096
+show("radix pass 0", buf[1], ["start", "load+prefix", "rank", "lookback", "scatter"], nrx)
+show("radix pass 1", buf[2], ["start", "load+prefix", "rank", "lookback", "scatter"], nrx)
+nb = st["owned_bins"]
+t = buf[3, :nb].astype(np.int64)
+base = t[:, 0].min()
+print(f"== k_tile: {nb} bins, start {base - T0} ns, span {t[:, 2].max() - base} ns")
+ne = t[:, 3]
+for lo, hi in ((0, 0), (1, 256), (257, 1024), (1025, 1 << 30)):
+    m = (ne >= lo) & (ne <= hi)
+    if m.any():
+        r1 = t[m, 1] - t[m, 0]
+        r2 = t[m, 2] - t[m, 1]
+        print(f"   bins with {lo}-{hi} pairs: {m.sum():5d}  raster median {np.median(r1):7.0f} p90 {np.percentile(r1,90):7.0f}"
+              f"  writeback median {np.median(r2):7.0f} p90 {np.percentile(r2,90):7.0f}")
+cta = t[:, 4]
+per = np.bincount(cta.astype(np.int64))
+busy = np.zeros(per.size)
+for c in range(per.size):
+    m = cta == c
+    if m.any():
+        busy[c] = (t[m, 2] - t[m, 0]).sum()
+print(f"   bins per CTA: min {per[per>0].min()} max {per.max()};  CTA busy ns: median {np.median(busy[busy>0]):.0f} max {busy.max():.0f}")
+print(f"   tile kernel first bin start {t[:,0].min()-base}, last bin end {t[:,2].max()-base}")
+
+c = buf[0, 7000:7000 + 1024].astype(np.int64)
+c = c[c[:, 0] > 0]
+b0 = c[:, 0].min()
+print(f"== k_tile per CTA ({len(c)} CTAs): start spread {c[:,0].max()-b0} ns")
+print(f"   work-list phase end: median {np.median(c[:,1]-b0):.0f} p90 {np.percentile(c[:,1]-b0,90):.0f} max {(c[:,1]-b0).max()}")
+print(f"   CTA end:             median {np.median(c[:,2]-b0):.0f} p90 {np.percentile(c[:,2]-b0,90):.0f} max {(c[:,2]-b0).max()}")
