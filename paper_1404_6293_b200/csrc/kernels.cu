@@ -233,8 +233,12 @@ __device__ __forceinline__ bool setup_tri(int4 c0, int4 c1, int4 c2, int i0, int
 }
 
 // number of bins b in tile rect [tx0,tx1]x[ty0,ty1] with b % R == r
+__device__ __noinline__ unsigned owned_in_rect_r(int tx0, int ty0, int tx1, int ty1, const Grid g);
 __device__ __forceinline__ unsigned owned_in_rect(int tx0, int ty0, int tx1, int ty1, const Grid& g) {
   if (g.nranks == 1) return (unsigned)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+  return owned_in_rect_r(tx0, ty0, tx1, ty1, g);
+}
+__device__ __noinline__ unsigned owned_in_rect_r(int tx0, int ty0, int tx1, int ty1, const Grid g) {
   unsigned n = 0;
   const int w = tx1 - tx0 + 1;
   for (int ty = ty0; ty <= ty1; ++ty) {
@@ -246,9 +250,14 @@ __device__ __forceinline__ unsigned owned_in_rect(int tx0, int ty0, int tx1, int
 }
 
 // r-th owned bin of the rect, row-major (inverse of owned_in_rect's order)
+__device__ __noinline__ int owned_bin_at_r(int tx0, int ty0, int tx1, int ty1, unsigned r, const Grid g);
 __device__ __forceinline__ int owned_bin_at(int tx0, int ty0, int tx1, int ty1, unsigned r, const Grid& g) {
   const int w = tx1 - tx0 + 1;
   if (g.nranks == 1) return (ty0 + (int)(r / w)) * g.binsX + tx0 + (int)(r % w);
+  return owned_bin_at_r(tx0, ty0, tx1, ty1, r, g);
+}
+__device__ __noinline__ int owned_bin_at_r(int tx0, int ty0, int tx1, int ty1, unsigned r, const Grid g) {
+  const int w = tx1 - tx0 + 1;
   for (int ty = ty0; ty <= ty1; ++ty) {
     const int base = ty * g.binsX + tx0;
     const int first = (g.rank - base % g.nranks + g.nranks) % g.nranks;
@@ -308,27 +317,28 @@ __global__ void __launch_bounds__(256) k_index_max(const int32_t* __restrict__ i
 }
 
 // ---------------------------------------------------------------------------
-// K1: triangle setup + count + chunk scan + pair expansion
+// K1: triangle setup (O2-O4, O6 plane) -- a streaming kernel: setup record and
+// tile rect per triangle, digit histograms of the radix passes.  The pairs are
+// expanded from the rects by radix pass 0 (no scan here).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
-  __shared__ unsigned s_off[K1_CHUNK];   // exclusive local pair offset per triangle
-  __shared__ unsigned s_r0[K1_CHUNK];    // tile rect tx0 | ty0 << 16
-  __shared__ unsigned s_r1[K1_CHUNK];    // tile rect tx1 | ty1 << 16
+constexpr int K1_BIG = 64;  // triangles with more owned bins go to the CTA-wide loop
+
+__global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
   __shared__ unsigned s_hist[MAX_PASSES][RX_RADIX];
-  __shared__ unsigned s_wsum[K1_THREADS / 32];
-  __shared__ u64 s_tk, s_base;
+  __shared__ uint2 s_big[K1_CHUNK];
+  __shared__ unsigned s_nbig;
+  __shared__ u64 s_tk;
   __shared__ unsigned s_live;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const Grid g = a.g;
 
-  pdl_wait();   // k_vertex output; the previous frame's tile kernel read rec / pairs
+  pdl_wait();   // k_vertex output; the previous frame's kernels read rec / rect
   pdl_trigger();
-  if (tid == 0) { s_tk = atomicAdd(&a.ctl->k1_ticket, 1ull); s_live = 0; }
+  if (tid == 0) { s_tk = atomicAdd(&a.ctl->k1_ticket, 1ull); s_live = 0; s_nbig = 0; }
   for (int i = tid; i < MAX_PASSES * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
   __syncthreads();
   const u64 frame = s_tk / gridDim.x;
   const long long chunk = (long long)(s_tk % gridDim.x);
-  const unsigned tag = frame_tag(frame);
   const long long t0 = chunk * K1_CHUNK;
   K1_MARK(0);
   if (chunk == 0 && tid == 0) {
@@ -338,7 +348,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
     if (a.ctl->vx_overflow) { a.ctl->vx_overflow = 0; atomicMax(&a.ctl->overflow_tag, frame + 1); }
   }
 
-  // ---- loads first (all independent): indices, then corner positions ------
+  // ---- loads first (all independent): indices, then vertex-stage records ---
   int vi[K1_TPT][3];
 #pragma unroll
   for (int k = 0; k < K1_TPT; ++k) {
@@ -356,135 +366,75 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_setup(SetupArgs a) {
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       cv[k][c] = vi[k][c] >= 0 ? __ldg(a.xv + vi[k][c]) : make_int4(VX_CULLED, 0, 0, 0);
-  // (a corner index of -1 reads as culled: out-of-range or past n_tris)
-
   K1_MARK(1);
-  // ---- setup, record write (coalesced: consecutive threads, consecutive t) -
-  unsigned cnt[K1_TPT];
+
+  // ---- setup, record + rect write (coalesced: consecutive threads, t) -------
   unsigned live = 0;
 #pragma unroll
   for (int k = 0; k < K1_TPT; ++k) {
-    const int l = tid + k * K1_THREADS;
-    const long long t = t0 + l;
-    cnt[k] = 0;
-    s_r0[l] = 0; s_r1[l] = 0;
+    const long long t = t0 + tid + k * K1_THREADS;
+    if (t >= a.n_tris) continue;
+    uint2 rr = make_uint2(1u, 0u);  // empty rect: tx0 = 1 > tx1 = 0
     Tri o;
-    if (!setup_tri(cv[k][0], cv[k][1], cv[k][2], vi[k][0], vi[k][1], vi[k][2], g.W, g.H, o))
-      continue;
-    const int tx0 = o.px0 >> g.bw_log2, tx1 = o.px1 >> g.bw_log2;
-    const int ty0 = o.py0 >> g.bh_log2, ty1 = o.py1 >> g.bh_log2;
-    const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
-    if (c == 0) continue;
-    cnt[k] = c;
-    s_r0[l] = (unsigned)tx0 | ((unsigned)ty0 << 16);
-    s_r1[l] = (unsigned)tx1 | ((unsigned)ty1 << 16);
-    ++live;
-    // depth plane (O6) through the snapped corners
-    const float dx1 = __int2float_rn(o.X1 - o.X0), dy1 = __int2float_rn(o.Y1 - o.Y0);
-    const float dx2 = __int2float_rn(o.X2 - o.X0), dy2 = __int2float_rn(o.Y2 - o.Y0);
-    const float dz1 = __fsub_rn(o.zw1, o.zw0), dz2 = __fsub_rn(o.zw2, o.zw0);
-    const float inv = __fdiv_rn(1.0f, __ll2float_rn(o.area2));
-    const float za = __fmul_rn(__fmaf_rn(dz1, dy2, -__fmul_rn(dz2, dy1)), inv);
-    const float zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
-    int4* r = a.rec + 3 * t;
-    r[0] = make_int4(o.X0, o.Y0, o.X1, o.Y1);
-    r[1] = make_int4(o.X2, o.Y2, __float_as_int(o.zw0), __float_as_int(za));
-    r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
-                     o.small ? REC_SMALL : 0);
+    if (setup_tri(cv[k][0], cv[k][1], cv[k][2], vi[k][0], vi[k][1], vi[k][2], g.W, g.H, o)) {
+      const int tx0 = o.px0 >> g.bw_log2, tx1 = o.px1 >> g.bw_log2;
+      const int ty0 = o.py0 >> g.bh_log2, ty1 = o.py1 >> g.bh_log2;
+      const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
+      if (c > 0) {
+        rr = make_uint2((unsigned)tx0 | ((unsigned)ty0 << 16), (unsigned)tx1 | ((unsigned)ty1 << 16));
+        ++live;
+        // depth plane (O6) through the snapped corners
+        const float dx1 = __int2float_rn(o.X1 - o.X0), dy1 = __int2float_rn(o.Y1 - o.Y0);
+        const float dx2 = __int2float_rn(o.X2 - o.X0), dy2 = __int2float_rn(o.Y2 - o.Y0);
+        const float dz1 = __fsub_rn(o.zw1, o.zw0), dz2 = __fsub_rn(o.zw2, o.zw0);
+        const float inv = __fdiv_rn(1.0f, __ll2float_rn(o.area2));
+        const float za = __fmul_rn(__fmaf_rn(dz1, dy2, -__fmul_rn(dz2, dy1)), inv);
+        const float zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
+        int4* r = a.rec + 3 * t;
+        r[0] = make_int4(o.X0, o.Y0, o.X1, o.Y1);
+        r[1] = make_int4(o.X2, o.Y2, __float_as_int(o.zw0), __float_as_int(za));
+        r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
+                         o.small ? REC_SMALL : 0);
+        // digit histograms of the radix passes over this triangle's pairs
+        if (c <= (unsigned)K1_BIG) {
+          for (unsigned j = 0; j < c; ++j) {
+            const int b = owned_bin_at(tx0, ty0, tx1, ty1, j, g);
+            for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], 1u);
+          }
+        } else {
+          s_big[atomicAdd(&s_nbig, 1u)] = rr;
+        }
+      }
+    }
+    a.rect[t] = rr;
   }
   K1_MARK(2);
   if (live) atomicAdd(&s_live, live);
-#pragma unroll
-  for (int k = 0; k < K1_TPT; ++k) s_off[tid + k * K1_THREADS] = cnt[k];
   __syncthreads();
-
-  // ---- CTA exclusive scan in triangle order (thread owns 4 consecutive) ----
-  unsigned c4[4], sum = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) { c4[j] = s_off[4 * tid + j]; sum += c4[j]; }
-  unsigned inc = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += v;
-  }
-  if (lane == 31) s_wsum[warp] = inc;
-  __syncthreads();
-  unsigned wbase = 0, total = 0;
-#pragma unroll
-  for (int w = 0; w < K1_THREADS / 32; ++w) {
-    const unsigned v = s_wsum[w];
-    wbase += (w < warp) ? v : 0u;
-    total += v;
-  }
-  {
-    unsigned run = wbase + inc - sum;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) { s_off[4 * tid + j] = run; run += c4[j]; }
-  }
-  __syncthreads();  // every triangle's offset is read by other warps below
-  K1_MARK(3);
-  // pair j of the chunk -> (bin, t): the triangle with the largest s_off <= j
-  auto pair_at = [&](unsigned j, int& b, int& t) {
-    int lo = 0, hi = K1_CHUNK - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= j) lo = mid; else hi = mid - 1;
-    }
-    const unsigned r0 = s_r0[lo], r1 = s_r1[lo];
-    b = owned_bin_at((int)(r0 & 0xffff), (int)(r0 >> 16), (int)(r1 & 0xffff), (int)(r1 >> 16),
-                     j - s_off[lo], g);
-    t = (int)(t0 + lo);
-  };
-  if (warp == 0) {
-    // look-back (its latency is hidden behind the counting done by warps 1..7)
-    const u64 ex = lookback_warp(a.status, chunk, total, tag, lane);
-    if (lane == 0) {
-      s_base = ex;
-      if (s_live) atomicAdd(&a.ctl->n_live[frame & 1], (u64)s_live);
-      if (chunk == (long long)gridDim.x - 1) a.ctl->n_pairs = ex + total;
-    }
-  } else {
-    // warp-aggregated per-bin counts and radix digit histograms
-    constexpr int CW = K1_THREADS - 32;
-    for (unsigned j0 = (unsigned)(warp - 1) * 32; j0 < total; j0 += CW) {
-      const unsigned j = j0 + lane;
-      int b = -1, t = 0;
-      if (j < total) pair_at(j, b, t);
-      const unsigned peers = __match_any_sync(0xffffffffu, b);
-      if (j < total && lane == __ffs(peers) - 1) {
-        const unsigned n = __popc(peers);
-        if (a.npass > 0) atomicAdd(&a.bin_count[b], n);
-        for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], n);
-      }
+  // large triangles: the whole CTA walks their bins
+  const unsigned nbig = s_nbig;
+  for (unsigned q = 0; q < nbig; ++q) {
+    const uint2 rr = s_big[q];
+    const int tx0 = rr.x & 0xffff, ty0 = rr.x >> 16, tx1 = rr.y & 0xffff, ty1 = rr.y >> 16;
+    const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
+    for (unsigned j = tid; j < c; j += K1_THREADS) {
+      const int b = owned_bin_at(tx0, ty0, tx1, ty1, j, g);
+      for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], 1u);
     }
   }
   __syncthreads();
-
-  K1_MARK(4);
-  // ---- expansion: coalesced writes of the pairs at the chunk's global base --
-  const u64 base = s_base;
-  if (base + total > a.cap) {
-    if (tid == 0 && total) atomicMax(&a.ctl->overflow_tag, frame + 1);
-  } else {
-    for (unsigned j = tid; j < total; j += K1_THREADS) {
-      int b, t;
-      pair_at(j, b, t);
-      a.pair_keys[base + j] = (uint32_t)b;
-      a.pair_vals[base + j] = t;
-    }
-  }
   for (int i = tid; i < a.npass * RX_RADIX; i += K1_THREADS) {
     const unsigned v = (&s_hist[0][0])[i];
     if (v) atomicAdd(&a.ctl->digit_hist[frame & 1][0][0] + i, v);
   }
+  if (tid == 0 && s_live) atomicAdd(&a.ctl->n_live[frame & 1], (u64)s_live);
   K1_MARK(5);
 }
 
 // ---------------------------------------------------------------------------
 // Bin scan (run by extra CTAs of radix pass 0): bin_count -> bin_start
 // ---------------------------------------------------------------------------
-__device__ void bin_scan_tile(const RadixArgs& a, long long tile, unsigned tag) {
+__device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, unsigned tag) {
   __shared__ unsigned s_wsum[SCAN_THREADS / 32];
   __shared__ u64 s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -565,146 +515,427 @@ __device__ void bin_scan_tile(const RadixArgs& a, long long tile, unsigned tag) 
 }
 
 // ---------------------------------------------------------------------------
-// K3: one stable LSD radix pass over the (bin, primID) pairs
+// K3: one stable LSD radix pass over the (bin, primID) pairs.
+// Pass 0 (expand) takes a chunk of triangles, expands their pairs in primitive
+// order from the tile rects, counts pairs per bin, ranks by digit 0.  Later
+// passes take chunks of RX_CHUNK pairs.  A chunk with more than RX_CHUNK pairs
+// is ranked in sub-blocks twice (count, then scatter).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
-  __shared__ unsigned s_whist[RX_WARPS][RX_RADIX];
-  __shared__ unsigned s_keys[RX_CHUNK];
-  __shared__ int s_vals[RX_CHUNK];
-  __shared__ unsigned s_lstart[RX_RADIX];
-  __shared__ unsigned s_gstart[RX_RADIX];
-  __shared__ unsigned s_wsum[RX_WARPS];
-  __shared__ u64 s_tk;
+struct RadixSmem {
+  unsigned whist[RX_WARPS][RX_RADIX];
+  unsigned keys[RX_CHUNK];
+  int vals[RX_CHUNK];
+  unsigned lstart[RX_RADIX];
+  unsigned gstart[RX_RADIX];
+  unsigned run[RX_RADIX];
+  unsigned wsum[RX_WARPS];
+  u64 red[RX_WARPS];
+  u64 tk;
+  unsigned n;
+};
+struct ExpandSmem {              // pass 0 only (dynamic shared memory tail)
+  unsigned off[EX_MAX_TRIS];     // exclusive pair offset per triangle of the chunk
+  uint2 rect[EX_MAX_TRIS];
+  unsigned cnt[EX_MAX_TRIS + EX_MAX_TRIS / 32];  // owned-bin count, padded index
+};
+__device__ __forceinline__ int cpad(int l) { return l + (l >> 5); }
+
+// Ranking of up to RX_CHUNK items held in registers (warp w owns items
+// [w*512, w*512+512), lane-strided): per-warp digit counters in shared memory.
+__device__ __forceinline__ void rank_items(const unsigned (&key)[RX_ITEMS], unsigned n, unsigned wb,
+                                           int shift, unsigned (*whist)[RX_RADIX], int warp, int lane,
+                                           unsigned (&rank)[RX_ITEMS]) {
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < RX_ITEMS; ++j) {
+    const unsigned pos = wb + j * 32;
+    const bool valid = pos < n;
+    const unsigned d = valid ? ((key[j] >> shift) & (RX_RADIX - 1)) : RX_RADIX;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    unsigned prev = 0;
+    if (valid) prev = whist[warp][d];
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) whist[warp][d] = prev + __popc(peers);
+    __syncwarp();
+    rank[j] = prev + __popc(peers & lanemask_lt);
+  }
+}
+
+// pair j of an expand chunk: the triangle with the largest off <= j owns it
+__device__ __noinline__ void expand_pair(const ExpandSmem& ex, int ntri, long long t0, unsigned j,
+                                         const Grid& g, unsigned& key, int& val) {
+  int lo = 0, hi = ntri - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ex.off[mid] <= j) lo = mid; else hi = mid - 1;
+  }
+  const uint2 rr = ex.rect[lo];
+  key = (unsigned)owned_bin_at(rr.x & 0xffff, rr.x >> 16, rr.y & 0xffff, rr.y >> 16, j - ex.off[lo], g);
+  val = (int)(t0 + lo);
+}
+
+// Expand chunk with more than RX_CHUNK pairs (rare: triangles covering many
+// bins): sub-blocks of RX_CHUNK pairs are expanded by binary search and ranked
+// twice -- first to count (publish), then to scatter with running offsets.
+// phase 0: count into sm.run[d], bin counts.  phase 1: scatter from sm.gstart.
+__device__ __noinline__ void expand_slow(const RadixArgs& a, RadixSmem& sm, const ExpandSmem& ex,
+                                         int ntri, long long t0, unsigned n, int phase) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lanemask_lt = (1u << lane) - 1u;
+  if (phase == 1) sm.lstart[tid] = sm.gstart[tid];
+  else sm.run[tid] = 0;
+  __syncthreads();
+#pragma unroll 1
+  for (unsigned sub = 0; sub * RX_CHUNK < n; ++sub) {
+#pragma unroll 1
+    for (int w = 0; w < RX_WARPS; ++w) sm.whist[w][tid] = 0;
+    __syncthreads();
+    const unsigned wb = sub * RX_CHUNK + (unsigned)warp * (RX_ITEMS * 32) + lane;
+    unsigned rk[RX_ITEMS], ky[RX_ITEMS];
+    int vl[RX_ITEMS];
+#pragma unroll 1
+    for (int j = 0; j < RX_ITEMS; ++j) {
+      const unsigned pos = wb + j * 32;
+      unsigned k = 0u;
+      int v = 0;
+      if (pos < n) expand_pair(ex, ntri, t0, pos, a.g, k, v);
+      if (phase == 0) {
+        const unsigned kb = pos < n ? k : 0xFFFFFFFFu;
+        const unsigned pb = __match_any_sync(0xffffffffu, kb);
+        if (pos < n && lane == __ffs(pb) - 1) atomicAdd(&a.bin_count[kb], (unsigned)__popc(pb));
+      }
+      const unsigned d = pos < n ? ((k >> a.shift) & (RX_RADIX - 1)) : RX_RADIX;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      unsigned prev = 0;
+      if (pos < n) prev = sm.whist[warp][d];
+      __syncwarp();
+      if (pos < n && lane == __ffs(peers) - 1) sm.whist[warp][d] = prev + __popc(peers);
+      __syncwarp();
+      rk[j] = prev + __popc(peers & lanemask_lt);
+      ky[j] = k;
+      vl[j] = v;
+    }
+    __syncthreads();
+    unsigned tot = 0;
+#pragma unroll 1
+    for (int w = 0; w < RX_WARPS; ++w) {
+      const unsigned c = sm.whist[w][tid];
+      sm.whist[w][tid] = tot;
+      tot += c;
+    }
+    __syncthreads();
+    if (phase == 1) {
+#pragma unroll 1
+      for (int j = 0; j < RX_ITEMS; ++j) {
+        const unsigned pos = wb + j * 32;
+        if (pos >= n) continue;
+        const unsigned d = (ky[j] >> a.shift) & (RX_RADIX - 1);
+        const unsigned gpos = sm.lstart[d] + sm.whist[warp][d] + rk[j];
+        if (a.keys_out) a.keys_out[gpos] = ky[j];
+        a.vals_out[gpos] = vl[j];
+      }
+    }
+    __syncthreads();
+    if (phase == 1) sm.lstart[tid] += tot;
+    else sm.run[tid] += tot;
+    __syncthreads();
+  }
+}
+
+template <bool EXPAND>
+__global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
+  extern __shared__ __align__(16) unsigned char rx_smem[];
+  RadixSmem& sm = *reinterpret_cast<RadixSmem*>(rx_smem);
+  ExpandSmem& ex = *reinterpret_cast<ExpandSmem*>(rx_smem + sizeof(RadixSmem));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   pdl_wait();
   pdl_trigger();
-  if (tid == 0) s_tk = atomicAdd(&a.ctl->rx_ticket[a.pass], 1ull);
-#pragma unroll
-  for (int w = 0; w < RX_WARPS; ++w) s_whist[w][tid] = 0;
+  if (tid == 0) sm.tk = atomicAdd(&a.ctl->rx_ticket[a.pass], 1ull);
   __syncthreads();
-  const u64 frame = s_tk / gridDim.x;
-  const long long chunk = (long long)(s_tk % gridDim.x);
+  const u64 frame = sm.tk / gridDim.x;
+  const long long chunk = (long long)(sm.tk % gridDim.x);
   const unsigned tag = frame_tag(frame);
-  // on overflow sort nothing, but pass 0 still runs the bin scan (it zeroes
-  // the per-bin counts for the next frame)
-  const u64 P = (a.ctl->overflow_tag == frame + 1) ? 0ull : a.ctl->n_pairs;
-  const long long nchunks = (long long)((P + RX_CHUNK - 1) / RX_CHUNK);
-  if (chunk >= nchunks) {
-    const long long tile = chunk - nchunks;
-    if (a.pass == 0 && tile < (a.NB + SCAN_CHUNK - 1) / SCAN_CHUNK) bin_scan_tile(a, tile, tag);
-    return;
-  }
 
-  // block exclusive scan of 256 values (one per thread)
-  auto block_excl = [&](unsigned v) -> unsigned {
+  auto block_excl = [&](unsigned v) -> unsigned {  // every thread must call it
     unsigned inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += t;
     }
-    if (lane == 31) s_wsum[warp] = inc;
+    if (lane == 31) sm.wsum[warp] = inc;
     __syncthreads();
     unsigned base = 0;
-    for (int w = 0; w < warp; ++w) base += s_wsum[w];
+    for (int w = 0; w < warp; ++w) base += sm.wsum[w];
     __syncthreads();
     return base + inc - v;
   };
-
+  const unsigned hist_d = a.ctl->digit_hist[frame & 1][a.pass][tid];
+  u64 P;
+  bool ovf = a.ctl->overflow_tag == frame + 1;
+  long long nchunks;
+  if (EXPAND) {
+    // P = sum of the digit-0 histogram; pass 0 checks the pair capacity
+    u64 v = hist_d;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sm.red[warp] = v;
+    __syncthreads();
+    P = 0;
+#pragma unroll
+    for (int w = 0; w < RX_WARPS; ++w) P += sm.red[w];
+    if (P > a.cap) ovf = true;
+    if (chunk == 0 && tid == 0) {
+      a.ctl->n_pairs = P;
+      if (P > a.cap) atomicMax(&a.ctl->overflow_tag, frame + 1);
+    }
+    nchunks = ovf ? 0 : (a.n_tris + a.tri_chunk - 1) / a.tri_chunk;
+  } else {
+    P = ovf ? 0ull : a.ctl->n_pairs;
+    nchunks = (long long)((P + RX_CHUNK - 1) / RX_CHUNK);
+  }
+  if (chunk >= nchunks) {
+    // extra CTAs: the CSR bin scan + work lists (counts are final: pass 0 done)
+    const long long tile = chunk - nchunks;
+    if (a.scan_here && tile < (a.NB + SCAN_CHUNK - 1) / SCAN_CHUNK) bin_scan_tile(a, tile, tag);
+    return;
+  }
   RX_MARK(0);
-  const u64 c0 = (u64)chunk * RX_CHUNK;
+#pragma unroll
+  for (int w = 0; w < RX_WARPS; ++w) sm.whist[w][tid] = 0;
+
+  // ---- chunk contents ----------------------------------------------------------
   unsigned key[RX_ITEMS];
   int val[RX_ITEMS];
   unsigned rank[RX_ITEMS];
-  const u64 wb = c0 + (u64)warp * (RX_ITEMS * 32) + lane;
+  unsigned n;
+  long long t0 = 0;
+  int ntri = 0;
+  bool fast = true;
+  const unsigned wb = (unsigned)warp * (RX_ITEMS * 32) + lane;
+  if (!EXPAND) {
+    const u64 c0 = (u64)chunk * RX_CHUNK;
+    n = (unsigned)min((u64)RX_CHUNK, P - c0);
 #pragma unroll
-  for (int j = 0; j < RX_ITEMS; ++j) {
-    const u64 pos = wb + j * 32;
-    const bool valid = pos < P;
-    key[j] = valid ? a.keys_in[pos] : 0u;
-    val[j] = valid ? a.vals_in[pos] : 0;
+    for (int j = 0; j < RX_ITEMS; ++j) {
+      const unsigned pos = wb + j * 32;
+      key[j] = pos < n ? a.keys_in[c0 + pos] : 0u;
+      val[j] = pos < n ? a.vals_in[c0 + pos] : 0;
+    }
+  } else {
+    // rect -> owned-bin count per triangle (coalesced: triangle tid + 256 k),
+    // exclusive scan in triangle order (thread owns tpt consecutive triangles)
+    t0 = chunk * (long long)a.tri_chunk;
+    ntri = (int)min((long long)a.tri_chunk, a.n_tris - t0);
+    const int tpt = a.tri_chunk / RX_THREADS;
+    constexpr int TPT_MAX = EX_MAX_TRIS / RX_THREADS;
+    uint2 rr[TPT_MAX];
+#pragma unroll
+    for (int k = 0; k < TPT_MAX; ++k) {  // all loads in flight together
+      const int l = tid + k * RX_THREADS;
+      rr[k] = (l < ntri) ? a.rect[t0 + l] : make_uint2(1u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < TPT_MAX; ++k) {
+      const int l = tid + k * RX_THREADS;
+      if (k < tpt) {
+        ex.rect[l] = rr[k];
+        ex.cnt[cpad(l)] = owned_in_rect(rr[k].x & 0xffff, rr[k].x >> 16, rr[k].y & 0xffff, rr[k].y >> 16, a.g);
+      }
+    }
+    __syncthreads();
+    unsigned sum = 0;
+#pragma unroll 1
+    for (int k = 0; k < tpt; ++k) sum += ex.cnt[cpad(tid * tpt + k)];
+    unsigned run = block_excl(sum);
+#pragma unroll 1
+    for (int k = 0; k < tpt; ++k) {
+      ex.off[tid * tpt + k] = run;
+      run += ex.cnt[cpad(tid * tpt + k)];
+    }
+    if (tid == RX_THREADS - 1) sm.n = run;
+    __syncthreads();
+    n = sm.n;
+    fast = n <= RX_CHUNK;
+    if (fast) {  // expand into shared memory, thread per triangle (coalesced order)
+#pragma unroll 1
+      for (int k = 0; k < tpt; ++k) {
+        const int l = tid + k * RX_THREADS;
+        if (l >= ntri) break;
+        const unsigned c = ex.cnt[cpad(l)];
+        if (c == 0) continue;
+        const uint2 r2 = ex.rect[l];
+        const int tx0 = r2.x & 0xffff, ty0 = r2.x >> 16, tx1 = r2.y & 0xffff, ty1 = r2.y >> 16;
+        const unsigned o = ex.off[l];
+#pragma unroll 1
+        for (unsigned j = 0; j < c; ++j) {
+          sm.keys[o + j] = (unsigned)owned_bin_at(tx0, ty0, tx1, ty1, j, a.g);
+          sm.vals[o + j] = (int)(t0 + l);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < RX_ITEMS; ++j) {
+        const unsigned pos = wb + j * 32;
+        key[j] = pos < n ? sm.keys[pos] : 0u;
+        val[j] = pos < n ? sm.vals[pos] : 0;
+      }
+    }
   }
-  const unsigned gprefix = block_excl(a.ctl->digit_hist[frame & 1][a.pass][tid]);
   RX_MARK(1);
+
+  // ---- per-digit chunk totals, published before the ranking ------------------
+  unsigned total;
+  if (fast) {
+    sm.run[tid] = 0;
+    __syncthreads();
 #pragma unroll
-  for (int j = 0; j < RX_ITEMS; ++j) {
-    const u64 pos = wb + j * 32;
-    const bool valid = pos < P;
-    const unsigned d = valid ? ((key[j] >> a.shift) & (RX_RADIX - 1)) : RX_RADIX;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    unsigned prev = 0;
-    if (valid) prev = s_whist[warp][d];
-    __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) s_whist[warp][d] = prev + __popc(peers);
-    __syncwarp();
-    rank[j] = prev + __popc(peers & lanemask_lt);
+    for (int j = 0; j < RX_ITEMS; ++j)
+      if (wb + j * 32 < n) atomicAdd(&sm.run[(key[j] >> a.shift) & (RX_RADIX - 1)], 1u);
+    __syncthreads();
+    total = sm.run[tid];
+  } else {
+    expand_slow(a, sm, ex, ntri, t0, n, 0);
+    total = sm.run[tid];
+  }
+  // two-level decoupled look-back, part 1: publish.  Chunks form groups of
+  // LB_GROUP; the last chunk of a group to arrive publishes the group aggregate.
+  const long long grp = chunk / LB_GROUP, g0 = grp * LB_GROUP;
+  const long long gsize = min((long long)LB_GROUP, nchunks - g0);
+  u64* st = a.status + (size_t)chunk * RX_RADIX + tid;
+  a.ccount[(size_t)chunk * RX_RADIX + tid] = total;
+  st_relaxed64(st, lb_pack(tag, chunk == 0 ? LB_INC : LB_AGG, total));
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    sm.n = (atomicAdd(&a.garrive[(frame & 1) * a.gcap + grp], 1u) + 1u == (unsigned)gsize) ? 1u : 0u;
   }
   __syncthreads();
-  // per digit d = tid: exclusive offsets over warps, chunk total
-  unsigned tot = 0;
-#pragma unroll
-  for (int w = 0; w < RX_WARPS; ++w) {
-    const unsigned c = s_whist[w][tid];
-    s_whist[w][tid] = tot;
-    tot += c;
+  if (sm.n) {  // last chunk of the group to arrive: publish the group aggregate
+    __threadfence();
+    unsigned gs = 0;
+    for (long long c = g0; c < g0 + gsize; ++c) gs += __ldcg(&a.ccount[(size_t)c * RX_RADIX + tid]);
+    u64* gw = a.gstatus + (size_t)grp * RX_RADIX + tid;
+    const u64 cur = ld_relaxed64(gw);
+    if (lb_flag(cur) != LB_INC || lb_tag(cur) != tag)
+      st_relaxed64(gw, lb_pack(tag, grp == 0 ? LB_INC : LB_AGG, gs));
   }
-  // decoupled look-back per digit (thread tid owns digit tid), 8 chunks per probe
-  u64* st = a.status + (size_t)chunk * RX_RADIX + tid;
-  u64 excl = 0;
-  if (chunk == 0) {
-    st_relaxed64(st, lb_pack(tag, LB_INC, tot));
-  } else {
-    st_relaxed64(st, lb_pack(tag, LB_AGG, tot));
-    long long c = chunk - 1;
-    bool done = false;
-    while (!done) {
-      constexpr int PROBE = 16;
-      u64 s[PROBE];
+  const unsigned gprefix = block_excl(hist_d);
+
+  // ---- rank (and, expanding, count pairs per bin) while predecessors publish --
+  if (fast) {
+    if (EXPAND) {
 #pragma unroll
-      for (int j = 0; j < PROBE; ++j)
-        s[j] = (c - j >= 0) ? ld_relaxed64(a.status + (size_t)(c - j) * RX_RADIX + tid)
-                            : lb_pack(tag, LB_INC, 0);
+      for (int j = 0; j < RX_ITEMS; ++j) {  // pairs per bin (CSR), warp-aggregated
+        const unsigned pos = wb + j * 32;
+        const unsigned kb = pos < n ? key[j] : 0xFFFFFFFFu;
+        const unsigned pb = __match_any_sync(0xffffffffu, kb);
+        if (pos < n && lane == __ffs(pb) - 1) atomicAdd(&a.bin_count[kb], (unsigned)__popc(pb));
+      }
+    }
+    rank_items(key, n, wb, a.shift, sm.whist, warp, lane, rank);
+    __syncthreads();
+    unsigned tot = 0;
+#pragma unroll
+    for (int w = 0; w < RX_WARPS; ++w) {  // exclusive over warps
+      const unsigned c = sm.whist[w][tid];
+      sm.whist[w][tid] = tot;
+      tot += c;
+    }
+  }
+  RX_MARK(2);
+
+  // ---- look-back part 2: walk (thread tid owns digit tid) ---------------------
+  u64 excl = 0;
+  if (chunk > 0) {
+    bool done = false;
+    // level 1: own group, chunks chunk-1 .. g0
+    long long c = chunk - 1;
+    while (!done && c >= g0) {
+      u64 sv[LB_GROUP];
+#pragma unroll
+      for (int j = 0; j < LB_GROUP; ++j)
+        sv[j] = (c - j >= g0) ? ld_relaxed64(a.status + (size_t)(c - j) * RX_RADIX + tid) : 0ull;
       int j = 0;
 #pragma unroll
-      for (int q = 0; q < PROBE; ++q) {
-        if (done || j != q) continue;  // stop at the first unready entry
-        if (lb_tag(s[q]) != tag) continue;
-        excl += lb_val(s[q]);
-        if (lb_flag(s[q]) == LB_INC) done = true;
+      for (int q = 0; q < LB_GROUP; ++q) {
+        if (done || j != q || c - q < g0) continue;
+        if (lb_tag(sv[q]) != tag) continue;  // not yet published: stop, re-probe
+        excl += lb_val(sv[q]);
+        if (lb_flag(sv[q]) == LB_INC) done = true;
         ++j;
       }
       c -= j;
+      if (!done && c >= g0 && j == 0) __nanosleep(32);
     }
-    st_relaxed64(st, lb_pack(tag, LB_INC, excl + tot));
-  }
-  RX_MARK(3);
-  const unsigned lstart = block_excl(tot);
-  s_lstart[tid] = lstart;
-  s_gstart[tid] = gprefix + (unsigned)excl;
-  __syncthreads();
-  // stage the chunk sorted by digit in shared memory
+    // level 2: previous groups
+    long long gq = grp - 1;
+    while (!done && gq >= 0) {
+      constexpr int GPROBE = 16;
+      u64 sv[GPROBE];
 #pragma unroll
-  for (int j = 0; j < RX_ITEMS; ++j) {
-    const u64 pos = wb + j * 32;
-    if (pos < P) {
-      const unsigned d = (key[j] >> a.shift) & (RX_RADIX - 1);
-      const unsigned lp = s_lstart[d] + s_whist[warp][d] + rank[j];
-      s_keys[lp] = key[j];
-      s_vals[lp] = val[j];
+      for (int j = 0; j < GPROBE; ++j)
+        sv[j] = (gq - j >= 0) ? ld_relaxed64(a.gstatus + (size_t)(gq - j) * RX_RADIX + tid)
+                              : lb_pack(tag, LB_INC, 0);
+      int j = 0;
+#pragma unroll
+      for (int q = 0; q < GPROBE; ++q) {
+        if (done || j != q) continue;
+        if (lb_tag(sv[q]) != tag) continue;
+        excl += lb_val(sv[q]);
+        if (lb_flag(sv[q]) == LB_INC) done = true;
+        ++j;
+      }
+      gq -= j;
+      if (!done && j == 0) __nanosleep(32);
     }
+    st_relaxed64(st, lb_pack(tag, LB_INC, excl + total));
   }
-  __syncthreads();
-  const unsigned n = (unsigned)min((u64)RX_CHUNK, P - c0);
-  for (unsigned i = tid; i < n; i += RX_THREADS) {
-    const unsigned k = s_keys[i];
-    const unsigned d = (k >> a.shift) & (RX_RADIX - 1);
-    const unsigned gpos = s_gstart[d] + (i - s_lstart[d]);
-    if (a.keys_out) a.keys_out[gpos] = k;
-    a.vals_out[gpos] = s_vals[i];
+  if (chunk == g0 + gsize - 1)  // last chunk of its group: the group's inclusive prefix
+    st_relaxed64(a.gstatus + (size_t)grp * RX_RADIX + tid, lb_pack(tag, LB_INC, excl + total));
+  sm.gstart[tid] = gprefix + (unsigned)excl;
+  RX_MARK(3);
+
+  // ---- phase B: scatter ----------------------------------------------------------
+  if (fast) {  // stage the chunk sorted by digit in shared memory, then write out
+    const unsigned lstart = block_excl(total);
+    sm.lstart[tid] = lstart;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RX_ITEMS; ++j) {
+      const unsigned pos = wb + j * 32;
+      if (pos < n) {
+        const unsigned d = (key[j] >> a.shift) & (RX_RADIX - 1);
+        const unsigned lp = sm.lstart[d] + sm.whist[warp][d] + rank[j];
+        sm.keys[lp] = key[j];
+        sm.vals[lp] = val[j];
+      }
+    }
+    __syncthreads();
+    for (unsigned i = tid; i < n; i += RX_THREADS) {
+      const unsigned k = sm.keys[i];
+      const unsigned d = (k >> a.shift) & (RX_RADIX - 1);
+      const unsigned gpos = sm.gstart[d] + (i - sm.lstart[d]);
+      if (a.keys_out) a.keys_out[gpos] = k;
+      a.vals_out[gpos] = sm.vals[i];
+    }
+  } else {
+    __syncthreads();
+    expand_slow(a, sm, ex, ntri, t0, n, 1);
   }
   RX_MARK(4);
+}
+
+// CSR bin scan + work lists for single-pass grids (after the expand pass)
+__global__ void __launch_bounds__(SCAN_THREADS) k_bin_scan(RadixArgs a) {
+  __shared__ u64 s_tk;
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) s_tk = atomicAdd(&a.ctl->scan_ticket, 1ull);
+  __syncthreads();
+  const u64 frame = s_tk / gridDim.x;
+  bin_scan_tile(a, (long long)(s_tk % gridDim.x), frame_tag(frame));
 }
 
 // ---------------------------------------------------------------------------
@@ -759,7 +990,7 @@ __device__ __forceinline__ u64 eval_key(const RecView& r, int Px, int Py, int t,
 
 // O7 shade of pixel sample (Px, Py) by triangle t (recomputes O2 from the
 // vertex-stage records; normals from the caller's vertex buffer).
-__device__ __forceinline__ float4 shade(const float* __restrict__ verts, const int4* __restrict__ xv,
+__device__ __noinline__ float4 shade(const float* __restrict__ verts, const int4* __restrict__ xv,
                                         const int32_t* __restrict__ idx, int W, int H,
                                         const float L[3], int t, int Px, int Py) {
   Tri o;
@@ -865,6 +1096,12 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 256 ? 3 : 8) k_tile(TileAr
       a.bin_start[0] = 0;
       a.bin_start[1] = ovf ? 0 : (int32_t)a.ctl->n_pairs;
     }
+  }
+  // next frame's look-back group arrival counters (every CTA a slice)
+  for (int p = 0; p < a.npass; ++p) {
+    uint32_t* ga = a.garrive + ((size_t)p * 2 + ((frame + 1) & 1)) * a.gcap;
+    for (long long i = (long long)blockIdx.x * THREADS + tid; i < a.gcap; i += (long long)gridDim.x * THREADS)
+      ga[i] = 0u;
   }
   // work-list sizes (single-bin grids have no bin scan: one job, bin 0)
   if (tid < NLIST) {
@@ -1202,7 +1439,19 @@ cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s)
   return launch_ex(k_setup, grid, K1_THREADS, 0, pdl, s, a);
 }
 cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream_t s) {
-  return launch_ex(k_radix_pass, grid, RX_THREADS, 0, pdl, s, a);
+  if (a.expand) {
+    const size_t smem = sizeof(RadixSmem) + sizeof(ExpandSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_radix_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return launch_ex(k_radix_pass<true>, grid, RX_THREADS, smem, pdl, s, a);
+  }
+  const size_t smem = sizeof(RadixSmem);
+  cudaError_t e = cudaFuncSetAttribute(k_radix_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_ex(k_radix_pass<false>, grid, RX_THREADS, smem, pdl, s, a);
+}
+cudaError_t launch_bin_scan(const RadixArgs& a, int grid, bool pdl, cudaStream_t s) {
+  return launch_ex(k_bin_scan, grid, SCAN_THREADS, 0, pdl, s, a);
 }
 
 struct TileKernel {

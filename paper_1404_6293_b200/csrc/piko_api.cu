@@ -87,12 +87,17 @@ struct piko_ctx {
   uint32_t* gcov = nullptr;          // [NB][bw*bh] coverage tiles (debug)
   uint32_t* arrive = nullptr;        // [NB] fragment arrival counters
   Control* ctl = nullptr;
-  unsigned long long* st_k1 = nullptr; long long st_k1_cap = 0;
+  uint2* rect = nullptr;                 // [rec_cap] tile rect per triangle
+  int tri_chunk = EX_MAX_TRIS;           // triangles per expand chunk (adapted to P/T)
   unsigned long long* st_scan = nullptr; long long st_scan_n = 0;
-  unsigned long long* st_rx = nullptr; long long st_rx_chunks = 0;
+  unsigned long long* st_rx = nullptr; long long st_rx_chunks = 0;  // [npass][chunks][256]
+  unsigned long long* st_grp = nullptr;   // [npass][groups][256] group look-back words
+  uint32_t* ccount = nullptr;             // [npass][chunks][256] per-chunk digit counts
+  uint32_t* garr = nullptr;               // [npass][2][groups] group arrival counters
+  long long gcap = 0;
   // grid sizes of the last frame: the ticket/tag scheme of Control needs them
   // constant, so a change forces a reset of the control block + status words
-  long long last_g1 = -1, last_grx = -1;
+  long long last_grids[4] = {-1, -1, -1, -1};
   bool need_reset = true;
   bool pdl = true;
   int32_t* primid = nullptr;
@@ -102,6 +107,7 @@ struct piko_ctx {
   bool pending = false;              // a frame's status not yet checked
   int last_status = PIKO_OK;
   long long last_T = 0;
+  int last_kernels = 0;                // kernels launched by the last frame
 
 
   // end-to-end staging
@@ -177,7 +183,7 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   set_ownership(ctx, 0, 1);
   int bits = 0;
   while ((1ll << bits) < (long long)g.NB) ++bits;
-  ctx->npass = (bits + RX_BITS - 1) / RX_BITS;
+  ctx->npass = std::max(1, (bits + RX_BITS - 1) / RX_BITS);  // pass 0 also expands the pairs
   const long long npx = (long long)width * height;
   bool ok = cudaMalloc(&ctx->bin_count, sizeof(uint32_t) * g.NB) == cudaSuccess &&
             cudaMalloc(&ctx->bin_start, sizeof(int32_t) * (g.NB + 1)) == cudaSuccess &&
@@ -209,7 +215,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   cudaDeviceSynchronize();
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
-                  ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->st_k1, ctx->st_scan, ctx->st_rx, ctx->primid,
+                  ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
                   ctx->all_keys};
   for (void* p : bufs)
@@ -225,20 +231,41 @@ extern "C" const char* piko_last_error(const piko_ctx* ctx) {
 }
 
 // ---- capacity management ----------------------------------------------------
+static int alloc_rx_status(piko_ctx* ctx);
+
 static int ensure_tris(piko_ctx* ctx, long long T) {
   if (T > ctx->rec_cap) {
     long long cap = std::max<long long>(T, 1024);
     if (ctx->rec) cudaFree(ctx->rec);
+    if (ctx->rect) cudaFree(ctx->rect);
     ctx->rec = nullptr;
+    ctx->rect = nullptr;
     CK(cudaMalloc(&ctx->rec, sizeof(int4) * 3 * cap));
+    CK(cudaMalloc(&ctx->rect, sizeof(uint2) * cap));
     ctx->rec_cap = cap;
+    return alloc_rx_status(ctx);
   }
-  const long long chunks = std::max<long long>((T + K1_CHUNK - 1) / K1_CHUNK, 1);
-  if (chunks > ctx->st_k1_cap) {
-    if (ctx->st_k1) cudaFree(ctx->st_k1);
-    ctx->st_k1 = nullptr;
-    CK(cudaMalloc(&ctx->st_k1, sizeof(unsigned long long) * chunks));
-    ctx->st_k1_cap = chunks;
+  return PIKO_OK;
+}
+
+// look-back status words: enough chunks for the expand pass (>= 256 triangles
+// per chunk) and for the pair passes
+static int alloc_rx_status(piko_ctx* ctx) {
+  const long long chunks = std::max<long long>(
+      std::max<long long>((ctx->rec_cap + RX_THREADS - 1) / RX_THREADS,
+                          (long long)((ctx->pair_cap + RX_CHUNK - 1) / RX_CHUNK)), 1);
+  if (chunks > ctx->st_rx_chunks) {
+    for (void* p : {(void*)ctx->st_rx, (void*)ctx->st_grp, (void*)ctx->ccount, (void*)ctx->garr})
+      if (p) cudaFree(p);
+    ctx->st_rx = nullptr; ctx->st_grp = nullptr; ctx->ccount = nullptr; ctx->garr = nullptr;
+    const long long groups = (chunks + LB_GROUP - 1) / LB_GROUP;
+    CK(cudaMalloc(&ctx->st_rx, sizeof(unsigned long long) * RX_RADIX * chunks * ctx->npass));
+    CK(cudaMalloc(&ctx->ccount, sizeof(uint32_t) * RX_RADIX * chunks * ctx->npass));
+    CK(cudaMalloc(&ctx->st_grp, sizeof(unsigned long long) * RX_RADIX * groups * ctx->npass));
+    CK(cudaMalloc(&ctx->garr, sizeof(uint32_t) * 2 * groups * ctx->npass));
+    ctx->st_rx_chunks = chunks;
+    ctx->gcap = groups;
+    ctx->need_reset = true;
   }
   return PIKO_OK;
 }
@@ -255,12 +282,8 @@ static int ensure_pairs(piko_ctx* ctx, unsigned long long P) {
     CK(cudaMalloc(&ctx->keys[k], sizeof(uint32_t) * cap));
     CK(cudaMalloc(&ctx->vals[k], sizeof(int32_t) * cap));
   }
-  const long long chunks = (long long)((cap + RX_CHUNK - 1) / RX_CHUNK);
-  if (ctx->st_rx) cudaFree(ctx->st_rx);
-  ctx->st_rx = nullptr;
-  CK(cudaMalloc(&ctx->st_rx, sizeof(unsigned long long) * RX_RADIX * chunks * std::max(ctx->npass, 1)));
-  ctx->st_rx_chunks = chunks;
   ctx->pair_cap = cap;
+  if (alloc_rx_status(ctx) != PIKO_OK) return PIKO_ECUDA;
   const long long fcap = (long long)(cap / (unsigned long long)tile_frag(ctx->bw, ctx->bh)) + ctx->g.NB + 1;
   if (ctx->frag_list) cudaFree(ctx->frag_list);
   ctx->frag_list = nullptr;
@@ -300,24 +323,29 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   auto mark = [&](int stage) -> cudaError_t { return ev ? cudaEventRecord(ev[stage], s) : cudaSuccess; };
   const long long g1 = std::max<long long>((T + K1_CHUNK - 1) / K1_CHUNK, 1);
   const long long ntiles = (ctx->g.NB + SCAN_CHUNK - 1) / SCAN_CHUNK;
-  const long long grx = ctx->st_rx_chunks + ntiles;  // pass 0: sort chunks + scan tiles
+  const long long gx = std::max<long long>((T + ctx->tri_chunk - 1) / ctx->tri_chunk, 1);  // pass 0
+  const long long gp = (long long)((ctx->pair_cap + RX_CHUNK - 1) / RX_CHUNK);              // passes >= 1
+  const long long grids[4] = {g1, gx, gp + ntiles, ntiles};
   CK(mark(0));
-  if (ctx->need_reset || g1 != ctx->last_g1 || grx != ctx->last_grx) {
+  bool changed = ctx->need_reset;
+  for (int k = 0; k < 4; ++k) changed |= grids[k] != ctx->last_grids[k];
+  if (changed) {
     // tickets restart at 0, so every tag-carrying status word must be cleared
     CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s));
-    CK(cudaMemsetAsync(ctx->st_k1, 0, sizeof(unsigned long long) * ctx->st_k1_cap, s));
     CK(cudaMemsetAsync(ctx->st_scan, 0, sizeof(unsigned long long) * ctx->st_scan_n, s));
-    if (ctx->npass > 0)
-      CK(cudaMemsetAsync(ctx->st_rx, 0, sizeof(unsigned long long) * RX_RADIX * ctx->st_rx_chunks * ctx->npass, s));
+    CK(cudaMemsetAsync(ctx->st_rx, 0, sizeof(unsigned long long) * RX_RADIX * ctx->st_rx_chunks * ctx->npass, s));
+    CK(cudaMemsetAsync(ctx->st_grp, 0, sizeof(unsigned long long) * RX_RADIX * ctx->gcap * ctx->npass, s));
+    CK(cudaMemsetAsync(ctx->garr, 0, sizeof(uint32_t) * 2 * ctx->gcap * ctx->npass, s));
     CK(cudaMemsetAsync(ctx->bin_count, 0, sizeof(uint32_t) * ctx->g.NB, s));
     CK(cudaMemsetAsync(ctx->arrive, 0, sizeof(uint32_t) * ctx->g.NB, s));
     CK(cudaMemsetAsync(ctx->gkey, 0xFF, sizeof(unsigned long long) * ctx->g.NB * ctx->bw * ctx->bh, s));
     if (ctx->gcov) CK(cudaMemsetAsync(ctx->gcov, 0, sizeof(uint32_t) * ctx->g.NB * ctx->bw * ctx->bh, s));
-    ctx->last_g1 = g1;
-    ctx->last_grx = grx;
+    for (int k = 0; k < 4; ++k) ctx->last_grids[k] = grids[k];
     ctx->need_reset = false;
   }
   CK(mark(1 + PIKO_STAGE_CLEAR));
+  ctx->last_kernels = 3 + ctx->npass + (ctx->npass == 1 ? 1 : 0) + (V < 0 && T > 0 ? 1 : 0) +
+                      (gather && ctx->g.rank == 0 ? 1 : 0);
   if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
   {
     VertexArgs a{};
@@ -329,25 +357,30 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   {
     SetupArgs a{};
     a.xv = ctx->xv; a.xv_cap = ctx->xv_cap; a.idx = idx; a.n_tris = T; a.g = ctx->g;
-    a.npass = ctx->npass;
-    a.rec = ctx->rec; a.pair_keys = ctx->keys[0]; a.pair_vals = ctx->vals[0];
-    a.bin_count = ctx->bin_count; a.status = ctx->st_k1; a.ctl = ctx->ctl; a.cap = ctx->pair_cap;
+    a.npass = ctx->npass; a.rec = ctx->rec; a.rect = ctx->rect; a.ctl = ctx->ctl;
     CK(launch_setup(a, (int)g1, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_SETUP));
   for (int p = 0; p < ctx->npass; ++p) {
     RadixArgs a{};
+    a.expand = p == 0; a.rect = ctx->rect; a.n_tris = T; a.tri_chunk = ctx->tri_chunk;
+    a.g = ctx->g; a.cap = ctx->pair_cap; a.scan_here = p == 1;
     a.keys_in = ctx->keys[p & 1]; a.vals_in = ctx->vals[p & 1];
     a.keys_out = (p + 1 < ctx->npass) ? ctx->keys[(p + 1) & 1] : nullptr;
     a.vals_out = ctx->vals[(p + 1) & 1];
     a.status = ctx->st_rx + (size_t)p * RX_RADIX * ctx->st_rx_chunks;
+    a.ccount = ctx->ccount + (size_t)p * RX_RADIX * ctx->st_rx_chunks;
+    a.gstatus = ctx->st_grp + (size_t)p * RX_RADIX * ctx->gcap;
+    a.garrive = ctx->garr + (size_t)p * 2 * ctx->gcap;
+    a.gcap = ctx->gcap;
     a.ctl = ctx->ctl; a.pass = p; a.shift = RX_BITS * p;
     a.bin_count = ctx->bin_count; a.bin_start = ctx->bin_start; a.scan_status = ctx->st_scan;
     a.NB = ctx->g.NB; a.rank = ctx->g.rank; a.nranks = ctx->g.nranks;
     a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
     a.gcov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->gcov : nullptr;
     a.frag = tile_frag(ctx->bw, ctx->bh); a.npx = ctx->bw * ctx->bh;
-    CK(launch_radix_pass(a, (int)(p == 0 ? grx : ctx->st_rx_chunks), ctx->pdl, s));
+    CK(launch_radix_pass(a, (int)(p == 0 ? gx : gp + (p == 1 ? ntiles : 0)), ctx->pdl, s));
+    if (p == 0 && ctx->npass == 1) CK(launch_bin_scan(a, (int)ntiles, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_RADIX));
   {
@@ -362,6 +395,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.owned = ctx->owned;
     a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
     a.gcov = ctx->gcov; a.arrive = ctx->arrive; a.frag = tile_frag(ctx->bw, ctx->bh);
+    a.garrive = ctx->garr; a.gcap = ctx->gcap;
     const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, gather)));
     CK(launch_tile(a, ctx->bw, ctx->bh, grid, a.out_cov != nullptr, gather, ctx->pdl, s));
   }
@@ -408,6 +442,17 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   return PIKO_OK;
 }
 
+// Expand chunk for the next frames: about RX_CHUNK pairs per chunk given the
+// last frame's pairs per triangle (a power of two in [256, EX_MAX_TRIS]).
+static void adapt_tri_chunk(piko_ctx* ctx) {
+  const double T = (double)ctx->last_T, P = (double)ctx->h_ctl->n_pairs;
+  if (T <= 0) return;
+  const double want = P > 0 ? RX_CHUNK * T / P : (double)EX_MAX_TRIS;
+  int tc = RX_THREADS;
+  while (tc * 2 <= EX_MAX_TRIS && tc * 2 <= want) tc *= 2;
+  ctx->tri_chunk = tc;
+}
+
 // Wait for the pending frame; PIKO_ECAPACITY (and grown capacity) on overflow.
 static int check_frame(piko_ctx* ctx) {
   if (!ctx->pending) return ctx->last_status;
@@ -421,6 +466,7 @@ static int check_frame(piko_ctx* ctx) {
     return ctx->last_status;
   }
   ctx->last_status = PIKO_OK;
+  adapt_tri_chunk(ctx);
   return PIKO_OK;
 }
 
@@ -628,7 +674,7 @@ extern "C" int piko_get_stats(const piko_ctx* cctx, piko_stats* out) {
   out->pair_capacity = (int64_t)ctx->pair_cap;
   out->radix_passes = ctx->npass;
   const bool gather = ctx->comm && ctx->g.nranks > 1;
-  out->kernels_per_frame = 1 + ctx->npass + 1 + (gather && ctx->g.rank == 0 ? 1 : 0);
+  out->kernels_per_frame = ctx->last_kernels;
   return PIKO_OK;
 }
 

@@ -9,9 +9,10 @@
 namespace piko {
 
 // ---- launch geometry -------------------------------------------------------
-constexpr int K1_THREADS = 256;                     // vertex+setup+AssignBin CTA
+constexpr int K1_THREADS = 256;                     // triangle-setup CTA
 constexpr int K1_TPT = 4;                           // triangles per thread (strided)
-constexpr int K1_CHUNK = K1_THREADS * K1_TPT;       // triangles per look-back chunk
+constexpr int K1_CHUNK = K1_THREADS * K1_TPT;       // triangles per CTA
+constexpr int EX_MAX_TRIS = 4096;                   // triangles per expand chunk (radix pass 0)
 constexpr int SCAN_THREADS = 256;                   // bin-count scan (inside radix pass 0)
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
@@ -20,6 +21,7 @@ constexpr int RX_WARPS = RX_THREADS / 32;
 constexpr int RX_ITEMS = 16;
 constexpr int RX_CHUNK = RX_THREADS * RX_ITEMS;     // pairs per chunk
 constexpr int RX_BITS = 8;
+constexpr int LB_GROUP = 16;                        // chunks per look-back group
 constexpr int RX_RADIX = 1 << RX_BITS;
 constexpr int MAX_PASSES = 3;                       // NB <= 2^24 bins
 constexpr unsigned long long MAX_PAIRS = 1ull << 31;  // bin_start is int32
@@ -43,6 +45,7 @@ constexpr int EMPTY_GROUP = 8;   // empty bins per k_tile queue ticket
 struct Control {
   unsigned long long k1_ticket;
   unsigned long long rx_ticket[MAX_PASSES];
+  unsigned long long scan_ticket;      // standalone bin-scan kernel (single-pass grids)
   unsigned long long frame;            // written by K1 chunk 0
   unsigned int tile_next;              // dynamic bin queue of k_tile (reset by K1 chunk 0)
   unsigned int list_n[NLIST];          // work-list sizes (reset by K1 chunk 0)
@@ -98,20 +101,28 @@ struct SetupArgs {
   Grid g;
   int npass;
   int4* rec;                    // [n_tris][3]
-  uint32_t* pair_keys;          // [cap] bin id per pair
-  int32_t* pair_vals;           // [cap] primID per pair
-  uint32_t* bin_count;          // [NB] pairs per bin (zeroed by the bin scan)
-  unsigned long long* status;   // [grid] decoupled look-back
+  uint2* rect;                  // [n_tris] tile rect {tx0|ty0<<16, tx1|ty1<<16}; empty if culled
   Control* ctl;
-  unsigned long long cap;       // pair capacity
 };
 
 struct RadixArgs {
+  // pass 0 expands the (bin, primID) pairs of a chunk of triangles from rects
+  int expand;
+  const uint2* rect;
+  long long n_tris;
+  int tri_chunk;                // triangles per expand chunk (<= EX_MAX_TRIS)
+  Grid g;
+  unsigned long long cap;       // pair capacity (pass 0 checks P against it)
+  int scan_here;                // extra CTAs of this launch run the bin scan
   const uint32_t* keys_in;
   const int32_t* vals_in;
   uint32_t* keys_out;           // may be null on the last pass
   int32_t* vals_out;
-  unsigned long long* status;   // [sort chunks][RX_RADIX]
+  unsigned long long* status;   // [sort chunks][RX_RADIX] chunk look-back words
+  unsigned long long* gstatus;  // [groups][RX_RADIX] group look-back words
+  uint32_t* ccount;             // [sort chunks][RX_RADIX] per-chunk digit counts
+  uint32_t* garrive;            // [2][gcap] chunks of a group that published (by frame parity)
+  long long gcap;               // group capacity
   Control* ctl;
   int pass;
   int shift;
@@ -152,6 +163,8 @@ struct TileArgs {
   uint32_t* gcov;
   uint32_t* arrive;             // [NB] fragments merged so far (self-resetting)
   int frag;
+  uint32_t* garrive;            // [npass][2][gcap] look-back group arrival counters;
+  long long gcap;               //   k_tile zeroes the next frame's parity
 };
 
 struct ResolveArgs {            // rank 0 after the NCCL gather
@@ -172,6 +185,7 @@ cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool
 cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s);
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s);
 cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream_t s);
+cudaError_t launch_bin_scan(const RadixArgs& a, int grid, bool pdl, cudaStream_t s);
 cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
                         bool pdl, cudaStream_t s);
 int tile_grid(int bw, int bh, bool cov, bool keys_only);  // persistent grid size

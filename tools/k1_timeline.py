@@ -59,10 +59,15 @@ def show(name, t, phases, n):
 
 
 n1 = (s.n_tris + 1023) // 1024
-show("k_setup", buf[0], ["start", "loads", "setup", "scan", "lookback+count", "expand"], n1)
+kk = buf[0, :n1].astype(np.int64)
+kk = kk[kk[:, 0] > 0]
+b0 = kk[:, 0].min()
+print(f"== k_setup: {len(kk)} CTAs, span {kk[:, 5].max() - b0} ns; loads median {np.median(kk[:,1]-kk[:,0]):.0f}, "
+      f"setup median {np.median(kk[:,2]-kk[:,1]):.0f}, hist median {np.median(kk[:,5]-kk[:,2]):.0f}")
+nrx0 = int((buf[1, :, 0] > 0).sum())
+show("radix pass 0 (expand)", buf[1], ["start", "expand", "rank", "lookback", "scatter"], nrx0)
 nrx = (st["n_pairs"] + 4095) // 4096
-show("radix pass 0", buf[1], ["start", "load+prefix", "rank", "lookback", "scatter"], nrx)
-show("radix pass 1", buf[2], ["start", "load+prefix", "rank", "lookback", "scatter"], nrx)
+show("radix pass 1", buf[2], ["start", "load", "rank", "lookback", "scatter"], nrx)
 nb = st["owned_bins"]
 t = buf[3, :nb].astype(np.int64)
 base = t[:, 0].min()
