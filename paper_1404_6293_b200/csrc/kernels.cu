@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(256) k_index_max(const int32_t* __restrict__ i
 // ---------------------------------------------------------------------------
 constexpr int K1_BIG = 64;  // triangles with more owned bins go to the CTA-wide loop
 
-__global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
+__global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
   __shared__ unsigned s_hist[MAX_PASSES][RX_RADIX];
   __shared__ uint2 s_big[K1_CHUNK];
   __shared__ unsigned s_nbig;
@@ -334,20 +334,14 @@ __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
 
   pdl_wait();   // k_vertex output; the previous frame's kernels read rec / rect
   pdl_trigger();
+  // every CTA takes one ticket per frame: frame = ticket / gridDim.x (the
+  // triangle chunk is simply blockIdx.x -- nothing here depends on CTA order)
   if (tid == 0) { s_tk = atomicAdd(&a.ctl->k1_ticket, 1ull); s_live = 0; s_nbig = 0; }
   for (int i = tid; i < MAX_PASSES * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
-  __syncthreads();
-  const u64 frame = s_tk / gridDim.x;
-  const long long chunk = (long long)(s_tk % gridDim.x);
+  __syncthreads();  // histogram cleared before any thread adds to it
+  const long long chunk = blockIdx.x;
   const long long t0 = chunk * K1_CHUNK;
   K1_MARK(0);
-  if (chunk == 0 && tid == 0) {
-    a.ctl->frame = frame; a.ctl->tile_next = 0; a.ctl->vmax = 0;
-    for (int k = 0; k < NLIST; ++k) a.ctl->list_n[k] = 0;
-    a.ctl->empty_next = 0;
-    if (a.ctl->vx_overflow) { a.ctl->vx_overflow = 0; atomicMax(&a.ctl->overflow_tag, frame + 1); }
-  }
-
   // ---- loads first (all independent): indices, then vertex-stage records ---
   int vi[K1_TPT][3];
 #pragma unroll
@@ -397,10 +391,12 @@ __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
                          o.small ? REC_SMALL : 0);
         // digit histograms of the radix passes over this triangle's pairs
         if (c <= (unsigned)K1_BIG) {
-          for (unsigned j = 0; j < c; ++j) {
-            const int b = owned_bin_at(tx0, ty0, tx1, ty1, j, g);
-            for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], 1u);
-          }
+          for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) {
+              const int b = ty * g.binsX + tx;
+              if (g.nranks > 1 && b % g.nranks != g.rank) continue;
+              for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], 1u);
+            }
         } else {
           s_big[atomicAdd(&s_nbig, 1u)] = rr;
         }
@@ -411,6 +407,13 @@ __global__ void __launch_bounds__(K1_THREADS) k_setup(SetupArgs a) {
   K1_MARK(2);
   if (live) atomicAdd(&s_live, live);
   __syncthreads();
+  const u64 frame = s_tk / gridDim.x;
+  if (chunk == 0 && tid == 0) {
+    a.ctl->frame = frame; a.ctl->tile_next = 0; a.ctl->vmax = 0;
+    for (int k = 0; k < NLIST; ++k) a.ctl->list_n[k] = 0;
+    a.ctl->empty_next = 0;
+    if (a.ctl->vx_overflow) { a.ctl->vx_overflow = 0; atomicMax(&a.ctl->overflow_tag, frame + 1); }
+  }
   // large triangles: the whole CTA walks their bins
   const unsigned nbig = s_nbig;
   for (unsigned q = 0; q < nbig; ++q) {
@@ -767,12 +770,17 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
         if (c == 0) continue;
         const uint2 r2 = ex.rect[l];
         const int tx0 = r2.x & 0xffff, ty0 = r2.x >> 16, tx1 = r2.y & 0xffff, ty1 = r2.y >> 16;
-        const unsigned o = ex.off[l];
+        unsigned o = ex.off[l];
 #pragma unroll 1
-        for (unsigned j = 0; j < c; ++j) {
-          sm.keys[o + j] = (unsigned)owned_bin_at(tx0, ty0, tx1, ty1, j, a.g);
-          sm.vals[o + j] = (int)(t0 + l);
-        }
+        for (int ty = ty0; ty <= ty1; ++ty)
+#pragma unroll 1
+          for (int tx = tx0; tx <= tx1; ++tx) {
+            const int b = ty * a.g.binsX + tx;
+            if (a.g.nranks > 1 && b % a.g.nranks != a.g.rank) continue;
+            sm.keys[o] = (unsigned)b;
+            sm.vals[o] = (int)(t0 + l);
+            ++o;
+          }
       }
       __syncthreads();
 #pragma unroll
