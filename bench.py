@@ -122,13 +122,14 @@ def cpu_baseline(s, budget):
 
 
 def algorithmic_bytes(stage, T, V, L, P, NB, npx, ncov, npass):
-    """Bytes the method must move per launch of a stage (DESIGN.md 'Rooflines')."""
-    if stage == "vertex":     # positions in (16 B of each 32 B vertex), 16 B record out
+    """Bytes the method must move per launch of a stage (DESIGN.md section 6)."""
+    if stage == "vertex":     # 16 B positions in, 16 B vertex record out
         return 16 * V + 16 * V
-    if stage == "setup":      # idx + vertex records in; setup records + pairs out
-        return 12 * T + 16 * V + 48 * L + 8 * P
-    if stage == "radix":      # per pass 8 B in + 8 B out (last pass 4 B out); CSR scan
-        return (npass * 16 * P - (4 * P if npass else 0)) + 12 * NB
+    if stage == "setup":      # idx + vertex records in; setup records (live) + tile rects out
+        return 12 * T + 16 * V + 48 * L + 8 * T
+    if stage == "radix":      # expand: rects in, pairs out; later passes 8 B in / 8 B out
+        rest = max(npass - 1, 0) * 16 * P - (4 * P if npass > 1 else 0)
+        return 8 * T + 8 * P + rest + 12 * NB
     if stage == "tile":       # CSR + records in; 24 B/px out; winner re-gather
         return 4 * (NB + 1) + 4 * P + 48 * P + 24 * npx + (12 + 3 * 32) * ncov
     if stage == "resolve":

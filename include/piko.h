@@ -148,6 +148,34 @@ int piko_get_coverage(const piko_ctx *ctx, const uint32_t **d_covcount);
  * the partition on one GPU.  nranks == 1 restores the full frame.            */
 int piko_set_partition(piko_ctx *ctx, int rank, int nranks);
 
+/* The two device steps of the sort-first exchange, exposed so the multi-GPU
+ * data path can be exercised on one GPU (NCCL needs one device per rank).
+ * piko_draw_tile_keys: with a partition set (piko_set_partition), render this
+ *   rank's owned bins into packed 64-bit (depth, primID) tile keys -- exactly
+ *   the payload rank r sends to rank 0 in piko_draw.
+ *     d_tile_keys  device, u64[owned_max][bin_w*bin_h]; owned bin k is
+ *                  b = rank + k*nranks; pixel p = ly*bin_w + lx;
+ *                  0xFFFFFFFFFFFFFFFF = no fragment.  owned_max =
+ *                  ceil(NB / nranks); piko_tile_keys_count gives its length.
+ * piko_resolve_keys: rank 0's step after the gather: shade gathered keys
+ *     d_all_keys   device, u64[nranks][owned_max][bin_w*bin_h], rank-major
+ *   into out_rgba / out_depth (and the context's primID buffer).
+ * Scene arguments as in piko_draw_indexed.  Both are asynchronous on stream. */
+int piko_draw_tile_keys(piko_ctx *ctx, const float *verts, int64_t n_verts, const int32_t *idx,
+                        int32_t n_tris, const float mvp[16], const float light[3],
+                        uint64_t *d_tile_keys, void *stream);
+int piko_resolve_keys(piko_ctx *ctx, const float *verts, int64_t n_verts, const int32_t *idx,
+                      int32_t n_tris, const float mvp[16], const float light[3], int nranks,
+                      const uint64_t *d_all_keys, float *out_rgba, float *out_depth, void *stream);
+int64_t piko_tile_keys_count(const piko_ctx *ctx);
+
+/* Host-only (no CUDA): the bins owned by `rank` of `nranks` in payload order
+ * (owned bin k = rank + k*nranks, DirectMap round robin P:688) for a
+ * width x height screen in bin_w x bin_h bins.  Writes min(count, cap) bin ids
+ * to out_bins (may be NULL) and returns the count, or PIKO_EINVAL.          */
+int64_t piko_owned_bins(int width, int height, int bin_w, int bin_h, int rank, int nranks,
+                        int32_t *out_bins, int64_t cap);
+
 /* Multi-GPU sort-first: attach an NCCL communicator built from a
  * 128-byte ncclUniqueId that the caller broadcast to all ranks (e.g. through
  * torch.distributed).  Each rank transforms all triangles, rasterizes the bins

@@ -28,7 +28,10 @@ CLEAR_KEY = 0xFFFFFFFFFFFFFFFF
 
 
 def build(force: bool = False) -> str:
-    """Compile piko_oracle.c into libpiko_oracle.so (gcc; a checker, not the product)."""
+    """Compile piko_oracle.c into libpiko_oracle.so (gcc; a checker, not the product).
+    ORACLE_LIB overrides the library path (tools/oracle_mutations.py only)."""
+    if os.environ.get("ORACLE_LIB"):
+        return os.environ["ORACLE_LIB"]
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lm"])

@@ -23,7 +23,8 @@ PIKO_SYNC_CHECKED, PIKO_SYNC_ASYNC = 0, 1
 EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_set_sync",
            "piko_destroy", "piko_last_error", "piko_get_primid", "piko_get_bins",
            "piko_set_debug", "piko_get_coverage", "piko_set_partition", "piko_attach_comm",
-           "piko_get_stats", "piko_nccl_unique_id", "piko_draw_indexed", "piko_set_profiling", "piko_get_profile")
+           "piko_get_stats", "piko_nccl_unique_id", "piko_draw_indexed",
+           "piko_draw_tile_keys", "piko_resolve_keys", "piko_tile_keys_count", "piko_owned_bins", "piko_set_profiling", "piko_get_profile")
 STAGES = ("clear", "vertex", "setup", "radix", "tile", "gather", "resolve")
 
 
@@ -51,6 +52,10 @@ def _load():
         "piko_draw": ([P, P, P, ctypes.c_int32, P, P, P, P, P], I),
         "piko_draw_host": ([P, P, I64, P, ctypes.c_int32, P, P, P, P, P], I),
         "piko_draw_indexed": ([P, P, I64, P, ctypes.c_int32, P, P, P, P, P], I),
+        "piko_draw_tile_keys": ([P, P, I64, P, ctypes.c_int32, P, P, P, P], I),
+        "piko_resolve_keys": ([P, P, I64, P, ctypes.c_int32, P, P, I, P, P, P, P], I),
+        "piko_tile_keys_count": ([P], I64),
+        "piko_owned_bins": ([I, I, I, I, I, I, P, I64], I64),
         "piko_finish": ([P], I),
         "piko_set_sync": ([P, I], I),
         "piko_destroy": ([P], None),
@@ -141,6 +146,44 @@ def piko_draw_indexed(ctx, verts, n_verts, idx, n_tris, mvp, light, out_rgba, ou
                                 _f32x(light, 3), _dev_ptr(out_rgba, torch.float32, "out_rgba"),
                                 _dev_ptr(out_depth, torch.float32, "out_depth"), _stream_ptr(stream))
     return _check(ctx, rc) if check else rc
+
+
+def piko_owned_bins(width, height, bin_w, bin_h, rank, nranks):
+    """Owned bins of a rank in sort-first payload order (host-only, no CUDA)."""
+    import numpy as np
+    n = _lib.piko_owned_bins(width, height, bin_w, bin_h, rank, nranks, None, 0)
+    if n < 0:
+        raise PikoError(int(n), "bad arguments")
+    out = np.zeros(max(int(n), 1), np.int32)
+    _lib.piko_owned_bins(width, height, bin_w, bin_h, rank, nranks,
+                         out.ctypes.data_as(ctypes.c_void_p), int(n))
+    return out[:n]
+
+
+def piko_tile_keys_count(ctx):
+    return int(_lib.piko_tile_keys_count(ctx))
+
+
+def piko_draw_tile_keys(ctx, verts, idx, mvp, light, tile_keys, stream=None):
+    """This rank's owned bins as packed u64 tile keys (the sort-first payload)."""
+    import torch
+    rc = _lib.piko_draw_tile_keys(ctx, _dev_ptr(verts, torch.float32, "verts"), verts.shape[0],
+                                  _dev_ptr(idx, torch.int32, "idx"), idx.shape[0], _f32x(mvp, 16),
+                                  _f32x(light, 3), _dev_ptr(tile_keys, torch.int64, "tile_keys"),
+                                  _stream_ptr(stream))
+    return _check(ctx, rc)
+
+
+def piko_resolve_keys(ctx, verts, idx, mvp, light, nranks, all_keys, out_rgba, out_depth, stream=None):
+    """Rank 0's resolve of gathered tile keys (u64[nranks][owned_max][bw*bh])."""
+    import torch
+    rc = _lib.piko_resolve_keys(ctx, _dev_ptr(verts, torch.float32, "verts"), verts.shape[0],
+                                _dev_ptr(idx, torch.int32, "idx"), idx.shape[0], _f32x(mvp, 16),
+                                _f32x(light, 3), int(nranks),
+                                _dev_ptr(all_keys, torch.int64, "all_keys"),
+                                _dev_ptr(out_rgba, torch.float32, "out_rgba"),
+                                _dev_ptr(out_depth, torch.float32, "out_depth"), _stream_ptr(stream))
+    return _check(ctx, rc)
 
 
 def piko_draw_host(ctx, verts, idx, mvp, light, out_rgba, out_depth, stream=None):

@@ -120,6 +120,7 @@ struct piko_ctx {
   unsigned long long* tile_keys = nullptr;  // [owned_max][bw*bh]
   unsigned long long* all_keys = nullptr;   // rank 0: [nranks][owned_max][bw*bh]
   int owned_max = 0;
+  bool keys_mode = false;                   // inside piko_draw_tile_keys
 
   // profiling: PIKO_NUM_STAGES + 1 boundary events per frame
   bool prof = false;
@@ -154,11 +155,13 @@ struct piko_ctx {
                        __FILE__, __LINE__);                                         \
   } while (0)
 
+extern "C" int64_t piko_owned_bins(int, int, int, int, int, int, int32_t*, int64_t);
+
 static void set_ownership(piko_ctx* ctx, int rank, int nranks) {
   ctx->g.rank = rank;
   ctx->g.nranks = nranks;
-  ctx->owned = rank < ctx->g.NB ? (ctx->g.NB - rank + nranks - 1) / nranks : 0;
-  ctx->owned_max = (ctx->g.NB + nranks - 1) / nranks;
+  ctx->owned = (int)piko_owned_bins(ctx->g.W, ctx->g.H, ctx->bw, ctx->bh, rank, nranks, nullptr, 0);
+  ctx->owned_max = (int)piko_owned_bins(ctx->g.W, ctx->g.H, ctx->bw, ctx->bh, 0, nranks, nullptr, 0);
 }
 
 extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
@@ -316,8 +319,9 @@ static int ensure_cov(piko_ctx* ctx) {
 // ---- one frame ---------------------------------------------------------------
 static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
                          long long T, const Mat4& M, const float L[3], float* rgba, float* depth,
-                         cudaStream_t s) {
-  const bool gather = ctx->comm != nullptr && ctx->g.nranks > 1;
+                         cudaStream_t s, unsigned long long* keys_out = nullptr) {
+  const bool gather = keys_out == nullptr && ctx->comm != nullptr && ctx->g.nranks > 1;
+  const bool keys_only = gather || keys_out != nullptr;
   cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
   if (ctx->prof && !ev) return ctx->fail(PIKO_ECUDA, "cannot create profiling events");
   auto mark = [&](int stage) -> cudaError_t { return ev ? cudaEventRecord(ev[stage], s) : cudaSuccess; };
@@ -391,13 +395,14 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.bin_prims = ctx->vals[ctx->npass & 1]; a.ctl = ctx->ctl;
     a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
     a.out_cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
-    a.tile_keys = gather ? ctx->tile_keys : nullptr;
+    a.tile_keys = keys_out ? keys_out : gather ? ctx->tile_keys : nullptr;
     a.owned = ctx->owned;
     a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
     a.gcov = ctx->gcov; a.arrive = ctx->arrive; a.frag = tile_frag(ctx->bw, ctx->bh);
     a.garrive = ctx->garr; a.gcap = ctx->gcap;
-    const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, gather)));
-    CK(launch_tile(a, ctx->bw, ctx->bh, grid, a.out_cov != nullptr, gather, ctx->pdl, s));
+    if (keys_only) a.out_cov = nullptr;
+    const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, keys_only)));
+    CK(launch_tile(a, ctx->bw, ctx->bh, grid, a.out_cov != nullptr, keys_only, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_TILE));
   if (gather) {
@@ -482,7 +487,7 @@ static int validate_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, 
                          float L[3]) {
   if (n_tris < 0) return ctx->fail(PIKO_EINVAL, "n_tris < 0");
   if (!mvp || !light) return ctx->fail(PIKO_EINVAL, "mvp and light must be non-null");
-  const bool need_out = !(ctx->comm && ctx->g.nranks > 1 && ctx->g.rank != 0);
+  const bool need_out = !(ctx->comm && ctx->g.nranks > 1 && ctx->g.rank != 0) && !ctx->keys_mode;
   if (need_out && (!rgba || !depth)) return ctx->fail(PIKO_EINVAL, "null output buffer");
   if (n_tris > 0 && (!verts || !idx)) return ctx->fail(PIKO_EINVAL, "null scene buffer");
   if ((reinterpret_cast<uintptr_t>(verts) | reinterpret_cast<uintptr_t>(idx) |
@@ -498,7 +503,8 @@ static int validate_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, 
 
 static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
                      int32_t n_tris, const float mvp[16], const float light[3], float* rgba,
-                     float* depth, cudaStream_t s, bool force_check) {
+                     float* depth, cudaStream_t s, bool force_check,
+                     unsigned long long* keys_out = nullptr) {
   float L[3] = {0.0f, 0.0f, 0.0f};
   int rc = validate_draw(ctx, verts, idx, n_tris, mvp, light, rgba, depth, L);
   if (rc != PIKO_OK) return rc;
@@ -517,7 +523,7 @@ static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32
     return rc;
   if ((rc = ensure_cov(ctx)) != PIKO_OK) return rc;
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if ((rc = enqueue_frame(ctx, verts, V, idx, n_tris, M, L, rgba, depth, s)) != PIKO_OK)
+    if ((rc = enqueue_frame(ctx, verts, V, idx, n_tris, M, L, rgba, depth, s, keys_out)) != PIKO_OK)
       return frame_failed(ctx, rc);
     if (ctx->sync_mode == PIKO_SYNC_ASYNC && !force_check) return prev == PIKO_ECAPACITY ? PIKO_OK : prev;
     rc = check_frame(ctx);
@@ -710,4 +716,66 @@ extern "C" int piko_get_profile(piko_ctx* ctx, double ms[PIKO_NUM_STAGES], int64
   }
   *frames = ctx->prof_frames;
   return PIKO_OK;
+}
+
+extern "C" int64_t piko_tile_keys_count(const piko_ctx* ctx) {
+  if (!ctx) return PIKO_EINVAL;
+  return (int64_t)ctx->owned_max * ctx->bw * ctx->bh;
+}
+
+extern "C" int piko_draw_tile_keys(piko_ctx* ctx, const float* verts, int64_t n_verts,
+                                   const int32_t* idx, int32_t n_tris, const float mvp[16],
+                                   const float light[3], uint64_t* d_tile_keys, void* stream) {
+  if (!ctx) return PIKO_EINVAL;
+  if (!d_tile_keys) return ctx->fail(PIKO_EINVAL, "null tile-key buffer");
+  if (n_verts < 0 || (n_tris > 0 && n_verts < 1)) return ctx->fail(PIKO_EINVAL, "bad n_verts");
+  ctx->keys_mode = true;
+  const int rc = draw_impl(ctx, verts, n_verts, idx, n_tris, mvp, light, nullptr, nullptr,
+                           static_cast<cudaStream_t>(stream), false,
+                           reinterpret_cast<unsigned long long*>(d_tile_keys));
+  ctx->keys_mode = false;
+  return rc;
+}
+
+extern "C" int piko_resolve_keys(piko_ctx* ctx, const float* verts, int64_t n_verts,
+                                 const int32_t* idx, int32_t n_tris, const float mvp[16],
+                                 const float light[3], int nranks, const uint64_t* d_all_keys,
+                                 float* out_rgba, float* out_depth, void* stream) {
+  if (!ctx) return PIKO_EINVAL;
+  if (!d_all_keys || !out_rgba || !out_depth || !mvp || !light)
+    return ctx->fail(PIKO_EINVAL, "null argument");
+  if (nranks < 1 || n_verts < 0 || n_tris < 0) return ctx->fail(PIKO_EINVAL, "bad size");
+  float L[3];
+  int rc = validate_draw(ctx, verts, idx, n_tris, mvp, light, out_rgba, out_depth, L);
+  if (rc != PIKO_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  if ((rc = ensure_verts(ctx, std::max<int64_t>(n_verts, 1))) != PIKO_OK) return rc;
+  Mat4 M;
+  memcpy(M.m, mvp, sizeof M.m);
+  VertexArgs va{};
+  va.verts = verts; va.n_verts = n_verts; va.cap = ctx->xv_cap; va.ctl = ctx->ctl; va.M = M;
+  va.W = ctx->g.W; va.H = ctx->g.H; va.xv = ctx->xv;
+  CK(launch_vertex(va, false, s));
+  ResolveArgs a{};
+  a.verts = verts; a.xv = ctx->xv; a.idx = idx;
+  a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
+  a.g = ctx->g; a.g.nranks = nranks; a.g.rank = 0;
+  a.all_keys = reinterpret_cast<const unsigned long long*>(d_all_keys);
+  a.owned_max = (ctx->g.NB + nranks - 1) / nranks;
+  a.out_rgba = out_rgba; a.out_depth = out_depth; a.out_primid = ctx->primid;
+  CK(launch_resolve(a, s));
+  return PIKO_OK;
+}
+
+extern "C" int64_t piko_owned_bins(int width, int height, int bin_w, int bin_h, int rank,
+                                   int nranks, int32_t* out_bins, int64_t cap) {
+  if (width < 1 || height < 1 || !pow2_in(bin_w, 8, 64) || !pow2_in(bin_h, 8, 64) || nranks < 1 ||
+      rank < 0 || rank >= nranks || cap < 0)
+    return PIKO_EINVAL;
+  const int64_t NB = (int64_t)((width + bin_w - 1) / bin_w) * ((height + bin_h - 1) / bin_h);
+  int64_t n = 0;
+  for (int64_t b = rank; b < NB; b += nranks, ++n)
+    if (out_bins && n < cap) out_bins[n] = (int32_t)b;
+  return n;
 }

@@ -259,9 +259,17 @@ def test_depth_vs_exact_plane(oracle_lib):
 
 
 def test_depth_range_discard(oracle_lib):
-    """Per-pixel z in [0,1] discard (R3): a triangle at zw = 1.25 is covered
-    but never wins; at exactly zw = 1.0 it is kept."""
+    """Per-pixel z in [0,1] discard (R3): a triangle at zw = 1.25 is covered but
+    never drawn (alone: background); one at zw = -0.25 in front of zw = 0.5 is
+    discarded (it would win the key comparison if kept); zw = 1.0 is kept."""
     tri = [(2.0, 2.0), (30.0, 4.0), (6.0, 28.0)]
+    v, i, m = pixel_scene([tri], [[1.25] * 3], 32, 32)
+    r = render(oracle_lib, v, i, m, 32, 32)
+    assert r["covcount"].sum() > 300 and (r["primid"] == -1).all()
+    v, i, m = pixel_scene([tri, tri], [[0.5] * 3, [-0.25] * 3], 32, 32)
+    r = render(oracle_lib, v, i, m, 32, 32)
+    cov = r["covcount"] > 0
+    assert (r["primid"][cov] == 0).all() and (r["depth"][cov] == 0.5).all()
     v, i, m = pixel_scene([tri, tri], [[1.25] * 3, [1.0] * 3], 32, 32)
     r = render(oracle_lib, v, i, m, 32, 32)
     cov = r["covcount"] > 0

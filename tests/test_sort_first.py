@@ -1,0 +1,130 @@
+"""Sort-first multi-GPU path (DirectMap round robin P:688).
+
+* CPU (gloo, world_size 2): the exchange protocol -- every rank packs the keys
+  of the bins it owns (library's host-only plan, piko_owned_bins) in payload
+  order, rank 0 gathers rank-major and unpacks with the resolve kernel's
+  indexing; the reassembled key image equals the oracle's.
+* GPU: the device data path on one GPU -- per-rank packed tile keys from the
+  tile kernel (piko_draw_tile_keys), concatenated rank-major, resolved by the
+  rank-0 kernel (piko_resolve_keys) == the oracle frame, bit-exact.  (NCCL
+  itself needs one GPU per rank; the transport is a byte copy of these buffers.)
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import scenes
+
+W, H, BW = 200, 120, 16
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _pack(keys_img, owned, bw, bh, binsX):
+    out = np.full((len(owned), bw * bh), np.uint64(0xFFFFFFFFFFFFFFFF), np.uint64)
+    for k, b in enumerate(owned):
+        by, bx = divmod(int(b), binsX)
+        tile = keys_img[by * bh:(by + 1) * bh, bx * bw:(bx + 1) * bw]
+        out[k].reshape(bh, bw)[:tile.shape[0], :tile.shape[1]] = tile
+    return out
+
+
+def _unpack(all_keys, R, owned_max, bw, bh, W_, H_):
+    """k_resolve's indexing: pixel -> bin b -> rank b % R, slot b // R."""
+    binsX = -(-W_ // bw)
+    img = np.empty((H_, W_), np.uint64)
+    for y in range(H_):
+        for x in range(W_):
+            b = (y // bh) * binsX + x // bw
+            img[y, x] = all_keys[b % R, b // R, (y % bh) * bw + (x % bw)]
+    return img
+
+
+def _gloo_worker(rank, world, port, keys_img, result):
+    import torch
+    import torch.distributed as dist
+    import paper_1404_6293_b200 as piko
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    binsX = -(-W // BW)
+    owned = piko.piko_owned_bins(W, H, BW, BW, rank, world)
+    owned_max = len(piko.piko_owned_bins(W, H, BW, BW, 0, world))
+    payload = np.full((owned_max, BW * BW), np.uint64(0xFFFFFFFFFFFFFFFF), np.uint64)
+    payload[:len(owned)] = _pack(keys_img, owned, BW, BW, binsX)
+    t = torch.from_numpy(payload.view(np.int64))
+    gathered = [torch.empty_like(t) for _ in range(world)] if rank == 0 else None
+    dist.gather(t, gathered, dst=0)
+    if rank == 0:
+        all_keys = np.stack([g.numpy().view(np.uint64) for g in gathered])
+        result["img"] = _unpack(all_keys, world, owned_max, BW, BW, W, H)
+    dist.destroy_process_group()
+
+
+def test_owned_bins_partition():
+    import paper_1404_6293_b200 as piko
+    NB = (-(-W // BW)) * (-(-H // BW))
+    for R in (1, 2, 3, 4, 8):
+        seen = np.concatenate([piko.piko_owned_bins(W, H, BW, BW, r, R) for r in range(R)])
+        assert sorted(seen.tolist()) == list(range(NB))
+
+
+def test_gloo_exchange_reassembles_frame(oracle_lib):
+    import multiprocessing as mp
+    import threading
+    s = scenes.scene_soup(4000, W, H, seed=71, name="soup")
+    keys = oracle_lib.render(s.verts, s.idx, s.mvp, s.light, W, H, want_keys=True)["keys"]
+    port = _free_port()
+    result = {}
+    # rank 1 in a subprocess, rank 0 in this process
+    ctx = mp.get_context("spawn")
+    p = ctx.Process(target=_gloo_worker, args=(1, 2, port, keys, {}))
+    p.start()
+    _gloo_worker(0, 2, port, keys, result)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    assert np.array_equal(result["img"], keys)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("R", [2, 3, 4])
+def test_gpu_tile_keys_gather_resolve(oracle_lib, R):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1404_6293_b200 as piko
+    s = scenes.scene_c2()
+    dev = torch.device("cuda:0")
+    v = torch.from_numpy(s.verts).to(dev)
+    i = torch.from_numpy(s.idx).to(dev)
+    renderers = [piko.Renderer(s.W, s.H, 16, device=dev) for _ in range(R)]
+    for r, rd in enumerate(renderers):
+        piko.piko_set_partition(rd.ctx, r, R)
+    n = piko.piko_tile_keys_count(renderers[0].ctx)
+    all_keys = torch.empty((R, n), dtype=torch.int64, device=dev)
+    for r, rd in enumerate(renderers):
+        piko.piko_draw_tile_keys(rd.ctx, v, i, s.mvp, s.light, all_keys[r])
+    r0 = renderers[0]
+    piko.piko_resolve_keys(r0.ctx, v, i, s.mvp, s.light, R, all_keys, r0.rgba, r0.depth)
+    torch.cuda.synchronize()
+    ref = oracle_lib.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
+    assert np.array_equal(r0.primid().cpu().numpy(), ref["primid"])
+    assert np.array_equal(r0.depth.cpu().numpy().view(np.uint32), ref["depth"].view(np.uint32))
+    assert np.abs(r0.rgba.cpu().numpy() - ref["rgba"]).max() <= 1e-5
+    # the gathered payload itself: every pixel's key is the oracle's
+    keys = oracle_lib.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H, want_keys=True)["keys"]
+    owned_max = n // (16 * 16)
+    img = _unpack(all_keys.cpu().numpy().view(np.uint64).reshape(R, owned_max, 256), R, owned_max,
+                  16, 16, s.W, s.H)
+    assert np.array_equal(img, keys)
+    for rd in renderers:
+        rd.close()
