@@ -37,12 +37,12 @@ M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
      "sm__throughput.avg.pct_of_peak_sustained_elapsed",
      "smsp__issue_active.avg.pct_of_peak_sustained_active",
      "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-     "launch__grid_size", "lts__t_bytes.sum"]
+     "launch__grid_size"]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(M)],
                      capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
 hh, units = rr[0], rr[1]
-cols = [hh.index(m) for m in M]
+cols = [hh.index(m) for m in M if m in hh]
 k2 = hh.index("Kernel Name")
 summ = [f"# ncu --set full ({tag}), one launch per kernel of one frame ({cfg}, {bw}x{bw} bins)",
         "# kernel, " + ", ".join(f"{hh[c]} [{units[c]}]" for c in cols)]
