@@ -748,6 +748,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
       }
     }
     __syncthreads();
+    RX_MARK(5);
     unsigned sum = 0;
 #pragma unroll 1
     for (int k = 0; k < tpt; ++k) sum += ex.cnt[cpad(tid * tpt + k)];
@@ -761,6 +762,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     __syncthreads();
     n = sm.n;
     fast = n <= RX_CHUNK;
+    RX_MARK(6);
     if (fast) {  // expand into shared memory, thread per triangle (coalesced order)
 #pragma unroll 1
       for (int k = 0; k < tpt; ++k) {
@@ -783,6 +785,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
           }
       }
       __syncthreads();
+      RX_MARK(7);
 #pragma unroll
       for (int j = 0; j < RX_ITEMS; ++j) {
         const unsigned pos = wb + j * 32;
@@ -1076,7 +1079,7 @@ __device__ __forceinline__ void store_pixel(const TileArgs& a, const float L[3],
 }
 
 template <int BW, int BH, int THREADS, bool COV, bool KEYS_ONLY>
-__global__ void __launch_bounds__(THREADS, THREADS >= 256 ? 3 : 8) k_tile(TileArgs a) {
+__global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(TileArgs a) {
   constexpr int NPX = BW * BH;
   constexpr int PPT = (NPX + THREADS - 1) / THREADS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1471,7 +1474,7 @@ struct TileKernel {
 template <int BW, int BH>
 static TileKernel tile_kernel_t(bool cov, bool keys_only) {
   constexpr int NPX = BW * BH;
-  constexpr int THREADS = NPX < 256 ? NPX : 256;
+  constexpr int THREADS = NPX < TILE_THREADS ? NPX : TILE_THREADS;
   TileKernel k;
   k.threads = THREADS;
   k.smem = sizeof(TileSmem<BW, BH, THREADS>) + (cov ? (size_t)NPX * 4 : 0);

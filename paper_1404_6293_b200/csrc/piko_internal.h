@@ -189,7 +189,8 @@ cudaError_t launch_bin_scan(const RadixArgs& a, int grid, bool pdl, cudaStream_t
 cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
                         bool pdl, cudaStream_t s);
 int tile_grid(int bw, int bh, bool cov, bool keys_only);  // persistent grid size
-inline int tile_threads(int bw, int bh) { return bw * bh < 256 ? bw * bh : 256; }
+constexpr int TILE_THREADS = 256;  // k_tile CTA size cap
+inline int tile_threads(int bw, int bh) { return bw * bh < TILE_THREADS ? bw * bh : TILE_THREADS; }
 inline int tile_frag(int bw, int bh) { return FRAG_ROUNDS * tile_threads(bw, bh); }
 cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s);
 

@@ -66,6 +66,10 @@ print(f"== k_setup: {len(kk)} CTAs, span {kk[:, 5].max() - b0} ns; loads median 
       f"setup median {np.median(kk[:,2]-kk[:,1]):.0f}, hist median {np.median(kk[:,5]-kk[:,2]):.0f}")
 nrx0 = int((buf[1, :, 0] > 0).sum())
 show("radix pass 0 (expand)", buf[1], ["start", "expand", "rank", "lookback", "scatter"], nrx0)
+e = buf[1, :nrx0].astype(np.int64)
+print("   expand detail: loads+counts median %.0f, scan %.0f, expansion %.0f, reload %.0f" % (
+    np.median(e[:, 5] - e[:, 0]), np.median(e[:, 6] - e[:, 5]), np.median(e[:, 7] - e[:, 6]),
+    np.median(e[:, 1] - e[:, 7])))
 nrx = (st["n_pairs"] + 4095) // 4096
 show("radix pass 1", buf[2], ["start", "load", "rank", "lookback", "scatter"], nrx)
 nb = st["owned_bins"]
