@@ -56,6 +56,13 @@ enum {
 /* piko_set_debug flags */
 #define PIKO_DEBUG_COVERAGE_COUNT 1u /* count covering triangles per pixel   */
 
+/* piko_set_pipeline pipelines */
+#define PIKO_PIPE_BINNED 0   /* default: the binned rasterizer (sec. 7.2.2)   */
+#define PIKO_PIPE_FREEPIPE 1 /* FreePipe design alternative (sec. 7.2.1,
+                                P:1273-1294): one fused kernel, one thread per
+                                triangle, full-screen 64-bit atomicMin keys, a
+                                resolve/shade pass; no bin lists, one GPU.   */
+
 /* piko_set_sync modes */
 #define PIKO_SYNC_CHECKED 0 /* default: piko_draw waits for the frame, checks
                                the pair capacity, regrows and re-issues on
@@ -119,6 +126,11 @@ int piko_finish(piko_ctx *ctx);
 
 /* Select PIKO_SYNC_CHECKED (default) or PIKO_SYNC_ASYNC.                      */
 int piko_set_sync(piko_ctx *ctx, int mode);
+
+/* Select the pipeline (PIKO_PIPE_BINNED or PIKO_PIPE_FREEPIPE).  Outputs are
+ * identical; FreePipe produces no bin lists (piko_get_bins -> PIKO_ESTATE)
+ * and does not support partitions or communicators (PIKO_ESTATE).            */
+int piko_set_pipeline(piko_ctx *ctx, int pipeline);
 
 /* Destroy; NULL-safe; synchronises internal work first.                       */
 void piko_destroy(piko_ctx *ctx);

@@ -18,13 +18,15 @@ LIB_PATH = os.path.join(_HERE, "libpiko.so")
 PIKO_OK, PIKO_EINVAL, PIKO_ENOMEM, PIKO_ECUDA, PIKO_ENCCL, PIKO_ECAPACITY, PIKO_ESTATE = 0, -1, -2, -3, -4, -5, -6
 PIKO_DEBUG_COVERAGE_COUNT = 1
 PIKO_SYNC_CHECKED, PIKO_SYNC_ASYNC = 0, 1
+PIKO_PIPE_BINNED, PIKO_PIPE_FREEPIPE = 0, 1
 
 # names of every symbol include/piko.h declares (checked by tests)
 EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_set_sync",
            "piko_destroy", "piko_last_error", "piko_get_primid", "piko_get_bins",
            "piko_set_debug", "piko_get_coverage", "piko_set_partition", "piko_attach_comm",
            "piko_get_stats", "piko_nccl_unique_id", "piko_draw_indexed",
-           "piko_draw_tile_keys", "piko_resolve_keys", "piko_tile_keys_count", "piko_owned_bins", "piko_set_profiling", "piko_get_profile")
+           "piko_draw_tile_keys", "piko_resolve_keys", "piko_tile_keys_count", "piko_owned_bins",
+           "piko_set_pipeline", "piko_set_profiling", "piko_get_profile")
 STAGES = ("clear", "vertex", "setup", "radix", "tile", "gather", "resolve")
 
 
@@ -56,6 +58,7 @@ def _load():
         "piko_resolve_keys": ([P, P, I64, P, ctypes.c_int32, P, P, I, P, P, P, P], I),
         "piko_tile_keys_count": ([P], I64),
         "piko_owned_bins": ([I, I, I, I, I, I, P, I64], I64),
+        "piko_set_pipeline": ([P, I], I),
         "piko_finish": ([P], I),
         "piko_set_sync": ([P, I], I),
         "piko_destroy": ([P], None),
@@ -204,6 +207,10 @@ def piko_finish(ctx):
 
 def piko_set_sync(ctx, mode):
     return _check(ctx, _lib.piko_set_sync(ctx, mode))
+
+
+def piko_set_pipeline(ctx, pipeline):
+    return _check(ctx, _lib.piko_set_pipeline(ctx, pipeline))
 
 
 def piko_get_primid(ctx):

@@ -1378,6 +1378,85 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(TileArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// FreePipe (NEXT-3 design alternative): the whole pipeline fused
+// into one kernel with static (DirectMap) triangle -> thread mapping; fragments
+// meet in a full-screen key buffer through 64-bit atomicMin (deterministic:
+// the min is order independent), then one resolve pass shades.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_freepipe(FreePipeArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int TPT = 4;
+  const long long tb = (long long)blockIdx.x * (256 * TPT) + threadIdx.x;
+  int vi[TPT][3];
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const long long t = tb + k * 256;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      vi[k][c] = t < a.n_tris ? __ldg(a.idx + 3 * t + c) : -1;
+      if (vi[k][c] >= a.xv_cap) vi[k][c] = -1;
+    }
+  }
+  int4 cv[TPT][3];
+#pragma unroll
+  for (int k = 0; k < TPT; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      cv[k][c] = vi[k][c] >= 0 ? __ldg(a.xv + vi[k][c]) : make_int4(VX_CULLED, 0, 0, 0);
+#pragma unroll 1
+  for (int k = 0; k < TPT; ++k) {
+    const long long t = tb + k * 256;
+    Tri o;
+    if (t >= a.n_tris ||
+        !setup_tri(cv[k][0], cv[k][1], cv[k][2], vi[k][0], vi[k][1], vi[k][2], a.W, a.H, o))
+      continue;
+    const float dx1 = __int2float_rn(o.X1 - o.X0), dy1 = __int2float_rn(o.Y1 - o.Y0);
+    const float dx2 = __int2float_rn(o.X2 - o.X0), dy2 = __int2float_rn(o.Y2 - o.Y0);
+    const float dz1 = __fsub_rn(o.zw1, o.zw0), dz2 = __fsub_rn(o.zw2, o.zw0);
+    const float inv = __fdiv_rn(1.0f, __ll2float_rn(o.area2));
+    RecView r;
+    r.X0 = o.X0; r.Y0 = o.Y0; r.X1 = o.X1; r.Y1 = o.Y1; r.X2 = o.X2; r.Y2 = o.Y2;
+    r.zw0 = o.zw0;
+    r.za = __fmul_rn(__fmaf_rn(dz1, dy2, -__fmul_rn(dz2, dy1)), inv);
+    r.zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
+    r.px0 = o.px0; r.py0 = o.py0; r.px1 = o.px1; r.py1 = o.py1;
+    r.small = o.small;
+    for (int y = o.py0; y <= o.py1; ++y)
+      for (int x = o.px0; x <= o.px1; ++x) {
+        bool cov;
+        const u64 key = eval_key(r, 256 * x + 128, 256 * y + 128, (int)t, cov);
+        const size_t p = (size_t)y * a.W + x;
+        if (a.cov && cov) atomicAdd(&a.cov[p], 1u);
+        if (key != CLEAR_KEY) atomicMin(&a.keys[p], key);
+      }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fp_resolve(FreePipeArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const long long p = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (p >= (long long)a.W * a.H) return;
+  const int x = (int)(p % a.W), y = (int)(p / a.W);
+  const u64 key = a.keys[p];
+  a.keys[p] = CLEAR_KEY;  // ready for the next frame
+  float L[3];
+  normalise_light(a.light, L);
+  float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+  float depth = 1.0f;
+  int prim = -1;
+  if (key != CLEAR_KEY) {
+    prim = (int)(unsigned)(key & 0xFFFFFFFFu);
+    depth = __uint_as_float((unsigned)(key >> 32));
+    c = shade(a.verts, a.xv, a.idx, a.W, a.H, L, prim, 256 * x + 128, 256 * y + 128);
+  }
+  reinterpret_cast<float4*>(a.out_rgba)[p] = c;
+  a.out_depth[p] = depth;
+  a.out_primid[p] = prim;
+}
+
+// ---------------------------------------------------------------------------
 // K7 (multi-GPU rank 0): resolve gathered tile keys -> shaded frame
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_resolve(ResolveArgs a) {
@@ -1514,6 +1593,15 @@ int tile_grid(int bw, int bh, bool cov, bool keys_only) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.threads, k.smem);
   }
   return sms * (occ > 0 ? occ : 1);
+}
+
+cudaError_t launch_freepipe(const FreePipeArgs& a, bool pdl, cudaStream_t s) {
+  const long long grid = (a.n_tris + 1023) / 1024;
+  return launch_ex(k_freepipe, (int)(grid > 0 ? grid : 1), 256, 0, pdl, s, a);
+}
+cudaError_t launch_fp_resolve(const FreePipeArgs& a, bool pdl, cudaStream_t s) {
+  const long long grid = ((long long)a.W * a.H + 255) / 256;
+  return launch_ex(k_fp_resolve, (int)grid, 256, 0, pdl, s, a);
 }
 
 cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s) {

@@ -121,6 +121,8 @@ struct piko_ctx {
   unsigned long long* all_keys = nullptr;   // rank 0: [nranks][owned_max][bw*bh]
   int owned_max = 0;
   bool keys_mode = false;                   // inside piko_draw_tile_keys
+  int pipeline = PIKO_PIPE_BINNED;
+  unsigned long long* fp_keys = nullptr;    // FreePipe full-screen key buffer
 
   // profiling: PIKO_NUM_STAGES + 1 boundary events per frame
   bool prof = false;
@@ -220,7 +222,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
                   ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
-                  ctx->all_keys};
+                  ctx->all_keys, ctx->fp_keys};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -317,9 +319,58 @@ static int ensure_cov(piko_ctx* ctx) {
 }
 
 // ---- one frame ---------------------------------------------------------------
+static int enqueue_freepipe(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
+                            long long T, const Mat4& M, const float L[3], float* rgba, float* depth,
+                            cudaStream_t s) {
+  cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
+  auto mark = [&](int stage) -> cudaError_t { return ev ? cudaEventRecord(ev[stage], s) : cudaSuccess; };
+  const size_t npx = (size_t)ctx->g.W * ctx->g.H;
+  CK(mark(0));
+  if (!ctx->fp_keys) {
+    CK(cudaMalloc(&ctx->fp_keys, sizeof(unsigned long long) * npx));
+    CK(cudaMemsetAsync(ctx->fp_keys, 0xFF, sizeof(unsigned long long) * npx, s));
+  }
+  if (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) CK(cudaMemsetAsync(ctx->cov, 0, sizeof(uint32_t) * npx, s));
+  // the control block is still used for the device vertex count
+  CK(cudaMemsetAsync(&ctx->ctl->vmax, 0, sizeof(unsigned), s));
+  CK(mark(1 + PIKO_STAGE_CLEAR));
+  ctx->last_kernels = 3 + (V < 0 && T > 0 ? 1 : 0);
+  if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
+  VertexArgs va{};
+  va.verts = verts; va.n_verts = T > 0 ? V : 0; va.cap = ctx->xv_cap; va.ctl = ctx->ctl; va.M = M;
+  va.W = ctx->g.W; va.H = ctx->g.H; va.xv = ctx->xv;
+  CK(launch_vertex(va, ctx->pdl, s));
+  CK(mark(1 + PIKO_STAGE_VERTEX));
+  FreePipeArgs a{};
+  a.verts = verts; a.xv = ctx->xv; a.xv_cap = ctx->xv_cap; a.idx = idx; a.n_tris = T;
+  a.W = ctx->g.W; a.H = ctx->g.H; a.keys = ctx->fp_keys;
+  a.cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
+  a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
+  a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
+  if (T > 0) CK(launch_freepipe(a, ctx->pdl, s));
+  CK(mark(1 + PIKO_STAGE_SETUP));
+  CK(mark(1 + PIKO_STAGE_RADIX));
+  CK(launch_fp_resolve(a, ctx->pdl, s));
+  CK(mark(1 + PIKO_STAGE_TILE));
+  CK(mark(1 + PIKO_STAGE_GATHER));
+  CK(mark(1 + PIKO_STAGE_RESOLVE));
+  if (ev) ++ctx->prof_frames;
+  // no capacity to check: report a clean frame to the host mirror
+  CK(cudaMemsetAsync(ctx->ctl, 0, offsetof(Control, n_pairs), s));
+  CK(cudaMemsetAsync(&ctx->ctl->n_pairs, 0, sizeof(unsigned long long) * 2, s));
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(ctx->done, s));
+  ctx->pending = true;
+  ctx->last_T = T;
+  ctx->need_reset = true;  // the binned path must not trust tickets touched here
+  return PIKO_OK;
+}
+
 static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
                          long long T, const Mat4& M, const float L[3], float* rgba, float* depth,
                          cudaStream_t s, unsigned long long* keys_out = nullptr) {
+  if (ctx->pipeline == PIKO_PIPE_FREEPIPE)
+    return enqueue_freepipe(ctx, verts, V, idx, T, M, L, rgba, depth, s);
   const bool gather = keys_out == nullptr && ctx->comm != nullptr && ctx->g.nranks > 1;
   const bool keys_only = gather || keys_out != nullptr;
   cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
@@ -618,6 +669,7 @@ extern "C" int piko_get_bins(const piko_ctx* cctx, const int32_t** d_bin_start,
                              const int32_t** d_bin_prims, int64_t* n_pairs) {
   piko_ctx* ctx = const_cast<piko_ctx*>(cctx);
   if (!ctx || !d_bin_start || !d_bin_prims || !n_pairs) return PIKO_EINVAL;
+  if (ctx->pipeline != PIKO_PIPE_BINNED) return ctx->fail(PIKO_ESTATE, "no bin lists in FreePipe");
   int rc = check_frame(ctx);
   if (rc != PIKO_OK) return rc;
   *d_bin_start = ctx->bin_start;
@@ -644,6 +696,8 @@ extern "C" int piko_set_partition(piko_ctx* ctx, int rank, int nranks) {
   if (!ctx) return PIKO_EINVAL;
   if (ctx->comm) return ctx->fail(PIKO_ESTATE, "communicator attached");
   if (nranks < 1 || rank < 0 || rank >= nranks) return ctx->fail(PIKO_EINVAL, "bad rank/nranks");
+  if (nranks > 1 && ctx->pipeline != PIKO_PIPE_BINNED)
+    return ctx->fail(PIKO_ESTATE, "partitions need the binned pipeline");
   set_ownership(ctx, rank, nranks);
   ctx->virt = nranks > 1;
   return PIKO_OK;
@@ -778,4 +832,16 @@ extern "C" int64_t piko_owned_bins(int width, int height, int bin_w, int bin_h, 
   for (int64_t b = rank; b < NB; b += nranks, ++n)
     if (out_bins && n < cap) out_bins[n] = (int32_t)b;
   return n;
+}
+
+extern "C" int piko_set_pipeline(piko_ctx* ctx, int pipeline) {
+  if (!ctx) return PIKO_EINVAL;
+  if (pipeline != PIKO_PIPE_BINNED && pipeline != PIKO_PIPE_FREEPIPE)
+    return ctx->fail(PIKO_EINVAL, "unknown pipeline");
+  if (pipeline == PIKO_PIPE_FREEPIPE && ctx->g.nranks > 1)
+    return ctx->fail(PIKO_ESTATE, "FreePipe renders the whole screen on one GPU");
+  if (ctx->pending) check_frame(ctx);
+  ctx->pipeline = pipeline;
+  ctx->need_reset = true;
+  return PIKO_OK;
 }

@@ -180,7 +180,27 @@ struct ResolveArgs {            // rank 0 after the NCCL gather
   int32_t* out_primid;
 };
 
+// FreePipe variant (sec. 7.2.1): one fused
+// kernel, one thread per triangle, global 64-bit atomicMin into a full-screen
+// key buffer, then a per-pixel resolve/shade pass.
+struct FreePipeArgs {
+  const float* verts;
+  const int4* xv;
+  long long xv_cap;
+  const int32_t* idx;
+  long long n_tris;
+  int W, H;
+  unsigned long long* keys;     // [H][W], CLEAR between frames (resolve resets)
+  uint32_t* cov;                // debug coverage counts or null
+  float light[3];
+  float* out_rgba;
+  float* out_depth;
+  int32_t* out_primid;
+};
+
 // ---- launchers (kernels.cu); pdl = programmatic dependent launch -----------
+cudaError_t launch_freepipe(const FreePipeArgs& a, bool pdl, cudaStream_t s);
+cudaError_t launch_fp_resolve(const FreePipeArgs& a, bool pdl, cudaStream_t s);
 cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool pdl, cudaStream_t s);
 cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s);
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s);

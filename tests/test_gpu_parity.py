@@ -27,7 +27,8 @@ def env(oracle_lib):
     return piko, oracle_lib, torch
 
 
-def gpu_render(env, s, bw, bh=None, cov=True, partition=None, sync=None, indexed=True):
+def gpu_render(env, s, bw, bh=None, cov=True, partition=None, sync=None, indexed=True,
+               pipeline=None, frames=1):
     piko, _, torch = env
     bh = bw if bh is None else bh
     dev = torch.device("cuda:0")
@@ -42,14 +43,18 @@ def gpu_render(env, s, bw, bh=None, cov=True, partition=None, sync=None, indexed
         r.depth.fill_(float("nan"))
     if sync is not None:
         piko.piko_set_sync(r.ctx, sync)
-    r.draw(verts, idx, s.mvp, s.light, indexed=indexed)
+    if pipeline is not None:
+        piko.piko_set_pipeline(r.ctx, pipeline)
+    for _ in range(frames):
+        r.draw(verts, idx, s.mvp, s.light, indexed=indexed)
     torch.cuda.synchronize()
     out = {"rgba": r.rgba.cpu().numpy(), "depth": r.depth.cpu().numpy(),
            "primid": r.primid().cpu().numpy()}
     if cov:
         out["covcount"] = r.coverage().cpu().numpy().view(np.uint32)
-    st, pr = r.bins()
-    out["bin_start"], out["bin_prims"] = st.cpu().numpy(), pr.cpu().numpy()
+    if pipeline in (None, piko.PIKO_PIPE_BINNED):
+        st, pr = r.bins()
+        out["bin_start"], out["bin_prims"] = st.cpu().numpy(), pr.cpu().numpy()
     out["stats"] = r.stats()
     r.close()
     return out
@@ -290,4 +295,39 @@ def test_argument_validation(env):
     vv = torch.empty(s.verts.size + 1, dtype=torch.float32, device="cuda")[1:].view(-1, 8)
     assert piko.piko_draw(r.ctx, vv, i, 16, s.mvp, s.light, r.rgba, r.depth, check=False) == piko.PIKO_EINVAL
     assert piko.piko_draw(r.ctx, None, None, 16, s.mvp, s.light, r.rgba, r.depth, check=False) == piko.PIKO_EINVAL
+    r.close()
+
+
+# ---- FreePipe design alternative -----------
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_freepipe_matches_oracle(env, name):
+    piko = env[0]
+    s = scenes.make(name)
+    got = gpu_render(env, s, 16, pipeline=piko.PIKO_PIPE_FREEPIPE, frames=2)
+    assert_frame_equal(got, oracle_frame(env, s))
+
+
+def test_freepipe_ragged_soup_and_piko_draw(env):
+    piko = env[0]
+    s = scenes.scene_soup(20000, 200, 120, seed=22, name="soup")
+    got = gpu_render(env, s, 16, pipeline=piko.PIKO_PIPE_FREEPIPE, indexed=False)
+    assert_frame_equal(got, oracle_frame(env, s))
+
+
+def test_freepipe_and_binned_switch_in_one_context(env):
+    """Switching pipelines inside one context keeps both exact (resets the
+    binned path's control block)."""
+    piko, _, torch = env
+    s = scenes.scene_c2()
+    ref = oracle_frame(env, s, cov=False)
+    dev = torch.device("cuda:0")
+    v = torch.from_numpy(s.verts).to(dev)
+    i = torch.from_numpy(s.idx).to(dev)
+    r = piko.Renderer(s.W, s.H, 16, device=dev)
+    for pipe in (0, 1, 0, 1, 0):
+        piko.piko_set_pipeline(r.ctx, pipe)
+        r.draw(v, i, s.mvp, s.light)
+        got = {"rgba": r.rgba.cpu().numpy(), "depth": r.depth.cpu().numpy(),
+               "primid": r.primid().cpu().numpy()}
+        assert_frame_equal(got, ref, cov=False)
     r.close()
