@@ -564,60 +564,57 @@ __device__ __forceinline__ void rank_items(const unsigned (&key)[RX_ITEMS], unsi
   }
 }
 
-// pair j of an expand chunk: the triangle with the largest off <= j owns it
-__device__ __noinline__ void expand_pair(const ExpandSmem& ex, int ntri, long long t0, unsigned j,
-                                         const Grid& g, unsigned& key, int& val) {
-  int lo = 0, hi = ntri - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (ex.off[mid] <= j) lo = mid; else hi = mid - 1;
-  }
-  const uint2 rr = ex.rect[lo];
-  key = (unsigned)owned_bin_at(rr.x & 0xffff, rr.x >> 16, rr.y & 0xffff, rr.y >> 16, j - ex.off[lo], g);
-  val = (int)(t0 + lo);
-}
-
-// Expand chunk with more than RX_CHUNK pairs (rare: triangles covering many
-// bins): sub-blocks of RX_CHUNK pairs are expanded by binary search and ranked
-// twice -- first to count (publish), then to scatter with running offsets.
-// phase 0: count into sm.run[d], bin counts.  phase 1: scatter from sm.gstart.
+// Expand chunk with more than RX_CHUNK pairs (triangles covering many bins):
+// windows of RX_CHUNK pairs are expanded cooperatively into shared memory
+// (each triangle writes the part of its pair range inside the window) and
+// ranked twice -- first to count (publish), then to scatter with running
+// offsets.  phase 0: count into sm.run[d] and the bin counts; phase 1: scatter
+// from sm.gstart.
 __device__ __noinline__ void expand_slow(const RadixArgs& a, RadixSmem& sm, const ExpandSmem& ex,
                                          int ntri, long long t0, unsigned n, int phase) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lanemask_lt = (1u << lane) - 1u;
   if (phase == 1) sm.lstart[tid] = sm.gstart[tid];
   else sm.run[tid] = 0;
-  __syncthreads();
 #pragma unroll 1
-  for (unsigned sub = 0; sub * RX_CHUNK < n; ++sub) {
+  for (unsigned lo = 0; lo < n; lo += RX_CHUNK) {
+    const unsigned hi = min(n, lo + RX_CHUNK);
 #pragma unroll 1
     for (int w = 0; w < RX_WARPS; ++w) sm.whist[w][tid] = 0;
-    __syncthreads();
-    const unsigned wb = sub * RX_CHUNK + (unsigned)warp * (RX_ITEMS * 32) + lane;
-    unsigned rk[RX_ITEMS], ky[RX_ITEMS];
-    int vl[RX_ITEMS];
+    __syncthreads();  // previous window fully consumed
 #pragma unroll 1
+    for (int l = tid; l < ntri; l += RX_THREADS) {
+      const unsigned c = ex.cnt[cpad(l)], o = ex.off[l];
+      if (c == 0 || o >= hi || o + c <= lo) continue;
+      const uint2 rr = ex.rect[l];
+      const int tx0 = rr.x & 0xffff, ty0 = rr.x >> 16, tx1 = rr.y & 0xffff, ty1 = rr.y >> 16;
+      const unsigned j0 = max(o, lo), j1 = min(o + c, hi);
+#pragma unroll 1
+      for (unsigned j = j0; j < j1; ++j) {
+        sm.keys[j - lo] = (unsigned)owned_bin_at(tx0, ty0, tx1, ty1, j - o, a.g);
+        sm.vals[j - lo] = (int)(t0 + l);
+      }
+    }
+    __syncthreads();
+    const unsigned m = hi - lo;
+    const unsigned wb = (unsigned)warp * (RX_ITEMS * 32) + lane;
+    unsigned key[RX_ITEMS], rank[RX_ITEMS];
+    int val[RX_ITEMS];
+#pragma unroll
     for (int j = 0; j < RX_ITEMS; ++j) {
       const unsigned pos = wb + j * 32;
-      unsigned k = 0u;
-      int v = 0;
-      if (pos < n) expand_pair(ex, ntri, t0, pos, a.g, k, v);
-      if (phase == 0) {
-        const unsigned kb = pos < n ? k : 0xFFFFFFFFu;
-        const unsigned pb = __match_any_sync(0xffffffffu, kb);
-        if (pos < n && lane == __ffs(pb) - 1) atomicAdd(&a.bin_count[kb], (unsigned)__popc(pb));
-      }
-      const unsigned d = pos < n ? ((k >> a.shift) & (RX_RADIX - 1)) : RX_RADIX;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      unsigned prev = 0;
-      if (pos < n) prev = sm.whist[warp][d];
-      __syncwarp();
-      if (pos < n && lane == __ffs(peers) - 1) sm.whist[warp][d] = prev + __popc(peers);
-      __syncwarp();
-      rk[j] = prev + __popc(peers & lanemask_lt);
-      ky[j] = k;
-      vl[j] = v;
+      key[j] = pos < m ? sm.keys[pos] : 0u;
+      val[j] = pos < m ? sm.vals[pos] : 0;
     }
+    if (phase == 0) {
+#pragma unroll
+      for (int j = 0; j < RX_ITEMS; ++j) {  // pairs per bin (CSR), warp-aggregated
+        const unsigned pos = wb + j * 32;
+        const unsigned kb = pos < m ? key[j] : 0xFFFFFFFFu;
+        const unsigned pb = __match_any_sync(0xffffffffu, kb);
+        if (pos < m && lane == __ffs(pb) - 1) atomicAdd(&a.bin_count[kb], (unsigned)__popc(pb));
+      }
+    }
+    rank_items(key, m, wb, a.shift, sm.whist, warp, lane, rank);
     __syncthreads();
     unsigned tot = 0;
 #pragma unroll 1
@@ -628,21 +625,21 @@ __device__ __noinline__ void expand_slow(const RadixArgs& a, RadixSmem& sm, cons
     }
     __syncthreads();
     if (phase == 1) {
-#pragma unroll 1
+#pragma unroll
       for (int j = 0; j < RX_ITEMS; ++j) {
         const unsigned pos = wb + j * 32;
-        if (pos >= n) continue;
-        const unsigned d = (ky[j] >> a.shift) & (RX_RADIX - 1);
-        const unsigned gpos = sm.lstart[d] + sm.whist[warp][d] + rk[j];
-        if (a.keys_out) a.keys_out[gpos] = ky[j];
-        a.vals_out[gpos] = vl[j];
+        if (pos >= m) continue;
+        const unsigned d = (key[j] >> a.shift) & (RX_RADIX - 1);
+        const unsigned gpos = sm.lstart[d] + sm.whist[warp][d] + rank[j];
+        if (a.keys_out) a.keys_out[gpos] = key[j];
+        a.vals_out[gpos] = val[j];
       }
     }
     __syncthreads();
     if (phase == 1) sm.lstart[tid] += tot;
     else sm.run[tid] += tot;
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 template <bool EXPAND>
@@ -999,6 +996,57 @@ __device__ __forceinline__ u64 eval_key(const RecView& r, int Px, int Py, int t,
   return ((u64)(__float_as_uint(z) & 0x7FFFFFFFu) << 32) | (unsigned)t;
 }
 
+// Prepared form of the same test (one setup per triangle, ~15 instructions per
+// sample): E_ab(P) = K_ab + B_ab*dy - A_ab*dx with dx = Px - X0, dy = Py - Y0,
+// A_ab = Yb - Ya, B_ab = Xb - Xa, K_ab = A_ab*(Xa - X0) - B_ab*(Ya - Y0) -- an
+// exact integer identity.  For small triangles (bbox extent < 2^15) the true
+// E at any sample inside the bbox fits int32, so the sum is formed modulo 2^32
+// (unsigned) and is exact; large triangles use int64.
+struct TriEval {
+  int X0, Y0;
+  int A0, B0, A1, B1, A2, B2;
+  long long K1, K2;            // K01 = 0
+  int thr0, thr1, thr2;        // -1 on top/left edges (R1), else 0
+  float zw0, za, zb;
+  int small;
+};
+__device__ __forceinline__ TriEval prepare(const RecView& r) {
+  TriEval e;
+  e.X0 = r.X0; e.Y0 = r.Y0;
+  e.A0 = r.Y1 - r.Y0; e.B0 = r.X1 - r.X0;
+  e.A1 = r.Y2 - r.Y1; e.B1 = r.X2 - r.X1;
+  e.A2 = r.Y0 - r.Y2; e.B2 = r.X0 - r.X2;
+  e.K1 = (long long)e.A1 * (r.X1 - r.X0) - (long long)e.B1 * (r.Y1 - r.Y0);
+  e.K2 = (long long)e.A2 * (r.X2 - r.X0) - (long long)e.B2 * (r.Y2 - r.Y0);
+  e.thr0 = tl_thr(r.X0, r.Y0, r.X1, r.Y1);
+  e.thr1 = tl_thr(r.X1, r.Y1, r.X2, r.Y2);
+  e.thr2 = tl_thr(r.X2, r.Y2, r.X0, r.Y0);
+  e.zw0 = r.zw0; e.za = r.za; e.zb = r.zb;
+  e.small = r.small;
+  return e;
+}
+__device__ __forceinline__ u64 eval_pre(const TriEval& e, int Px, int Py, int t, bool& covered) {
+  const int dx = Px - e.X0, dy = Py - e.Y0;
+  bool in;
+  if (e.small) {
+    const unsigned udx = (unsigned)dx, udy = (unsigned)dy;
+    const int E0 = (int)((unsigned)e.B0 * udy - (unsigned)e.A0 * udx);
+    const int E1 = (int)((unsigned)e.K1 + (unsigned)e.B1 * udy - (unsigned)e.A1 * udx);
+    const int E2 = (int)((unsigned)e.K2 + (unsigned)e.B2 * udy - (unsigned)e.A2 * udx);
+    in = E0 > e.thr0 && E1 > e.thr1 && E2 > e.thr2;
+  } else {
+    const long long E0 = (long long)e.B0 * dy - (long long)e.A0 * dx;
+    const long long E1 = e.K1 + (long long)e.B1 * dy - (long long)e.A1 * dx;
+    const long long E2 = e.K2 + (long long)e.B2 * dy - (long long)e.A2 * dx;
+    in = E0 > e.thr0 && E1 > e.thr1 && E2 > e.thr2;
+  }
+  covered = in;
+  if (!in) return CLEAR_KEY;
+  const float z = __fmaf_rn(e.za, __int2float_rn(dx), __fmaf_rn(e.zb, __int2float_rn(dy), e.zw0));
+  if (!(z >= 0.0f && z <= 1.0f)) return CLEAR_KEY;
+  return ((u64)(__float_as_uint(z) & 0x7FFFFFFFu) << 32) | (unsigned)t;
+}
+
 // O7 shade of pixel sample (Px, Py) by triangle t (recomputes O2 from the
 // vertex-stage records; normals from the caller's vertex buffer).
 __device__ __noinline__ float4 shade(const float* __restrict__ verts, const int4* __restrict__ xv,
@@ -1043,14 +1091,29 @@ __device__ __forceinline__ void normalise_light(const float in[3], float L[3]) {
 }
 
 constexpr int TINY_AREA = 4;    // clipped rect area a thread rasterizes alone
-constexpr int NSTAGE = 4;       // setup-record pipeline depth (rounds in flight per warp)
+constexpr int NSTAGE = 3;       // setup-record pipeline depth (rounds in flight per warp)
 constexpr int TQ = NSTAGE + 2;  // primIDs are fetched two rounds before their records
+
+// Queue of larger triangles of the current bin (structure of arrays of the
+// prepared evaluator + clipped rect), rasterized at the end of the bin by all
+// threads over the flattened (triangle, pixel) index space.
+template <int Q>
+struct BigQueue {
+  int X0[Q], Y0[Q], A0[Q], B0[Q], A1[Q], B1[Q], A2[Q], B2[Q];
+  long long K1[Q], K2[Q];
+  int thr[Q];                    // thr0 | thr1 << 1 | thr2 << 2 (bit set: -1), small << 3
+  float zw0[Q], za[Q], zb[Q], invw[Q];
+  int t[Q], rx0[Q], ry0[Q], w[Q];
+  unsigned pre[Q + 1];           // exclusive prefix of the clipped areas
+};
 
 template <int BW, int BH, int THREADS>
 struct TileSmem {
   static constexpr int NPX = BW * BH;
+  static constexpr int BIGQ = THREADS;  // queued per bin (overflow: warp-cooperative path)
   u64 key[NPX];
   int4 rec[NSTAGE][THREADS][3];
+  BigQueue<BIGQ> q;
 };
 
 // Write one pixel of the frame (or the keys-only tile) from its resolved key.
@@ -1087,6 +1150,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(TileArgs a) {
   unsigned* s_cov = reinterpret_cast<unsigned*>(smem_raw + sizeof(TileSmem<BW, BH, THREADS>));
   __shared__ int s_bin;     // current bin (-1: work list exhausted)
   __shared__ int s_rng[3];  // its CSR sub-range [s, e) and fragment count (0: whole bin)
+  __shared__ int s_nbig;    // large triangles queued for the pixel-parallel pass
   __shared__ unsigned s_ln[NLIST];
   __shared__ int s_last;
 
@@ -1188,6 +1252,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(TileArgs a) {
         if (COV) s_cov[p] = 0;
       }
     }
+    if (tid == 0) s_nbig = 0;
     __syncthreads();  // tile cleared before any warp rasterizes into it
     // Each warp streams its share of the bin's list (items s + k*THREADS +
     // warp*32 + lane) through its own cp.async pipeline: no CTA barrier until
@@ -1242,10 +1307,11 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(TileArgs a) {
 #ifdef PIKO_EXP_NORASTER
           if (r.X0 == 123456789) sm.key[0] = t_cur;
 #else
+          const TriEval ev = prepare(r);
           for (int y = ry0; y < ry0 + h; ++y)
             for (int x = rx0; x < rx0 + w; ++x) {
               bool cov;
-              const u64 key = eval_key(r, 256 * x + 128, 256 * y + 128, t_cur, cov);
+              const u64 key = eval_pre(ev, 256 * x + 128, 256 * y + 128, t_cur, cov);
               const int p = (y - y0) * BW + (x - x0);
               if (COV && cov) atomicAdd(&s_cov[p], 1u);
 #ifndef PIKO_EXP_NOATOM
@@ -1256,9 +1322,24 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(TileArgs a) {
             }
 #endif
           area = 0;
+        } else {
+          const int slot = atomicAdd(&s_nbig, 1);
+          if (slot < TileSmem<BW, BH, THREADS>::BIGQ) {
+            const TriEval ev = prepare(r);
+            auto& Q = sm.q;
+            Q.X0[slot] = ev.X0; Q.Y0[slot] = ev.Y0;
+            Q.A0[slot] = ev.A0; Q.B0[slot] = ev.B0; Q.A1[slot] = ev.A1; Q.B1[slot] = ev.B1;
+            Q.A2[slot] = ev.A2; Q.B2[slot] = ev.B2; Q.K1[slot] = ev.K1; Q.K2[slot] = ev.K2;
+            Q.thr[slot] = (ev.thr0 ? 1 : 0) | (ev.thr1 ? 2 : 0) | (ev.thr2 ? 4 : 0) | (ev.small ? 8 : 0);
+            Q.zw0[slot] = ev.zw0; Q.za[slot] = ev.za; Q.zb[slot] = ev.zb;
+            Q.invw[slot] = __frcp_rn((float)w);
+            Q.t[slot] = t_cur; Q.rx0[slot] = rx0; Q.ry0[slot] = ry0; Q.w[slot] = w;
+            Q.pre[slot] = (unsigned)area;  // turned into the prefix at the end of the bin
+            area = 0;
+          }  // queue full: this one takes the warp-cooperative path
         }
       }
-      if (__any_sync(0xffffffffu, area > 0)) {
+      if (__any_sync(0xffffffffu, area > 0)) {  // queue overflow: warp-cooperative
         unsigned incl = (unsigned)area;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1298,6 +1379,70 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(TileArgs a) {
     }
     cp_async_wait<0>();
     __syncthreads();
+    {  // queued triangles: all threads over the flattened (triangle, pixel) items
+      const int nq = min(s_nbig, TileSmem<BW, BH, THREADS>::BIGQ);
+      if (nq > 0) {
+        auto& Q = sm.q;
+        // exclusive prefix of the clipped areas (one entry per thread)
+        const unsigned ar = tid < nq ? Q.pre[tid] : 0u;
+        unsigned inc = ar;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += v;
+        }
+        __shared__ unsigned s_qw[THREADS / 32];
+        if (lane == 31) s_qw[warp] = inc;
+        __syncthreads();
+        unsigned wbase = 0, tot = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < THREADS / 32; ++w2) {
+          const unsigned v = s_qw[w2];
+          wbase += (w2 < warp) ? v : 0u;
+          tot += v;
+        }
+        if (tid < nq) Q.pre[tid] = wbase + inc - ar;
+        if (tid == 0) Q.pre[nq] = tot;
+        __syncthreads();
+        // warp-contiguous items: the warp's first item locates its entry once
+        // (monotone across iterations), each lane then walks a few entries
+        int qw = 0;
+        for (unsigned base = (unsigned)warp * 32; base < tot; base += THREADS) {
+          if (lane == 0) {
+            int lo = qw, hi = nq - 1;  // the entry with the largest pre <= base
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (Q.pre[mid] <= base) lo = mid; else hi = mid - 1;
+            }
+            qw = lo;
+          }
+          qw = __shfl_sync(0xffffffffu, qw, 0);
+          const unsigned i = base + lane;
+          if (i >= tot) continue;
+          int q = qw;
+          while (Q.pre[q + 1] <= i) ++q;
+          const unsigned off = i - Q.pre[q];
+          const int wq = Q.w[q];
+          const int row = __float2int_rz(((float)off + 0.5f) * Q.invw[q]);  // exact: off < 2^12
+          const int col = (int)off - row * wq;
+          const int x = Q.rx0[q] + col, y = Q.ry0[q] + row;
+          TriEval ev;
+          ev.X0 = Q.X0[q]; ev.Y0 = Q.Y0[q];
+          ev.A0 = Q.A0[q]; ev.B0 = Q.B0[q]; ev.A1 = Q.A1[q]; ev.B1 = Q.B1[q];
+          ev.A2 = Q.A2[q]; ev.B2 = Q.B2[q]; ev.K1 = Q.K1[q]; ev.K2 = Q.K2[q];
+          const int th = Q.thr[q];
+          ev.thr0 = (th & 1) ? -1 : 0; ev.thr1 = (th & 2) ? -1 : 0; ev.thr2 = (th & 4) ? -1 : 0;
+          ev.small = (th >> 3) & 1;
+          ev.zw0 = Q.zw0[q]; ev.za = Q.za[q]; ev.zb = Q.zb[q];
+          bool cov;
+          const u64 key = eval_pre(ev, 256 * x + 128, 256 * y + 128, Q.t[q], cov);
+          const int p = (y - y0) * BW + (x - x0);
+          if (COV && cov) atomicAdd(&s_cov[p], 1u);
+          if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
+        }
+        __syncthreads();
+      }
+    }
     TL_MARK(b, 1);
 
     // ---- write-back ----------------------------------------------------------
@@ -1422,10 +1567,11 @@ __global__ void __launch_bounds__(256) k_freepipe(FreePipeArgs a) {
     r.zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
     r.px0 = o.px0; r.py0 = o.py0; r.px1 = o.px1; r.py1 = o.py1;
     r.small = o.small;
+    const TriEval ev = prepare(r);
     for (int y = o.py0; y <= o.py1; ++y)
       for (int x = o.px0; x <= o.px1; ++x) {
         bool cov;
-        const u64 key = eval_key(r, 256 * x + 128, 256 * y + 128, (int)t, cov);
+        const u64 key = eval_pre(ev, 256 * x + 128, 256 * y + 128, (int)t, cov);
         const size_t p = (size_t)y * a.W + x;
         if (a.cov && cov) atomicAdd(&a.cov[p], 1u);
         if (key != CLEAR_KEY) atomicMin(&a.keys[p], key);
