@@ -733,7 +733,6 @@ extern "C" int piko_get_stats(const piko_ctx* cctx, piko_stats* out) {
   out->owned_bins = ctx->owned;
   out->pair_capacity = (int64_t)ctx->pair_cap;
   out->radix_passes = ctx->npass;
-  const bool gather = ctx->comm && ctx->g.nranks > 1;
   out->kernels_per_frame = ctx->last_kernels;
   return PIKO_OK;
 }
@@ -799,7 +798,7 @@ extern "C" int piko_resolve_keys(piko_ctx* ctx, const float* verts, int64_t n_ve
   if (!d_all_keys || !out_rgba || !out_depth || !mvp || !light)
     return ctx->fail(PIKO_EINVAL, "null argument");
   if (nranks < 1 || n_verts < 0 || n_tris < 0) return ctx->fail(PIKO_EINVAL, "bad size");
-  float L[3];
+  float L[3] = {0.0f, 0.0f, 0.0f};
   int rc = validate_draw(ctx, verts, idx, n_tris, mvp, light, out_rgba, out_depth, L);
   if (rc != PIKO_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

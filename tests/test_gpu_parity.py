@@ -331,3 +331,65 @@ def test_freepipe_and_binned_switch_in_one_context(env):
                "primid": r.primid().cpu().numpy()}
         assert_frame_equal(got, ref, cov=False)
     r.close()
+
+
+# ---- API behaviour ---------------------------------------------------------------
+def test_stats_and_profile(env):
+    piko, _, torch = env
+    s = scenes.scene_c3()
+    dev = torch.device("cuda:0")
+    v = torch.from_numpy(s.verts).to(dev)
+    i = torch.from_numpy(s.idx).to(dev)
+    r = piko.Renderer(s.W, s.H, 16, device=dev)
+    piko.piko_set_profiling(r.ctx, 1)
+    for _ in range(3):
+        r.draw(v, i, s.mvp, s.light)
+    prof, n = piko.piko_get_profile(r.ctx)
+    assert n == 3 and all(ms >= 0 for ms in prof.values()) and prof["tile"] > 0
+    st = r.stats()
+    ostart, oprims = env[1].bins(s.verts, s.idx, s.mvp, s.W, s.H, 16, 16)
+    assert st["n_pairs"] == len(oprims) and st["n_bins"] == len(ostart) - 1
+    oi, _ = env[1].setup(s.verts, s.idx, s.mvp, s.W, s.H)
+    assert st["n_live"] == int(oi[:, 0].sum())
+    assert st["radix_passes"] == 2 and st["kernels_per_frame"] >= 5
+    r.close()
+
+
+def test_async_overflow_is_reported_then_recovers(env):
+    """ASYNC mode: a frame that overflows the pair capacity is reported by
+    piko_finish (PIKO_ECAPACITY) and the capacity grows; the next frame is exact."""
+    piko, _, torch = env
+    from tests.helpers import pixel_scene
+    tris = [[(-10.0, -10.0), (3000.0, -10.0), (-10.0, 3000.0)]] * 40
+    zs = np.linspace(0.1, 0.9, 40)[:, None].repeat(3, 1)
+    v, i, m = pixel_scene(tris, zs, 1024, 768)
+    s = scenes.Scene("cap", 1024, 768, (8,), v, i, m)
+    dev = torch.device("cuda:0")
+    vt, it = torch.from_numpy(v).to(dev), torch.from_numpy(i).to(dev)
+    r = piko.Renderer(1024, 768, 8, device=dev)
+    piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
+    r.draw(vt, it, m, s.light)
+    assert piko.piko_finish(r.ctx) == piko.PIKO_ECAPACITY
+    r.draw(vt, it, m, s.light)
+    assert piko.piko_finish(r.ctx) == piko.PIKO_OK
+    ref = oracle_frame(env, s, cov=False)
+    got = {"rgba": r.rgba.cpu().numpy(), "depth": r.depth.cpu().numpy(), "primid": r.primid().cpu().numpy()}
+    assert_frame_equal(got, ref, cov=False)
+    r.close()
+
+
+@pytest.mark.parametrize("bw,bh", [(8, 32), (32, 8), (64, 16)])
+def test_c3_non_square_bins(env, bw, bh):
+    s = scenes.scene_c3()
+    got = gpu_render(env, s, bw, bh, cov=False)
+    assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
+    assert_bins_equal(got, env, s, bw, bh)
+
+
+@pytest.mark.parametrize("W,H", [(16384, 24), (24, 16384), (1, 1), (4097, 3)])
+def test_extreme_screens(env, W, H):
+    """Maximum width / height (guard band limit R2), 1x1 and odd sizes."""
+    s = scenes.scene_soup(3000, W, H, seed=81, name="soup")
+    got = gpu_render(env, s, 16, cov=False)
+    assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
+    assert_bins_equal(got, env, s, 16)
