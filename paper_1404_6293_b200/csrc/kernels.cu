@@ -323,6 +323,11 @@ __global__ void __launch_bounds__(256) k_index_max(const int32_t* __restrict__ i
 // ---------------------------------------------------------------------------
 constexpr int K1_BIG = 64;  // triangles with more owned bins go to the CTA-wide loop
 
+// FUSED: no k_vertex launch; the corners are transformed here from the raw
+// positions (each shared vertex is transformed once per triangle using it --
+// same arithmetic, so the same bits -- and one kernel and its 16 B/vertex
+// round trip through HBM/L2 disappear).
+template <bool FUSED>
 __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
   __shared__ unsigned s_hist[MAX_PASSES][RX_RADIX];
   __shared__ uint2 s_big[K1_CHUNK];
@@ -351,15 +356,30 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       vi[k][c] = in ? __ldg(a.idx + 3 * t + c) : -1;
-      if (vi[k][c] >= a.xv_cap) vi[k][c] = -1;  // overflowed frame: stay in bounds
+      if (!FUSED && vi[k][c] >= a.xv_cap) vi[k][c] = -1;  // overflowed frame: stay in bounds
     }
   }
   int4 cv[K1_TPT][3];
+  if constexpr (FUSED) {
+    float4 pp[K1_TPT][3];
 #pragma unroll
-  for (int k = 0; k < K1_TPT; ++k)
+    for (int k = 0; k < K1_TPT; ++k)
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-      cv[k][c] = vi[k][c] >= 0 ? __ldg(a.xv + vi[k][c]) : make_int4(VX_CULLED, 0, 0, 0);
+      for (int c = 0; c < 3; ++c)
+        pp[k][c] = vi[k][c] >= 0 ? load_pos(a.verts, vi[k][c]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < K1_TPT; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        cv[k][c] = vi[k][c] >= 0 ? transform_vertex(pp[k][c], a.M, g.W, g.H)
+                                 : make_int4(VX_CULLED, 0, 0, 0);
+  } else {
+#pragma unroll
+    for (int k = 0; k < K1_TPT; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        cv[k][c] = vi[k][c] >= 0 ? __ldg(a.xv + vi[k][c]) : make_int4(VX_CULLED, 0, 0, 0);
+  }
   K1_MARK(1);
 
   // ---- setup, record + rect write (coalesced: consecutive threads, t) -------
@@ -1050,11 +1070,19 @@ __device__ __forceinline__ u64 eval_pre(const TriEval& e, int Px, int Py, int t,
 // O7 shade of pixel sample (Px, Py) by triangle t (recomputes O2 from the
 // vertex-stage records; normals from the caller's vertex buffer).
 __device__ __noinline__ float4 shade(const float* __restrict__ verts, const int4* __restrict__ xv,
-                                        const int32_t* __restrict__ idx, int W, int H,
+                                        const Mat4* M, const int32_t* __restrict__ idx, int W, int H,
                                         const float L[3], int t, int Px, int Py) {
   Tri o;
   const int i0 = __ldg(idx + 3ll * t), i1 = __ldg(idx + 3ll * t + 1), i2 = __ldg(idx + 3ll * t + 2);
-  const int4 c0 = __ldg(xv + i0), c1 = __ldg(xv + i1), c2 = __ldg(xv + i2);
+  int4 c0, c1, c2;
+  if (xv) {
+    c0 = __ldg(xv + i0); c1 = __ldg(xv + i1); c2 = __ldg(xv + i2);
+  } else {  // fused vertex stage: the same O1 transform, recomputed
+    const float4 p0 = load_pos(verts, i0), p1 = load_pos(verts, i1), p2 = load_pos(verts, i2);
+    c0 = transform_vertex(p0, *M, W, H);
+    c1 = transform_vertex(p1, *M, W, H);
+    c2 = transform_vertex(p2, *M, W, H);
+  }
   const float4 m0 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i0 + 4));
   const float4 m1 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i1 + 4));
   const float4 m2 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i2 + 4));
@@ -1132,7 +1160,7 @@ __device__ __forceinline__ void store_pixel(const TileArgs& a, const float L[3],
     prim = (int)(unsigned)(key & 0xFFFFFFFFu);
     depth = __uint_as_float((unsigned)(key >> 32));
 #ifndef PIKO_EXP_NOSHADE
-    c = shade(a.verts, a.xv, a.idx, a.g.W, a.g.H, L, prim, 256 * x + 128, 256 * y + 128);
+    c = shade(a.verts, a.xv, &a.M, a.idx, a.g.W, a.g.H, L, prim, 256 * x + 128, 256 * y + 128);
 #endif
   }
   reinterpret_cast<float4*>(a.out_rgba)[o] = c;
@@ -1142,7 +1170,7 @@ __device__ __forceinline__ void store_pixel(const TileArgs& a, const float L[3],
 }
 
 template <int BW, int BH, int THREADS, bool COV, bool KEYS_ONLY>
-__global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(TileArgs a) {
+__global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_constant__ TileArgs a) {
   constexpr int NPX = BW * BH;
   constexpr int PPT = (NPX + THREADS - 1) / THREADS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1540,7 +1568,7 @@ __global__ void __launch_bounds__(256) k_freepipe(FreePipeArgs a) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       vi[k][c] = t < a.n_tris ? __ldg(a.idx + 3 * t + c) : -1;
-      if (vi[k][c] >= a.xv_cap) vi[k][c] = -1;
+      if (a.xv && vi[k][c] >= a.xv_cap) vi[k][c] = -1;
     }
   }
   int4 cv[TPT][3];
@@ -1548,7 +1576,9 @@ __global__ void __launch_bounds__(256) k_freepipe(FreePipeArgs a) {
   for (int k = 0; k < TPT; ++k)
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      cv[k][c] = vi[k][c] >= 0 ? __ldg(a.xv + vi[k][c]) : make_int4(VX_CULLED, 0, 0, 0);
+      cv[k][c] = vi[k][c] < 0 ? make_int4(VX_CULLED, 0, 0, 0)
+                 : a.xv     ? __ldg(a.xv + vi[k][c])
+                            : transform_vertex(load_pos(a.verts, vi[k][c]), a.M, a.W, a.H);
 #pragma unroll 1
   for (int k = 0; k < TPT; ++k) {
     const long long t = tb + k * 256;
@@ -1579,7 +1609,7 @@ __global__ void __launch_bounds__(256) k_freepipe(FreePipeArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_fp_resolve(FreePipeArgs a) {
+__global__ void __launch_bounds__(256) k_fp_resolve(const __grid_constant__ FreePipeArgs a) {
   pdl_wait();
   pdl_trigger();
   const long long p = (long long)blockIdx.x * 256 + threadIdx.x;
@@ -1595,7 +1625,7 @@ __global__ void __launch_bounds__(256) k_fp_resolve(FreePipeArgs a) {
   if (key != CLEAR_KEY) {
     prim = (int)(unsigned)(key & 0xFFFFFFFFu);
     depth = __uint_as_float((unsigned)(key >> 32));
-    c = shade(a.verts, a.xv, a.idx, a.W, a.H, L, prim, 256 * x + 128, 256 * y + 128);
+    c = shade(a.verts, a.xv, &a.M, a.idx, a.W, a.H, L, prim, 256 * x + 128, 256 * y + 128);
   }
   reinterpret_cast<float4*>(a.out_rgba)[p] = c;
   a.out_depth[p] = depth;
@@ -1605,7 +1635,7 @@ __global__ void __launch_bounds__(256) k_fp_resolve(FreePipeArgs a) {
 // ---------------------------------------------------------------------------
 // K7 (multi-GPU rank 0): resolve gathered tile keys -> shaded frame
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_resolve(ResolveArgs a) {
+__global__ void __launch_bounds__(256) k_resolve(const __grid_constant__ ResolveArgs a) {
   const Grid g = a.g;
   const int x = blockIdx.x * 32 + (threadIdx.x & 31);
   const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -1624,7 +1654,7 @@ __global__ void __launch_bounds__(256) k_resolve(ResolveArgs a) {
   if (key != CLEAR_KEY) {
     prim = (int)(unsigned)(key & 0xFFFFFFFFu);
     depth = __uint_as_float((unsigned)(key >> 32));
-    c = shade(a.verts, a.xv, a.idx, g.W, g.H, L, prim, 256 * x + 128, 256 * y + 128);
+    c = shade(a.verts, a.xv, &a.M, a.idx, g.W, g.H, L, prim, 256 * x + 128, 256 * y + 128);
   }
   reinterpret_cast<float4*>(a.out_rgba)[o] = c;
   a.out_depth[o] = depth;
@@ -1672,7 +1702,8 @@ cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool
   return launch_ex(k_index_max, (int)(want > 0 ? want : 1), 256, 0, pdl, s, idx, n, ctl);
 }
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s) {
-  return launch_ex(k_setup, grid, K1_THREADS, 0, pdl, s, a);
+  if (!a.xv) return launch_ex(k_setup<true>, grid, K1_THREADS, 0, pdl, s, a);
+  return launch_ex(k_setup<false>, grid, K1_THREADS, 0, pdl, s, a);
 }
 cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream_t s) {
   if (a.expand) {

@@ -100,6 +100,7 @@ struct piko_ctx {
   long long last_grids[4] = {-1, -1, -1, -1};
   bool need_reset = true;
   bool pdl = true;
+  int vs_mode = -1;        // vertex stage: -1 auto, 0 fused into k_setup, 1 separate k_vertex
   int32_t* primid = nullptr;
   uint32_t* cov = nullptr;
   Control* h_ctl = nullptr;          // pinned mirror of the control block
@@ -211,6 +212,7 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   }
   memset(ctx->h_ctl, 0, sizeof(Control));
   if (const char* e = getenv("PIKO_NO_PDL")) ctx->pdl = e[0] == '0';
+  if (const char* e = getenv("PIKO_SEPARATE_VS")) ctx->vs_mode = e[0] == '0' ? 0 : 1;
   return ctx;
 }
 
@@ -298,6 +300,16 @@ static int ensure_pairs(piko_ctx* ctx, unsigned long long P) {
   return PIKO_OK;
 }
 
+// Vertex stage placement.  Separate (k_vertex: each vertex transformed once,
+// 16 B records gathered by k_setup) wins on meshes whose vertices are shared by
+// several triangles; fused (k_setup transforms its three corners from the raw
+// 32 B vertices) wins when vertices are barely shared (soups: V ~ 3T) and for
+// piko_draw without a vertex count (no k_index_max + k_vertex launches).
+static bool separate_vs(const piko_ctx* ctx, long long V, long long T) {
+  if (ctx->vs_mode >= 0) return ctx->vs_mode == 1;
+  return V >= 0 && 2 * V <= 3 * T;
+}
+
 // xv capacity for V vertices (V < 0: unknown; sized from an upper bound)
 static int ensure_verts(piko_ctx* ctx, long long V) {
   if (V > ctx->xv_cap) {
@@ -332,17 +344,21 @@ static int enqueue_freepipe(piko_ctx* ctx, const float* verts, long long V, cons
   }
   if (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) CK(cudaMemsetAsync(ctx->cov, 0, sizeof(uint32_t) * npx, s));
   // the control block is still used for the device vertex count
-  CK(cudaMemsetAsync(&ctx->ctl->vmax, 0, sizeof(unsigned), s));
   CK(mark(1 + PIKO_STAGE_CLEAR));
-  ctx->last_kernels = 3 + (V < 0 && T > 0 ? 1 : 0);
-  if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
-  VertexArgs va{};
-  va.verts = verts; va.n_verts = T > 0 ? V : 0; va.cap = ctx->xv_cap; va.ctl = ctx->ctl; va.M = M;
-  va.W = ctx->g.W; va.H = ctx->g.H; va.xv = ctx->xv;
-  CK(launch_vertex(va, ctx->pdl, s));
+  const bool sep = separate_vs(ctx, V, T);
+  ctx->last_kernels = 2 + (T > 0 ? 1 : 0) + (sep && V < 0 && T > 0 ? 1 : 0);
+  if (sep) {  // vmax and vx_overflow (adjacent) start at 0
+    CK(cudaMemsetAsync(&ctx->ctl->vmax, 0, 2 * sizeof(unsigned), s));
+    if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
+    VertexArgs va{};
+    va.verts = verts; va.n_verts = T > 0 ? V : 0; va.cap = ctx->xv_cap; va.ctl = ctx->ctl; va.M = M;
+    va.W = ctx->g.W; va.H = ctx->g.H; va.xv = ctx->xv;
+    CK(launch_vertex(va, ctx->pdl, s));
+  }
   CK(mark(1 + PIKO_STAGE_VERTEX));
   FreePipeArgs a{};
-  a.verts = verts; a.xv = ctx->xv; a.xv_cap = ctx->xv_cap; a.idx = idx; a.n_tris = T;
+  a.verts = verts; a.xv = sep ? ctx->xv : nullptr; a.xv_cap = ctx->xv_cap; a.M = M;
+  a.idx = idx; a.n_tris = T;
   a.W = ctx->g.W; a.H = ctx->g.H; a.keys = ctx->fp_keys;
   a.cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
   a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
@@ -355,8 +371,9 @@ static int enqueue_freepipe(piko_ctx* ctx, const float* verts, long long V, cons
   CK(mark(1 + PIKO_STAGE_GATHER));
   CK(mark(1 + PIKO_STAGE_RESOLVE));
   if (ev) ++ctx->prof_frames;
-  // no capacity to check: report a clean frame to the host mirror
-  CK(cudaMemsetAsync(ctx->ctl, 0, offsetof(Control, n_pairs), s));
+  // no pair capacity to check: report a clean frame to the host mirror, except
+  // a vertex-capacity overflow of k_vertex (vx_overflow / vx_need kept)
+  CK(cudaMemsetAsync(ctx->ctl, 0, offsetof(Control, vx_overflow), s));
   CK(cudaMemsetAsync(&ctx->ctl->n_pairs, 0, sizeof(unsigned long long) * 2, s));
   CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s));
   CK(cudaEventRecord(ctx->done, s));
@@ -399,10 +416,11 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     ctx->need_reset = false;
   }
   CK(mark(1 + PIKO_STAGE_CLEAR));
-  ctx->last_kernels = 3 + ctx->npass + (ctx->npass == 1 ? 1 : 0) + (V < 0 && T > 0 ? 1 : 0) +
-                      (gather && ctx->g.rank == 0 ? 1 : 0);
-  if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
-  {
+  const bool sep = separate_vs(ctx, V, T);
+  ctx->last_kernels = 2 + ctx->npass + (ctx->npass == 1 ? 1 : 0) +
+                      (sep ? 1 + (V < 0 && T > 0 ? 1 : 0) : 0) + (gather && ctx->g.rank == 0 ? 1 : 0);
+  if (sep) {
+    if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
     VertexArgs a{};
     a.verts = verts; a.n_verts = T > 0 ? V : 0; a.cap = ctx->xv_cap; a.ctl = ctx->ctl; a.M = M;
     a.W = ctx->g.W; a.H = ctx->g.H; a.xv = ctx->xv;
@@ -411,7 +429,8 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   CK(mark(1 + PIKO_STAGE_VERTEX));
   {
     SetupArgs a{};
-    a.xv = ctx->xv; a.xv_cap = ctx->xv_cap; a.idx = idx; a.n_tris = T; a.g = ctx->g;
+    a.xv = sep ? ctx->xv : nullptr; a.xv_cap = ctx->xv_cap; a.verts = verts; a.M = M;
+    a.idx = idx; a.n_tris = T; a.g = ctx->g;
     a.npass = ctx->npass; a.rec = ctx->rec; a.rect = ctx->rect; a.ctl = ctx->ctl;
     CK(launch_setup(a, (int)g1, ctx->pdl, s));
   }
@@ -440,7 +459,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   CK(mark(1 + PIKO_STAGE_RADIX));
   {
     TileArgs a{};
-    a.verts = verts; a.xv = ctx->xv; a.idx = idx;
+    a.verts = verts; a.xv = sep ? ctx->xv : nullptr; a.M = M; a.idx = idx;
     a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
     a.g = ctx->g; a.npass = ctx->npass; a.rec = ctx->rec; a.bin_start = ctx->bin_start;
     a.bin_prims = ctx->vals[ctx->npass & 1]; a.ctl = ctx->ctl;
@@ -480,7 +499,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     CK(mark(1 + PIKO_STAGE_GATHER));
     if (ctx->g.rank == 0) {
       ResolveArgs a{};
-      a.verts = verts; a.xv = ctx->xv; a.idx = idx;
+      a.verts = verts; a.xv = sep ? ctx->xv : nullptr; a.M = M; a.idx = idx;
       a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
       a.g = ctx->g; a.all_keys = ctx->all_keys; a.owned_max = ctx->owned_max;
       a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
@@ -514,7 +533,7 @@ static int check_frame(piko_ctx* ctx) {
   if (!ctx->pending) return ctx->last_status;
   ctx->pending = false;
   CK(cudaEventSynchronize(ctx->done));
-  if (ctx->h_ctl->overflow_tag == ctx->h_ctl->frame + 1) {
+  if (ctx->h_ctl->overflow_tag == ctx->h_ctl->frame + 1 || ctx->h_ctl->vx_overflow) {
     int rc = ensure_pairs(ctx, ctx->h_ctl->n_pairs);
     if (rc == PIKO_OK) rc = ensure_verts(ctx, (long long)ctx->h_ctl->vx_need);
     ctx->last_status = rc != PIKO_OK ? rc : PIKO_ECAPACITY;
@@ -569,7 +588,7 @@ static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32
   if ((rc = ensure_tris(ctx, n_tris)) != PIKO_OK) return rc;
   // without a vertex count the device derives max(idx)+1; start at 3 n_tris
   // (every corner distinct) and grow on a reported vertex overflow
-  if ((rc = ensure_verts(ctx, V >= 0 ? V : 3ll * n_tris)) != PIKO_OK) return rc;
+  if (separate_vs(ctx, V, n_tris) && (rc = ensure_verts(ctx, V >= 0 ? V : 3ll * n_tris)) != PIKO_OK) return rc;
   if ((rc = ensure_pairs(ctx, std::max<unsigned long long>(ctx->pair_cap, 2ull * n_tris + 4096))) != PIKO_OK)
     return rc;
   if ((rc = ensure_cov(ctx)) != PIKO_OK) return rc;
@@ -803,15 +822,10 @@ extern "C" int piko_resolve_keys(piko_ctx* ctx, const float* verts, int64_t n_ve
   if (rc != PIKO_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(ctx->device));
-  if ((rc = ensure_verts(ctx, std::max<int64_t>(n_verts, 1))) != PIKO_OK) return rc;
   Mat4 M;
   memcpy(M.m, mvp, sizeof M.m);
-  VertexArgs va{};
-  va.verts = verts; va.n_verts = n_verts; va.cap = ctx->xv_cap; va.ctl = ctx->ctl; va.M = M;
-  va.W = ctx->g.W; va.H = ctx->g.H; va.xv = ctx->xv;
-  CK(launch_vertex(va, false, s));
-  ResolveArgs a{};
-  a.verts = verts; a.xv = ctx->xv; a.idx = idx;
+  ResolveArgs a{};  // shade re-transforms the winning triangles' corners (no vertex stage)
+  a.verts = verts; a.xv = nullptr; a.M = M; a.idx = idx;
   a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
   a.g = ctx->g; a.g.nranks = nranks; a.g.rank = 0;
   a.all_keys = reinterpret_cast<const unsigned long long*>(d_all_keys);

@@ -94,8 +94,10 @@ struct VertexArgs {
 };
 
 struct SetupArgs {
-  const int4* xv;               // transformed vertices
+  const int4* xv;               // transformed vertices; null: fused vertex stage (below)
   long long xv_cap;             // corners with idx >= xv_cap are culled (overflowed frame)
+  const float* verts;           // fused mode: corners transformed here from verts ...
+  Mat4 M;                       // ... with M (same O1 arithmetic as k_vertex)
   const int32_t* idx;
   long long n_tris;
   Grid g;
@@ -142,7 +144,8 @@ struct RadixArgs {
 
 struct TileArgs {
   const float* verts;
-  const int4* xv;
+  const int4* xv;               // null: shade re-transforms corners from verts with M
+  Mat4 M;
   const int32_t* idx;
   float light[3];
   Grid g;
@@ -170,6 +173,7 @@ struct TileArgs {
 struct ResolveArgs {            // rank 0 after the NCCL gather
   const float* verts;
   const int4* xv;
+  Mat4 M;
   const int32_t* idx;
   float light[3];
   Grid g;
@@ -185,7 +189,8 @@ struct ResolveArgs {            // rank 0 after the NCCL gather
 // key buffer, then a per-pixel resolve/shade pass.
 struct FreePipeArgs {
   const float* verts;
-  const int4* xv;
+  const int4* xv;               // null: fused vertex stage (corners transformed in k_freepipe)
+  Mat4 M;
   long long xv_cap;
   const int32_t* idx;
   long long n_tris;

@@ -82,6 +82,15 @@ def oracle_frame(env, s, cov=True):
     return env[1].render(s.verts, s.idx, s.mvp, s.light, s.W, s.H, want_covcount=cov)
 
 
+@pytest.fixture(params=["fused", "separate"])
+def vs(request, monkeypatch):
+    """Vertex-stage mode of the contexts created in the test: transform fused
+    into k_setup or the separate k_vertex stage, forced through
+    PIKO_SEPARATE_VS (read by piko_create; unset = chosen per frame from V/T)."""
+    monkeypatch.setenv("PIKO_SEPARATE_VS", "1" if request.param == "separate" else "0")
+    return request.param
+
+
 # ------------------------------------------------------------------------------
 @pytest.mark.parametrize("bw,bh", [(8, 8), (16, 16), (32, 32), (64, 64), (8, 32), (64, 16)])
 def test_c1_all_bin_sizes(env, bw, bh):
@@ -136,7 +145,7 @@ def test_capacity_overflow_regrows(env):
 
 
 @pytest.mark.parametrize("name", ["c1", "c2"])
-def test_north_star_piko_draw_without_vertex_count(env, name):
+def test_north_star_piko_draw_without_vertex_count(env, name, vs):
     """piko_draw (no n_verts; derived on device as max(idx)+1) == oracle."""
     s = scenes.make(name)
     got = gpu_render(env, s, 16, indexed=False)
@@ -144,7 +153,7 @@ def test_north_star_piko_draw_without_vertex_count(env, name):
     assert_bins_equal(got, env, s, 16)
 
 
-def test_sparse_indices_vertex_overflow_regrows(env):
+def test_sparse_indices_vertex_overflow_regrows(env, vs):
     """piko_draw with indices far beyond 3*n_tris: the vertex-stage capacity
     overflows, grows and the frame is re-issued; still exact."""
     s = scenes.scene_soup(50, 128, 96, seed=61, name="sparse")
@@ -157,6 +166,8 @@ def test_sparse_indices_vertex_overflow_regrows(env):
     got = gpu_render(env, sp, 16, indexed=False)
     assert_frame_equal(got, oracle_frame(env, sp))
     assert_bins_equal(got, env, sp, 16)
+    fp = gpu_render(env, sp, 16, indexed=False, pipeline=env[0].PIKO_PIPE_FREEPIPE)
+    assert_frame_equal(fp, oracle_frame(env, sp))
 
 
 def test_empty_and_all_culled(env):
@@ -172,7 +183,7 @@ def test_empty_and_all_culled(env):
     assert_frame_equal(got, oracle_frame(env, c))
 
 
-def test_c2_full(env):
+def test_c2_full(env, vs):
     s = scenes.scene_c2()
     got = gpu_render(env, s, 16)
     assert_frame_equal(got, oracle_frame(env, s))
@@ -300,7 +311,7 @@ def test_argument_validation(env):
 
 # ---- FreePipe design alternative -----------
 @pytest.mark.parametrize("name", ["c1", "c2", "c3"])
-def test_freepipe_matches_oracle(env, name):
+def test_freepipe_matches_oracle(env, name, vs):
     piko = env[0]
     s = scenes.make(name)
     got = gpu_render(env, s, 16, pipeline=piko.PIKO_PIPE_FREEPIPE, frames=2)
@@ -351,7 +362,8 @@ def test_stats_and_profile(env):
     assert st["n_pairs"] == len(oprims) and st["n_bins"] == len(ostart) - 1
     oi, _ = env[1].setup(s.verts, s.idx, s.mvp, s.W, s.H)
     assert st["n_live"] == int(oi[:, 0].sum())
-    assert st["radix_passes"] == 2 and st["kernels_per_frame"] >= 5
+    # c3 is a shared-vertex mesh (2V <= 3T): separate vertex stage, 2 radix passes
+    assert st["radix_passes"] == 2 and st["kernels_per_frame"] == 5
     r.close()
 
 
