@@ -84,14 +84,22 @@ __device__ u64 g_k1_times[4][8192][8];
 #define TL_MARK(slot, i) do { if (threadIdx.x == 0 && (slot) < 8192) g_k1_times[3][slot][i] = gtimer(); } while (0)
 __device__ __forceinline__ void g_tl_extra(int job, int n, int cta) { g_k1_times[3][job][3] = n; g_k1_times[3][job][4] = cta; }
 #define TL_CTA(i) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_k1_times[0][7000 + blockIdx.x][i] = gtimer(); } while (0)
+// look-back detail of radix passes 0/1 (thread 0 = digit 0): [pass][chunk]
+// {level-1 end time, level-1 probes, level-2 probes, group-aggregate publish time}
+__device__ u64 g_rx_lb[2][8192][8];
+#define RX_LB(i, v) do { if (threadIdx.x == 0 && chunk < 8192 && a.pass < 2) g_rx_lb[a.pass][chunk][i] = (v); } while (0)
 }  // namespace piko
 extern "C" int piko_dbg_k1_times(void* host, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(host, piko::g_k1_times, bytes);
+}
+extern "C" int piko_dbg_rx_lb(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, piko::g_rx_lb, bytes);
 }
 namespace piko {
 #else
 #define K1_MARK(i) do { } while (0)
 #define RX_MARK(i) do { } while (0)
+#define RX_LB(i, v) do { } while (0)
 #define TL_MARK(slot, i) do { } while (0)
 #define g_tl_extra(a, b, c) do { } while (0)
 #define TL_CTA(i) do { } while (0)
@@ -524,15 +532,19 @@ __device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, u
       for (unsigned j = 0; j < nf; ++j)
         a.frag_list[base + incl - nf + j] = make_int2((int)b, (int)j);
     }
-    // single-fragment and empty bins
-    const int kind = !own ? 3 : (nf > 0 ? 4 : (cnt > 0 ? 1 : 2));
+    // single-fragment bins by size class (4 cnt > 3 frag, 2 frag, frag, else)
+    // and empty bins; kind < 0: not appended here
+    const unsigned q4 = 4u * cnt;
+    const int cls = q4 > 3u * (unsigned)a.frag ? 0 : q4 > 2u * (unsigned)a.frag ? 1
+                  : q4 > (unsigned)a.frag ? 2 : 3;
+    const int kind = !own ? -1 : (nf > 0 ? -2 : (cnt > 0 ? 1 + cls : LIST_EMPTY));
     const unsigned peers = __match_any_sync(0xffffffffu, kind);
     const int leader = __ffs(peers) - 1;
     unsigned pos = 0;
-    if ((kind == 1 || kind == 2) && lane == leader)
+    if (kind > 0 && lane == leader)
       pos = atomicAdd(&a.ctl->list_n[kind], (unsigned)__popc(peers));
     pos = __shfl_sync(0xffffffffu, pos, leader);
-    if (kind == 1 || kind == 2)
+    if (kind > 0)
       a.bin_list[(size_t)(kind - 1) * a.NB + pos + __popc(peers & lanemask_lt)] = (int32_t)b;
   }
 }
@@ -836,18 +848,30 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
   st_relaxed64(st, lb_pack(tag, chunk == 0 ? LB_INC : LB_AGG, total));
   __syncthreads();
   if (tid == 0) {
+    RX_LB(3, 0);
     __threadfence();
     sm.n = (atomicAdd(&a.garrive[(frame & 1) * a.gcap + grp], 1u) + 1u == (unsigned)gsize) ? 1u : 0u;
+    RX_LB(4, gtimer());  // arrival counted
   }
   __syncthreads();
   if (sm.n) {  // last chunk of the group to arrive: publish the group aggregate
     __threadfence();
+    // all LB_GROUP loads in flight together: a runtime-bounded loop would issue
+    // them one L2 round trip apart (in-order issue stalls on each add), which
+    // under a saturated memory system delays the group aggregate by ~20 us
+    unsigned cv[LB_GROUP];
+#pragma unroll
+    for (int j = 0; j < LB_GROUP; ++j)
+      cv[j] = j < gsize ? __ldcg(&a.ccount[(size_t)(g0 + j) * RX_RADIX + tid]) : 0u;
     unsigned gs = 0;
-    for (long long c = g0; c < g0 + gsize; ++c) gs += __ldcg(&a.ccount[(size_t)c * RX_RADIX + tid]);
+#pragma unroll
+    for (int j = 0; j < LB_GROUP; ++j) gs += cv[j];
+    RX_LB(5, gs ? gtimer() : gtimer());
     u64* gw = a.gstatus + (size_t)grp * RX_RADIX + tid;
     const u64 cur = ld_relaxed64(gw);
     if (lb_flag(cur) != LB_INC || lb_tag(cur) != tag)
       st_relaxed64(gw, lb_pack(tag, grp == 0 ? LB_INC : LB_AGG, gs));
+    RX_LB(3, gtimer());
   }
   const unsigned gprefix = block_excl(hist_d);
 
@@ -878,9 +902,11 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
   u64 excl = 0;
   if (chunk > 0) {
     bool done = false;
+    unsigned np1 = 0, np2 = 0;
     // level 1: own group, chunks chunk-1 .. g0
     long long c = chunk - 1;
     while (!done && c >= g0) {
+      ++np1;
       u64 sv[LB_GROUP];
 #pragma unroll
       for (int j = 0; j < LB_GROUP; ++j)
@@ -897,9 +923,11 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
       c -= j;
       if (!done && c >= g0 && j == 0) __nanosleep(32);
     }
+    RX_LB(0, gtimer());
     // level 2: previous groups
     long long gq = grp - 1;
     while (!done && gq >= 0) {
+      ++np2;
       constexpr int GPROBE = 16;
       u64 sv[GPROBE];
 #pragma unroll
@@ -919,6 +947,9 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
       if (!done && j == 0) __nanosleep(32);
     }
     st_relaxed64(st, lb_pack(tag, LB_INC, excl + total));
+    RX_LB(1, np1);
+    RX_LB(2, np2);
+    (void)np1; (void)np2;
   }
   if (chunk == g0 + gsize - 1)  // last chunk of its group: the group's inclusive prefix
     st_relaxed64(a.gstatus + (size_t)grp * RX_RADIX + tid, lb_pack(tag, LB_INC, excl + total));
@@ -1210,15 +1241,18 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   if (tid < NLIST) {
     unsigned n;
     if (a.npass > 0 && !ovf) n = a.ctl->list_n[tid];
-    else if (ovf) n = (tid == 2) ? (unsigned)a.owned : 0u;
+    else if (ovf) n = (tid == LIST_EMPTY) ? (unsigned)a.owned : 0u;
     else {
       const bool one = a.owned > 0, any = a.ctl->n_pairs > 0;
-      n = (tid == 1) ? (one && any) : (tid == 2) ? (one && !any) : 0u;
+      n = (tid == 1) ? (one && any) : (tid == LIST_EMPTY) ? (one && !any) : 0u;
     }
     s_ln[tid] = n;
   }
   __syncthreads();
-  const unsigned n_frag = s_ln[0], n_work = s_ln[0] + s_ln[1], n_empty = s_ln[2];
+  unsigned n_work = 0;
+#pragma unroll
+  for (int k = 0; k < LIST_EMPTY; ++k) n_work += s_ln[k];
+  const unsigned n_frag = s_ln[0], n_empty = s_ln[LIST_EMPTY];
   auto bin_range = [&](int b, int& rs, int& re) {
     if (a.npass == 0) { rs = 0; re = (int)a.ctl->n_pairs; return; }
     rs = a.bin_start[b];
@@ -1235,7 +1269,14 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
       rs = s0 + it.y * a.frag;
       re = min(rs + a.frag, e0);
     } else if (w < n_work) {
-      b = (a.npass == 0) ? 0 : a.bin_list[w - n_frag];
+      if (a.npass == 0) {
+        b = 0;
+      } else {  // size classes, largest first: list k >= 1 lives at bin_list[(k-1) NB]
+        unsigned r = w - n_frag;
+        int k = 1;
+        while (r >= s_ln[k]) r -= s_ln[k++];
+        b = a.bin_list[(size_t)(k - 1) * g.NB + r];
+      }
       bin_range(b, rs, re);
       nf = 0;
     } else {
@@ -1245,7 +1286,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   auto empty_bin = [&](unsigned e) -> int {  // e < n_empty
     if (ovf) return g.rank + (int)e * g.nranks;
     if (a.npass == 0) return 0;
-    return a.bin_list[(size_t)g.NB + e];
+    return a.bin_list[(size_t)(LIST_EMPTY - 1) * g.NB + e];
   };
 
   // ---- LoadBalance schedule over the work list ----------------

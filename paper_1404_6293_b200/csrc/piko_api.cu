@@ -82,7 +82,7 @@ struct piko_ctx {
   uint32_t* bin_count = nullptr;
   int32_t* bin_start = nullptr;
   int2* frag_list = nullptr; long long frag_cap = 0;  // split-bin fragments
-  int32_t* bin_list = nullptr;       // [2][NB] single-fragment and empty bins
+  int32_t* bin_list = nullptr;       // [NLIST-1][NB] single-fragment bins by size class, empty bins
   unsigned long long* gkey = nullptr;  // [NB][bw*bh] key tiles of split bins
   uint32_t* gcov = nullptr;          // [NB][bw*bh] coverage tiles (debug)
   uint32_t* arrive = nullptr;        // [NB] fragment arrival counters
@@ -193,7 +193,7 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   const long long npx = (long long)width * height;
   bool ok = cudaMalloc(&ctx->bin_count, sizeof(uint32_t) * g.NB) == cudaSuccess &&
             cudaMalloc(&ctx->bin_start, sizeof(int32_t) * (g.NB + 1)) == cudaSuccess &&
-            cudaMalloc(&ctx->bin_list, sizeof(int32_t) * 2 * (size_t)g.NB) == cudaSuccess &&
+            cudaMalloc(&ctx->bin_list, sizeof(int32_t) * (NLIST - 1) * (size_t)g.NB) == cudaSuccess &&
             cudaMalloc(&ctx->gkey, sizeof(unsigned long long) * (size_t)g.NB * bin_w * bin_h) == cudaSuccess &&
             cudaMalloc(&ctx->arrive, sizeof(uint32_t) * (size_t)g.NB) == cudaSuccess &&
             cudaMalloc(&ctx->ctl, sizeof(Control)) == cudaSuccess &&
@@ -522,10 +522,13 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
 static void adapt_tri_chunk(piko_ctx* ctx) {
   const double T = (double)ctx->last_T, P = (double)ctx->h_ctl->n_pairs;
   if (T <= 0) return;
-  const double want = P > 0 ? RX_CHUNK * T / P : (double)EX_MAX_TRIS;
-  int tc = RX_THREADS;
-  while (tc * 2 <= EX_MAX_TRIS && tc * 2 <= want) tc *= 2;
-  ctx->tri_chunk = tc;
+  // Expected pairs per chunk at most 3/4 of RX_CHUNK: a chunk over RX_CHUNK
+  // takes the windowed slow path (several times slower), and because its group
+  // aggregate is then published late it stalls the look-back of every later
+  // chunk.  Any multiple of RX_THREADS works (tpt = tri_chunk / RX_THREADS).
+  const double want = P > 0 ? 0.75 * RX_CHUNK * T / P : (double)EX_MAX_TRIS;
+  const long long tc = (long long)(want / RX_THREADS) * RX_THREADS;
+  ctx->tri_chunk = (int)std::max<long long>(RX_THREADS, std::min<long long>(EX_MAX_TRIS, tc));
 }
 
 // Wait for the pending frame; PIKO_ECAPACITY (and grown capacity) on overflow.

@@ -29,9 +29,13 @@ constexpr unsigned long long MAX_PAIRS = 1ull << 31;  // bin_start is int32
 // `frag` pairs is split into fragments of `frag` consecutive CSR entries that
 // different CTAs rasterize and merge into a global key tile (64-bit atomicMin);
 // the last fragment to arrive shades the bin.  Lists: [0] fragments of split
-// bins (processed first: longest bins first, LPT), [1] single-fragment bins,
-// [2] empty bins.
-constexpr int NLIST = 3;
+// bins, [1 .. SIZE_CLASSES] single-fragment bins by size class (pairs >
+// 3/4, 1/2, 1/4 of a fragment, rest), [NLIST-1] empty bins.  k_tile drains
+// them in that order: largest work first (an LPT approximation without a sort,
+// so a CTA left with a second item gets a small one).
+constexpr int SIZE_CLASSES = 4;
+constexpr int NLIST = 2 + SIZE_CLASSES;
+constexpr int LIST_EMPTY = NLIST - 1;
 constexpr int FRAG_ROUNDS = 4;   // fragment = FRAG_ROUNDS * threads-per-CTA pairs
 constexpr int EMPTY_GROUP = 8;   // empty bins per k_tile queue ticket
 
@@ -135,7 +139,7 @@ struct RadixArgs {
   int NB;
   int rank, nranks;             // only owned bins enter the work lists
   int2* frag_list;              // [frag_cap] {bin, fragment}
-  int32_t* bin_list;            // [2][NB] single-fragment bins, empty bins
+  int32_t* bin_list;            // [NLIST-1][NB] single-fragment bins by size class, empty bins
   unsigned long long* gkey;     // [NB][bw*bh] key tiles of split bins
   uint32_t* gcov;               // [NB][bw*bh] coverage tiles (debug) or null
   int frag;                     // pairs per fragment

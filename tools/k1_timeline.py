@@ -70,6 +70,30 @@ e = buf[1, :nrx0].astype(np.int64)
 print("   expand detail: loads+counts median %.0f, scan %.0f, expansion %.0f, reload %.0f" % (
     np.median(e[:, 5] - e[:, 0]), np.median(e[:, 6] - e[:, 5]), np.median(e[:, 7] - e[:, 6]),
     np.median(e[:, 1] - e[:, 7])))
+lb = np.zeros((2, 8192, 8), np.uint64)
+if h.piko_dbg_rx_lb(lb.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(lb.nbytes)) == 0:
+    for p_, n_ in ((0, nrx0), (1, (st["n_pairs"] + 4095) // 4096)):
+        tt = buf[1 + p_, :n_].astype(np.int64)
+        ll = lb[p_, :n_].astype(np.int64)
+        ok = (tt[:, 2] > 0) & (ll[:, 0] > 0)
+        l1 = ll[ok, 0] - tt[ok, 2]
+        l2 = tt[ok, 3] - ll[ok, 0]
+        print(f"   pass {p_} look-back: level-1 median {np.median(l1):.0f} p90 {np.percentile(l1, 90):.0f};"
+              f" level-2 median {np.median(l2):.0f} p90 {np.percentile(l2, 90):.0f};"
+              f" probes l1 median {np.median(ll[ok, 1]):.0f} max {ll[ok, 1].max()},"
+              f" l2 median {np.median(ll[ok, 2]):.0f} max {ll[ok, 2].max()}")
+        ga = ll[:, 3]
+        gm = (ga > 0) & (tt[:, 0] > 0) & (ga > tt[:, 0])
+        if gm.any():
+            # group aggregate published vs the arriving chunk's expand end
+            d = ga[gm] - tt[gm, 1]
+            print(f"   pass {p_} group aggregate publish after own expand/load end: median {np.median(d):.0f} p90 {np.percentile(d, 90):.0f}")
+            a1 = ll[gm, 4] - tt[gm, 1]
+            a2 = ll[gm, 5] - ll[gm, 4]
+            a3 = ll[gm, 3] - ll[gm, 5]
+            print(f"      -> arrival atomic done {np.median(a1):.0f} (p90 {np.percentile(a1, 90):.0f}),"
+                  f" group loads {np.median(a2):.0f} (p90 {np.percentile(a2, 90):.0f}),"
+                  f" read-check-store {np.median(a3):.0f} (p90 {np.percentile(a3, 90):.0f})")
 nrx = (st["n_pairs"] + 4095) // 4096
 show("radix pass 1", buf[2], ["start", "load", "rank", "lookback", "scatter"], nrx)
 nb = st["owned_bins"]
