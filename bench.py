@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle work")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--multi", default="sort-first", choices=["sort-first", "sort-last"],
+                    help="N > 1 decomposition: screen bins (sort-first) or triangle ranges + "
+                         "ncclReduce(min) of the key images (sort-last)")
     return ap.parse_args()
 
 
@@ -162,6 +165,8 @@ def run_piko(args):
     idx = torch.from_numpy(s.idx).to(dev)
     r = piko.Renderer(s.W, s.H, bw, device=dev)
     if world > 1:
+        if args.multi == "sort-last":
+            piko.piko_set_multi(r.ctx, piko.PIKO_MULTI_SORT_LAST)
         obj = [piko.piko_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         piko.piko_attach_comm(r.ctx, obj[0], rank, world)
@@ -309,8 +314,9 @@ def run_piko(args):
         "config": {"workload": workload_name(args.config, s, bw), "config": args.config,
                    "width": s.W, "height": s.H, "bin": bw, "n_tris": T, "n_verts": V,
                    "n_pairs": P, "n_live": L, "covered_px": ncov, "l2": "flushed (256 MiB) before every step",
-                   "parallelism": f"sort-first x{world}" if world > 1 else "1 GPU"},
+                   "parallelism": f"{args.multi} x{world}" if world > 1 else "1 GPU"},
         "fps": 1e3 / ms,
+        "ms_p10_p50_p90": [float(x) for x in np.percentile(step_ms, [10, 50, 90])],
         "frame_roofline": {"algorithmic_bytes": frame_bytes, "frac": frame_bytes / (ms / 1e3) / 1e9 / peak},
         "kernel_ms": per_frame,
         "kernel_ms_note": "per-stage CUDA-event times from a second K-step pass (events between kernels)",

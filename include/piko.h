@@ -196,6 +196,28 @@ int64_t piko_owned_bins(int width, int height, int bin_w, int bin_h, int rank, i
  * the frame.  NCCL is loaded at run time (libnccl.so.2).                      */
 int piko_attach_comm(piko_ctx *ctx, const void *nccl_unique_id, int rank, int nranks);
 
+/* Multi-GPU decomposition used by piko_attach_comm / piko_set_partition
+ * (call before them; PIKO_ESTATE once a communicator is attached).
+ *   PIKO_MULTI_SORT_FIRST (default): screen partition, above.
+ *   PIKO_MULTI_SORT_LAST (the "Tiled Depth-Based
+ *     Composition" row of the paper's Table 1): rank r renders the
+ *     triangle range [t0_r, t0_{r+1}), t0_r = floor(n_tris*r/nranks) rounded
+ *     down to a multiple of 4 (t0_nranks = n_tris), over ALL bins into packed
+ *     keys with global primIDs; the key images are combined on rank 0 with
+ *     ncclReduce(ncclMin, ncclUint64) -- the (depth, primID) minimum is
+ *     associative and commutative, so the result is bit-identical -- and rank 0
+ *     shades.  With a partition (virtual rank) piko_draw_tile_keys writes that
+ *     rank's full key image, u64[NB][bin_w*bin_h] (owned_max = NB), and
+ *     piko_resolve_keys(nranks = 1) shades the element-wise minimum.         */
+#define PIKO_MULTI_SORT_FIRST 0
+#define PIKO_MULTI_SORT_LAST 1
+int piko_set_multi(piko_ctx *ctx, int mode);
+
+/* Host-only (no CUDA): sort-last triangle range [*t0, *t1) of `rank` of
+ * `nranks` for n_tris triangles (see PIKO_MULTI_SORT_LAST).  PIKO_EINVAL on
+ * bad arguments.                                                             */
+int piko_triangle_range(int64_t n_tris, int rank, int nranks, int64_t *t0, int64_t *t1);
+
 /* Frame statistics of the last frame (blocks until it completed).            */
 typedef struct {
   int64_t n_tris;       /* triangles submitted                                */

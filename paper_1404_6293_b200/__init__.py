@@ -19,6 +19,7 @@ PIKO_OK, PIKO_EINVAL, PIKO_ENOMEM, PIKO_ECUDA, PIKO_ENCCL, PIKO_ECAPACITY, PIKO_
 PIKO_DEBUG_COVERAGE_COUNT = 1
 PIKO_SYNC_CHECKED, PIKO_SYNC_ASYNC = 0, 1
 PIKO_PIPE_BINNED, PIKO_PIPE_FREEPIPE = 0, 1
+PIKO_MULTI_SORT_FIRST, PIKO_MULTI_SORT_LAST = 0, 1
 
 # names of every symbol include/piko.h declares (checked by tests)
 EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_set_sync",
@@ -26,7 +27,8 @@ EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_se
            "piko_set_debug", "piko_get_coverage", "piko_set_partition", "piko_attach_comm",
            "piko_get_stats", "piko_nccl_unique_id", "piko_draw_indexed",
            "piko_draw_tile_keys", "piko_resolve_keys", "piko_tile_keys_count", "piko_owned_bins",
-           "piko_set_pipeline", "piko_set_profiling", "piko_get_profile")
+           "piko_set_pipeline", "piko_set_profiling", "piko_get_profile", "piko_set_multi",
+           "piko_triangle_range")
 STAGES = ("clear", "vertex", "setup", "radix", "tile", "gather", "resolve")
 
 
@@ -68,6 +70,8 @@ def _load():
         "piko_set_debug": ([P, U], I),
         "piko_get_coverage": ([P, ctypes.POINTER(P)], I),
         "piko_set_partition": ([P, I, I], I),
+        "piko_set_multi": ([P, I], I),
+        "piko_triangle_range": ([I64, I, I, ctypes.POINTER(I64), ctypes.POINTER(I64)], I),
         "piko_attach_comm": ([P, P, I, I], I),
         "piko_get_stats": ([P, ctypes.POINTER(piko_stats)], I),
         "piko_nccl_unique_id": ([P], I),
@@ -237,6 +241,19 @@ def piko_get_coverage(ctx):
 
 def piko_set_partition(ctx, rank, nranks):
     return _check(ctx, _lib.piko_set_partition(ctx, rank, nranks))
+
+
+def piko_set_multi(ctx, mode):
+    return _check(ctx, _lib.piko_set_multi(ctx, mode))
+
+
+def piko_triangle_range(n_tris, rank, nranks):
+    """Sort-last triangle range (t0, t1) of a rank (host-only, no CUDA)."""
+    t0, t1 = ctypes.c_int64(), ctypes.c_int64()
+    rc = _lib.piko_triangle_range(int(n_tris), rank, nranks, ctypes.byref(t0), ctypes.byref(t1))
+    if rc != PIKO_OK:
+        raise PikoError(rc, "bad arguments")
+    return t0.value, t1.value
 
 
 def piko_attach_comm(ctx, unique_id: bytes, rank, nranks):

@@ -1179,8 +1179,8 @@ struct TileSmem {
 template <bool COV, bool KEYS_ONLY>
 __device__ __forceinline__ void store_pixel(const TileArgs& a, const float L[3], int job, int p,
                                             int npx, int x, int y, u64 key, unsigned cov) {
-  if (KEYS_ONLY) {
-    a.tile_keys[(size_t)job * npx + p] = key;
+  if (KEYS_ONLY) {  // sort-last ranks render a triangle range: global primIDs
+    a.tile_keys[(size_t)job * npx + p] = key == CLEAR_KEY ? key : key + a.prim_base;
     return;
   }
   const size_t o = (size_t)y * a.g.W + x;

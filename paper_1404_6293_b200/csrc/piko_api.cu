@@ -30,7 +30,8 @@ namespace {
 typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef int ncclResult_t;
-enum { ncclUint8_ = 1 };  // ncclDataType_t value for ncclUint8
+enum { ncclUint8_ = 1, ncclUint64_ = 5 };  // ncclDataType_t values
+enum { ncclMin_ = 3 };                      // ncclRedOp_t value
 
 struct Nccl {
   void* h = nullptr;
@@ -38,6 +39,7 @@ struct Nccl {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -48,7 +50,7 @@ struct Nccl {
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) { err = "cannot dlopen libnccl.so.2"; return false; }
 #define PIKO_SYM(n) n = reinterpret_cast<decltype(n)>(dlsym(h, "nccl" #n)); if (!n) { err = "missing nccl" #n; return false; }
-    PIKO_SYM(CommInitRank) PIKO_SYM(CommDestroy) PIKO_SYM(Send) PIKO_SYM(Recv)
+    PIKO_SYM(CommInitRank) PIKO_SYM(CommDestroy) PIKO_SYM(Send) PIKO_SYM(Recv) PIKO_SYM(Reduce)
     PIKO_SYM(GroupStart) PIKO_SYM(GroupEnd) PIKO_SYM(GetErrorString) PIKO_SYM(GetUniqueId)
 #undef PIKO_SYM
     return true;
@@ -71,6 +73,9 @@ struct piko_ctx {
   unsigned debug = 0;
   int sync_mode = PIKO_SYNC_CHECKED;
   bool virt = false;        // virtual rank (partition without communicator)
+  int multi = PIKO_MULTI_SORT_FIRST;
+  int mrank = 0, mnranks = 1;  // multi-GPU rank / size (sort-last: g.rank = 0, g.nranks = 1)
+  long long prim_base = 0;     // sort-last: first triangle of this rank's range
   std::string err;
 
   // scratch
@@ -161,6 +166,9 @@ struct piko_ctx {
 extern "C" int64_t piko_owned_bins(int, int, int, int, int, int, int32_t*, int64_t);
 
 static void set_ownership(piko_ctx* ctx, int rank, int nranks) {
+  ctx->mrank = rank;
+  ctx->mnranks = nranks;
+  if (ctx->multi == PIKO_MULTI_SORT_LAST) { rank = 0; nranks = 1; }  // every rank owns every bin
   ctx->g.rank = rank;
   ctx->g.nranks = nranks;
   ctx->owned = (int)piko_owned_bins(ctx->g.W, ctx->g.H, ctx->bw, ctx->bh, rank, nranks, nullptr, 0);
@@ -388,7 +396,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
                          cudaStream_t s, unsigned long long* keys_out = nullptr) {
   if (ctx->pipeline == PIKO_PIPE_FREEPIPE)
     return enqueue_freepipe(ctx, verts, V, idx, T, M, L, rgba, depth, s);
-  const bool gather = keys_out == nullptr && ctx->comm != nullptr && ctx->g.nranks > 1;
+  const bool gather = keys_out == nullptr && ctx->comm != nullptr && ctx->mnranks > 1;
   const bool keys_only = gather || keys_out != nullptr;
   cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
   if (ctx->prof && !ev) return ctx->fail(PIKO_ECUDA, "cannot create profiling events");
@@ -418,7 +426,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   CK(mark(1 + PIKO_STAGE_CLEAR));
   const bool sep = separate_vs(ctx, V, T);
   ctx->last_kernels = 2 + ctx->npass + (ctx->npass == 1 ? 1 : 0) +
-                      (sep ? 1 + (V < 0 && T > 0 ? 1 : 0) : 0) + (gather && ctx->g.rank == 0 ? 1 : 0);
+                      (sep ? 1 + (V < 0 && T > 0 ? 1 : 0) : 0) + (gather && ctx->mrank == 0 ? 1 : 0);
   if (sep) {
     if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
     VertexArgs a{};
@@ -470,6 +478,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
     a.gcov = ctx->gcov; a.arrive = ctx->arrive; a.frag = tile_frag(ctx->bw, ctx->bh);
     a.garrive = ctx->garr; a.gcap = ctx->gcap;
+    a.prim_base = (unsigned)ctx->prim_base;
     if (keys_only) a.out_cov = nullptr;
     const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, keys_only)));
     CK(launch_tile(a, ctx->bw, ctx->bh, grid, a.out_cov != nullptr, keys_only, ctx->pdl, s));
@@ -478,8 +487,14 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   if (gather) {
     const size_t tile_bytes = sizeof(unsigned long long) * ctx->bw * ctx->bh;
     const size_t bytes = tile_bytes * ctx->owned_max;
-    if (g_nccl.GroupStart() != 0) return ctx->fail(PIKO_ENCCL, "ncclGroupStart failed");
     int rc = 0;
+    if (ctx->multi == PIKO_MULTI_SORT_LAST) {
+      // element-wise (depth, primID) minimum of the full key images on rank 0
+      rc = g_nccl.Reduce(ctx->tile_keys, ctx->mrank == 0 ? ctx->all_keys : nullptr,
+                         (size_t)ctx->owned * ctx->bw * ctx->bh, ncclUint64_, ncclMin_, 0, ctx->comm, s);
+      if (rc != 0) return ctx->fail(PIKO_ENCCL, "ncclReduce failed: %s", g_nccl.GetErrorString(rc));
+    } else {
+    if (g_nccl.GroupStart() != 0) return ctx->fail(PIKO_ENCCL, "ncclGroupStart failed");
     if (ctx->g.rank == 0) {
       CK(cudaMemcpyAsync(ctx->all_keys, ctx->tile_keys, tile_bytes * ctx->owned,
                          cudaMemcpyDeviceToDevice, s));
@@ -495,11 +510,14 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     const int rc2 = g_nccl.GroupEnd();
     if (rc != 0 || rc2 != 0)
       return ctx->fail(PIKO_ENCCL, "NCCL gather failed: %s", g_nccl.GetErrorString(rc ? rc : rc2));
+    }
     (void)bytes;
     CK(mark(1 + PIKO_STAGE_GATHER));
-    if (ctx->g.rank == 0) {
+    if (ctx->mrank == 0) {
+      // winners may come from any rank's triangles: re-transform their corners
+      // from verts (xv may cover only this rank's range) with the full idx
       ResolveArgs a{};
-      a.verts = verts; a.xv = sep ? ctx->xv : nullptr; a.M = M; a.idx = idx;
+      a.verts = verts; a.xv = nullptr; a.M = M; a.idx = idx - 3 * ctx->prim_base;
       a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
       a.g = ctx->g; a.all_keys = ctx->all_keys; a.owned_max = ctx->owned_max;
       a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
@@ -560,7 +578,7 @@ static int validate_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, 
                          float L[3]) {
   if (n_tris < 0) return ctx->fail(PIKO_EINVAL, "n_tris < 0");
   if (!mvp || !light) return ctx->fail(PIKO_EINVAL, "mvp and light must be non-null");
-  const bool need_out = !(ctx->comm && ctx->g.nranks > 1 && ctx->g.rank != 0) && !ctx->keys_mode;
+  const bool need_out = !(ctx->comm && ctx->mnranks > 1 && ctx->mrank != 0) && !ctx->keys_mode;
   if (need_out && (!rgba || !depth)) return ctx->fail(PIKO_EINVAL, "null output buffer");
   if (n_tris > 0 && (!verts || !idx)) return ctx->fail(PIKO_EINVAL, "null scene buffer");
   if ((reinterpret_cast<uintptr_t>(verts) | reinterpret_cast<uintptr_t>(idx) |
@@ -582,6 +600,14 @@ static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32
   int rc = validate_draw(ctx, verts, idx, n_tris, mvp, light, rgba, depth, L);
   if (rc != PIKO_OK) return rc;
   CK(cudaSetDevice(ctx->device));
+  ctx->prim_base = 0;
+  if (ctx->multi == PIKO_MULTI_SORT_LAST && ctx->mnranks > 1) {  // this rank's triangle range
+    int64_t t0 = 0, t1 = 0;
+    piko_triangle_range(n_tris, ctx->mrank, ctx->mnranks, &t0, &t1);
+    idx += 3 * t0;
+    n_tris = (int32_t)(t1 - t0);
+    ctx->prim_base = t0;
+  }
   // status of a previous asynchronous frame (grows capacity if it overflowed)
   int prev = PIKO_OK;
   if (ctx->pending) prev = check_frame(ctx);
@@ -604,7 +630,7 @@ static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32
     if (rc != PIKO_ECAPACITY) return rc;
     // multi-rank: every rank must re-issue together; a capacity miss is
     // reported instead of re-issued so ranks cannot diverge.
-    if (ctx->comm && ctx->g.nranks > 1) return rc;
+    if (ctx->comm && ctx->mnranks > 1) return rc;
   }
   return rc;
 }
@@ -660,7 +686,7 @@ extern "C" int piko_draw_host(piko_ctx* ctx, const float* h_verts, int64_t n_ver
   int rc = draw_impl(ctx, ctx->d_verts, n_verts, ctx->d_idx, n_tris, mvp, light, ctx->d_rgba,
                      ctx->d_depth, s, true);
   if (rc != PIKO_OK) return rc;
-  const bool has_out = !(ctx->comm && ctx->g.nranks > 1 && ctx->g.rank != 0);
+  const bool has_out = !(ctx->comm && ctx->mnranks > 1 && ctx->mrank != 0);
   if (has_out) {
     CK(cudaMemcpyAsync(h_rgba, ctx->d_rgba, sizeof(float) * 4 * npx, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(h_depth, ctx->d_depth, sizeof(float) * npx, cudaMemcpyDeviceToHost, s));
@@ -714,6 +740,27 @@ extern "C" int piko_get_coverage(const piko_ctx* ctx, const uint32_t** d_cov) {
   return PIKO_OK;
 }
 
+// boundaries are multiples of 4 triangles so idx + 3 t0 keeps idx's 16-byte alignment
+extern "C" int piko_triangle_range(int64_t n_tris, int rank, int nranks, int64_t* t0, int64_t* t1) {
+  if (n_tris < 0 || nranks < 1 || rank < 0 || rank >= nranks || !t0 || !t1) return PIKO_EINVAL;
+  auto cut = [&](int r) -> int64_t { return r >= nranks ? n_tris : (n_tris * r / nranks) & ~int64_t(3); };
+  *t0 = cut(rank);
+  *t1 = cut(rank + 1);
+  return PIKO_OK;
+}
+
+extern "C" int piko_set_multi(piko_ctx* ctx, int mode) {
+  if (!ctx) return PIKO_EINVAL;
+  if (mode != PIKO_MULTI_SORT_FIRST && mode != PIKO_MULTI_SORT_LAST)
+    return ctx->fail(PIKO_EINVAL, "unknown multi-GPU mode");
+  if (ctx->comm) return ctx->fail(PIKO_ESTATE, "communicator attached");
+  if (ctx->pending) check_frame(ctx);
+  ctx->multi = mode;
+  set_ownership(ctx, ctx->mrank, ctx->mnranks);  // re-derive bin ownership
+  ctx->need_reset = true;
+  return PIKO_OK;
+}
+
 extern "C" int piko_set_partition(piko_ctx* ctx, int rank, int nranks) {
   if (!ctx) return PIKO_EINVAL;
   if (ctx->comm) return ctx->fail(PIKO_ESTATE, "communicator attached");
@@ -739,7 +786,9 @@ extern "C" int piko_attach_comm(piko_ctx* ctx, const void* uid, int rank, int nr
   set_ownership(ctx, rank, nranks);
   const size_t tile_bytes = sizeof(unsigned long long) * ctx->bw * ctx->bh;
   CK(cudaMalloc(&ctx->tile_keys, tile_bytes * std::max(ctx->owned_max, 1)));
-  if (rank == 0) CK(cudaMalloc(&ctx->all_keys, tile_bytes * ctx->owned_max * (size_t)nranks));
+  // rank 0's receive buffer: every rank's tiles (sort-first), or one reduced image (sort-last)
+  const size_t slots = ctx->multi == PIKO_MULTI_SORT_LAST ? 1 : (size_t)nranks;
+  if (rank == 0) CK(cudaMalloc(&ctx->all_keys, tile_bytes * ctx->owned_max * slots));
   return PIKO_OK;
 }
 
@@ -854,7 +903,7 @@ extern "C" int piko_set_pipeline(piko_ctx* ctx, int pipeline) {
   if (!ctx) return PIKO_EINVAL;
   if (pipeline != PIKO_PIPE_BINNED && pipeline != PIKO_PIPE_FREEPIPE)
     return ctx->fail(PIKO_EINVAL, "unknown pipeline");
-  if (pipeline == PIKO_PIPE_FREEPIPE && ctx->g.nranks > 1)
+  if (pipeline == PIKO_PIPE_FREEPIPE && ctx->mnranks > 1)
     return ctx->fail(PIKO_ESTATE, "FreePipe renders the whole screen on one GPU");
   if (ctx->pending) check_frame(ctx);
   ctx->pipeline = pipeline;

@@ -172,6 +172,7 @@ struct TileArgs {
   int frag;
   uint32_t* garrive;            // [npass][2][gcap] look-back group arrival counters;
   long long gcap;               //   k_tile zeroes the next frame's parity
+  unsigned prim_base;           // keys-only: added to the primID of every stored key (sort-last)
 };
 
 struct ResolveArgs {            // rank 0 after the NCCL gather
