@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--multi", default="sort-first", choices=["sort-first", "sort-last"],
                     help="N > 1 decomposition: screen bins (sort-first) or triangle ranges + "
                          "ncclReduce(min) of the key images (sort-last)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="sort-first tile exchange: tile kernel stores keys into rank 0's memory "
+                         "over NVLink (p2p) or NCCL send/recv; auto = p2p, NCCL if any rank "
+                         "cannot map the peer buffers")
     return ap.parse_args()
 
 
@@ -164,12 +168,33 @@ def run_piko(args):
     verts = torch.from_numpy(s.verts).to(dev)
     idx = torch.from_numpy(s.idx).to(dev)
     r = piko.Renderer(s.W, s.H, bw, device=dev)
+    transport = None
     if world > 1:
-        if args.multi == "sort-last":
-            piko.piko_set_multi(r.ctx, piko.PIKO_MULTI_SORT_LAST)
-        obj = [piko.piko_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        piko.piko_attach_comm(r.ctx, obj[0], rank, world)
+        def attach(rd, xport):
+            if args.multi == "sort-last":
+                piko.piko_set_multi(rd.ctx, piko.PIKO_MULTI_SORT_LAST)
+            elif xport == "p2p":
+                piko.piko_set_transport(rd.ctx, piko.PIKO_XPORT_P2P)
+            obj = [piko.piko_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            try:
+                piko.piko_attach_comm(rd.ctx, obj[0], rank, world)
+                ok = 1
+            except piko.PikoError as e:
+                print(f"rank {rank}: attach ({xport}) failed: {e}", file=sys.stderr)
+                ok = 0
+            t = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)  # every rank agrees on the transport
+            return bool(t.item())
+        transport = "nccl" if args.multi == "sort-last" or args.transport == "nccl" else "p2p"
+        if not attach(r, transport):
+            if args.transport != "auto" or transport == "nccl":
+                raise SystemExit("multi-GPU attach failed")
+            r.close()
+            r = piko.Renderer(s.W, s.H, bw, device=dev)
+            transport = "nccl"
+            if not attach(r, transport):
+                raise SystemExit("multi-GPU attach failed")
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
@@ -314,7 +339,7 @@ def run_piko(args):
         "config": {"workload": workload_name(args.config, s, bw), "config": args.config,
                    "width": s.W, "height": s.H, "bin": bw, "n_tris": T, "n_verts": V,
                    "n_pairs": P, "n_live": L, "covered_px": ncov, "l2": "flushed (256 MiB) before every step",
-                   "parallelism": f"{args.multi} x{world}" if world > 1 else "1 GPU"},
+                   "parallelism": f"{args.multi} x{world} ({transport})" if world > 1 else "1 GPU"},
         "fps": 1e3 / ms,
         "ms_p10_p50_p90": [float(x) for x in np.percentile(step_ms, [10, 50, 90])],
         "frame_roofline": {"algorithmic_bytes": frame_bytes, "frac": frame_bytes / (ms / 1e3) / 1e9 / peak},

@@ -213,6 +213,29 @@ int piko_attach_comm(piko_ctx *ctx, const void *nccl_unique_id, int rank, int nr
 #define PIKO_MULTI_SORT_LAST 1
 int piko_set_multi(piko_ctx *ctx, int mode);
 
+/* Transport of the sort-first tile exchange (call before piko_attach_comm):
+ *   PIKO_XPORT_NCCL (default): k_tile writes keys locally, then grouped
+ *     ncclSend/ncclRecv to rank 0, then rank 0's resolve kernel.
+ *   PIKO_XPORT_P2P (SURVEY 8(e) "fused v2"): rank 0 owns the exchange buffer
+ *     u64[2][nranks][owned_max][bin_w*bin_h] (double-buffered by frame parity)
+ *     plus arrival flags; the other ranks map it with CUDA IPC over NVLink
+ *     during piko_attach_comm.  Each rank's tile kernel stores its keys
+ *     straight into rank 0's buffer as bins finish (the transfer overlaps the
+ *     raster), then its last CTA raises the rank's arrival flag (system-scope
+ *     release); rank 0's resolve kernel waits for all flags (acquire) and
+ *     releases the slot when read.  No NCCL call per frame.  A flag wait that
+ *     exceeds 10 s reports PIKO_ENCCL instead of hanging.  Sort-first only. */
+#define PIKO_XPORT_NCCL 0
+#define PIKO_XPORT_P2P 1
+int piko_set_transport(piko_ctx *ctx, int transport);
+
+/* The P2P transport between contexts of ONE process on one device ("virtual
+ * ranks", for tests): attach rank 0 with root == ctx first, then the other
+ * ranks with the rank-0 context as root; they share its buffers.  Draw ranks
+ * 1..nranks-1 before rank 0 (rank 0's resolve waits for their flags), and
+ * destroy rank 0 last.                                                       */
+int piko_attach_local_peers(piko_ctx *ctx, piko_ctx *root, int rank, int nranks);
+
 /* Host-only (no CUDA): sort-last triangle range [*t0, *t1) of `rank` of
  * `nranks` for n_tris triangles (see PIKO_MULTI_SORT_LAST).  PIKO_EINVAL on
  * bad arguments.                                                             */

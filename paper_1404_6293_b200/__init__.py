@@ -20,6 +20,7 @@ PIKO_DEBUG_COVERAGE_COUNT = 1
 PIKO_SYNC_CHECKED, PIKO_SYNC_ASYNC = 0, 1
 PIKO_PIPE_BINNED, PIKO_PIPE_FREEPIPE = 0, 1
 PIKO_MULTI_SORT_FIRST, PIKO_MULTI_SORT_LAST = 0, 1
+PIKO_XPORT_NCCL, PIKO_XPORT_P2P = 0, 1
 
 # names of every symbol include/piko.h declares (checked by tests)
 EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_set_sync",
@@ -28,7 +29,7 @@ EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_se
            "piko_get_stats", "piko_nccl_unique_id", "piko_draw_indexed",
            "piko_draw_tile_keys", "piko_resolve_keys", "piko_tile_keys_count", "piko_owned_bins",
            "piko_set_pipeline", "piko_set_profiling", "piko_get_profile", "piko_set_multi",
-           "piko_triangle_range")
+           "piko_triangle_range", "piko_set_transport", "piko_attach_local_peers")
 STAGES = ("clear", "vertex", "setup", "radix", "tile", "gather", "resolve")
 
 
@@ -71,6 +72,8 @@ def _load():
         "piko_get_coverage": ([P, ctypes.POINTER(P)], I),
         "piko_set_partition": ([P, I, I], I),
         "piko_set_multi": ([P, I], I),
+        "piko_set_transport": ([P, I], I),
+        "piko_attach_local_peers": ([P, P, I, I], I),
         "piko_triangle_range": ([I64, I, I, ctypes.POINTER(I64), ctypes.POINTER(I64)], I),
         "piko_attach_comm": ([P, P, I, I], I),
         "piko_get_stats": ([P, ctypes.POINTER(piko_stats)], I),
@@ -245,6 +248,14 @@ def piko_set_partition(ctx, rank, nranks):
 
 def piko_set_multi(ctx, mode):
     return _check(ctx, _lib.piko_set_multi(ctx, mode))
+
+
+def piko_set_transport(ctx, transport):
+    return _check(ctx, _lib.piko_set_transport(ctx, transport))
+
+
+def piko_attach_local_peers(ctx, root, rank, nranks):
+    return _check(ctx, _lib.piko_attach_local_peers(ctx, root, rank, nranks))
 
 
 def piko_triangle_range(n_tris, rank, nranks):

@@ -60,6 +60,26 @@ __device__ __forceinline__ u64 ld_relaxed64(const u64* p) {
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// system scope: flags exchanged with peer GPUs over NVLink (P2P transport)
+__device__ __forceinline__ void st_release_sys64(u64* p, u64 v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 ld_acquire_sys64(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 gtimer_ns();
+// Spin until *p >= want (signed compare); after P2P_TIMEOUT_NS a peer is
+// presumed dead: flag the frame (host reports PIKO_ENCCL) instead of hanging.
+constexpr unsigned long long P2P_TIMEOUT_NS = 10ull * 1000 * 1000 * 1000;
+__device__ __noinline__ void p2p_wait_geq(const u64* p, long long want, unsigned* timeout_flag) {
+  const u64 t0 = gtimer_ns();
+  while ((long long)ld_acquire_sys64(p) < want) {
+    __nanosleep(256);
+    if (gtimer_ns() - t0 > P2P_TIMEOUT_NS) { atomicExch(timeout_flag, 1u); return; }
+  }
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
@@ -76,6 +96,7 @@ __device__ __forceinline__ u64 gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+__device__ __forceinline__ u64 gtimer_ns() { return gtimer(); }
 #ifdef PIKO_K1_TIMING
 // [kernel: 0 setup, 1 radix pass 0, 2 radix pass 1, 3 tile][slot][phase]
 __device__ u64 g_k1_times[4][8192][8];
@@ -1221,6 +1242,10 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   pdl_trigger();
   const u64 frame = a.ctl->frame;
   const bool ovf = a.ctl->overflow_tag == frame + 1;
+  if (KEYS_ONLY && a.p2p_done) {  // P2P: rank 0 has finished reading this key slot
+    if (tid == 0) p2p_wait_geq(a.p2p_done, (long long)a.epoch - 2, &a.ctl->p2p_timeout);
+    __syncthreads();
+  }
   TL_CTA(0);
   if (blockIdx.x == 0) {  // reset the next frame's double-buffered accumulators
     unsigned* h = &a.ctl->digit_hist[(frame + 1) & 1][0][0];
@@ -1589,6 +1614,20 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     }
   }
   TL_CTA(2);
+  if (KEYS_ONLY && a.p2p_flag) {
+    // P2P: every CTA's key stores (straight into rank 0's memory over NVLink)
+    // are made visible system-wide before it is counted; the last CTA counted
+    // raises this rank's arrival flag at rank 0 (release, system scope)
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      const u64 t = atomicAdd(&a.ctl->p2p_arrive, 1ull);
+      if ((t + 1) % gridDim.x == 0) {
+        __threadfence_system();
+        st_release_sys64(a.p2p_flag, a.epoch);
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1680,12 +1719,32 @@ __global__ void __launch_bounds__(256) k_resolve(const __grid_constant__ Resolve
   const Grid g = a.g;
   const int x = blockIdx.x * 32 + (threadIdx.x & 31);
   const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (x >= g.W || y >= g.H) return;
-  const int bw = 1 << g.bw_log2, bh = 1 << g.bh_log2;
-  const int b = (y >> g.bh_log2) * g.binsX + (x >> g.bw_log2);
-  const int r = b % g.nranks, k = b / g.nranks;
-  const int p = (y & (bh - 1)) * bw + (x & (bw - 1));
-  const u64 key = a.all_keys[((size_t)r * a.owned_max + k) * (size_t)(bw * bh) + p];
+  if (a.p2p_flags) {  // P2P: every rank's keys have arrived (acquire, system scope)
+    if (threadIdx.x == 0)
+      for (int q = 0; q < g.nranks; ++q) p2p_wait_geq(a.p2p_flags + q, (long long)a.epoch, a.p2p_timeout);
+    __syncthreads();
+  }
+  const bool in = x < g.W && y < g.H;
+  u64 key = CLEAR_KEY;
+  int bw = 0, bh = 0;
+  if (in) {
+    bw = 1 << g.bw_log2; bh = 1 << g.bh_log2;
+    const int b = (y >> g.bh_log2) * g.binsX + (x >> g.bw_log2);
+    const int r = b % g.nranks, k = b / g.nranks;
+    const int p = (y & (bh - 1)) * bw + (x & (bw - 1));
+    // written by peers: bypass L1
+    key = __ldcg(&a.all_keys[((size_t)r * a.owned_max + k) * (size_t)(bw * bh) + p]);
+  }
+  if (a.p2p_flags) {  // this CTA's keys are read: the last CTA releases the slot
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned nblk = gridDim.x * gridDim.y;
+      __threadfence();  // this CTA's key loads are ordered before its ticket (WAR vs the peers)
+      const unsigned long long t = atomicAdd(a.p2p_count, 1ull);
+      if ((t + 1) % nblk == 0) st_release_sys64(a.p2p_done, a.epoch);
+    }
+  }
+  if (!in) return;
   float L[3];
   normalise_light(a.light, L);
   const size_t o = (size_t)y * g.W + x;

@@ -40,6 +40,7 @@ struct Nccl {
   ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Reduce)(const void*, void*, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -50,7 +51,7 @@ struct Nccl {
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) { err = "cannot dlopen libnccl.so.2"; return false; }
 #define PIKO_SYM(n) n = reinterpret_cast<decltype(n)>(dlsym(h, "nccl" #n)); if (!n) { err = "missing nccl" #n; return false; }
-    PIKO_SYM(CommInitRank) PIKO_SYM(CommDestroy) PIKO_SYM(Send) PIKO_SYM(Recv) PIKO_SYM(Reduce)
+    PIKO_SYM(CommInitRank) PIKO_SYM(CommDestroy) PIKO_SYM(Send) PIKO_SYM(Recv) PIKO_SYM(Reduce) PIKO_SYM(Broadcast)
     PIKO_SYM(GroupStart) PIKO_SYM(GroupEnd) PIKO_SYM(GetErrorString) PIKO_SYM(GetUniqueId)
 #undef PIKO_SYM
     return true;
@@ -76,6 +77,14 @@ struct piko_ctx {
   int multi = PIKO_MULTI_SORT_FIRST;
   int mrank = 0, mnranks = 1;  // multi-GPU rank / size (sort-last: g.rank = 0, g.nranks = 1)
   long long prim_base = 0;     // sort-last: first triangle of this rank's range
+  // P2P transport (sort-first): rank 0 owns the exchange buffers; the other
+  // ranks map them (CUDA IPC over NVLink, or the same pointers for virtual
+  // ranks on one device) and k_tile stores its keys straight into them
+  int transport = PIKO_XPORT_NCCL;
+  unsigned long long* p2p_keys = nullptr;  // rank 0: [2][nranks][owned_max][bw*bh]
+  unsigned long long* p2p_sync = nullptr;  // rank 0: [nranks] arrival epochs + [1] done epoch
+  bool p2p_owner = false, p2p_ipc = false;
+  unsigned long long epoch = 0;            // exchange epoch of the last frame
   std::string err;
 
   // scratch
@@ -165,6 +174,22 @@ struct piko_ctx {
 
 extern "C" int64_t piko_owned_bins(int, int, int, int, int, int, int32_t*, int64_t);
 
+// ranks exchange keys with rank 0 (NCCL communicator or P2P buffers)
+static bool exchanging(const piko_ctx* ctx) {
+  return (ctx->comm != nullptr || ctx->p2p_keys != nullptr) && ctx->mnranks > 1;
+}
+
+// rank 0: allocate the P2P exchange buffers (zeroed epochs)
+static int p2p_alloc(piko_ctx* ctx) {
+  const size_t tile = (size_t)ctx->bw * ctx->bh;
+  const size_t nkeys = 2 * (size_t)ctx->mnranks * ctx->owned_max * tile;
+  CK(cudaMalloc(&ctx->p2p_keys, sizeof(unsigned long long) * std::max<size_t>(nkeys, 1)));
+  CK(cudaMalloc(&ctx->p2p_sync, 4096));
+  CK(cudaMemset(ctx->p2p_sync, 0, 4096));
+  ctx->p2p_owner = true;
+  return PIKO_OK;
+}
+
 static void set_ownership(piko_ctx* ctx, int rank, int nranks) {
   ctx->mrank = rank;
   ctx->mnranks = nranks;
@@ -229,6 +254,13 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+  if (ctx->p2p_ipc) {
+    cudaIpcCloseMemHandle(ctx->p2p_keys);
+    cudaIpcCloseMemHandle(ctx->p2p_sync);
+  } else if (ctx->p2p_owner) {
+    cudaFree(ctx->p2p_keys);
+    cudaFree(ctx->p2p_sync);
+  }
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
                   ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
@@ -396,7 +428,13 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
                          cudaStream_t s, unsigned long long* keys_out = nullptr) {
   if (ctx->pipeline == PIKO_PIPE_FREEPIPE)
     return enqueue_freepipe(ctx, verts, V, idx, T, M, L, rgba, depth, s);
-  const bool gather = keys_out == nullptr && ctx->comm != nullptr && ctx->mnranks > 1;
+  const bool gather = keys_out == nullptr && exchanging(ctx);
+  const bool p2p = gather && ctx->p2p_keys != nullptr;
+  const size_t tile_px = (size_t)ctx->bw * ctx->bh;
+  if (p2p) ++ctx->epoch;
+  // P2P: this frame's key slot (epoch parity) at rank 0
+  unsigned long long* p2p_slot = p2p ? ctx->p2p_keys + (size_t)(ctx->epoch & 1) * ctx->mnranks * ctx->owned_max * tile_px
+                                     : nullptr;
   const bool keys_only = gather || keys_out != nullptr;
   cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
   if (ctx->prof && !ev) return ctx->fail(PIKO_ECUDA, "cannot create profiling events");
@@ -473,7 +511,14 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.bin_prims = ctx->vals[ctx->npass & 1]; a.ctl = ctx->ctl;
     a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
     a.out_cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
-    a.tile_keys = keys_out ? keys_out : gather ? ctx->tile_keys : nullptr;
+    a.tile_keys = keys_out ? keys_out
+                : p2p    ? p2p_slot + (size_t)ctx->mrank * ctx->owned_max * tile_px
+                : gather ? ctx->tile_keys : nullptr;
+    if (p2p) {
+      a.p2p_flag = ctx->p2p_sync + ctx->mrank;
+      a.p2p_done = ctx->p2p_sync + ctx->mnranks;
+      a.epoch = ctx->epoch;
+    }
     a.owned = ctx->owned;
     a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
     a.gcov = ctx->gcov; a.arrive = ctx->arrive; a.frag = tile_frag(ctx->bw, ctx->bh);
@@ -488,7 +533,9 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     const size_t tile_bytes = sizeof(unsigned long long) * ctx->bw * ctx->bh;
     const size_t bytes = tile_bytes * ctx->owned_max;
     int rc = 0;
-    if (ctx->multi == PIKO_MULTI_SORT_LAST) {
+    if (p2p) {
+      // keys already at rank 0 (stored by k_tile over NVLink); nothing to send
+    } else if (ctx->multi == PIKO_MULTI_SORT_LAST) {
       // element-wise (depth, primID) minimum of the full key images on rank 0
       rc = g_nccl.Reduce(ctx->tile_keys, ctx->mrank == 0 ? ctx->all_keys : nullptr,
                          (size_t)ctx->owned * ctx->bw * ctx->bh, ncclUint64_, ncclMin_, 0, ctx->comm, s);
@@ -521,6 +568,14 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
       a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
       a.g = ctx->g; a.all_keys = ctx->all_keys; a.owned_max = ctx->owned_max;
       a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
+      if (p2p) {
+        a.all_keys = p2p_slot;
+        a.p2p_flags = ctx->p2p_sync;
+        a.p2p_done = ctx->p2p_sync + ctx->mnranks;
+        a.p2p_count = &ctx->ctl->p2p_count;
+        a.p2p_timeout = &ctx->ctl->p2p_timeout;
+        a.epoch = ctx->epoch;
+      }
       CK(launch_resolve(a, s));
     }
   } else {
@@ -554,6 +609,13 @@ static int check_frame(piko_ctx* ctx) {
   if (!ctx->pending) return ctx->last_status;
   ctx->pending = false;
   CK(cudaEventSynchronize(ctx->done));
+  if (ctx->h_ctl->p2p_timeout) {
+    CK(cudaMemsetAsync(&ctx->ctl->p2p_timeout, 0, sizeof(unsigned), 0));
+    CK(cudaDeviceSynchronize());
+    ctx->last_status = PIKO_ENCCL;
+    ctx->fail(PIKO_ENCCL, "P2P exchange: a peer flag wait timed out");
+    return ctx->last_status;
+  }
   if (ctx->h_ctl->overflow_tag == ctx->h_ctl->frame + 1 || ctx->h_ctl->vx_overflow) {
     int rc = ensure_pairs(ctx, ctx->h_ctl->n_pairs);
     if (rc == PIKO_OK) rc = ensure_verts(ctx, (long long)ctx->h_ctl->vx_need);
@@ -578,7 +640,7 @@ static int validate_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, 
                          float L[3]) {
   if (n_tris < 0) return ctx->fail(PIKO_EINVAL, "n_tris < 0");
   if (!mvp || !light) return ctx->fail(PIKO_EINVAL, "mvp and light must be non-null");
-  const bool need_out = !(ctx->comm && ctx->mnranks > 1 && ctx->mrank != 0) && !ctx->keys_mode;
+  const bool need_out = !(exchanging(ctx) && ctx->mrank != 0) && !ctx->keys_mode;
   if (need_out && (!rgba || !depth)) return ctx->fail(PIKO_EINVAL, "null output buffer");
   if (n_tris > 0 && (!verts || !idx)) return ctx->fail(PIKO_EINVAL, "null scene buffer");
   if ((reinterpret_cast<uintptr_t>(verts) | reinterpret_cast<uintptr_t>(idx) |
@@ -630,7 +692,7 @@ static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32
     if (rc != PIKO_ECAPACITY) return rc;
     // multi-rank: every rank must re-issue together; a capacity miss is
     // reported instead of re-issued so ranks cannot diverge.
-    if (ctx->comm && ctx->mnranks > 1) return rc;
+    if (exchanging(ctx)) return rc;
   }
   return rc;
 }
@@ -686,7 +748,7 @@ extern "C" int piko_draw_host(piko_ctx* ctx, const float* h_verts, int64_t n_ver
   int rc = draw_impl(ctx, ctx->d_verts, n_verts, ctx->d_idx, n_tris, mvp, light, ctx->d_rgba,
                      ctx->d_depth, s, true);
   if (rc != PIKO_OK) return rc;
-  const bool has_out = !(ctx->comm && ctx->mnranks > 1 && ctx->mrank != 0);
+  const bool has_out = !(exchanging(ctx) && ctx->mrank != 0);
   if (has_out) {
     CK(cudaMemcpyAsync(h_rgba, ctx->d_rgba, sizeof(float) * 4 * npx, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(h_depth, ctx->d_depth, sizeof(float) * npx, cudaMemcpyDeviceToHost, s));
@@ -753,7 +815,9 @@ extern "C" int piko_set_multi(piko_ctx* ctx, int mode) {
   if (!ctx) return PIKO_EINVAL;
   if (mode != PIKO_MULTI_SORT_FIRST && mode != PIKO_MULTI_SORT_LAST)
     return ctx->fail(PIKO_EINVAL, "unknown multi-GPU mode");
-  if (ctx->comm) return ctx->fail(PIKO_ESTATE, "communicator attached");
+  if (ctx->comm || ctx->p2p_keys) return ctx->fail(PIKO_ESTATE, "ranks attached");
+  if (mode == PIKO_MULTI_SORT_LAST && ctx->transport == PIKO_XPORT_P2P)
+    return ctx->fail(PIKO_ESTATE, "the P2P transport carries the sort-first tile exchange");
   if (ctx->pending) check_frame(ctx);
   ctx->multi = mode;
   set_ownership(ctx, ctx->mrank, ctx->mnranks);  // re-derive bin ownership
@@ -761,9 +825,42 @@ extern "C" int piko_set_multi(piko_ctx* ctx, int mode) {
   return PIKO_OK;
 }
 
+extern "C" int piko_set_transport(piko_ctx* ctx, int transport) {
+  if (!ctx) return PIKO_EINVAL;
+  if (transport != PIKO_XPORT_NCCL && transport != PIKO_XPORT_P2P)
+    return ctx->fail(PIKO_EINVAL, "unknown transport");
+  if (ctx->comm || ctx->p2p_keys) return ctx->fail(PIKO_ESTATE, "ranks already attached");
+  if (transport == PIKO_XPORT_P2P && ctx->multi != PIKO_MULTI_SORT_FIRST)
+    return ctx->fail(PIKO_ESTATE, "the P2P transport carries the sort-first tile exchange");
+  ctx->transport = transport;
+  return PIKO_OK;
+}
+
+extern "C" int piko_attach_local_peers(piko_ctx* ctx, piko_ctx* root, int rank, int nranks) {
+  if (!ctx || !root) return PIKO_EINVAL;
+  if (nranks < 2 || rank < 0 || rank >= nranks) return ctx->fail(PIKO_EINVAL, "bad rank/nranks");
+  if ((rank == 0) != (root == ctx)) return ctx->fail(PIKO_EINVAL, "rank 0 is the root context");
+  if (ctx->comm || ctx->p2p_keys) return ctx->fail(PIKO_ESTATE, "ranks already attached");
+  if (ctx->multi != PIKO_MULTI_SORT_FIRST || ctx->pipeline != PIKO_PIPE_BINNED)
+    return ctx->fail(PIKO_ESTATE, "P2P peers need sort-first and the binned pipeline");
+  if (root->device != ctx->device || root->g.W != ctx->g.W || root->g.H != ctx->g.H ||
+      root->bw != ctx->bw || root->bh != ctx->bh)
+    return ctx->fail(PIKO_EINVAL, "root context differs in device, screen or bins");
+  if (rank != 0 && (!root->p2p_keys || root->mnranks != nranks))
+    return ctx->fail(PIKO_ESTATE, "attach the root (rank 0) first");
+  CK(cudaSetDevice(ctx->device));
+  set_ownership(ctx, rank, nranks);
+  ctx->virt = true;
+  ctx->transport = PIKO_XPORT_P2P;
+  if (rank == 0) return p2p_alloc(ctx);
+  ctx->p2p_keys = root->p2p_keys;
+  ctx->p2p_sync = root->p2p_sync;
+  return PIKO_OK;
+}
+
 extern "C" int piko_set_partition(piko_ctx* ctx, int rank, int nranks) {
   if (!ctx) return PIKO_EINVAL;
-  if (ctx->comm) return ctx->fail(PIKO_ESTATE, "communicator attached");
+  if (ctx->comm || ctx->p2p_keys) return ctx->fail(PIKO_ESTATE, "ranks attached");
   if (nranks < 1 || rank < 0 || rank >= nranks) return ctx->fail(PIKO_EINVAL, "bad rank/nranks");
   if (nranks > 1 && ctx->pipeline != PIKO_PIPE_BINNED)
     return ctx->fail(PIKO_ESTATE, "partitions need the binned pipeline");
@@ -784,6 +881,35 @@ extern "C" int piko_attach_comm(piko_ctx* ctx, const void* uid, int rank, int nr
   const int rc = g_nccl.CommInitRank(&ctx->comm, nranks, id, rank);
   if (rc != 0) { ctx->comm = nullptr; return ctx->fail(PIKO_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(rc)); }
   set_ownership(ctx, rank, nranks);
+  if (ctx->transport == PIKO_XPORT_P2P && nranks > 1) {
+    // rank 0 allocates the exchange buffers and broadcasts their CUDA IPC
+    // handles over the new communicator; the other ranks map them (NVLink P2P)
+    struct { cudaIpcMemHandle_t keys, sync; } h;
+    memset(&h, 0, sizeof h);
+    if (rank == 0) {
+      int rc0 = p2p_alloc(ctx);
+      if (rc0 != PIKO_OK) return rc0;
+      CK(cudaIpcGetMemHandle(&h.keys, ctx->p2p_keys));
+      CK(cudaIpcGetMemHandle(&h.sync, ctx->p2p_sync));
+    }
+    void* d = nullptr;
+    CK(cudaMalloc(&d, sizeof h));
+    CK(cudaMemcpy(d, &h, sizeof h, cudaMemcpyHostToDevice));
+    const int rb = g_nccl.Broadcast(d, d, sizeof h, ncclUint8_, 0, ctx->comm, nullptr);
+    if (rb != 0) { cudaFree(d); return ctx->fail(PIKO_ENCCL, "ncclBroadcast: %s", g_nccl.GetErrorString(rb)); }
+    CK(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));  // (synchronises the broadcast)
+    CK(cudaFree(d));
+    if (rank != 0) {
+      void* pk = nullptr;
+      void* ps = nullptr;
+      CK(cudaIpcOpenMemHandle(&pk, h.keys, cudaIpcMemLazyEnablePeerAccess));
+      CK(cudaIpcOpenMemHandle(&ps, h.sync, cudaIpcMemLazyEnablePeerAccess));
+      ctx->p2p_keys = static_cast<unsigned long long*>(pk);
+      ctx->p2p_sync = static_cast<unsigned long long*>(ps);
+      ctx->p2p_ipc = true;
+    }
+    return PIKO_OK;
+  }
   const size_t tile_bytes = sizeof(unsigned long long) * ctx->bw * ctx->bh;
   CK(cudaMalloc(&ctx->tile_keys, tile_bytes * std::max(ctx->owned_max, 1)));
   // rank 0's receive buffer: every rank's tiles (sort-first), or one reduced image (sort-last)

@@ -60,6 +60,9 @@ struct Control {
   unsigned long long n_pairs;          // P, written by K1's last chunk
   unsigned long long overflow_tag;     // frame+1 of the last frame whose P > capacity
   unsigned long long n_live[2];        // parity double buffer (statistics)
+  unsigned long long p2p_arrive;       // k_tile CTA tickets (P2P arrival, modulo grid)
+  unsigned long long p2p_count;        // k_resolve CTA tickets (P2P slot release)
+  unsigned int p2p_timeout;            // a peer flag wait timed out (sticky)
   unsigned int digit_hist[2][MAX_PASSES][RX_RADIX];  // parity double buffer
 };
 
@@ -173,6 +176,10 @@ struct TileArgs {
   uint32_t* garrive;            // [npass][2][gcap] look-back group arrival counters;
   long long gcap;               //   k_tile zeroes the next frame's parity
   unsigned prim_base;           // keys-only: added to the primID of every stored key (sort-last)
+  // P2P transport (sort-first): tile_keys points into rank 0's memory
+  unsigned long long* p2p_flag;         // rank 0's arrival flag of this rank (null: no P2P)
+  const unsigned long long* p2p_done;   // rank 0's last resolved epoch
+  unsigned long long epoch;             // this frame's exchange epoch (1, 2, ...)
 };
 
 struct ResolveArgs {            // rank 0 after the NCCL gather
@@ -187,6 +194,12 @@ struct ResolveArgs {            // rank 0 after the NCCL gather
   float* out_rgba;
   float* out_depth;
   int32_t* out_primid;
+  // P2P transport: wait for every rank's arrival flag, then release the slot
+  const unsigned long long* p2p_flags;  // [nranks] (null: keys already local)
+  unsigned long long* p2p_done;
+  unsigned long long* p2p_count;        // CTA ticket (self-resetting modulo grid)
+  unsigned* p2p_timeout;
+  unsigned long long epoch;
 };
 
 // FreePipe variant (sec. 7.2.1): one fused

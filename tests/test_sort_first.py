@@ -128,3 +128,40 @@ def test_gpu_tile_keys_gather_resolve(oracle_lib, R):
     assert np.array_equal(img, keys)
     for rd in renderers:
         rd.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("R", [2, 3, 4])
+def test_gpu_p2p_transport_virtual_ranks(oracle_lib, R):
+    """P2P transport (tile kernel stores keys straight into rank 0's buffer,
+    arrival flags, rank-0 resolve waits): virtual ranks sharing rank 0's
+    buffers on one device, several frames with alternating views so a wrong
+    slot parity or a stale key image fails."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1404_6293_b200 as piko
+    s = scenes.scene_c2()
+    dev = torch.device("cuda:0")
+    v = torch.from_numpy(s.verts).to(dev)
+    i = torch.from_numpy(s.idx).to(dev)
+    rds = [piko.Renderer(s.W, s.H, 16, device=dev) for _ in range(R)]
+    piko.piko_attach_local_peers(rds[0].ctx, rds[0].ctx, 0, R)
+    for r in range(1, R):
+        piko.piko_attach_local_peers(rds[r].ctx, rds[0].ctx, r, R)
+    views = [s.mvp, scenes.perspective_mvp(fovy_deg=50.0)]  # two views: different keys
+    refs = [oracle_lib.render(s.verts, s.idx, mv, s.light, s.W, s.H) for mv in views]
+    for f in range(5):
+        mv = views[f % 2]
+        for r in list(range(1, R)) + [0]:
+            rds[r].draw(v, i, mv, s.light)
+        torch.cuda.synchronize()
+        ref = refs[f % 2]
+        r0 = rds[0]
+        assert np.array_equal(r0.primid().cpu().numpy(), ref["primid"]), f"frame {f}"
+        assert np.array_equal(r0.depth.cpu().numpy().view(np.uint32), ref["depth"].view(np.uint32))
+        assert np.abs(r0.rgba.cpu().numpy() - ref["rgba"]).max() <= 1e-5
+    for rd in rds[1:] + rds[:1]:
+        rd.close()
