@@ -134,9 +134,10 @@ def algorithmic_bytes(stage, T, V, L, P, NB, npx, ncov, npass):
         return 16 * V + 16 * V
     if stage == "setup":      # idx + vertex records in; setup records (live) + tile rects out
         return 12 * T + 16 * V + 48 * L + 8 * T
-    if stage == "radix":      # expand: rects in, pairs out; later passes 8 B in / 8 B out
-        rest = max(npass - 1, 0) * 16 * P - (4 * P if npass > 1 else 0)
-        return 8 * T + 8 * P + rest + 12 * NB
+    if stage == "expand":     # radix pass 0: rects in, (key, primID) pairs out, bin counts
+        return 8 * T + (8 * P if npass > 1 else 4 * P) + 4 * NB + (12 * NB if npass == 1 else 0)
+    if stage == "sort":       # passes >= 1: 8 B in / 8 B out (last: primIDs only) + CSR scan
+        return (npass - 1) * 16 * P - 4 * P + 12 * NB if npass > 1 else 0
     if stage == "tile":       # CSR + records in; 24 B/px out; winner re-gather
         return 4 * (NB + 1) + 4 * P + 48 * P + 24 * npx + (12 + 3 * 32) * ncov
     if stage == "resolve":
@@ -310,7 +311,7 @@ def run_piko(args):
     P, L, NB = stats["n_pairs"], stats["n_live"], stats["n_bins"]
     npx = s.W * s.H
     per_frame = {k: v / max(nprof, 1) for k, v in prof.items()}
-    cand = {k: per_frame[k] for k in ("vertex", "setup", "radix", "tile", "resolve") if per_frame[k] > 0}
+    cand = {k: per_frame[k] for k in ("vertex", "setup", "expand", "sort", "tile", "resolve") if per_frame[k] > 0}
     dom = max(cand, key=cand.get)
     nb = algorithmic_bytes(dom, T, V, L, P, NB, npx, ncov, stats["radix_passes"])
     peaks = {}
@@ -324,12 +325,17 @@ def run_piko(args):
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}_b{bw}.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get(dom)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+    kname = {"vertex": "k_vertex", "setup": "k_setup", "expand": "k_radix_pass<EXPAND=true> (pass 0)",
+             "sort": "k_radix_pass<EXPAND=false> (passes >= 1)", "tile": "k_tile",
+             "resolve": "k_resolve"}[dom]
+    roofline = {"bound": "hbm", "kernel": kname, "stage": dom,
+                "launches_per_step": max(stats["radix_passes"] - 1, 1) if dom == "sort" else 1,
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": nb,
                 "ms_per_launch": per_frame[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
     frame_bytes = sum(algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"])
-                      for k in ("vertex", "setup", "radix", "tile"))
+                      for k in ("vertex", "setup", "expand", "sort", "tile"))
     ms = total_ms / args.steps
     out = {
         "metric": METRIC, "value": T * args.steps / (total_ms / 1e3) / 1e6, "unit": UNIT,

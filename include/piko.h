@@ -264,11 +264,13 @@ int piko_nccl_unique_id(void *out_id128);
 #define PIKO_STAGE_CLEAR 0   /* resets (only when a grid size changed)        */
 #define PIKO_STAGE_VERTEX 1  /* k_index_max (piko_draw only) + k_vertex      */
 #define PIKO_STAGE_SETUP 2   /* k_setup: setup, count, scan, pairs           */
-#define PIKO_STAGE_RADIX 3   /* k_radix_pass x radix_passes (+ CSR bin scan)  */
-#define PIKO_STAGE_TILE 4    /* k_tile: per-bin raster, depth, shade, store   */
-#define PIKO_STAGE_GATHER 5  /* NCCL tile-key gather (multi-GPU)              */
-#define PIKO_STAGE_RESOLVE 6 /* k_resolve: rank-0 shade of gathered keys      */
-#define PIKO_NUM_STAGES 7
+#define PIKO_STAGE_EXPAND 3  /* k_radix_pass pass 0: expand pairs + digit-0 rank
+                                (+ k_bin_scan when radix_passes == 1)           */
+#define PIKO_STAGE_SORT 4    /* k_radix_pass passes >= 1 (+ CSR bin scan CTAs)  */
+#define PIKO_STAGE_TILE 5    /* k_tile: per-bin raster, depth, shade, store   */
+#define PIKO_STAGE_GATHER 6  /* tile-key gather (multi-GPU: NCCL, or nothing for P2P) */
+#define PIKO_STAGE_RESOLVE 7 /* k_resolve: rank-0 shade of gathered keys      */
+#define PIKO_NUM_STAGES 8
 /* on != 0 enables recording and resets the totals. */
 int piko_set_profiling(piko_ctx *ctx, int on);
 /* Synchronises, then returns per-stage total milliseconds and frame count

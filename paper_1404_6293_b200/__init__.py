@@ -30,7 +30,7 @@ EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_se
            "piko_draw_tile_keys", "piko_resolve_keys", "piko_tile_keys_count", "piko_owned_bins",
            "piko_set_pipeline", "piko_set_profiling", "piko_get_profile", "piko_set_multi",
            "piko_triangle_range", "piko_set_transport", "piko_attach_local_peers")
-STAGES = ("clear", "vertex", "setup", "radix", "tile", "gather", "resolve")
+STAGES = ("clear", "vertex", "setup", "expand", "sort", "tile", "gather", "resolve")
 
 
 class PikoError(RuntimeError):

@@ -405,7 +405,8 @@ static int enqueue_freepipe(piko_ctx* ctx, const float* verts, long long V, cons
   a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
   if (T > 0) CK(launch_freepipe(a, ctx->pdl, s));
   CK(mark(1 + PIKO_STAGE_SETUP));
-  CK(mark(1 + PIKO_STAGE_RADIX));
+  CK(mark(1 + PIKO_STAGE_EXPAND));
+  CK(mark(1 + PIKO_STAGE_SORT));
   CK(launch_fp_resolve(a, ctx->pdl, s));
   CK(mark(1 + PIKO_STAGE_TILE));
   CK(mark(1 + PIKO_STAGE_GATHER));
@@ -501,8 +502,10 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.frag = tile_frag(ctx->bw, ctx->bh); a.npx = ctx->bw * ctx->bh;
     CK(launch_radix_pass(a, (int)(p == 0 ? gx : gp + (p == 1 ? ntiles : 0)), ctx->pdl, s));
     if (p == 0 && ctx->npass == 1) CK(launch_bin_scan(a, (int)ntiles, ctx->pdl, s));
+    if (p == 0) CK(mark(1 + PIKO_STAGE_EXPAND));
   }
-  CK(mark(1 + PIKO_STAGE_RADIX));
+  if (ctx->npass == 0) CK(mark(1 + PIKO_STAGE_EXPAND));
+  CK(mark(1 + PIKO_STAGE_SORT));
   {
     TileArgs a{};
     a.verts = verts; a.xv = sep ? ctx->xv : nullptr; a.M = M; a.idx = idx;

@@ -16,13 +16,27 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 out_dir = os.path.join(ROOT, "profiles")
 os.makedirs(out_dir, exist_ok=True)
 
+def kname(full):
+    """'void piko::k_radix_pass<(bool)1>(piko::RadixArgs)' -> 'piko::k_radix_pass<(bool)1>'"""
+    full = full.replace("void ", "")
+    return full[:full.rfind("(")] if full.endswith(")") else full
+
+
+def stage(name):
+    base = name.split("<")[0].split("::")[-1]
+    if base == "k_radix_pass":  # template argument EXPAND: pass 0 vs passes >= 1
+        return "expand" if any(t in name for t in ("<(bool)1>", "<true>", "<1>")) else "sort"
+    return {"k_vertex": "vertex", "k_setup": "setup", "k_tile": "tile", "k_resolve": "resolve",
+            "k_bin_scan": "expand", "k_index_max": "vertex"}.get(base)
+
+
 rows = [r for r in csv.reader(open(launches)) if r and not r[0].startswith("==")]
 h = rows[0]
 ki, vi = h.index("Kernel Name"), h.index("Metric Value")
 tot = {}
 for r in rows[1:]:
-    if r[ki].startswith("piko::") or "piko::" in r[ki] or r[ki].startswith("void piko"):
-        name = r[ki].split("(")[0].replace("void ", "")
+    if stage(kname(r[ki])) is not None:
+        name = kname(r[ki])
         tot.setdefault(name, []).append(float(r[vi]) / 1000.0)
 lines = [f"# ncu launch list ({tag}): gpu__time_duration per launch, cold-cache, serialised",
          "# kernel, launches, mean_us, share_of_frame"]
@@ -47,13 +61,10 @@ k2 = hh.index("Kernel Name")
 summ = [f"# ncu --set full ({tag}), one launch per kernel of one frame ({cfg}, {bw}x{bw} bins)",
         "# kernel, " + ", ".join(f"{hh[c]} [{units[c]}]" for c in cols)]
 traffic = {}
-stage_of = {"k_vertex": "vertex", "k_setup": "setup", "k_radix_pass": "radix", "k_tile": "tile",
-            "k_resolve": "resolve", "k_bin_scan": "radix", "k_index_max": "vertex"}
 for r in rr[2:]:
-    name = r[k2].split("(")[0].replace("void ", "")
+    name = kname(r[k2])
     summ.append(name + ", " + ", ".join(r[c] for c in cols))
-    base = name.split("<")[0].split("::")[-1]
-    st = stage_of.get(base)
+    st = stage(name)
     if st:
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rd = float(r[cols[1]]) * mult.get(units[cols[1]], 1)
