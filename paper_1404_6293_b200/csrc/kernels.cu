@@ -199,7 +199,9 @@ __device__ __forceinline__ bool xform_corner(const float4 p, const Mat4& M, floa
   const float cw = __fmaf_rn(M.m[12], p.x, __fmaf_rn(M.m[13], p.y, __fmaf_rn(M.m[14], p.z, M.m[15])));
   if (!(isfinite(cx) && isfinite(cy) && isfinite(cz) && isfinite(cw))) return false;
   if (!(cw > W_EPS)) return false;
-  const float r = __fdiv_rn(1.0f, cw);
+  // 1/w: __frcp_rn is the correctly rounded IEEE reciprocal, bit-identical to
+  // the oracle's 1.0f / w (round to nearest even) without a general division
+  const float r = __frcp_rn(cw);
   const float xn = __fmul_rn(cx, r), yn = __fmul_rn(cy, r), zn = __fmul_rn(cz, r);
   const float sx = __fmaf_rn(xn, hw, hw);
   const float sy = __fmaf_rn(-yn, hh, hh);            // y down, row 0 = top
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
         const float dx1 = __int2float_rn(o.X1 - o.X0), dy1 = __int2float_rn(o.Y1 - o.Y0);
         const float dx2 = __int2float_rn(o.X2 - o.X0), dy2 = __int2float_rn(o.Y2 - o.Y0);
         const float dz1 = __fsub_rn(o.zw1, o.zw0), dz2 = __fsub_rn(o.zw2, o.zw0);
-        const float inv = __fdiv_rn(1.0f, __ll2float_rn(o.area2));
+        const float inv = __frcp_rn(__ll2float_rn(o.area2));
         const float za = __fmul_rn(__fmaf_rn(dz1, dy2, -__fmul_rn(dz2, dy1)), inv);
         const float zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
         int4* r = a.rec + 3 * t;
@@ -1146,7 +1148,7 @@ __device__ __noinline__ float4 shade(const float* __restrict__ verts, const int4
   const long long w0 = (long long)(o.X2 - o.X1) * (Py - o.Y1) - (long long)(o.Y2 - o.Y1) * (Px - o.X1);
   const long long w1 = (long long)(o.X0 - o.X2) * (Py - o.Y2) - (long long)(o.Y0 - o.Y2) * (Px - o.X2);
   const long long w2 = (long long)(o.X1 - o.X0) * (Py - o.Y0) - (long long)(o.Y1 - o.Y0) * (Px - o.X0);
-  const float inv = __fdiv_rn(1.0f, __ll2float_rn(o.area2));
+  const float inv = __frcp_rn(__ll2float_rn(o.area2));
   const float l0 = __fmul_rn(__fmul_rn(__ll2float_rn(w0), inv), o.rw0);
   const float l1 = __fmul_rn(__fmul_rn(__ll2float_rn(w1), inv), o.rw1);
   const float l2 = __fmul_rn(__fmul_rn(__ll2float_rn(w2), inv), o.rw2);
@@ -1669,7 +1671,7 @@ __global__ void __launch_bounds__(256) k_freepipe(FreePipeArgs a) {
     const float dx1 = __int2float_rn(o.X1 - o.X0), dy1 = __int2float_rn(o.Y1 - o.Y0);
     const float dx2 = __int2float_rn(o.X2 - o.X0), dy2 = __int2float_rn(o.Y2 - o.Y0);
     const float dz1 = __fsub_rn(o.zw1, o.zw0), dz2 = __fsub_rn(o.zw2, o.zw0);
-    const float inv = __fdiv_rn(1.0f, __ll2float_rn(o.area2));
+    const float inv = __frcp_rn(__ll2float_rn(o.area2));
     RecView r;
     r.X0 = o.X0; r.Y0 = o.Y0; r.X1 = o.X1; r.Y1 = o.Y1; r.X2 = o.X2; r.Y2 = o.Y2;
     r.zw0 = o.zw0;
