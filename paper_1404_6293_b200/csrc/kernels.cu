@@ -1500,23 +1500,34 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
         if (tid < nq) Q.pre[tid] = wbase + inc - ar;
         if (tid == 0) Q.pre[nq] = tot;
         __syncthreads();
-        // warp-contiguous items: the warp's first item locates its entry once
-        // (monotone across iterations), each lane then walks a few entries
+        // warp-contiguous items.  qw = the entry holding the warp's first item
+        // (monotone): lanes load the next 32 entry starts and a ballot advances
+        // qw (pre is strictly increasing, so the mask is a prefix).  Every
+        // entry covers >= TINY_AREA + 1 items, so the warp's 32 items lie in
+        // entries qw .. qw+31 and each lane finds its own with a 5-step shuffle
+        // search over the loaded starts -- no serial per-warp search.
         int qw = 0;
         for (unsigned base = (unsigned)warp * 32; base < tot; base += THREADS) {
-          if (lane == 0) {
-            int lo = qw, hi = nq - 1;  // the entry with the largest pre <= base
-            while (lo < hi) {
-              const int mid = (lo + hi + 1) >> 1;
-              if (Q.pre[mid] <= base) lo = mid; else hi = mid - 1;
+          unsigned pk;
+          for (;;) {
+            const int k = qw + 1 + lane;
+            pk = k <= nq ? Q.pre[k] : 0xFFFFFFFFu;
+            const unsigned m = __ballot_sync(0xffffffffu, pk <= base);
+            qw += __popc(m);
+            if (m != 0xFFFFFFFFu) {
+              if (m) pk = (qw + 1 + lane <= nq) ? Q.pre[qw + 1 + lane] : 0xFFFFFFFFu;
+              break;
             }
-            qw = lo;
           }
-          qw = __shfl_sync(0xffffffffu, qw, 0);
           const unsigned i = base + lane;
+          int c = 0;  // entries after qw starting at or before item i
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const unsigned v = __shfl_sync(0xffffffffu, pk, c + st - 1);
+            if (v <= i) c += st;
+          }
           if (i >= tot) continue;
-          int q = qw;
-          while (Q.pre[q + 1] <= i) ++q;
+          const int q = qw + c;
           const unsigned off = i - Q.pre[q];
           const int wq = Q.w[q];
           const int row = __float2int_rz(((float)off + 0.5f) * Q.invw[q]);  // exact: off < 2^12
