@@ -1235,6 +1235,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   __shared__ int s_nbig;    // large triangles queued for the pixel-parallel pass
   __shared__ unsigned s_ln[NLIST];
   __shared__ int s_last;
+  __shared__ int s_nx[3];   // the next item's bin and CSR sub-range (prologue issued early)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Grid g = a.g;
@@ -1328,6 +1329,28 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     s_bin = b0; s_rng[0] = s0; s_rng[1] = e0; s_rng[2] = nf0;
   }
   __syncthreads();
+  // Pipeline prologue of an item: primIDs of the first TQ rounds and the
+  // records of the first NSTAGE-1 rounds (cp.async).  For every item after the
+  // first it is issued as soon as the previous item's raster has freed the
+  // record stages, so it overlaps that item's queue pass and write-back.
+  int tq[TQ];
+  auto prologue = [&](int s_, int e_) {
+#pragma unroll
+    for (int j = 0; j < TQ; ++j) {
+      const int i = s_ + j * THREADS + tid;
+      tq[j] = i < e_ ? a.bin_prims[i] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < NSTAGE - 1; ++j) {
+      if (tq[j] >= 0) {
+        const int4* rp = a.rec + 3ll * tq[j];
+        cp_async16(&sm.rec[j][tid][0], rp); cp_async16(&sm.rec[j][tid][1], rp + 1);
+        cp_async16(&sm.rec[j][tid][2], rp + 2);
+      }
+      cp_async_commit();
+    }
+  };
+  bool pre = false;  // prologue of the current item already issued (CTA-uniform)
   for (;;) {
     const int b = s_bin;
     if (b < 0) break;
@@ -1336,6 +1359,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     if (tid == 0) {  // prefetch the next item
       work_item(q_tk, q_bin, q_s, q_e, q_nf);
       if (q_bin >= 0) q_tk = atomicAdd(&a.ctl->tile_next, 1u);
+      s_nx[0] = q_bin; s_nx[1] = q_s; s_nx[2] = q_e;
     }
     const int bx = b % g.binsX, by = b / g.binsX;
     const int x0 = bx * BW, y0 = by * BH;
@@ -1355,21 +1379,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     // the bin is done.  Tiny triangles: one thread loops over its pixels;
     // larger ones: warp-cooperative (triangle, pixel) expansion.
     const int nround = (e - s + THREADS - 1) / THREADS;
-    int tq[TQ];
-#pragma unroll
-    for (int j = 0; j < TQ; ++j) {
-      const int i = s + j * THREADS + tid;
-      tq[j] = i < e ? a.bin_prims[i] : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < NSTAGE - 1; ++j) {
-      if (tq[j] >= 0) {
-        const int4* rp = a.rec + 3ll * tq[j];
-        cp_async16(&sm.rec[j][tid][0], rp); cp_async16(&sm.rec[j][tid][1], rp + 1);
-        cp_async16(&sm.rec[j][tid][2], rp + 2);
-      }
-      cp_async_commit();
-    }
+    if (!pre) prologue(s, e);
     for (int k = 0; k < nround; ++k) {
       const int buf = k % NSTAGE;
       const int t_cur = tq[0];
@@ -1475,6 +1485,9 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     }
     cp_async_wait<0>();
     __syncthreads();
+    // record stages are free: start the next item's loads now
+    pre = s_nx[0] >= 0;
+    if (pre) prologue(s_nx[1], s_nx[2]);
     {  // queued triangles: all threads over the flattened (triangle, pixel) items
       const int nq = min(s_nbig, TileSmem<BW, BH, THREADS>::BIGQ);
       if (nq > 0) {
