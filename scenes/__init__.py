@@ -207,6 +207,66 @@ def scene_soup(T: int, W: int, H: int, seed: int, name: str, bin_sizes=(16,)) ->
     return Scene(name, W, H, bin_sizes, pack_verts(pos, nrm), idx, np.eye(4, dtype=np.float32).reshape(16))
 
 
+def scene_fuzz(seed: int) -> Scene:
+    """Randomised small case for differential testing (geometry only): random
+    screen (1..300 px, odd sizes included) and bins, T in [0, 2500], and a mix
+    of triangle kinds -- tiny, medium, screen-covering, slivers, degenerate
+    (repeated corner), off-screen, beyond the guard band, behind the camera,
+    non-finite corners, lattice-aligned shared edges with equal depths (ties),
+    and vertex sharing (random index reuse)."""
+    rng = np.random.default_rng(10_000 + seed)
+    W, H = int(rng.integers(1, 301)), int(rng.integers(1, 301))
+    if rng.random() < 0.3:
+        W, H = int(rng.choice([16, 64, 128, 256])), int(rng.choice([16, 64, 128, 256]))
+    bins = (int(rng.choice([8, 16, 32, 64])), int(rng.choice([8, 16, 32, 64])))
+    T = int(rng.integers(0, 2501)) if rng.random() > 0.05 else 0
+    pk = np.array([.30, .20, .05, .08, .04, .05, .04, .06, .03, .15])
+    if rng.random() < 0.6:  # most cases without screen-covering triangles: background stays visible
+        pk[2] = 0.0
+    kind = rng.choice(10, size=T, p=pk / pk.sum())
+    persp = rng.random() < 0.4
+    # positions in NDC (identity mvp) or camera space in front of the camera (perspective)
+    c = rng.uniform(-1.1, 1.1, (T, 2))
+    px = np.array([2.0 / max(W, 1), 2.0 / max(H, 1)])
+    rad = np.where(kind == 0, rng.uniform(0.2, 2.0, T),          # tiny (px)
+          np.where(kind == 1, rng.uniform(2.0, 30.0, T),         # medium
+          np.where(kind == 2, rng.uniform(200.0, 2000.0, T),     # covering / beyond screen
+                   rng.uniform(1.0, 20.0, T))))
+    ang = rng.uniform(0, 2 * math.pi, (T, 3))
+    xy = c[:, None, :] + rad[:, None, None] * px[None, None, :] * np.stack([np.cos(ang), np.sin(ang)], -1)
+    z = rng.uniform(-0.9, 0.9, (T, 1)) + rng.uniform(-0.05, 0.05, (T, 3))
+    pos = np.concatenate([xy, z[..., None]], -1)                  # [T][3][3]
+    sl = kind == 3                                                # slivers: corner 2 near edge 0-1
+    pos[sl, 2, :2] = 0.5 * (pos[sl, 0, :2] + pos[sl, 1, :2]) + rng.normal(0, 1e-4, (sl.sum(), 2))
+    dg = kind == 4                                                # degenerate: repeated corner
+    pos[dg, 2] = pos[dg, 0]
+    off = kind == 5                                               # off-screen
+    pos[off, :, :2] += np.sign(rng.uniform(-1, 1, (off.sum(), 1, 2))) * 3.0
+    gb = kind == 6                                                # beyond the guard band
+    pos[gb, 0, :2] = rng.choice([-1, 1], (gb.sum(), 2)) * rng.uniform(1e4, 1e6, (gb.sum(), 2))
+    lat = kind == 9                                               # half-pixel lattice, shared depth
+    pos[lat, :, :2] = (np.round((pos[lat, :, :2] + 1) / px * 2) / 2) * px - 1
+    pos[lat, :, 2] = 0.25
+    if persp:   # NDC -> camera space at depth d with x, y scaled into the frustum
+        d = rng.uniform(1.0, 20.0, (T, 1, 1))
+        f = 1.0 / math.tan(math.radians(30.0))
+        cam = np.concatenate([pos[..., :1] * d * (W / max(H, 1)) / f, pos[..., 1:2] * d / f,
+                              -d + pos[..., 2:3] * 0.5], -1)
+        beh = kind == 7                                           # behind the camera / straddling
+        cam[beh, 0, 2] = rng.uniform(0.0, 5.0, beh.sum())
+        pos = cam
+    nf = kind == 8                                                # non-finite corner
+    pos[nf, 1, rng.integers(0, 3)] = rng.choice([np.inf, -np.inf, np.nan])
+    verts = pack_verts(pos.reshape(-1, 3).astype(np.float32), random_unit(rng, 3 * T))
+    idx = np.arange(3 * T, dtype=np.int64).reshape(T, 3)
+    if T > 1 and rng.random() < 0.5:                              # vertex sharing
+        share = rng.random((T, 3)) < 0.2
+        idx[share] = rng.integers(0, 3 * T, share.sum())
+    mvp = perspective_mvp(aspect=W / max(H, 1)) if persp else np.eye(4, dtype=np.float32).reshape(16)
+    light = random_unit(rng, 1)[0] if rng.random() < 0.5 else LIGHT.copy()
+    return Scene(f"fuzz{seed}", W, H, bins, verts, idx.astype(np.int32), mvp, light)
+
+
 def scene_c4(T: int = 4_000_000) -> Scene:
     """1920x1080, 16x16 bins, 4M-triangle random soup (sort-first case)."""
     return scene_soup(T, 1920, 1080, 4, "c4")
