@@ -97,9 +97,11 @@ if h.piko_dbg_rx_lb(lb.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(lb.nbyte
 nrx = (st["n_pairs"] + 4095) // 4096
 show("radix pass 1", buf[2], ["start", "load", "rank", "lookback", "scatter"], nrx)
 nb = st["owned_bins"]
-t = buf[3, :nb].astype(np.int64)
+t = buf[3, :min(nb, 8192)].astype(np.int64)
+t = t[(t[:, 0] > T0) & (t[:, 2] >= t[:, 0])]   # bins recorded in this frame
 base = t[:, 0].min()
-print(f"== k_tile: {nb} bins, start {base - T0} ns, span {t[:, 2].max() - base} ns")
+print(f"== k_tile: {len(t)} bins recorded, first bin start {base - T0} ns after k_setup chunk 0, "
+      f"last bin end {t[:, 2].max() - T0} ns")
 ne = t[:, 3]
 for lo, hi in ((0, 0), (1, 256), (257, 1024), (1025, 1 << 30)):
     m = (ne >= lo) & (ne <= hi)
@@ -116,11 +118,32 @@ for c in range(per.size):
     if m.any():
         busy[c] = (t[m, 2] - t[m, 0]).sum()
 print(f"   bins per CTA: min {per[per>0].min()} max {per.max()};  CTA busy ns: median {np.median(busy[busy>0]):.0f} max {busy.max():.0f}")
-print(f"   tile kernel first bin start {t[:,0].min()-base}, last bin end {t[:,2].max()-base}")
+print(f"   frame timeline (ns after k_setup chunk 0): expand {int(buf[1, :nrx0, 0].astype(np.int64).min() - T0)}"
+      f"..{int(buf[1, :nrx0, 4].astype(np.int64).max() - T0)}, sort "
+      f"{int(buf[2, :nrx, 0][buf[2, :nrx, 0] > 0].astype(np.int64).min() - T0)}.."
+      f"{int(buf[2, :nrx, 4].astype(np.int64).max() - T0)}, tile {base - T0}..{t[:, 2].max() - T0}")
 
 c = buf[0, 7000:7000 + 1024].astype(np.int64)
-c = c[c[:, 0] > 0]
+c = c[c[:, 0] > T0]
 b0 = c[:, 0].min()
+print(f"   k_tile CTAs first start {b0 - T0} ns after k_setup chunk 0")
 print(f"== k_tile per CTA ({len(c)} CTAs): start spread {c[:,0].max()-b0} ns")
 print(f"   work-list phase end: median {np.median(c[:,1]-b0):.0f} p90 {np.percentile(c[:,1]-b0,90):.0f} max {(c[:,1]-b0).max()}")
 print(f"   CTA end:             median {np.median(c[:,2]-b0):.0f} p90 {np.percentile(c[:,2]-b0,90):.0f} max {(c[:,2]-b0).max()}")
+
+# slowest CTAs: the bins they processed (pairs, start/raster/writeback ns relative to the first bin)
+tt = buf[3, :min(nb, 8192)].astype(np.int64)
+ok = (tt[:, 0] > T0) & (tt[:, 2] >= tt[:, 0])
+rows = [(int(tt[b, 4]), b, int(tt[b, 3]), tt[b, 0] - base, tt[b, 1] - tt[b, 0], tt[b, 2] - tt[b, 1])
+        for b in np.nonzero(ok)[0]]
+by = {}
+for cta, b, n, st_, ra, wb in rows:
+    by.setdefault(cta, []).append((st_, b, n, ra, wb))
+ends = sorted(((max(s_ + r_ + w_ for s_, _, _, r_, w_ in v), c) for c, v in by.items()), reverse=True)
+print("   slowest CTAs (end ns): bins as (start, pairs, raster, writeback)")
+for e_, c in ends[:8]:
+    print(f"     cta {c:4d} end {e_:6d}: " + "  ".join(f"({s_},{n},{r_},{w_})" for s_, _, n, r_, w_ in sorted(by[c])))
+firsts = sorted(v[0][0] for v in (sorted(x) for x in by.values()))
+print(f"   first-bin start across CTAs: p50 {np.median(firsts):.0f} max {max(firsts)}")
+pairs_sorted = sorted((n for _, _, n, _, _, _ in rows), reverse=True)
+print(f"   pair counts: top {pairs_sorted[:5]}, #bins {len(rows)}, sum {sum(pairs_sorted)}")
