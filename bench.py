@@ -336,6 +336,13 @@ def run_piko(args):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
     frame_bytes = sum(algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"])
                       for k in ("vertex", "setup", "expand", "sort", "tile"))
+    # BASELINE.md's frame metric: ncu-measured DRAM bytes of the frame's kernels
+    measured = None
+    if os.path.exists(tf):
+        tj = json.load(open(tf))
+        ran = [k for k in ("vertex", "setup", "expand", "sort", "tile") if per_frame.get(k, 0) > 0.004]
+        if all(k in tj for k in ran):
+            measured = int(sum(tj[k] for k in ran))
     ms = total_ms / args.steps
     out = {
         "metric": METRIC, "value": T * args.steps / (total_ms / 1e3) / 1e6, "unit": UNIT,
@@ -348,7 +355,11 @@ def run_piko(args):
                    "parallelism": f"{args.multi} x{world} ({transport})" if world > 1 else "1 GPU"},
         "fps": 1e3 / ms,
         "ms_p10_p50_p90": [float(x) for x in np.percentile(step_ms, [10, 50, 90])],
-        "frame_roofline": {"algorithmic_bytes": frame_bytes, "frac": frame_bytes / (ms / 1e3) / 1e9 / peak},
+        "frame_roofline": {"algorithmic_bytes": frame_bytes, "frac": frame_bytes / (ms / 1e3) / 1e9 / peak,
+                           "measured_bytes": measured,
+                           "frac_measured": measured / (ms / 1e3) / 1e9 / peak if measured else None,
+                           "measured_note": "sum of ncu dram__bytes_read+write per kernel of one frame "
+                                            "(profiles/traffic_*.json; ncu replays each kernel cold)"},
         "kernel_ms": per_frame,
         "kernel_ms_note": "per-stage CUDA-event times from a second K-step pass (events between kernels)",
         "api": "piko_draw_indexed (C ABI via ctypes)",
