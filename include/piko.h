@@ -236,6 +236,18 @@ int piko_set_transport(piko_ctx *ctx, int transport);
  * destroy rank 0 last.                                                       */
 int piko_attach_local_peers(piko_ctx *ctx, piko_ctx *root, int rank, int nranks);
 
+/* The P2P transport without a communicator, between processes (the handle
+ * bytes travel by any channel, e.g. torch.distributed):
+ *   rank 0:  piko_p2p_export fills PIKO_P2P_HANDLE_BYTES of CUDA IPC handles
+ *            of its exchange buffers (allocated here);
+ *   rank r:  piko_p2p_import maps them.
+ * Afterwards piko_draw runs the P2P exchange exactly as after
+ * piko_attach_comm with PIKO_XPORT_P2P (which uses these two steps with an
+ * ncclBroadcast of the handles).  Destroy rank 0's context last.            */
+#define PIKO_P2P_HANDLE_BYTES 128
+int piko_p2p_export(piko_ctx *ctx, int nranks, void *out_handles);
+int piko_p2p_import(piko_ctx *ctx, const void *handles, int rank, int nranks);
+
 /* Host-only (no CUDA): sort-last triangle range [*t0, *t1) of `rank` of
  * `nranks` for n_tris triangles (see PIKO_MULTI_SORT_LAST).  PIKO_EINVAL on
  * bad arguments.                                                             */

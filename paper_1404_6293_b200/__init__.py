@@ -29,7 +29,8 @@ EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_se
            "piko_get_stats", "piko_nccl_unique_id", "piko_draw_indexed",
            "piko_draw_tile_keys", "piko_resolve_keys", "piko_tile_keys_count", "piko_owned_bins",
            "piko_set_pipeline", "piko_set_profiling", "piko_get_profile", "piko_set_multi",
-           "piko_triangle_range", "piko_set_transport", "piko_attach_local_peers")
+           "piko_triangle_range", "piko_set_transport", "piko_attach_local_peers",
+           "piko_p2p_export", "piko_p2p_import")
 STAGES = ("clear", "vertex", "setup", "expand", "sort", "tile", "gather", "resolve")
 
 
@@ -74,6 +75,8 @@ def _load():
         "piko_set_multi": ([P, I], I),
         "piko_set_transport": ([P, I], I),
         "piko_attach_local_peers": ([P, P, I, I], I),
+        "piko_p2p_export": ([P, I, P], I),
+        "piko_p2p_import": ([P, P, I, I], I),
         "piko_triangle_range": ([I64, I, I, ctypes.POINTER(I64), ctypes.POINTER(I64)], I),
         "piko_attach_comm": ([P, P, I, I], I),
         "piko_get_stats": ([P, ctypes.POINTER(piko_stats)], I),
@@ -256,6 +259,17 @@ def piko_set_transport(ctx, transport):
 
 def piko_attach_local_peers(ctx, root, rank, nranks):
     return _check(ctx, _lib.piko_attach_local_peers(ctx, root, rank, nranks))
+
+
+def piko_p2p_export(ctx, nranks) -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(ctx, _lib.piko_p2p_export(ctx, nranks, buf))
+    return buf.raw
+
+
+def piko_p2p_import(ctx, handles: bytes, rank, nranks):
+    buf = ctypes.create_string_buffer(bytes(handles), 128)
+    return _check(ctx, _lib.piko_p2p_import(ctx, buf, rank, nranks))
 
 
 def piko_triangle_range(n_tris, rank, nranks):

@@ -179,6 +179,10 @@ static bool exchanging(const piko_ctx* ctx) {
   return (ctx->comm != nullptr || ctx->p2p_keys != nullptr) && ctx->mnranks > 1;
 }
 
+static int p2p_export(piko_ctx* ctx, int nranks, void* h);
+static int p2p_import(piko_ctx* ctx, const void* h, int rank, int nranks);
+static_assert(2 * sizeof(cudaIpcMemHandle_t) <= PIKO_P2P_HANDLE_BYTES, "IPC handle bytes");
+
 // rank 0: allocate the P2P exchange buffers (zeroed epochs)
 static int p2p_alloc(piko_ctx* ctx) {
   const size_t tile = (size_t)ctx->bw * ctx->bh;
@@ -828,6 +832,56 @@ extern "C" int piko_set_multi(piko_ctx* ctx, int mode) {
   return PIKO_OK;
 }
 
+// rank 0: exchange buffers + their CUDA IPC handles (keys, sync) into h
+static int p2p_export(piko_ctx* ctx, int nranks, void* h) {
+  set_ownership(ctx, 0, nranks);
+  ctx->transport = PIKO_XPORT_P2P;
+  int rc = p2p_alloc(ctx);
+  if (rc != PIKO_OK) return rc;
+  cudaIpcMemHandle_t* hh = static_cast<cudaIpcMemHandle_t*>(h);
+  CK(cudaIpcGetMemHandle(&hh[0], ctx->p2p_keys));
+  CK(cudaIpcGetMemHandle(&hh[1], ctx->p2p_sync));
+  return PIKO_OK;
+}
+
+// rank > 0: map rank 0's exchange buffers
+static int p2p_import(piko_ctx* ctx, const void* h, int rank, int nranks) {
+  set_ownership(ctx, rank, nranks);
+  ctx->transport = PIKO_XPORT_P2P;
+  cudaIpcMemHandle_t hh[2];
+  memcpy(hh, h, sizeof hh);
+  void* pk = nullptr;
+  void* ps = nullptr;
+  CK(cudaIpcOpenMemHandle(&pk, hh[0], cudaIpcMemLazyEnablePeerAccess));
+  CK(cudaIpcOpenMemHandle(&ps, hh[1], cudaIpcMemLazyEnablePeerAccess));
+  ctx->p2p_keys = static_cast<unsigned long long*>(pk);
+  ctx->p2p_sync = static_cast<unsigned long long*>(ps);
+  ctx->p2p_ipc = true;
+  return PIKO_OK;
+}
+
+static int p2p_check(piko_ctx* ctx, int rank, int nranks) {
+  if (nranks < 2 || rank < 0 || rank >= nranks) return ctx->fail(PIKO_EINVAL, "bad rank/nranks");
+  if (ctx->comm || ctx->p2p_keys) return ctx->fail(PIKO_ESTATE, "ranks already attached");
+  if (ctx->multi != PIKO_MULTI_SORT_FIRST || ctx->pipeline != PIKO_PIPE_BINNED)
+    return ctx->fail(PIKO_ESTATE, "P2P peers need sort-first and the binned pipeline");
+  CK(cudaSetDevice(ctx->device));
+  return PIKO_OK;
+}
+
+extern "C" int piko_p2p_export(piko_ctx* ctx, int nranks, void* out_handles) {
+  if (!ctx || !out_handles) return PIKO_EINVAL;
+  int rc = p2p_check(ctx, 0, nranks);
+  return rc != PIKO_OK ? rc : p2p_export(ctx, nranks, out_handles);
+}
+
+extern "C" int piko_p2p_import(piko_ctx* ctx, const void* handles, int rank, int nranks) {
+  if (!ctx || !handles) return PIKO_EINVAL;
+  if (rank == 0) return ctx->fail(PIKO_EINVAL, "rank 0 exports");
+  int rc = p2p_check(ctx, rank, nranks);
+  return rc != PIKO_OK ? rc : p2p_import(ctx, handles, rank, nranks);
+}
+
 extern "C" int piko_set_transport(piko_ctx* ctx, int transport) {
   if (!ctx) return PIKO_EINVAL;
   if (transport != PIKO_XPORT_NCCL && transport != PIKO_XPORT_P2P)
@@ -887,31 +941,20 @@ extern "C" int piko_attach_comm(piko_ctx* ctx, const void* uid, int rank, int nr
   if (ctx->transport == PIKO_XPORT_P2P && nranks > 1) {
     // rank 0 allocates the exchange buffers and broadcasts their CUDA IPC
     // handles over the new communicator; the other ranks map them (NVLink P2P)
-    struct { cudaIpcMemHandle_t keys, sync; } h;
-    memset(&h, 0, sizeof h);
+    unsigned char h[PIKO_P2P_HANDLE_BYTES];
+    memset(h, 0, sizeof h);
     if (rank == 0) {
-      int rc0 = p2p_alloc(ctx);
+      const int rc0 = p2p_export(ctx, nranks, h);
       if (rc0 != PIKO_OK) return rc0;
-      CK(cudaIpcGetMemHandle(&h.keys, ctx->p2p_keys));
-      CK(cudaIpcGetMemHandle(&h.sync, ctx->p2p_sync));
     }
     void* d = nullptr;
     CK(cudaMalloc(&d, sizeof h));
-    CK(cudaMemcpy(d, &h, sizeof h, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice));
     const int rb = g_nccl.Broadcast(d, d, sizeof h, ncclUint8_, 0, ctx->comm, nullptr);
     if (rb != 0) { cudaFree(d); return ctx->fail(PIKO_ENCCL, "ncclBroadcast: %s", g_nccl.GetErrorString(rb)); }
-    CK(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));  // (synchronises the broadcast)
+    CK(cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost));  // (synchronises the broadcast)
     CK(cudaFree(d));
-    if (rank != 0) {
-      void* pk = nullptr;
-      void* ps = nullptr;
-      CK(cudaIpcOpenMemHandle(&pk, h.keys, cudaIpcMemLazyEnablePeerAccess));
-      CK(cudaIpcOpenMemHandle(&ps, h.sync, cudaIpcMemLazyEnablePeerAccess));
-      ctx->p2p_keys = static_cast<unsigned long long*>(pk);
-      ctx->p2p_sync = static_cast<unsigned long long*>(ps);
-      ctx->p2p_ipc = true;
-    }
-    return PIKO_OK;
+    return rank == 0 ? PIKO_OK : p2p_import(ctx, h, rank, nranks);
   }
   const size_t tile_bytes = sizeof(unsigned long long) * ctx->bw * ctx->bh;
   CK(cudaMalloc(&ctx->tile_keys, tile_bytes * std::max(ctx->owned_max, 1)));

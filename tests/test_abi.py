@@ -25,7 +25,7 @@ def piko():
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(piko_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(piko_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_the_north_star_calls():
@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol(piko):
         assert hasattr(lib, n), n
     assert sorted(piko.EXPORTS) == names
     out = subprocess.check_output(["nm", "-D", "--defined-only", piko.LIB_PATH], text=True)
-    exported = set(re.findall(r" T (piko_[a-z_]+)$", out, flags=re.M))
+    exported = set(re.findall(r" T (piko_[a-z0-9_]+)$", out, flags=re.M))
     assert set(names) <= exported
 
 

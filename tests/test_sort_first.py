@@ -165,3 +165,70 @@ def test_gpu_p2p_transport_virtual_ranks(oracle_lib, R):
         assert np.abs(r0.rgba.cpu().numpy() - ref["rgba"]).max() <= 1e-5
     for rd in rds[1:] + rds[:1]:
         rd.close()
+
+
+def _p2p_ipc_worker(rank, world, port, result):
+    """One process of the two-process P2P test (both on cuda:0): CUDA IPC
+    handles travel over gloo, then every frame rank 1's tile kernel stores its
+    keys into rank 0's buffer and raises its flag; rank 0 resolves."""
+    import torch
+    import torch.distributed as dist
+    import paper_1404_6293_b200 as piko
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    s = scenes.scene_soup(20000, 333, 200, seed=91, name="soup")
+    dev = torch.device("cuda:0")
+    v = torch.from_numpy(s.verts).to(dev)
+    i = torch.from_numpy(s.idx).to(dev)
+    r = piko.Renderer(s.W, s.H, 16, device=dev)
+    obj = [piko.piko_p2p_export(r.ctx, world) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    if rank != 0:
+        piko.piko_p2p_import(r.ctx, obj[0], rank, world)
+    dist.barrier()  # every rank mapped and ready before the first frame
+    views = [s.mvp, np.array([[0.9, 0.1, 0, 0.05], [-0.1, 0.9, 0, 0], [0, 0, 1, 0], [0, 0, 0, 1]],
+                             np.float32).reshape(16)]
+    frames = []
+    for f in range(4):
+        r.draw(v, i, views[f % 2], s.light)
+        torch.cuda.synchronize()
+        if rank == 0:
+            frames.append((r.primid().cpu().numpy(), r.depth.cpu().numpy().copy(),
+                           r.rgba.cpu().numpy().copy()))
+    dist.barrier()  # rank 0's buffers outlive the peers' mappings
+    if rank != 0:
+        r.close()
+    dist.barrier()
+    if rank == 0:
+        r.close()
+        result["frames"] = frames
+        result["scene"] = s
+        result["views"] = views
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_p2p_transport_two_processes(oracle_lib):
+    """The cross-process part of the P2P transport (CUDA IPC handle export /
+    import, system-scope flags between processes) on one device: rank 0 in this
+    process, rank 1 in a spawned one; rank 0's frames == oracle, bit-exact."""
+    import multiprocessing as mp
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    port = _free_port()
+    result = {}
+    ctx = mp.get_context("spawn")
+    p = ctx.Process(target=_p2p_ipc_worker, args=(1, 2, port, {}))
+    p.start()
+    _p2p_ipc_worker(0, 2, port, result)
+    p.join(timeout=300)
+    assert p.exitcode == 0
+    s = result["scene"]
+    for f, (prim, depth, rgba) in enumerate(result["frames"]):
+        ref = oracle_lib.render(s.verts, s.idx, result["views"][f % 2], s.light, s.W, s.H)
+        assert np.array_equal(prim, ref["primid"]), f"frame {f}"
+        assert np.array_equal(depth.view(np.uint32), ref["depth"].view(np.uint32)), f"frame {f}"
+        assert np.abs(rgba - ref["rgba"]).max() <= 1e-5
