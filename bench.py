@@ -174,16 +174,27 @@ def run_piko(args):
         def attach(rd, xport):
             if args.multi == "sort-last":
                 piko.piko_set_multi(rd.ctx, piko.PIKO_MULTI_SORT_LAST)
-            elif xport == "p2p":
-                piko.piko_set_transport(rd.ctx, piko.PIKO_XPORT_P2P)
-            obj = [piko.piko_nccl_unique_id() if rank == 0 else None]
+            # rank 0 always broadcasts (None on failure) so no rank waits forever
+            h = None
+            if rank == 0:
+                try:
+                    h = (piko.piko_p2p_export(rd.ctx, world) if xport == "p2p"
+                         else piko.piko_nccl_unique_id())
+                except piko.PikoError as e:
+                    print(f"rank 0: {xport} setup failed: {e}", file=sys.stderr)
+            obj = [h]
             dist.broadcast_object_list(obj, src=0)
-            try:
-                piko.piko_attach_comm(rd.ctx, obj[0], rank, world)
-                ok = 1
-            except piko.PikoError as e:
-                print(f"rank {rank}: attach ({xport}) failed: {e}", file=sys.stderr)
-                ok = 0
+            ok = int(obj[0] is not None)
+            if ok:
+                try:
+                    if xport == "p2p":  # CUDA IPC handles of rank 0's exchange buffers
+                        if rank != 0:
+                            piko.piko_p2p_import(rd.ctx, obj[0], rank, world)
+                    else:
+                        piko.piko_attach_comm(rd.ctx, obj[0], rank, world)
+                except piko.PikoError as e:
+                    print(f"rank {rank}: attach ({xport}) failed: {e}", file=sys.stderr)
+                    ok = 0
             t = torch.tensor([ok], dtype=torch.int32, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MIN)  # every rank agrees on the transport
             return bool(t.item())
@@ -191,7 +202,12 @@ def run_piko(args):
         if not attach(r, transport):
             if args.transport != "auto" or transport == "nccl":
                 raise SystemExit("multi-GPU attach failed")
-            r.close()
+            dist.barrier()  # peers unmap before rank 0 frees its exchange buffers
+            if rank != 0:
+                r.close()
+            dist.barrier()
+            if rank == 0:
+                r.close()
             r = piko.Renderer(s.W, s.H, bw, device=dev)
             transport = "nccl"
             if not attach(r, transport):
@@ -299,11 +315,11 @@ def run_piko(args):
                "d2h_bytes_per_step": int((hrgba.numel() + hdepth.numel()) * 4) if rank == 0 else 0,
                "ms_per_step": e_ms / ke, "steps": ke}
 
-    if rank != 0:
+    if rank != 0:  # peers close (unmap rank 0's P2P buffers) before rank 0 frees them
+        r.close()
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
-        r.close()
         return
 
     clocks = sampler.summary()
