@@ -158,11 +158,20 @@ def run_piko(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # test hook: PIKO_BENCH_SHARE_GPU=1 puts every rank on cuda:0 with gloo for
+    # torch.distributed -- exercises the N > 1 control flow (P2P transport) on a
+    # one-GPU box; its timings are meaningless (ranks time-slice one GPU)
+    share = os.environ.get("PIKO_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     s = scenes.make(args.config)
     bw = args.bin
