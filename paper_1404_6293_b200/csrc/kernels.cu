@@ -1442,7 +1442,21 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
             Q.t[slot] = t_cur; Q.rx0[slot] = rx0; Q.ry0[slot] = ry0; Q.w[slot] = w;
             Q.pre[slot] = (unsigned)area;  // turned into the prefix at the end of the bin
             area = 0;
-          }  // queue full: this one takes the warp-cooperative path
+          } else if (a.ovq && slot - TileSmem<BW, BH, THREADS>::BIGQ < OVQ_CAP) {
+            // queue full: spill the prepared entry to this CTA's global overflow
+            // region (L2); drained by all threads after the main loop, so no
+            // warp is left rasterizing alone while the others wait
+            const TriEval ev = prepare(r);
+            int4* q = a.ovq + ((size_t)blockIdx.x * OVQ_CAP + (slot - TileSmem<BW, BH, THREADS>::BIGQ)) * 6;
+            const int thr = (ev.thr0 ? 1 : 0) | (ev.thr1 ? 2 : 0) | (ev.thr2 ? 4 : 0) | (ev.small ? 8 : 0);
+            q[0] = make_int4(ev.X0, ev.Y0, ev.A0, ev.B0);
+            q[1] = make_int4(ev.A1, ev.B1, ev.A2, ev.B2);
+            q[2] = make_int4((int)(unsigned)ev.K1, (int)(ev.K1 >> 32), (int)(unsigned)ev.K2, (int)(ev.K2 >> 32));
+            q[3] = make_int4(thr, __float_as_int(ev.zw0), __float_as_int(ev.za), __float_as_int(ev.zb));
+            q[4] = make_int4(__float_as_int(__frcp_rn((float)w)), t_cur, rx0, ry0);
+            q[5] = make_int4(w, area, 0, 0);
+            area = 0;
+          }  // both full: this one takes the warp-cooperative path
         }
       }
       if (__any_sync(0xffffffffu, area > 0)) {  // queue overflow: warp-cooperative
@@ -1488,9 +1502,9 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     // record stages are free: start the next item's loads now
     pre = s_nx[0] >= 0;
     if (pre) prologue(s_nx[1], s_nx[2]);
-    {  // queued triangles: all threads over the flattened (triangle, pixel) items
-      const int nq = min(s_nbig, TileSmem<BW, BH, THREADS>::BIGQ);
-      if (nq > 0) {
+    // queued triangles: all threads over the flattened (triangle, pixel) items
+    auto drain = [&](const int nq) {
+      {
         auto& Q = sm.q;
         // exclusive prefix of the clipped areas (one entry per thread)
         const unsigned ar = tid < nq ? Q.pre[tid] : 0u;
@@ -1561,6 +1575,31 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
           if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
         }
         __syncthreads();
+      }
+    };
+    {
+      constexpr int BIGQ = TileSmem<BW, BH, THREADS>::BIGQ;
+      const int nbig = s_nbig;
+      if (nbig > 0) drain(min(nbig, BIGQ));
+      // spilled entries, BIGQ at a time through the same shared-memory queue
+      const int nov = a.ovq ? min(max(nbig - BIGQ, 0), OVQ_CAP) : 0;
+      for (int o0 = 0; o0 < nov; o0 += BIGQ) {
+        const int nq = min(BIGQ, nov - o0);
+        if (tid < nq) {
+          const int4* q = a.ovq + ((size_t)blockIdx.x * OVQ_CAP + o0 + tid) * 6;
+          const int4 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3], q4 = q[4], q5 = q[5];
+          auto& Q = sm.q;
+          Q.X0[tid] = q0.x; Q.Y0[tid] = q0.y; Q.A0[tid] = q0.z; Q.B0[tid] = q0.w;
+          Q.A1[tid] = q1.x; Q.B1[tid] = q1.y; Q.A2[tid] = q1.z; Q.B2[tid] = q1.w;
+          Q.K1[tid] = (long long)(((unsigned long long)(unsigned)q2.y << 32) | (unsigned)q2.x);
+          Q.K2[tid] = (long long)(((unsigned long long)(unsigned)q2.w << 32) | (unsigned)q2.z);
+          Q.thr[tid] = q3.x; Q.zw0[tid] = __int_as_float(q3.y); Q.za[tid] = __int_as_float(q3.z);
+          Q.zb[tid] = __int_as_float(q3.w);
+          Q.invw[tid] = __int_as_float(q4.x); Q.t[tid] = q4.y; Q.rx0[tid] = q4.z; Q.ry0[tid] = q4.w;
+          Q.w[tid] = q5.x; Q.pre[tid] = (unsigned)q5.y;
+        }
+        __syncthreads();  // batch staged (the previous drain ended with a barrier)
+        drain(nq);
       }
     }
     TL_MARK(b, 1);

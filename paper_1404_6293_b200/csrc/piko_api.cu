@@ -100,6 +100,7 @@ struct piko_ctx {
   unsigned long long* gkey = nullptr;  // [NB][bw*bh] key tiles of split bins
   uint32_t* gcov = nullptr;          // [NB][bw*bh] coverage tiles (debug)
   uint32_t* arrive = nullptr;        // [NB] fragment arrival counters
+  int4* ovq = nullptr; long long ovq_ctas = 0;  // k_tile queue overflow [ctas][OVQ_CAP][6]
   Control* ctl = nullptr;
   uint2* rect = nullptr;                 // [rec_cap] tile rect per triangle
   int tri_chunk = EX_MAX_TRIS;           // triangles per expand chunk (adapted to P/T)
@@ -268,7 +269,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
                   ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
-                  ctx->all_keys, ctx->fp_keys};
+                  ctx->all_keys, ctx->fp_keys, ctx->ovq};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -533,6 +534,14 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.prim_base = (unsigned)ctx->prim_base;
     if (keys_only) a.out_cov = nullptr;
     const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, keys_only)));
+    if (grid > ctx->ovq_ctas) {  // spill space of the per-bin large-triangle queue
+      if (ctx->ovq) cudaFree(ctx->ovq);
+      ctx->ovq = nullptr;
+      ctx->ovq_ctas = 0;
+      CK(cudaMalloc(&ctx->ovq, sizeof(int4) * 6 * OVQ_CAP * (size_t)grid));
+      ctx->ovq_ctas = grid;
+    }
+    a.ovq = ctx->ovq;
     CK(launch_tile(a, ctx->bw, ctx->bh, grid, a.out_cov != nullptr, keys_only, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_TILE));

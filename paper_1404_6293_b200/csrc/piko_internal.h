@@ -38,6 +38,7 @@ constexpr int NLIST = 2 + SIZE_CLASSES;
 constexpr int LIST_EMPTY = NLIST - 1;
 constexpr int FRAG_ROUNDS = 4;   // fragment = FRAG_ROUNDS * threads-per-CTA pairs
 constexpr int EMPTY_GROUP = 8;   // empty bins per k_tile queue ticket
+constexpr int OVQ_CAP = 1024;    // k_tile: spilled large-triangle entries per CTA (96 B each)
 
 // ---- persistent device control block ----------------------------------------
 // Never memset per frame: every kernel of a frame takes exactly gridDim.x
@@ -176,6 +177,7 @@ struct TileArgs {
   uint32_t* garrive;            // [npass][2][gcap] look-back group arrival counters;
   long long gcap;               //   k_tile zeroes the next frame's parity
   unsigned prim_base;           // keys-only: added to the primID of every stored key (sort-last)
+  int4* ovq;                    // [grid][OVQ_CAP][6] overflow of the per-bin queue (null: none)
   // P2P transport (sort-first): tile_keys points into rank 0's memory
   unsigned long long* p2p_flag;         // rank 0's arrival flag of this rank (null: no P2P)
   const unsigned long long* p2p_done;   // rank 0's last resolved epoch

@@ -405,3 +405,15 @@ def test_extreme_screens(env, W, H):
     got = gpu_render(env, s, 16, cov=False)
     assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
     assert_bins_equal(got, env, s, 16)
+
+
+@pytest.mark.parametrize("T", [200, 1000, 3000])
+def test_large_triangle_queue_spill_and_fallback(env, T):
+    """One 64x64 bin (single-bin grid: the work item is the whole pair list)
+    with T medium triangles (clipped area > TINY_AREA): T=200 fits the shared
+    queue (256), 1000 spills to the global overflow region (1024 per CTA), 3000
+    also takes the warp-cooperative fallback.  Bit-exact either way."""
+    s = scenes.scene_soup(T, 64, 64, seed=95 + T, name="spill")
+    got = gpu_render(env, s, 64)
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, 64)
