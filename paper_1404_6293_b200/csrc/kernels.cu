@@ -105,6 +105,7 @@ __device__ u64 g_k1_times[4][8192][8];
 #define TL_MARK(slot, i) do { if (threadIdx.x == 0 && (slot) < 8192) g_k1_times[3][slot][i] = gtimer(); } while (0)
 __device__ __forceinline__ void g_tl_extra(int job, int n, int cta) { g_k1_times[3][job][3] = n; g_k1_times[3][job][4] = cta; }
 #define TL_CTA(i) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_k1_times[0][7000 + blockIdx.x][i] = gtimer(); } while (0)
+#define SCAN_MARK(tile, i) do { if (threadIdx.x == 0 && (tile) < 64 && a.pass < 2) g_k1_times[1 + a.pass][8100 + (tile)][i] = gtimer(); } while (0)
 // look-back detail of radix passes 0/1 (thread 0 = digit 0): [pass][chunk]
 // {level-1 end time, level-1 probes, level-2 probes, group-aggregate publish time}
 __device__ u64 g_rx_lb[2][8192][8];
@@ -124,6 +125,7 @@ namespace piko {
 #define TL_MARK(slot, i) do { } while (0)
 #define g_tl_extra(a, b, c) do { } while (0)
 #define TL_CTA(i) do { } while (0)
+#define SCAN_MARK(tile, i) do { } while (0)
 #endif
 
 // Look-back status word: tag (frame+1, 20 bits) | flag (2 bits) | value (42 bits)
@@ -507,6 +509,7 @@ __device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, u
   }
   if (lane == 31) s_wsum[warp] = inc;
   __syncthreads();
+  SCAN_MARK(tile, 2);
   unsigned wbase = 0, total = 0;
 #pragma unroll
   for (int w = 0; w < SCAN_THREADS / 32; ++w) {
@@ -519,6 +522,7 @@ __device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, u
     if (lane == 0) s_base = ex;
   }
   __syncthreads();
+  SCAN_MARK(tile, 3);
   u64 run = s_base + wbase + inc - sum;
 #pragma unroll
   for (int k = 0; k < SCAN_ITEMS; ++k) {
@@ -529,46 +533,55 @@ __device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, u
     run += c[k];
   }
   if (b0 < a.NB && b0 + SCAN_ITEMS >= a.NB) a.bin_start[a.NB] = (int32_t)run;
-  // Schedule: owned bins into k_tile's work lists (warp-aggregated appends;
-  // the order inside a list does not affect the result).  Bins with more than
-  // a.frag pairs become fragments (their global key tiles are CLEAR: k_tile's
-  // last fragment resets a tile after reading it).
+  // Schedule: owned bins into k_tile's work lists (the order inside a list
+  // does not affect the result).  Bins with more than a.frag pairs become
+  // fragments (their global key tiles are CLEAR: k_tile's last fragment resets
+  // a tile after reading it).  Appends are aggregated per CTA in shared memory:
+  // one global atomic per list and CTA (a chain of dependent per-warp global
+  // atomics made these CTAs the last of their grid, ~16 us on c3).
+  __shared__ unsigned s_ln[NLIST];
+  if (tid < NLIST) s_ln[tid] = 0u;
+  __syncthreads();
   const unsigned lanemask_lt = (1u << lane) - 1u;
-#pragma unroll 1
+  int kd[SCAN_ITEMS];
+  unsigned loc[SCAN_ITEMS], nfk[SCAN_ITEMS];
+#pragma unroll
   for (int k = 0; k < SCAN_ITEMS; ++k) {
     const long long b = b0 + k;
     const bool own = b < a.NB && (a.nranks == 1 || (int)(b % a.nranks) == a.rank);
     const unsigned cnt = own ? c[k] : 0u;
     const unsigned nf = (own && cnt > (unsigned)a.frag) ? (cnt + a.frag - 1) / a.frag : 0u;
-    // fragments of split bins: variable-length append
-    unsigned incl = nf;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
-    if (tot) {
-      unsigned base = 0;
-      if (lane == 0) base = atomicAdd(&a.ctl->list_n[0], tot);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      for (unsigned j = 0; j < nf; ++j)
-        a.frag_list[base + incl - nf + j] = make_int2((int)b, (int)j);
-    }
-    // single-fragment bins by size class (4 cnt > 3 frag, 2 frag, frag, else)
-    // and empty bins; kind < 0: not appended here
+    // list 0: fragments of split bins; 1..SIZE_CLASSES: single-fragment bins by
+    // size class (4 cnt > 3 frag, 2 frag, frag, else); LIST_EMPTY; -1: not owned
     const unsigned q4 = 4u * cnt;
     const int cls = q4 > 3u * (unsigned)a.frag ? 0 : q4 > 2u * (unsigned)a.frag ? 1
                   : q4 > (unsigned)a.frag ? 2 : 3;
-    const int kind = !own ? -1 : (nf > 0 ? -2 : (cnt > 0 ? 1 + cls : LIST_EMPTY));
-    const unsigned peers = __match_any_sync(0xffffffffu, kind);
+    const int kind = !own ? -1 : (nf > 0 ? 0 : (cnt > 0 ? 1 + cls : LIST_EMPTY));
+    const unsigned peers = __match_any_sync(0xffffffffu, kind);  // whole warp
     const int leader = __ffs(peers) - 1;
-    unsigned pos = 0;
-    if (kind > 0 && lane == leader)
-      pos = atomicAdd(&a.ctl->list_n[kind], (unsigned)__popc(peers));
-    pos = __shfl_sync(0xffffffffu, pos, leader);
-    if (kind > 0)
-      a.bin_list[(size_t)(kind - 1) * a.NB + pos + __popc(peers & lanemask_lt)] = (int32_t)b;
+    unsigned l = 0;
+    if (kind == 0) l = atomicAdd(&s_ln[0], nf);  // rare: variable-length append
+    else if (kind > 0 && lane == leader) l = atomicAdd(&s_ln[kind], (unsigned)__popc(peers));
+    const unsigned lb = __shfl_sync(0xffffffffu, l, leader);
+    if (kind != 0) l = lb + __popc(peers & lanemask_lt);
+    kd[k] = kind; loc[k] = l; nfk[k] = nf;
+  }
+  __syncthreads();
+  SCAN_MARK(tile, 4);
+  if (tid < NLIST) {
+    const unsigned n = s_ln[tid];
+    s_ln[tid] = n ? atomicAdd(&a.ctl->list_n[tid], n) : 0u;
+  }
+  __syncthreads();
+  SCAN_MARK(tile, 5);
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    const int b = (int)(b0 + k);
+    if (kd[k] == 0) {
+      for (unsigned j = 0; j < nfk[k]; ++j) a.frag_list[s_ln[0] + loc[k] + j] = make_int2(b, (int)j);
+    } else if (kd[k] > 0) {
+      a.bin_list[(size_t)(kd[k] - 1) * a.NB + s_ln[kd[k]] + loc[k]] = (int32_t)b;
+    }
   }
 }
 
@@ -580,7 +593,7 @@ __device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, u
 // is ranked in sub-blocks twice (count, then scatter).
 // ---------------------------------------------------------------------------
 struct RadixSmem {
-  unsigned whist[RX_WARPS][RX_RADIX];
+  unsigned short whist[RX_WARPS][RX_RADIX];  // per-warp digit counts (<= RX_CHUNK)
   unsigned keys[RX_CHUNK];
   int vals[RX_CHUNK];
   unsigned lstart[RX_RADIX];
@@ -601,7 +614,7 @@ __device__ __forceinline__ int cpad(int l) { return l + (l >> 5); }
 // Ranking of up to RX_CHUNK items held in registers (warp w owns items
 // [w*512, w*512+512), lane-strided): per-warp digit counters in shared memory.
 __device__ __forceinline__ void rank_items(const unsigned (&key)[RX_ITEMS], unsigned n, unsigned wb,
-                                           int shift, unsigned (*whist)[RX_RADIX], int warp, int lane,
+                                           int shift, unsigned short (*whist)[RX_RADIX], int warp, int lane,
                                            unsigned (&rank)[RX_ITEMS]) {
   const unsigned lanemask_lt = (1u << lane) - 1u;
 #pragma unroll
@@ -613,7 +626,7 @@ __device__ __forceinline__ void rank_items(const unsigned (&key)[RX_ITEMS], unsi
     unsigned prev = 0;
     if (valid) prev = whist[warp][d];
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) whist[warp][d] = prev + __popc(peers);
+    if (valid && lane == __ffs(peers) - 1) whist[warp][d] = (unsigned short)(prev + __popc(peers));
     __syncwarp();
     rank[j] = prev + __popc(peers & lanemask_lt);
   }
@@ -628,13 +641,16 @@ __device__ __forceinline__ void rank_items(const unsigned (&key)[RX_ITEMS], unsi
 __device__ __noinline__ void expand_slow(const RadixArgs& a, RadixSmem& sm, const ExpandSmem& ex,
                                          int ntri, long long t0, unsigned n, int phase) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (phase == 1) sm.lstart[tid] = sm.gstart[tid];
-  else sm.run[tid] = 0;
+  const bool dig = tid < RX_RADIX;  // thread tid owns digit tid
+  if (dig) {
+    if (phase == 1) sm.lstart[tid] = sm.gstart[tid];
+    else sm.run[tid] = 0;
+  }
 #pragma unroll 1
   for (unsigned lo = 0; lo < n; lo += RX_CHUNK) {
     const unsigned hi = min(n, lo + RX_CHUNK);
 #pragma unroll 1
-    for (int w = 0; w < RX_WARPS; ++w) sm.whist[w][tid] = 0;
+    for (int i = tid; i < RX_WARPS * RX_RADIX; i += RX_THREADS) (&sm.whist[0][0])[i] = 0;
     __syncthreads();  // previous window fully consumed
 #pragma unroll 1
     for (int l = tid; l < ntri; l += RX_THREADS) {
@@ -672,11 +688,13 @@ __device__ __noinline__ void expand_slow(const RadixArgs& a, RadixSmem& sm, cons
     rank_items(key, m, wb, a.shift, sm.whist, warp, lane, rank);
     __syncthreads();
     unsigned tot = 0;
+    if (dig) {
 #pragma unroll 1
-    for (int w = 0; w < RX_WARPS; ++w) {
-      const unsigned c = sm.whist[w][tid];
-      sm.whist[w][tid] = tot;
-      tot += c;
+      for (int w = 0; w < RX_WARPS; ++w) {
+        const unsigned c = sm.whist[w][tid];
+        sm.whist[w][tid] = (unsigned short)tot;
+        tot += c;
+      }
     }
     __syncthreads();
     if (phase == 1) {
@@ -691,18 +709,21 @@ __device__ __noinline__ void expand_slow(const RadixArgs& a, RadixSmem& sm, cons
       }
     }
     __syncthreads();
-    if (phase == 1) sm.lstart[tid] += tot;
-    else sm.run[tid] += tot;
+    if (dig) {
+      if (phase == 1) sm.lstart[tid] += tot;
+      else sm.run[tid] += tot;
+    }
   }
   __syncthreads();
 }
 
 template <bool EXPAND>
-__global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
+__global__ void __launch_bounds__(RX_THREADS, RX_MIN_CTAS) k_radix_pass(RadixArgs a) {
   extern __shared__ __align__(16) unsigned char rx_smem[];
   RadixSmem& sm = *reinterpret_cast<RadixSmem*>(rx_smem);
   ExpandSmem& ex = *reinterpret_cast<ExpandSmem*>(rx_smem + sizeof(RadixSmem));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool dig = tid < RX_RADIX;  // thread tid owns digit tid (look-back, offsets)
 
   pdl_wait();
   pdl_trigger();
@@ -726,7 +747,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     __syncthreads();
     return base + inc - v;
   };
-  const unsigned hist_d = a.ctl->digit_hist[frame & 1][a.pass][tid];
+  const unsigned hist_d = dig ? a.ctl->digit_hist[frame & 1][a.pass][tid] : 0u;
   u64 P;
   bool ovf = a.ctl->overflow_tag == frame + 1;
   long long nchunks;
@@ -753,12 +774,16 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
   if (chunk >= nchunks) {
     // extra CTAs: the CSR bin scan + work lists (counts are final: pass 0 done)
     const long long tile = chunk - nchunks;
-    if (a.scan_here && tile < (a.NB + SCAN_CHUNK - 1) / SCAN_CHUNK) bin_scan_tile(a, tile, tag);
+    if (a.scan_here && tile < (a.NB + SCAN_CHUNK - 1) / SCAN_CHUNK) {
+      SCAN_MARK(tile, 0);
+      bin_scan_tile(a, tile, tag);
+      SCAN_MARK(tile, 1);
+    }
     return;
   }
   RX_MARK(0);
 #pragma unroll
-  for (int w = 0; w < RX_WARPS; ++w) sm.whist[w][tid] = 0;
+  for (int i = tid; i < RX_WARPS * RX_RADIX; i += RX_THREADS) (&sm.whist[0][0])[i] = 0;
 
   // ---- chunk contents ----------------------------------------------------------
   unsigned key[RX_ITEMS];
@@ -851,24 +876,30 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
   // ---- per-digit chunk totals, published before the ranking ------------------
   unsigned total;
   if (fast) {
-    sm.run[tid] = 0;
+    if (dig) sm.run[tid] = 0;
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < RX_ITEMS; ++j)
-      if (wb + j * 32 < n) atomicAdd(&sm.run[(key[j] >> a.shift) & (RX_RADIX - 1)], 1u);
+    for (int j = 0; j < RX_ITEMS; ++j) {  // warp-aggregated: few distinct digits per chunk
+      const bool valid = wb + j * 32 < n;  // (spatially coherent bins, high digits) would
+      const unsigned d = valid ? ((key[j] >> a.shift) & (RX_RADIX - 1)) : RX_RADIX;  // serialise
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      if (valid && lane == __ffs(peers) - 1) atomicAdd(&sm.run[d], (unsigned)__popc(peers));
+    }
     __syncthreads();
-    total = sm.run[tid];
+    total = dig ? sm.run[tid] : 0u;
   } else {
     expand_slow(a, sm, ex, ntri, t0, n, 0);
-    total = sm.run[tid];
+    total = dig ? sm.run[tid] : 0u;
   }
   // two-level decoupled look-back, part 1: publish.  Chunks form groups of
   // LB_GROUP; the last chunk of a group to arrive publishes the group aggregate.
   const long long grp = chunk / LB_GROUP, g0 = grp * LB_GROUP;
   const long long gsize = min((long long)LB_GROUP, nchunks - g0);
   u64* st = a.status + (size_t)chunk * RX_RADIX + tid;
-  a.ccount[(size_t)chunk * RX_RADIX + tid] = total;
-  st_relaxed64(st, lb_pack(tag, chunk == 0 ? LB_INC : LB_AGG, total));
+  if (dig) {
+    a.ccount[(size_t)chunk * RX_RADIX + tid] = total;
+    st_relaxed64(st, lb_pack(tag, chunk == 0 ? LB_INC : LB_AGG, total));
+  }
   __syncthreads();
   if (tid == 0) {
     RX_LB(3, 0);
@@ -877,7 +908,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     RX_LB(4, gtimer());  // arrival counted
   }
   __syncthreads();
-  if (sm.n) {  // last chunk of the group to arrive: publish the group aggregate
+  if (sm.n && dig) {  // last chunk of the group to arrive: publish the group aggregate
     __threadfence();
     // all LB_GROUP loads in flight together: a runtime-bounded loop would issue
     // them one L2 round trip apart (in-order issue stalls on each add), which
@@ -911,32 +942,35 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     }
     rank_items(key, n, wb, a.shift, sm.whist, warp, lane, rank);
     __syncthreads();
-    unsigned tot = 0;
+    if (dig) {
+      unsigned tot = 0;
 #pragma unroll
-    for (int w = 0; w < RX_WARPS; ++w) {  // exclusive over warps
-      const unsigned c = sm.whist[w][tid];
-      sm.whist[w][tid] = tot;
-      tot += c;
+      for (int w = 0; w < RX_WARPS; ++w) {  // exclusive over warps
+        const unsigned c = sm.whist[w][tid];
+        sm.whist[w][tid] = (unsigned short)tot;
+        tot += c;
+      }
     }
   }
   RX_MARK(2);
 
   // ---- look-back part 2: walk (thread tid owns digit tid) ---------------------
   u64 excl = 0;
-  if (chunk > 0) {
+  if (chunk > 0 && dig) {
     bool done = false;
     unsigned np1 = 0, np2 = 0;
     // level 1: own group, chunks chunk-1 .. g0
     long long c = chunk - 1;
     while (!done && c >= g0) {
       ++np1;
-      u64 sv[LB_GROUP];
+      constexpr int LPROBE = LB_GROUP / 2;  // register budget of 2 CTAs/SM
+      u64 sv[LPROBE];
 #pragma unroll
-      for (int j = 0; j < LB_GROUP; ++j)
+      for (int j = 0; j < LPROBE; ++j)
         sv[j] = (c - j >= g0) ? ld_relaxed64(a.status + (size_t)(c - j) * RX_RADIX + tid) : 0ull;
       int j = 0;
 #pragma unroll
-      for (int q = 0; q < LB_GROUP; ++q) {
+      for (int q = 0; q < LPROBE; ++q) {
         if (done || j != q || c - q < g0) continue;
         if (lb_tag(sv[q]) != tag) continue;  // not yet published: stop, re-probe
         excl += lb_val(sv[q]);
@@ -951,7 +985,7 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     long long gq = grp - 1;
     while (!done && gq >= 0) {
       ++np2;
-      constexpr int GPROBE = 16;
+      constexpr int GPROBE = 8;
       u64 sv[GPROBE];
 #pragma unroll
       for (int j = 0; j < GPROBE; ++j)
@@ -974,15 +1008,17 @@ __global__ void __launch_bounds__(RX_THREADS) k_radix_pass(RadixArgs a) {
     RX_LB(2, np2);
     (void)np1; (void)np2;
   }
-  if (chunk == g0 + gsize - 1)  // last chunk of its group: the group's inclusive prefix
-    st_relaxed64(a.gstatus + (size_t)grp * RX_RADIX + tid, lb_pack(tag, LB_INC, excl + total));
-  sm.gstart[tid] = gprefix + (unsigned)excl;
+  if (dig) {
+    if (chunk == g0 + gsize - 1)  // last chunk of its group: the group's inclusive prefix
+      st_relaxed64(a.gstatus + (size_t)grp * RX_RADIX + tid, lb_pack(tag, LB_INC, excl + total));
+    sm.gstart[tid] = gprefix + (unsigned)excl;
+  }
   RX_MARK(3);
 
   // ---- phase B: scatter ----------------------------------------------------------
   if (fast) {  // stage the chunk sorted by digit in shared memory, then write out
     const unsigned lstart = block_excl(total);
-    sm.lstart[tid] = lstart;
+    if (dig) sm.lstart[tid] = lstart;
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < RX_ITEMS; ++j) {
@@ -1241,6 +1277,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   const Grid g = a.g;
   float L[3];
   normalise_light(a.light, L);
+  TL_CTA(3);  // resident
   pdl_wait();
   pdl_trigger();
   const u64 frame = a.ctl->frame;

@@ -10,17 +10,25 @@ namespace piko {
 
 // ---- launch geometry -------------------------------------------------------
 constexpr int K1_THREADS = 256;                     // triangle-setup CTA
-constexpr int K1_TPT = 4;                           // triangles per thread (strided)
+#ifndef PIKO_K1_TPT
+#define PIKO_K1_TPT 4
+#endif
+constexpr int K1_TPT = PIKO_K1_TPT;                 // triangles per thread (strided)
 constexpr int K1_CHUNK = K1_THREADS * K1_TPT;       // triangles per CTA
 constexpr int EX_MAX_TRIS = 4096;                   // triangles per expand chunk (radix pass 0)
-constexpr int SCAN_THREADS = 256;                   // bin-count scan (inside radix pass 0)
+#ifndef PIKO_RX_THREADS
+#define PIKO_RX_THREADS 256
+#endif
+constexpr int SCAN_THREADS = PIKO_RX_THREADS;       // bin-count scan (run by radix-pass CTAs: == RX_THREADS)
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
-constexpr int RX_THREADS = 256;                     // stable LSD radix pass CTA
+constexpr int RX_THREADS = PIKO_RX_THREADS;         // stable LSD radix pass CTA
+constexpr int RX_MIN_CTAS = 2;                      // resident per SM (shared memory allows 2)
 constexpr int RX_WARPS = RX_THREADS / 32;
-constexpr int RX_ITEMS = 16;
+constexpr int RX_ITEMS = 4096 / RX_THREADS;        // RX_CHUNK = 4096 pairs
 constexpr int RX_CHUNK = RX_THREADS * RX_ITEMS;     // pairs per chunk
 constexpr int RX_BITS = 8;
+static_assert(SCAN_THREADS == RX_THREADS && RX_THREADS >= (1 << RX_BITS), "digit-owner threads");
 constexpr int LB_GROUP = 16;                        // chunks per look-back group
 constexpr int RX_RADIX = 1 << RX_BITS;
 constexpr int MAX_PASSES = 3;                       // NB <= 2^24 bins

@@ -64,7 +64,7 @@ kk = kk[kk[:, 0] > 0]
 b0 = kk[:, 0].min()
 print(f"== k_setup: {len(kk)} CTAs, span {kk[:, 5].max() - b0} ns; loads median {np.median(kk[:,1]-kk[:,0]):.0f}, "
       f"setup median {np.median(kk[:,2]-kk[:,1]):.0f}, hist median {np.median(kk[:,5]-kk[:,2]):.0f}")
-nrx0 = int((buf[1, :, 0] > 0).sum())
+nrx0 = int((buf[1, :8000, 0] > 0).sum())
 show("radix pass 0 (expand)", buf[1], ["start", "expand", "rank", "lookback", "scatter"], nrx0)
 e = buf[1, :nrx0].astype(np.int64)
 print("   expand detail: loads+counts median %.0f, scan %.0f, expansion %.0f, reload %.0f" % (
@@ -127,7 +127,16 @@ c = buf[0, 7000:7000 + 1024].astype(np.int64)
 c = c[c[:, 0] > T0]
 b0 = c[:, 0].min()
 print(f"   k_tile CTAs first start {b0 - T0} ns after k_setup chunk 0")
-print(f"== k_tile per CTA ({len(c)} CTAs): start spread {c[:,0].max()-b0} ns")
+print(f"== k_tile per CTA ({len(c)} CTAs): start spread {c[:,0].max()-b0} ns; resident (before griddepcontrol.wait):"
+      f" first {c[:,3].min()-T0} p50 {int(np.median(c[:,3]))-T0} last {c[:,3].max()-T0} ns after k_setup chunk 0")
+for p_ in (0, 1):
+    sc = buf[1 + p_, 8100:8164].astype(np.int64)
+    sc = sc[sc[:, 0] > T0]
+    if len(sc):
+        print(f"   bin-scan tiles in radix pass {p_}: {len(sc)}, start {sc[:,0].min()-T0}..{sc[:,0].max()-T0}, end max {sc[:,1].max()-T0} ns")
+        for r_ in sc:
+            print("      tile: start %d  +load/scan %d  +lookback %d  +kinds %d  +atomics %d  +stores %d" % (
+                r_[0] - T0, r_[2] - r_[0], r_[3] - r_[2], r_[4] - r_[3], r_[5] - r_[4], r_[1] - r_[5]))
 print(f"   work-list phase end: median {np.median(c[:,1]-b0):.0f} p90 {np.percentile(c[:,1]-b0,90):.0f} max {(c[:,1]-b0).max()}")
 print(f"   CTA end:             median {np.median(c[:,2]-b0):.0f} p90 {np.percentile(c[:,2]-b0,90):.0f} max {(c[:,2]-b0).max()}")
 
