@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """A/B timing of compile-time variants of libpiko (experiments only).
-usage: python tools/ab.py CONFIG BIN 'name=-DFLAG ...' ['name2=...' ...]
+usage: python tools/ab.py CONFIG BIN 'name=-DFLAG ...' ['name2:alt/kernels.cu=...' ...]
 Each variant is compiled to /tmp and timed in its own process: median frame
 time over 30 frames (L2 flushed before each, CUDA events on the draw stream)."""
 import os
@@ -11,13 +11,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def build(name, flags):
+def build(name, flags, alt=None):
     import __graft_entry__ as ge
     lib = f"/tmp/libpiko_ab_{name}.so"
     objs = []
     for src in ge.SOURCES:
         o = f"/tmp/{src}.ab_{name}.o"
-        subprocess.check_call([ge._nvcc(), *ge.NVCC_FLAGS, *flags, "-c", os.path.join(ge.CSRC, src), "-o", o])
+        path = alt if (alt and src == "kernels.cu") else os.path.join(ge.CSRC, src)
+        subprocess.check_call([ge._nvcc(), *ge.NVCC_FLAGS, *flags, "-I", ge.CSRC, "-c", path, "-o", o])
         objs.append(o)
     subprocess.check_call([ge._nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
                            "-o", lib, "-ldl", "-lcudart"])
@@ -59,7 +60,8 @@ if __name__ == "__main__":
     libs = []
     for spec in sys.argv[3:]:
         name, _, fl = spec.partition("=")
-        libs.append((name, build(name, [f for f in fl.split() if f])))
+        name, _, alt = name.partition(":")  # name:ALT_KERNELS_CU (another kernels.cu)
+        libs.append((name, build(name, [f for f in fl.split() if f], alt or None)))
     for rep in range(2):
         for name, lib in libs:
             out = subprocess.run([sys.executable, __file__, "--run", lib, cfg, str(bw)], capture_output=True, text=True)
