@@ -132,6 +132,22 @@ int piko_set_sync(piko_ctx *ctx, int mode);
  * and does not support partitions or communicators (PIKO_ESTATE).            */
 int piko_set_pipeline(piko_ctx *ctx, int pipeline);
 
+/* Pixel-shader complexity (the paper's design-space axis, sec. 7.2.1,
+ * "As shader complexity increases, the computation time of
+ * shading a primitive significantly outweighs the time spent loading the
+ * primitive").  Adds `iters` dependent float FMAs per shaded fragment:
+ * forward = 1 charges every covered fragment that passes the depth range,
+ * inside the raster loop (binned: per-bin CTAs, LoadBalance; FreePipe: the
+ * triangle's own thread, DirectMap) -- the paper's pipelines shade before the
+ * depth test; forward = 0 charges once per resolved pixel (deferred).
+ * The extra result never reaches the outputs (which stay bit-identical for
+ * every setting); it is kept live through a never-taken store.  Single-GPU
+ * pipelines only (the multi-GPU resolve ignores it).  Applies from the next
+ * draw.  EINVAL unless 0 <= iters <= PIKO_MAX_SHADER_ITERS and forward is 0
+ * or 1.                                                                      */
+#define PIKO_MAX_SHADER_ITERS (1 << 20)
+int piko_set_shader_cost(piko_ctx *ctx, int iters, int forward);
+
 /* Destroy; NULL-safe; synchronises internal work first.                       */
 void piko_destroy(piko_ctx *ctx);
 

@@ -19,6 +19,7 @@ PIKO_OK, PIKO_EINVAL, PIKO_ENOMEM, PIKO_ECUDA, PIKO_ENCCL, PIKO_ECAPACITY, PIKO_
 PIKO_DEBUG_COVERAGE_COUNT = 1
 PIKO_SYNC_CHECKED, PIKO_SYNC_ASYNC = 0, 1
 PIKO_PIPE_BINNED, PIKO_PIPE_FREEPIPE = 0, 1
+PIKO_MAX_SHADER_ITERS = 1 << 20
 PIKO_MULTI_SORT_FIRST, PIKO_MULTI_SORT_LAST = 0, 1
 PIKO_XPORT_NCCL, PIKO_XPORT_P2P = 0, 1
 
@@ -30,7 +31,7 @@ EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_se
            "piko_draw_tile_keys", "piko_resolve_keys", "piko_tile_keys_count", "piko_owned_bins",
            "piko_set_pipeline", "piko_set_profiling", "piko_get_profile", "piko_set_multi",
            "piko_triangle_range", "piko_set_transport", "piko_attach_local_peers",
-           "piko_p2p_export", "piko_p2p_import")
+           "piko_p2p_export", "piko_p2p_import", "piko_set_shader_cost")
 STAGES = ("clear", "vertex", "setup", "expand", "sort", "tile", "gather", "resolve")
 
 
@@ -63,6 +64,7 @@ def _load():
         "piko_tile_keys_count": ([P], I64),
         "piko_owned_bins": ([I, I, I, I, I, I, P, I64], I64),
         "piko_set_pipeline": ([P, I], I),
+        "piko_set_shader_cost": ([P, I, I], I),
         "piko_finish": ([P], I),
         "piko_set_sync": ([P, I], I),
         "piko_destroy": ([P], None),
@@ -221,6 +223,10 @@ def piko_set_sync(ctx, mode):
 
 def piko_set_pipeline(ctx, pipeline):
     return _check(ctx, _lib.piko_set_pipeline(ctx, pipeline))
+
+
+def piko_set_shader_cost(ctx, iters, forward):
+    return _check(ctx, _lib.piko_set_shader_cost(ctx, iters, forward))
 
 
 def piko_get_primid(ctx):

@@ -1234,6 +1234,18 @@ struct TileSmem {
   BigQueue<BIGQ> q;
 };
 
+// Stand-in for a longer pixel shader (ShaderCost): `iters` dependent FMAs that
+// keep x in [0, 1] for x in [0, 1] (x -> x * (1 - 2^-10) + 2^-10).
+__device__ __forceinline__ float shader_work(int iters, float x) {
+#pragma unroll 1
+  for (int i = 0; i < iters; ++i) x = __fmaf_rn(x, 0.9990234375f, 0.0009765625f);
+  return x;
+}
+__device__ __forceinline__ float key_depth(u64 key) { return __uint_as_float((unsigned)(key >> 32)); }
+__device__ __forceinline__ void shader_sink(const ShaderCost& sc, float v) {
+  if (v < 0.0f) *sc.sink = v;  // unreachable: keeps the work observable
+}
+
 // Write one pixel of the frame (or the keys-only tile) from its resolved key.
 template <bool COV, bool KEYS_ONLY>
 __device__ __forceinline__ void store_pixel(const TileArgs& a, const float L[3], int job, int p,
@@ -1251,6 +1263,7 @@ __device__ __forceinline__ void store_pixel(const TileArgs& a, const float L[3],
     depth = __uint_as_float((unsigned)(key >> 32));
 #ifndef PIKO_EXP_NOSHADE
     c = shade(a.verts, a.xv, &a.M, a.idx, a.g.W, a.g.H, L, prim, 256 * x + 128, 256 * y + 128);
+    if (a.sc.iters && !a.sc.forward) shader_sink(a.sc, shader_work(a.sc.iters, depth));
 #endif
   }
   reinterpret_cast<float4*>(a.out_rgba)[o] = c;
@@ -1277,6 +1290,8 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   const Grid g = a.g;
   float L[3];
   normalise_light(a.light, L);
+  const int fwd = a.sc.forward ? a.sc.iters : 0;  // forward shader cost per fragment
+  float facc = 0.0f;
   TL_CTA(3);  // resident
   pdl_wait();
   pdl_trigger();
@@ -1458,7 +1473,10 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
               const int p = (y - y0) * BW + (x - x0);
               if (COV && cov) atomicAdd(&s_cov[p], 1u);
 #ifndef PIKO_EXP_NOATOM
-              if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
+              if (key != CLEAR_KEY) {
+                atomicMin(&sm.key[p], key);
+                if (fwd) facc = __fadd_rn(facc, shader_work(fwd, key_depth(key)));
+              }
 #else
               if (key == 12345) sm.key[p] = key;
 #endif
@@ -1528,7 +1546,10 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
             const u64 key = eval_key(rs, 256 * x + 128, 256 * y + 128, t_s, cov);
             const int p = (y - y0) * BW + (x - x0);
             if (COV && cov) atomicAdd(&s_cov[p], 1u);
-            if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
+            if (key != CLEAR_KEY) {
+              atomicMin(&sm.key[p], key);
+              if (fwd) facc = __fadd_rn(facc, shader_work(fwd, key_depth(key)));
+            }
           }
         }
       }
@@ -1609,7 +1630,10 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
           const u64 key = eval_pre(ev, 256 * x + 128, 256 * y + 128, Q.t[q], cov);
           const int p = (y - y0) * BW + (x - x0);
           if (COV && cov) atomicAdd(&s_cov[p], 1u);
-          if (key != CLEAR_KEY) atomicMin(&sm.key[p], key);
+          if (key != CLEAR_KEY) {
+            atomicMin(&sm.key[p], key);
+            if (fwd) facc = __fadd_rn(facc, shader_work(fwd, key_depth(key)));
+          }
         }
         __syncthreads();
       }
@@ -1716,6 +1740,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     }
   }
   TL_CTA(2);
+  if (fwd) shader_sink(a.sc, facc);
   if (KEYS_ONLY && a.p2p_flag) {
     // P2P: every CTA's key stores (straight into rank 0's memory over NVLink)
     // are made visible system-wide before it is counted; the last CTA counted
@@ -1741,6 +1766,8 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
 __global__ void __launch_bounds__(256) k_freepipe(FreePipeArgs a) {
   pdl_wait();
   pdl_trigger();
+  const int fwd = a.sc.forward ? a.sc.iters : 0;  // forward shader cost per fragment
+  float facc = 0.0f;
   constexpr int TPT = 4;
   const long long tb = (long long)blockIdx.x * (256 * TPT) + threadIdx.x;
   int vi[TPT][3];
@@ -1786,9 +1813,13 @@ __global__ void __launch_bounds__(256) k_freepipe(FreePipeArgs a) {
         const u64 key = eval_pre(ev, 256 * x + 128, 256 * y + 128, (int)t, cov);
         const size_t p = (size_t)y * a.W + x;
         if (a.cov && cov) atomicAdd(&a.cov[p], 1u);
-        if (key != CLEAR_KEY) atomicMin(&a.keys[p], key);
+        if (key != CLEAR_KEY) {
+          atomicMin(&a.keys[p], key);
+          if (fwd) facc = __fadd_rn(facc, shader_work(fwd, key_depth(key)));
+        }
       }
   }
+  if (fwd) shader_sink(a.sc, facc);
 }
 
 __global__ void __launch_bounds__(256) k_fp_resolve(const __grid_constant__ FreePipeArgs a) {
@@ -1808,6 +1839,7 @@ __global__ void __launch_bounds__(256) k_fp_resolve(const __grid_constant__ Free
     prim = (int)(unsigned)(key & 0xFFFFFFFFu);
     depth = __uint_as_float((unsigned)(key >> 32));
     c = shade(a.verts, a.xv, &a.M, a.idx, a.W, a.H, L, prim, 256 * x + 128, 256 * y + 128);
+    if (a.sc.iters && !a.sc.forward) shader_sink(a.sc, shader_work(a.sc.iters, depth));
   }
   reinterpret_cast<float4*>(a.out_rgba)[p] = c;
   a.out_depth[p] = depth;

@@ -139,6 +139,7 @@ struct piko_ctx {
   bool keys_mode = false;                   // inside piko_draw_tile_keys
   int pipeline = PIKO_PIPE_BINNED;
   unsigned long long* fp_keys = nullptr;    // FreePipe full-screen key buffer
+  ShaderCost sc{};                          // pixel-shader complexity knob (NEXT-3)
 
   // profiling: PIKO_NUM_STAGES + 1 boundary events per frame
   bool prof = false;
@@ -236,6 +237,7 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
             cudaMalloc(&ctx->arrive, sizeof(uint32_t) * (size_t)g.NB) == cudaSuccess &&
             cudaMalloc(&ctx->ctl, sizeof(Control)) == cudaSuccess &&
             cudaMalloc(&ctx->primid, sizeof(int32_t) * npx) == cudaSuccess &&
+            cudaMalloc(&ctx->sc.sink, 16) == cudaSuccess &&
             cudaMallocHost(&ctx->h_ctl, sizeof(Control)) == cudaSuccess &&
             cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming) == cudaSuccess;
   ctx->st_scan_n = (g.NB + SCAN_CHUNK - 1) / SCAN_CHUNK;
@@ -269,7 +271,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
                   ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
-                  ctx->all_keys, ctx->fp_keys, ctx->ovq};
+                  ctx->all_keys, ctx->fp_keys, ctx->ovq, ctx->sc.sink};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -408,6 +410,7 @@ static int enqueue_freepipe(piko_ctx* ctx, const float* verts, long long V, cons
   a.cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
   a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
   a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
+  a.sc = ctx->sc;
   if (T > 0) CK(launch_freepipe(a, ctx->pdl, s));
   CK(mark(1 + PIKO_STAGE_SETUP));
   CK(mark(1 + PIKO_STAGE_EXPAND));
@@ -513,6 +516,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   CK(mark(1 + PIKO_STAGE_SORT));
   {
     TileArgs a{};
+    a.sc = ctx->sc;
     a.verts = verts; a.xv = sep ? ctx->xv : nullptr; a.M = M; a.idx = idx;
     a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
     a.g = ctx->g; a.npass = ctx->npass; a.rec = ctx->rec; a.bin_start = ctx->bin_start;
@@ -1078,6 +1082,15 @@ extern "C" int64_t piko_owned_bins(int width, int height, int bin_w, int bin_h, 
   for (int64_t b = rank; b < NB; b += nranks, ++n)
     if (out_bins && n < cap) out_bins[n] = (int32_t)b;
   return n;
+}
+
+extern "C" int piko_set_shader_cost(piko_ctx* ctx, int iters, int forward) {
+  if (!ctx) return PIKO_EINVAL;
+  if (iters < 0 || iters > PIKO_MAX_SHADER_ITERS || (forward != 0 && forward != 1))
+    return ctx->fail(PIKO_EINVAL, "shader cost: 0 <= iters <= PIKO_MAX_SHADER_ITERS, forward 0 or 1");
+  ctx->sc.iters = iters;
+  ctx->sc.forward = forward;
+  return PIKO_OK;
 }
 
 extern "C" int piko_set_pipeline(piko_ctx* ctx, int pipeline) {

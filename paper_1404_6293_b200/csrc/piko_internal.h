@@ -158,6 +158,18 @@ struct RadixArgs {
   int npx;                      // pixels per bin
 };
 
+// Pixel-shader complexity: `iters` extra
+// dependent FMAs per shaded fragment -- forward: every covered fragment that
+// passes the depth range pays them inside the raster loop (the paper's
+// pipelines shade before the depth test); deferred: once per resolved
+// pixel.  The result only reaches `sink` on an impossible branch (it is
+// always >= 0), so images are bit-identical for every setting.
+struct ShaderCost {
+  int iters;                    // 0: off
+  int forward;                  // 1: per fragment, 0: per pixel
+  float* sink;                  // never written in practice (result < 0 only)
+};
+
 struct TileArgs {
   const float* verts;
   const int4* xv;               // null: shade re-transforms corners from verts with M
@@ -190,6 +202,7 @@ struct TileArgs {
   unsigned long long* p2p_flag;         // rank 0's arrival flag of this rank (null: no P2P)
   const unsigned long long* p2p_done;   // rank 0's last resolved epoch
   unsigned long long epoch;             // this frame's exchange epoch (1, 2, ...)
+  ShaderCost sc;
 };
 
 struct ResolveArgs {            // rank 0 after the NCCL gather
@@ -229,6 +242,7 @@ struct FreePipeArgs {
   float* out_rgba;
   float* out_depth;
   int32_t* out_primid;
+  ShaderCost sc;
 };
 
 // ---- launchers (kernels.cu); pdl = programmatic dependent launch -----------

@@ -28,7 +28,7 @@ def env(oracle_lib):
 
 
 def gpu_render(env, s, bw, bh=None, cov=True, partition=None, sync=None, indexed=True,
-               pipeline=None, frames=1):
+               pipeline=None, frames=1, shader=None):
     piko, _, torch = env
     bh = bw if bh is None else bh
     dev = torch.device("cuda:0")
@@ -45,6 +45,8 @@ def gpu_render(env, s, bw, bh=None, cov=True, partition=None, sync=None, indexed
         piko.piko_set_sync(r.ctx, sync)
     if pipeline is not None:
         piko.piko_set_pipeline(r.ctx, pipeline)
+    if shader is not None:
+        piko.piko_set_shader_cost(r.ctx, *shader)
     for _ in range(frames):
         r.draw(verts, idx, s.mvp, s.light, indexed=indexed)
     torch.cuda.synchronize()
@@ -417,3 +419,29 @@ def test_large_triangle_queue_spill_and_fallback(env, T):
     got = gpu_render(env, s, 64)
     assert_frame_equal(got, oracle_frame(env, s))
     assert_bins_equal(got, env, s, 64)
+
+
+# ------------------------------------------------------------------------------
+# Pixel-shader complexity knob (NEXT-3): extra per-fragment
+# (forward) or per-pixel (deferred) work must leave every output bit unchanged.
+@pytest.mark.parametrize("pipeline", ["binned", "freepipe"])
+@pytest.mark.parametrize("iters,forward", [(64, 1), (64, 0), (1000, 1)])
+def test_shader_cost_output_invariant(env, pipeline, iters, forward):
+    piko = env[0]
+    pl = piko.PIKO_PIPE_BINNED if pipeline == "binned" else piko.PIKO_PIPE_FREEPIPE
+    for s, bw in ((scenes.scene_c1(), 8),
+                  (scenes.scene_soup(20000, 200, 120, seed=23, name="soup", bin_sizes=(16,)), 16)):
+        got = gpu_render(env, s, bw, pipeline=pl, shader=(iters, forward), frames=2)
+        assert_frame_equal(got, oracle_frame(env, s))
+        if pipeline == "binned":
+            assert_bins_equal(got, env, s, bw)
+
+
+def test_shader_cost_rejects_bad_args(env):
+    piko = env[0]
+    r = piko.Renderer(64, 64, 8)
+    for args in ((-1, 0), (piko.PIKO_MAX_SHADER_ITERS + 1, 1), (4, 2)):
+        with pytest.raises(piko.PikoError):
+            piko.piko_set_shader_cost(r.ctx, *args)
+    piko.piko_set_shader_cost(r.ctx, 0, 0)
+    r.close()
