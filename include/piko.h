@@ -62,6 +62,14 @@ enum {
                                 P:1273-1294): one fused kernel, one thread per
                                 triangle, full-screen 64-bit atomicMin keys, a
                                 resolve/shade pass; no bin lists, one GPU.   */
+#define PIKO_PIPE_BASELINE 2 /* Baseline design alternative (sec. 7.1,
+                                P:1160-1164): VS, Rasterizer,
+                                Fragment Shader, Depth Test, Composite as
+                                separate kernels, full-screen bins,
+                                LoadBalance (thread per triangle / fragment),
+                                fragment buffers in HBM between stages (grown
+                                on overflow: PIKO_ECAPACITY + re-issue); no
+                                bin lists, one GPU.                           */
 
 /* piko_set_sync modes */
 #define PIKO_SYNC_CHECKED 0 /* default: piko_draw waits for the frame, checks
@@ -127,9 +135,9 @@ int piko_finish(piko_ctx *ctx);
 /* Select PIKO_SYNC_CHECKED (default) or PIKO_SYNC_ASYNC.                      */
 int piko_set_sync(piko_ctx *ctx, int mode);
 
-/* Select the pipeline (PIKO_PIPE_BINNED or PIKO_PIPE_FREEPIPE).  Outputs are
- * identical; FreePipe produces no bin lists (piko_get_bins -> PIKO_ESTATE)
- * and does not support partitions or communicators (PIKO_ESTATE).            */
+/* Select the pipeline (PIKO_PIPE_BINNED, _FREEPIPE or _BASELINE).  Outputs
+ * are identical; FreePipe and Baseline produce no bin lists (piko_get_bins ->
+ * PIKO_ESTATE) and do not support partitions or communicators (PIKO_ESTATE). */
 int piko_set_pipeline(piko_ctx *ctx, int pipeline);
 
 /* Pixel-shader complexity (the paper's design-space axis, sec. 7.2.1,

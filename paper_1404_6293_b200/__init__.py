@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libpiko.so")
 PIKO_OK, PIKO_EINVAL, PIKO_ENOMEM, PIKO_ECUDA, PIKO_ENCCL, PIKO_ECAPACITY, PIKO_ESTATE = 0, -1, -2, -3, -4, -5, -6
 PIKO_DEBUG_COVERAGE_COUNT = 1
 PIKO_SYNC_CHECKED, PIKO_SYNC_ASYNC = 0, 1
-PIKO_PIPE_BINNED, PIKO_PIPE_FREEPIPE = 0, 1
+PIKO_PIPE_BINNED, PIKO_PIPE_FREEPIPE, PIKO_PIPE_BASELINE = 0, 1, 2
 PIKO_MAX_SHADER_ITERS = 1 << 20
 PIKO_MULTI_SORT_FIRST, PIKO_MULTI_SORT_LAST = 0, 1
 PIKO_XPORT_NCCL, PIKO_XPORT_P2P = 0, 1

@@ -1847,6 +1847,143 @@ __global__ void __launch_bounds__(256) k_fp_resolve(const __grid_constant__ Free
 }
 
 // ---------------------------------------------------------------------------
+// Baseline (NEXT-3 design alternative): the five
+// stages as separate kernels with full-screen bins, each reading its input
+// from and writing its output to off-chip memory.  Rasterizer: thread per
+// triangle, fragments appended to a global buffer (count, warp-aggregated
+// reservation, emit); Fragment Shader: thread per fragment; Depth Test:
+// 64-bit atomicMin per fragment; Composite: the winning fragment of each
+// pixel writes it, then a per-pixel pass writes background and clears the
+// depth buffer.  Same arithmetic as the binned path: bit-identical frames.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool bl_setup(const BaselineArgs& a, long long t, TriEval& ev, int& px0,
+                                         int& py0, int& px1, int& py1) {
+  if (t >= a.n_tris) return false;
+  int vi[3];
+  int4 cv[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    vi[c] = __ldg(a.idx + 3 * t + c);
+    cv[c] = vi[c] < a.xv_cap ? __ldg(a.xv + vi[c]) : make_int4(VX_CULLED, 0, 0, 0);
+  }
+  Tri o;
+  if (!setup_tri(cv[0], cv[1], cv[2], vi[0], vi[1], vi[2], a.W, a.H, o)) return false;
+  const float dx1 = __int2float_rn(o.X1 - o.X0), dy1 = __int2float_rn(o.Y1 - o.Y0);
+  const float dx2 = __int2float_rn(o.X2 - o.X0), dy2 = __int2float_rn(o.Y2 - o.Y0);
+  const float dz1 = __fsub_rn(o.zw1, o.zw0), dz2 = __fsub_rn(o.zw2, o.zw0);
+  const float inv = __frcp_rn(__ll2float_rn(o.area2));
+  RecView r;
+  r.X0 = o.X0; r.Y0 = o.Y0; r.X1 = o.X1; r.Y1 = o.Y1; r.X2 = o.X2; r.Y2 = o.Y2;
+  r.zw0 = o.zw0;
+  r.za = __fmul_rn(__fmaf_rn(dz1, dy2, -__fmul_rn(dz2, dy1)), inv);
+  r.zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
+  r.px0 = o.px0; r.py0 = o.py0; r.px1 = o.px1; r.py1 = o.py1;
+  r.small = o.small;
+  ev = prepare(r);
+  px0 = o.px0; py0 = o.py0; px1 = o.px1; py1 = o.py1;
+  return true;
+}
+
+__global__ void __launch_bounds__(256) k_bl_raster(BaselineArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const long long t = (long long)blockIdx.x * 256 + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  TriEval ev;
+  int px0 = 0, py0 = 0, px1 = -1, py1 = -1;
+  const bool live = bl_setup(a, t, ev, px0, py0, px1, py1);
+  // pass 1: count this triangle's fragments (covered, depth in range)
+  unsigned n = 0;
+  if (live)
+    for (int y = py0; y <= py1; ++y)
+      for (int x = px0; x <= px1; ++x) {
+        bool cov;
+        const u64 key = eval_pre(ev, 256 * x + 128, 256 * y + 128, (int)t, cov);
+        if (a.cov && cov) atomicAdd(&a.cov[(size_t)y * a.W + x], 1u);
+        n += key != CLEAR_KEY;
+      }
+  // one reservation per warp
+  unsigned incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+  u64 base = 0;
+  if (lane == 31 && tot) base = atomicAdd(a.n_frag, (u64)tot);
+  base = __shfl_sync(0xffffffffu, base, 31) + (incl - n);
+  // pass 2: emit (fragments beyond the capacity are counted, not stored)
+  if (n)
+    for (int y = py0; y <= py1; ++y)
+      for (int x = px0; x <= px1; ++x) {
+        bool cov;
+        const u64 key = eval_pre(ev, 256 * x + 128, 256 * y + 128, (int)t, cov);
+        if (key == CLEAR_KEY) continue;
+        if ((long long)base < a.frag_cap) {
+          a.frag_key[base] = key;
+          a.frag_px[base] = (uint32_t)((size_t)y * a.W + x);
+        }
+        ++base;
+      }
+}
+
+__global__ void __launch_bounds__(256) k_bl_fs(BaselineArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  float L[3];
+  normalise_light(a.light, L);
+  const long long n = min((long long)*a.n_frag, a.frag_cap);
+  const int fwd = a.sc.forward ? a.sc.iters : 0;
+  float facc = 0.0f;
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const u64 key = a.frag_key[i];
+    const uint32_t p = a.frag_px[i];
+    const int x = (int)(p % (uint32_t)a.W), y = (int)(p / (uint32_t)a.W);
+    a.frag_rgba[i] = shade(a.verts, a.xv, &a.M, a.idx, a.W, a.H, L, (int)(unsigned)(key & 0xFFFFFFFFu),
+                           256 * x + 128, 256 * y + 128);
+    if (fwd) facc = __fadd_rn(facc, shader_work(fwd, key_depth(key)));
+  }
+  if (fwd) shader_sink(a.sc, facc);
+}
+
+__global__ void __launch_bounds__(256) k_bl_depth(BaselineArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const long long n = min((long long)*a.n_frag, a.frag_cap);
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+    atomicMin(&a.keys[a.frag_px[i]], a.frag_key[i]);
+}
+
+__global__ void __launch_bounds__(256) k_bl_composite(BaselineArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const long long n = min((long long)*a.n_frag, a.frag_cap);
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const u64 key = a.frag_key[i];
+    const uint32_t p = a.frag_px[i];
+    if (a.keys[p] != key) continue;  // keys are unique per pixel: one winner
+    reinterpret_cast<float4*>(a.out_rgba)[p] = a.frag_rgba[i];
+    a.out_depth[p] = key_depth(key);
+    a.out_primid[p] = (int)(unsigned)(key & 0xFFFFFFFFu);
+    if (a.sc.iters && !a.sc.forward) shader_sink(a.sc, shader_work(a.sc.iters, key_depth(key)));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bl_clear(BaselineArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const long long p = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (p >= (long long)a.W * a.H) return;
+  if (a.keys[p] == CLEAR_KEY) {
+    reinterpret_cast<float4*>(a.out_rgba)[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+    a.out_depth[p] = 1.0f;
+    a.out_primid[p] = -1;
+  }
+  a.keys[p] = CLEAR_KEY;  // ready for the next frame
+}
+
+// ---------------------------------------------------------------------------
 // K7 (multi-GPU rank 0): resolve gathered tile keys -> shaded frame
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_resolve(const __grid_constant__ ResolveArgs a) {
@@ -2013,6 +2150,21 @@ cudaError_t launch_freepipe(const FreePipeArgs& a, bool pdl, cudaStream_t s) {
 cudaError_t launch_fp_resolve(const FreePipeArgs& a, bool pdl, cudaStream_t s) {
   const long long grid = ((long long)a.W * a.H + 255) / 256;
   return launch_ex(k_fp_resolve, (int)grid, 256, 0, pdl, s, a);
+}
+
+// Baseline stages: 0 raster, 1 fragment shader, 2 depth test, 3 composite
+// (winners), 4 composite (background + depth-buffer clear)
+cudaError_t launch_baseline(const BaselineArgs& a, int stage, bool pdl, cudaStream_t s) {
+  const long long npx = (long long)a.W * a.H;
+  const int frag_grid = 16 * sm_count();  // grid-stride over the device-side count
+  switch (stage) {
+    case 0: return launch_ex(k_bl_raster, (int)std::max<long long>((a.n_tris + 255) / 256, 1), 256, 0, pdl, s, a);
+    case 1: return launch_ex(k_bl_fs, frag_grid, 256, 0, pdl, s, a);
+    case 2: return launch_ex(k_bl_depth, frag_grid, 256, 0, pdl, s, a);
+    case 3: return launch_ex(k_bl_composite, frag_grid, 256, 0, pdl, s, a);
+    case 4: return launch_ex(k_bl_clear, (int)((npx + 255) / 256), 256, 0, pdl, s, a);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s) {

@@ -140,6 +140,12 @@ struct piko_ctx {
   int pipeline = PIKO_PIPE_BINNED;
   unsigned long long* fp_keys = nullptr;    // FreePipe full-screen key buffer
   ShaderCost sc{};                          // pixel-shader complexity knob (NEXT-3)
+  // Baseline pipeline (NEXT-3): full-screen depth buffer + fragment buffers
+  unsigned long long* bl_keys = nullptr;    // [H][W]
+  unsigned long long* frag_key = nullptr;   // [bl_cap]
+  uint32_t* frag_px = nullptr;
+  float4* frag_rgba = nullptr;
+  long long bl_cap = 0;                     // Baseline fragment capacity
 
   // profiling: PIKO_NUM_STAGES + 1 boundary events per frame
   bool prof = false;
@@ -271,7 +277,8 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
                   ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
-                  ctx->all_keys, ctx->fp_keys, ctx->ovq, ctx->sc.sink};
+                  ctx->all_keys, ctx->fp_keys, ctx->ovq, ctx->sc.sink, ctx->bl_keys, ctx->frag_key,
+                  ctx->frag_px, ctx->frag_rgba};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -353,6 +360,7 @@ static int ensure_pairs(piko_ctx* ctx, unsigned long long P) {
 // 32 B vertices) wins when vertices are barely shared (soups: V ~ 3T) and for
 // piko_draw without a vertex count (no k_index_max + k_vertex launches).
 static bool separate_vs(const piko_ctx* ctx, long long V, long long T) {
+  if (ctx->pipeline == PIKO_PIPE_BASELINE) return true;  // VS is its own stage
   if (ctx->vs_mode >= 0) return ctx->vs_mode == 1;
   return V >= 0 && 2 * V <= 3 * T;
 }
@@ -432,11 +440,86 @@ static int enqueue_freepipe(piko_ctx* ctx, const float* verts, long long V, cons
   return PIKO_OK;
 }
 
+// fragment buffers of the Baseline pipeline for n fragments
+static int ensure_frags(piko_ctx* ctx, long long n) {
+  if (n <= ctx->bl_cap) return PIKO_OK;
+  cudaFree(ctx->frag_key); cudaFree(ctx->frag_px); cudaFree(ctx->frag_rgba);
+  ctx->frag_key = nullptr; ctx->frag_px = nullptr; ctx->frag_rgba = nullptr; ctx->bl_cap = 0;
+  const long long cap = std::max<long long>(n + n / 4, 1 << 16);
+  CK(cudaMalloc(&ctx->frag_key, sizeof(unsigned long long) * cap));
+  CK(cudaMalloc(&ctx->frag_px, sizeof(uint32_t) * cap));
+  CK(cudaMalloc(&ctx->frag_rgba, sizeof(float4) * cap));
+  ctx->bl_cap = cap;
+  return PIKO_OK;
+}
+
+// Baseline: VS, Rasterizer, Fragment Shader, Depth Test,
+// Composite as separate kernels with off-chip buffers between them.  Profiling
+// stages: VERTEX = VS, SETUP = Rasterizer, EXPAND = Fragment Shader, SORT =
+// Depth Test, TILE = Composite.  The fragment count is read back by
+// check_frame; a frame that overflowed the buffers is grown and re-issued.
+static int enqueue_baseline(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
+                            long long T, const Mat4& M, const float L[3], float* rgba, float* depth,
+                            cudaStream_t s) {
+  cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
+  auto mark = [&](int stage) -> cudaError_t { return ev ? cudaEventRecord(ev[stage], s) : cudaSuccess; };
+  const size_t npx = (size_t)ctx->g.W * ctx->g.H;
+  CK(mark(0));
+  if (!ctx->bl_keys) {
+    CK(cudaMalloc(&ctx->bl_keys, sizeof(unsigned long long) * npx));
+    CK(cudaMemsetAsync(ctx->bl_keys, 0xFF, sizeof(unsigned long long) * npx, s));
+  }
+  int rc = ensure_frags(ctx, std::max<long long>(4ll * (long long)npx, 2 * T));
+  if (rc != PIKO_OK) return rc;
+  if (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) CK(cudaMemsetAsync(ctx->cov, 0, sizeof(uint32_t) * npx, s));
+  // clean control block (the fragment count lives in n_pairs)
+  CK(cudaMemsetAsync(ctx->ctl, 0, offsetof(Control, vx_overflow), s));
+  CK(cudaMemsetAsync(&ctx->ctl->n_pairs, 0, sizeof(unsigned long long) * 2, s));
+  CK(mark(1 + PIKO_STAGE_CLEAR));
+  ctx->last_kernels = 6 + (V < 0 && T > 0 ? 1 : 0);
+  CK(cudaMemsetAsync(&ctx->ctl->vmax, 0, 2 * sizeof(unsigned), s));
+  if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
+  VertexArgs va{};
+  va.verts = verts; va.n_verts = T > 0 ? V : 0; va.cap = ctx->xv_cap; va.ctl = ctx->ctl; va.M = M;
+  va.W = ctx->g.W; va.H = ctx->g.H; va.xv = ctx->xv;
+  CK(launch_vertex(va, ctx->pdl, s));
+  CK(mark(1 + PIKO_STAGE_VERTEX));
+  BaselineArgs a{};
+  a.verts = verts; a.xv = ctx->xv; a.xv_cap = ctx->xv_cap; a.M = M; a.idx = idx; a.n_tris = T;
+  a.W = ctx->g.W; a.H = ctx->g.H;
+  a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
+  a.keys = ctx->bl_keys; a.frag_key = ctx->frag_key; a.frag_px = ctx->frag_px;
+  a.frag_rgba = ctx->frag_rgba; a.frag_cap = ctx->bl_cap; a.n_frag = &ctx->ctl->n_pairs;
+  a.cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
+  a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
+  a.sc = ctx->sc;
+  CK(launch_baseline(a, 0, ctx->pdl, s));
+  CK(mark(1 + PIKO_STAGE_SETUP));
+  CK(launch_baseline(a, 1, ctx->pdl, s));
+  CK(mark(1 + PIKO_STAGE_EXPAND));
+  CK(launch_baseline(a, 2, ctx->pdl, s));
+  CK(mark(1 + PIKO_STAGE_SORT));
+  CK(launch_baseline(a, 3, ctx->pdl, s));
+  CK(launch_baseline(a, 4, ctx->pdl, s));
+  CK(mark(1 + PIKO_STAGE_TILE));
+  CK(mark(1 + PIKO_STAGE_GATHER));
+  CK(mark(1 + PIKO_STAGE_RESOLVE));
+  if (ev) ++ctx->prof_frames;
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(ctx->done, s));
+  ctx->pending = true;
+  ctx->last_T = T;
+  ctx->need_reset = true;  // the binned path must not trust tickets touched here
+  return PIKO_OK;
+}
+
 static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
                          long long T, const Mat4& M, const float L[3], float* rgba, float* depth,
                          cudaStream_t s, unsigned long long* keys_out = nullptr) {
   if (ctx->pipeline == PIKO_PIPE_FREEPIPE)
     return enqueue_freepipe(ctx, verts, V, idx, T, M, L, rgba, depth, s);
+  if (ctx->pipeline == PIKO_PIPE_BASELINE)
+    return enqueue_baseline(ctx, verts, V, idx, T, M, L, rgba, depth, s);
   const bool gather = keys_out == nullptr && exchanging(ctx);
   const bool p2p = gather && ctx->p2p_keys != nullptr;
   const size_t tile_px = (size_t)ctx->bw * ctx->bh;
@@ -636,6 +719,14 @@ static int check_frame(piko_ctx* ctx) {
     ctx->fail(PIKO_ENCCL, "P2P exchange: a peer flag wait timed out");
     return ctx->last_status;
   }
+  if (ctx->pipeline == PIKO_PIPE_BASELINE &&
+      ((long long)ctx->h_ctl->n_pairs > ctx->bl_cap || ctx->h_ctl->vx_overflow)) {
+    int rc = ensure_frags(ctx, (long long)ctx->h_ctl->n_pairs);
+    if (rc == PIKO_OK) rc = ensure_verts(ctx, (long long)ctx->h_ctl->vx_need);
+    ctx->last_status = rc != PIKO_OK ? rc : PIKO_ECAPACITY;
+    if (rc == PIKO_OK) ctx->fail(PIKO_ECAPACITY, "fragment capacity exceeded (%llu); grown", ctx->h_ctl->n_pairs);
+    return ctx->last_status;
+  }
   if (ctx->h_ctl->overflow_tag == ctx->h_ctl->frame + 1 || ctx->h_ctl->vx_overflow) {
     int rc = ensure_pairs(ctx, ctx->h_ctl->n_pairs);
     if (rc == PIKO_OK) rc = ensure_verts(ctx, (long long)ctx->h_ctl->vx_need);
@@ -799,7 +890,7 @@ extern "C" int piko_get_bins(const piko_ctx* cctx, const int32_t** d_bin_start,
                              const int32_t** d_bin_prims, int64_t* n_pairs) {
   piko_ctx* ctx = const_cast<piko_ctx*>(cctx);
   if (!ctx || !d_bin_start || !d_bin_prims || !n_pairs) return PIKO_EINVAL;
-  if (ctx->pipeline != PIKO_PIPE_BINNED) return ctx->fail(PIKO_ESTATE, "no bin lists in FreePipe");
+  if (ctx->pipeline != PIKO_PIPE_BINNED) return ctx->fail(PIKO_ESTATE, "no bin lists outside the binned pipeline");
   int rc = check_frame(ctx);
   if (rc != PIKO_OK) return rc;
   *d_bin_start = ctx->bin_start;
@@ -1095,10 +1186,10 @@ extern "C" int piko_set_shader_cost(piko_ctx* ctx, int iters, int forward) {
 
 extern "C" int piko_set_pipeline(piko_ctx* ctx, int pipeline) {
   if (!ctx) return PIKO_EINVAL;
-  if (pipeline != PIKO_PIPE_BINNED && pipeline != PIKO_PIPE_FREEPIPE)
+  if (pipeline != PIKO_PIPE_BINNED && pipeline != PIKO_PIPE_FREEPIPE && pipeline != PIKO_PIPE_BASELINE)
     return ctx->fail(PIKO_EINVAL, "unknown pipeline");
-  if (pipeline == PIKO_PIPE_FREEPIPE && ctx->mnranks > 1)
-    return ctx->fail(PIKO_ESTATE, "FreePipe renders the whole screen on one GPU");
+  if (pipeline != PIKO_PIPE_BINNED && ctx->mnranks > 1)
+    return ctx->fail(PIKO_ESTATE, "FreePipe and Baseline render the whole screen on one GPU");
   if (ctx->pending) check_frame(ctx);
   ctx->pipeline = pipeline;
   ctx->need_reset = true;

@@ -245,7 +245,34 @@ struct FreePipeArgs {
   ShaderCost sc;
 };
 
+// Baseline design alternative (sec. 7.1,
+// P:404-410): one kernel per stage of VS -> Rasterizer -> Fragment Shader ->
+// Depth Test -> Composite with full-screen bins and LoadBalance (thread per
+// primitive / per fragment), every stage reading and writing off-chip memory.
+struct BaselineArgs {
+  const float* verts;
+  const int4* xv;               // vertex-stage records (the VS kernel always runs)
+  long long xv_cap;
+  Mat4 M;
+  const int32_t* idx;
+  long long n_tris;
+  int W, H;
+  float light[3];
+  unsigned long long* keys;      // [H][W] depth buffer, CLEAR between frames
+  unsigned long long* frag_key;  // [frag_cap] fragment (depth, primID) keys
+  uint32_t* frag_px;             // [frag_cap] fragment pixel index y*W + x
+  float4* frag_rgba;             // [frag_cap] shaded fragment colours
+  long long frag_cap;
+  unsigned long long* n_frag;    // fragments emitted this frame (may exceed frag_cap)
+  uint32_t* cov;                 // debug coverage counts or null
+  float* out_rgba;
+  float* out_depth;
+  int32_t* out_primid;
+  ShaderCost sc;
+};
+
 // ---- launchers (kernels.cu); pdl = programmatic dependent launch -----------
+cudaError_t launch_baseline(const BaselineArgs& a, int stage, bool pdl, cudaStream_t s);
 cudaError_t launch_freepipe(const FreePipeArgs& a, bool pdl, cudaStream_t s);
 cudaError_t launch_fp_resolve(const FreePipeArgs& a, bool pdl, cudaStream_t s);
 cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool pdl, cudaStream_t s);

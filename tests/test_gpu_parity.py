@@ -424,11 +424,12 @@ def test_large_triangle_queue_spill_and_fallback(env, T):
 # ------------------------------------------------------------------------------
 # Pixel-shader complexity knob (NEXT-3): extra per-fragment
 # (forward) or per-pixel (deferred) work must leave every output bit unchanged.
-@pytest.mark.parametrize("pipeline", ["binned", "freepipe"])
+@pytest.mark.parametrize("pipeline", ["binned", "freepipe", "baseline"])
 @pytest.mark.parametrize("iters,forward", [(64, 1), (64, 0), (1000, 1)])
 def test_shader_cost_output_invariant(env, pipeline, iters, forward):
     piko = env[0]
-    pl = piko.PIKO_PIPE_BINNED if pipeline == "binned" else piko.PIKO_PIPE_FREEPIPE
+    pl = {"binned": piko.PIKO_PIPE_BINNED, "freepipe": piko.PIKO_PIPE_FREEPIPE,
+          "baseline": piko.PIKO_PIPE_BASELINE}[pipeline]
     for s, bw in ((scenes.scene_c1(), 8),
                   (scenes.scene_soup(20000, 200, 120, seed=23, name="soup", bin_sizes=(16,)), 16)):
         got = gpu_render(env, s, bw, pipeline=pl, shader=(iters, forward), frames=2)
@@ -445,3 +446,35 @@ def test_shader_cost_rejects_bad_args(env):
             piko.piko_set_shader_cost(r.ctx, *args)
     piko.piko_set_shader_cost(r.ctx, 0, 0)
     r.close()
+
+
+# ------------------------------------------------------------------------------
+# Baseline design alternative (NEXT-3): one kernel per stage with
+# fragment buffers in HBM -- the same frame, bit for bit.
+@pytest.mark.parametrize("indexed", [True, False])
+def test_baseline_pipeline(env, indexed):
+    piko = env[0]
+    for s, bw in ((scenes.scene_c1(), 8),
+                  (scenes.scene_soup(20000, 200, 120, seed=29, name="soup", bin_sizes=(16,)), 16),
+                  (scenes.scene_c2(), 16)):
+        got = gpu_render(env, s, bw, pipeline=piko.PIKO_PIPE_BASELINE, indexed=indexed, frames=2)
+        assert_frame_equal(got, oracle_frame(env, s))
+
+
+def test_baseline_fragment_overflow_regrows(env):
+    """Depth complexity 64 on 64x64 (131072 fragments against an initial
+    capacity of 4 W H = 16384): the checked draw grows the fragment buffers
+    and re-issues; the frame matches the oracle."""
+    from tests.helpers import pixel_scene
+    piko = env[0]
+    rng = np.random.default_rng(31)
+    tris, zw = [], []
+    for k in range(64):
+        tris.append([(-8.0, -8.0), (140.0, -8.0), (-8.0, 140.0)] if k % 2 else
+                    [(72.0, 72.0), (-76.0, 72.0), (72.0, -76.0)])
+        zw.append(float(rng.uniform(0.1, 0.9)))
+    verts, idx, mvp = pixel_scene(tris, zw, 64, 64)
+    s = scenes.Scene("stack", 64, 64, (8,), verts, idx, mvp)
+    got = gpu_render(env, s, 8, pipeline=piko.PIKO_PIPE_BASELINE)
+    assert got["stats"]["n_pairs"] == 64 * 64 * 64  # both triangles cover every pixel centre
+    assert_frame_equal(got, oracle_frame(env, s))

@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Pixel-shader complexity sweep (the paper's sec. 7.2.1 axis, P:1281-1294;
 SURVEY 8(f) NEXT-3): ms/frame of the binned pipeline (LoadBalance: per-bin
-CTAs) and of FreePipe (DirectMap: the triangle's own thread) as the per-fragment
+CTAs), of FreePipe (DirectMap: the triangle's own thread) and of Baseline
+(LoadBalance, one kernel per stage, fragments in HBM) as the per-fragment
 shader cost grows, forward (every covered fragment pays, the paper's order:
 shade before the depth test) and deferred (once per resolved pixel).
 Protocol as tools/sweep.py (inputs in HBM, L2 flushed before each frame outside
@@ -27,7 +28,7 @@ for cfg in cfgs:
     s = scenes.make(cfg)
     v = torch.from_numpy(s.verts).cuda()
     i = torch.from_numpy(s.idx).cuda()
-    for pipe in (piko.PIKO_PIPE_BINNED, piko.PIKO_PIPE_FREEPIPE):
+    for pipe in (piko.PIKO_PIPE_BINNED, piko.PIKO_PIPE_FREEPIPE, piko.PIKO_PIPE_BASELINE):
         r = piko.Renderer(s.W, s.H, 16)
         piko.piko_set_pipeline(r.ctx, pipe)
         for it in iters_list:
@@ -48,18 +49,19 @@ for cfg in cfgs:
                 torch.cuda.synchronize()
                 assert piko.piko_finish(r.ctx) == 0
                 ms = sorted(a.elapsed_time(b) for a, b in ev)[steps // 2]
-                res.append({"config": cfg, "pipeline": "freepipe" if pipe else "binned",
+                res.append({"config": cfg, "pipeline": ("binned", "freepipe", "baseline")[pipe],
                             "shader_iters": it, "shading": "forward" if fwd else "deferred",
                             "median_ms": ms})
                 print(res[-1], flush=True)
         r.close()
 json.dump(res, open(os.path.join(ROOT, "profiles", f"shader_sweep_{tag}.json"), "w"), indent=1)
-print("| config | shading | iters | binned ms | FreePipe ms | FreePipe / binned |")
-print("|---|---|---|---|---|---|")
+print("| config | shading | iters | binned ms | FreePipe ms | Baseline ms | FreePipe / binned | Baseline / binned |")
+print("|---|---|---|---|---|---|---|---|")
 for x in res:
     if x["pipeline"] != "binned":
         continue
-    f = next(y for y in res if y["pipeline"] == "freepipe" and y["config"] == x["config"]
-             and y["shader_iters"] == x["shader_iters"] and y["shading"] == x["shading"])
+    o = {y["pipeline"]: y["median_ms"] for y in res if y["config"] == x["config"]
+         and y["shader_iters"] == x["shader_iters"] and y["shading"] == x["shading"]}
     print(f"| {x['config']} | {x['shading'] if x['shader_iters'] else '-'} | {x['shader_iters']} | "
-          f"{x['median_ms']:.3f} | {f['median_ms']:.3f} | {f['median_ms'] / x['median_ms']:.2f} |")
+          f"{x['median_ms']:.3f} | {o['freepipe']:.3f} | {o['baseline']:.3f} | "
+          f"{o['freepipe'] / x['median_ms']:.2f} | {o['baseline'] / x['median_ms']:.2f} |")
