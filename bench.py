@@ -272,26 +272,31 @@ def run_piko(args):
     # same protocol; reported beside the binned headline (1 GPU only)
     variants = {}
     if world == 1:
-        piko.piko_set_pipeline(r.ctx, piko.PIKO_PIPE_FREEPIPE)
-        piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_CHECKED)
-        for _ in range(max(args.warmup, 3)):
-            r.draw(verts, idx, s.mvp, s.light, stream)
-        piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
-        fe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
-        torch.cuda.synchronize(dev)
-        for k in range(args.steps):
-            flush.fill_(float(k))
-            fe[k][0].record(stream)
-            r.draw(verts, idx, s.mvp, s.light, stream)
-            fe[k][1].record(stream)
-        torch.cuda.synchronize(dev)
-        fms = sum(a.elapsed_time(b) for a, b in fe) / args.steps
-        variants["freepipe"] = {"ms_per_step": fms, "value": s.n_tris / (fms / 1e3) / 1e6, "unit": UNIT,
-                                "what": "sec. 7.2.1 FreePipe: 1 fused kernel, thread per triangle, "
-                                        "global 64-bit atomicMin + resolve; no bins"}
+        what = {piko.PIKO_PIPE_FREEPIPE: ("freepipe", "sec. 7.2.1 FreePipe: 1 fused kernel, thread per triangle, "
+                                                      "global 64-bit atomicMin + resolve; no bins"),
+                piko.PIKO_PIPE_BASELINE: ("baseline", "sec. 7.1 Baseline: VS, Rasterizer, Fragment Shader, Depth "
+                                                      "Test, Composite as separate kernels, fragments in HBM; no bins")}
+        for pipe, (name, desc) in what.items():
+            piko.piko_set_pipeline(r.ctx, pipe)
+            piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_CHECKED)
+            for _ in range(max(args.warmup, 3)):
+                r.draw(verts, idx, s.mvp, s.light, stream)
+            piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
+            fe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+            torch.cuda.synchronize(dev)
+            for k in range(args.steps):
+                flush.fill_(float(k))
+                fe[k][0].record(stream)
+                r.draw(verts, idx, s.mvp, s.light, stream)
+                fe[k][1].record(stream)
+            torch.cuda.synchronize(dev)
+            fms = sum(a.elapsed_time(b) for a, b in fe) / args.steps
+            variants[name] = {"ms_per_step": fms, "value": s.n_tris / (fms / 1e3) / 1e6, "unit": UNIT,
+                              "what": desc}
+            piko.piko_finish(r.ctx)
         piko.piko_set_pipeline(r.ctx, piko.PIKO_PIPE_BINNED)
-        piko.piko_finish(r.ctx)
+        piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_CHECKED)
 
     # end-to-end through the public host-buffer call (H2D + frame + D2H per step)
     e2e = None
