@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(VX_THREADS) k_vertex(VertexArgs a) {
     if (V > a.cap) a.ctl->vx_overflow = 1;
   }
   V = V < a.cap ? V : a.cap;
-  constexpr int VPT = 4;  // vertices per thread, loads issued together
+  constexpr int VPT = VX_VPT;
   for (long long v0 = (long long)blockIdx.x * VX_THREADS * VPT + threadIdx.x; v0 < V;
        v0 += (long long)gridDim.x * VX_THREADS * VPT) {
     float4 p[VPT];
@@ -2064,7 +2064,7 @@ static int sm_count() {
 
 cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s) {
   // known count: one thread per vertex; unknown (device-side count): persistent
-  const long long want = a.n_verts >= 0 ? (a.n_verts + 4 * VX_THREADS - 1) / (4 * VX_THREADS) : 8ll * sm_count();
+  const long long want = a.n_verts >= 0 ? (a.n_verts + VX_VPT * VX_THREADS - 1) / (VX_VPT * VX_THREADS) : 8ll * sm_count();
   return launch_ex(k_vertex, (int)(want > 0 ? want : 1), VX_THREADS, 0, pdl, s, a);
 }
 

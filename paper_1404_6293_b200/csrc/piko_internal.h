@@ -98,6 +98,10 @@ constexpr int REC_SMALL = 1;
 // bits(zw), bits(rw); X == VX_CULLED marks a corner that culls its triangles.
 constexpr int VX_CULLED = (int)0x80000000;
 constexpr int VX_THREADS = 256;
+#ifndef PIKO_VX_VPT
+#define PIKO_VX_VPT 4
+#endif
+constexpr int VX_VPT = PIKO_VX_VPT;             // vertices per k_vertex thread (loads issued together)
 
 struct VertexArgs {
   const float* verts;
