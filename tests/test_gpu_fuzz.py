@@ -1,4 +1,4 @@
-"""Randomised differential test: the CUDA path (binned and FreePipe, through
+"""Randomised differential test: the CUDA path (binned, FreePipe and Baseline, through
 the C ABI) against the CPU oracle on seeded random small scenes
 (scenes.scene_fuzz: random screens and bin shapes, tiny / covering / sliver /
 degenerate / off-screen / guard-band / behind-camera / non-finite triangles,
@@ -25,13 +25,14 @@ def test_fuzz_generator_is_deterministic_and_varied():
 
 
 @pytest.mark.parametrize("seed", SEEDS)
-def test_fuzz_binned_and_freepipe_match_oracle(env, seed):
+def test_fuzz_all_pipelines_match_oracle(env, seed):
     piko, oracle_lib, _ = env
     s = scenes.scene_fuzz(seed)
     bw, bh = s.bin_sizes
     ref = oracle_frame(env, s)
     start, prims = oracle_lib.bins(s.verts, s.idx, s.mvp, s.W, s.H, bw, bh)
-    for pipeline, indexed in ((None, seed % 2 == 0), (piko.PIKO_PIPE_FREEPIPE, True)):
+    for pipeline, indexed in ((None, seed % 2 == 0), (piko.PIKO_PIPE_FREEPIPE, True),
+                              (piko.PIKO_PIPE_BASELINE, seed % 2 == 1)):
         got = gpu_render(env, s, bw, bh, pipeline=pipeline, indexed=indexed)
         tag = f"seed {seed} ({s.W}x{s.H}, bins {bw}x{bh}, T={s.n_tris}, pipeline {pipeline})"
         assert np.array_equal(got["primid"], ref["primid"]), tag
