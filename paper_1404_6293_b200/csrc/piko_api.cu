@@ -311,6 +311,17 @@ static int ensure_tris(piko_ctx* ctx, long long T) {
 
 // look-back status words: enough chunks for the expand pass (>= 256 triangles
 // per chunk) and for the pair passes
+static long long rx_slots() {  // radix CTAs resident at once
+  static long long slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    slots = (long long)RX_MIN_CTAS * (sms > 0 ? sms : 148);
+  }
+  return slots;
+}
+
 static int alloc_rx_status(piko_ctx* ctx) {
   const long long chunks = std::max<long long>(
       std::max<long long>((ctx->rec_cap + RX_THREADS - 1) / RX_THREADS,
@@ -703,7 +714,16 @@ static void adapt_tri_chunk(piko_ctx* ctx) {
   // aggregate is then published late it stalls the look-back of every later
   // chunk.  Any multiple of RX_THREADS works (tpt = tri_chunk / RX_THREADS).
   const double want = P > 0 ? 0.75 * RX_CHUNK * T / P : (double)EX_MAX_TRIS;
-  const long long tc = (long long)(want / RX_THREADS) * RX_THREADS;
+  long long tc = (long long)(want / RX_THREADS) * RX_THREADS;
+#ifndef PIKO_NO_WAVE_CHUNKS
+  // Frames with few triangles: shrink chunks while every chunk still fits in
+  // one wave of resident radix CTAs.  Smaller chunks finish sooner and are
+  // less likely to exceed RX_CHUNK where the pairs per triangle vary a lot
+  // (c2: near spheres' triangles cover several bins, far ones one).
+  const long long slots = rx_slots();
+  const long long per_wave = ((long long)T + slots - 1) / slots;
+  tc = std::min<long long>(tc, (per_wave + RX_THREADS - 1) / RX_THREADS * RX_THREADS);
+#endif
   ctx->tri_chunk = (int)std::max<long long>(RX_THREADS, std::min<long long>(EX_MAX_TRIS, tc));
 }
 

@@ -72,7 +72,7 @@ print("   expand detail: loads+counts median %.0f, scan %.0f, expansion %.0f, re
     np.median(e[:, 1] - e[:, 7])))
 lb = np.zeros((2, 8192, 8), np.uint64)
 if h.piko_dbg_rx_lb(lb.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(lb.nbytes)) == 0:
-    for p_, n_ in ((0, nrx0), (1, (st["n_pairs"] + 4095) // 4096)):
+    for p_, n_ in ((0, nrx0), (1, int((buf[2, :8000, 0] > 0).sum()))):
         tt = buf[1 + p_, :n_].astype(np.int64)
         ll = lb[p_, :n_].astype(np.int64)
         ok = (tt[:, 2] > 0) & (ll[:, 0] > 0)
@@ -94,7 +94,7 @@ if h.piko_dbg_rx_lb(lb.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(lb.nbyte
             print(f"      -> arrival atomic done {np.median(a1):.0f} (p90 {np.percentile(a1, 90):.0f}),"
                   f" group loads {np.median(a2):.0f} (p90 {np.percentile(a2, 90):.0f}),"
                   f" read-check-store {np.median(a3):.0f} (p90 {np.percentile(a3, 90):.0f})")
-nrx = (st["n_pairs"] + 4095) // 4096
+nrx = int((buf[2, :8000, 0] > 0).sum())
 show("radix pass 1", buf[2], ["start", "load", "rank", "lookback", "scatter"], nrx)
 nb = st["owned_bins"]
 t = buf[3, :min(nb, 8192)].astype(np.int64)
