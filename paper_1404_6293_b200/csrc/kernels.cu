@@ -1209,6 +1209,11 @@ __device__ __forceinline__ void normalise_light(const float in[3], float L[3]) {
 }
 
 constexpr int TINY_AREA = 4;    // clipped rect area a thread rasterizes alone
+#ifndef PIKO_QSEG
+#define PIKO_QSEG 4
+#endif
+constexpr int QSEG = PIKO_QSEG; // queued triangles: pixels of a row per work item (amortises
+                                // the item search and the evaluator loads)
 constexpr int NSTAGE = 3;       // setup-record pipeline depth (rounds in flight per warp)
 constexpr int TQ = NSTAGE + 2;  // primIDs are fetched two rounds before their records
 
@@ -1493,9 +1498,9 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
             Q.A2[slot] = ev.A2; Q.B2[slot] = ev.B2; Q.K1[slot] = ev.K1; Q.K2[slot] = ev.K2;
             Q.thr[slot] = (ev.thr0 ? 1 : 0) | (ev.thr1 ? 2 : 0) | (ev.thr2 ? 4 : 0) | (ev.small ? 8 : 0);
             Q.zw0[slot] = ev.zw0; Q.za[slot] = ev.za; Q.zb[slot] = ev.zb;
-            Q.invw[slot] = __frcp_rn((float)w);
+            Q.invw[slot] = __frcp_rn((float)((w + QSEG - 1) / QSEG));  // 1 / segments per row
             Q.t[slot] = t_cur; Q.rx0[slot] = rx0; Q.ry0[slot] = ry0; Q.w[slot] = w;
-            Q.pre[slot] = (unsigned)area;  // turned into the prefix at the end of the bin
+            Q.pre[slot] = (unsigned)(h * ((w + QSEG - 1) / QSEG));  // segments; prefix at the end of the bin
             area = 0;
           } else if (a.ovq && slot - TileSmem<BW, BH, THREADS>::BIGQ < OVQ_CAP) {
             // queue full: spill the prepared entry to this CTA's global overflow
@@ -1508,8 +1513,8 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
             q[1] = make_int4(ev.A1, ev.B1, ev.A2, ev.B2);
             q[2] = make_int4((int)(unsigned)ev.K1, (int)(ev.K1 >> 32), (int)(unsigned)ev.K2, (int)(ev.K2 >> 32));
             q[3] = make_int4(thr, __float_as_int(ev.zw0), __float_as_int(ev.za), __float_as_int(ev.zb));
-            q[4] = make_int4(__float_as_int(__frcp_rn((float)w)), t_cur, rx0, ry0);
-            q[5] = make_int4(w, area, 0, 0);
+            q[4] = make_int4(__float_as_int(__frcp_rn((float)((w + QSEG - 1) / QSEG))), t_cur, rx0, ry0);
+            q[5] = make_int4(w, h * ((w + QSEG - 1) / QSEG), 0, 0);
             area = 0;
           }  // both full: this one takes the warp-cooperative path
         }
@@ -1588,7 +1593,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
         // warp-contiguous items.  qw = the entry holding the warp's first item
         // (monotone): lanes load the next 32 entry starts and a ballot advances
         // qw (pre is strictly increasing, so the mask is a prefix).  Every
-        // entry covers >= TINY_AREA + 1 items, so the warp's 32 items lie in
+        // entry covers >= 1 item (a row segment of <= QSEG pixels), so the warp's 32 items lie in
         // entries qw .. qw+31 and each lane finds its own with a 5-step shuffle
         // search over the loaded starts -- no serial per-warp search.
         int qw = 0;
@@ -1614,10 +1619,11 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
           if (i >= tot) continue;
           const int q = qw + c;
           const unsigned off = i - Q.pre[q];
-          const int wq = Q.w[q];
+          const int wq = Q.w[q], spr = (wq + QSEG - 1) / QSEG;
           const int row = __float2int_rz(((float)off + 0.5f) * Q.invw[q]);  // exact: off < 2^12
-          const int col = (int)off - row * wq;
-          const int x = Q.rx0[q] + col, y = Q.ry0[q] + row;
+          const int seg = (int)off - row * spr;
+          const int xs = Q.rx0[q] + seg * QSEG, y = Q.ry0[q] + row;
+          const int nseg = min(QSEG, wq - seg * QSEG);  // pixels of this segment
           TriEval ev;
           ev.X0 = Q.X0[q]; ev.Y0 = Q.Y0[q];
           ev.A0 = Q.A0[q]; ev.B0 = Q.B0[q]; ev.A1 = Q.A1[q]; ev.B1 = Q.B1[q];
@@ -1626,13 +1632,19 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
           ev.thr0 = (th & 1) ? -1 : 0; ev.thr1 = (th & 2) ? -1 : 0; ev.thr2 = (th & 4) ? -1 : 0;
           ev.small = (th >> 3) & 1;
           ev.zw0 = Q.zw0[q]; ev.za = Q.za[q]; ev.zb = Q.zb[q];
-          bool cov;
-          const u64 key = eval_pre(ev, 256 * x + 128, 256 * y + 128, Q.t[q], cov);
-          const int p = (y - y0) * BW + (x - x0);
-          if (COV && cov) atomicAdd(&s_cov[p], 1u);
-          if (key != CLEAR_KEY) {
-            atomicMin(&sm.key[p], key);
-            if (fwd) facc = __fadd_rn(facc, shader_work(fwd, key_depth(key)));
+          const int tq = Q.t[q];
+#pragma unroll
+          for (int u = 0; u < QSEG; ++u) {
+            if (u >= nseg) break;
+            const int x = xs + u;
+            bool cov;
+            const u64 key = eval_pre(ev, 256 * x + 128, 256 * y + 128, tq, cov);
+            const int p = (y - y0) * BW + (x - x0);
+            if (COV && cov) atomicAdd(&s_cov[p], 1u);
+            if (key != CLEAR_KEY) {
+              atomicMin(&sm.key[p], key);
+              if (fwd) facc = __fadd_rn(facc, shader_work(fwd, key_depth(key)));
+            }
           }
         }
         __syncthreads();
