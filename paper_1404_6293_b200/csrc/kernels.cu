@@ -1208,7 +1208,10 @@ __device__ __forceinline__ void normalise_light(const float in[3], float L[3]) {
   L[2] = __fdiv_rn(in[2], s);
 }
 
-constexpr int TINY_AREA = 4;    // clipped rect area a thread rasterizes alone
+#ifndef PIKO_TINY_AREA
+#define PIKO_TINY_AREA 4
+#endif
+constexpr int TINY_AREA = PIKO_TINY_AREA;  // clipped rect area a thread rasterizes alone
 #ifndef PIKO_QSEG
 #define PIKO_QSEG 4
 #endif
