@@ -63,15 +63,46 @@ def workload_name(cfg, s, bw):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 100 ms in a thread."""
+    """SM clocks and throttle reasons sampled during the run.  NVML (pynvml)
+    polled every 2 ms in a thread, so even a few-millisecond timed region holds
+    samples; nvidia-smi -lms 100 is the fallback when NVML is unavailable."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits (nvml.h): sw power cap, hw slowdown, sw / hw thermal
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu_index):
-        self.samples = []
+        self.samples = []   # (time, sm_mhz, max_mhz, [reason names])
         self.window = None
         self.proc = None
+        self.stop = False
+        self.source = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def poll():
+                while not self.stop:
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        r = get_reasons(h)
+                        self.samples.append((time.time(), float(sm), float(mx),
+                                             [n for n, b in self.BITS.items() if r & b]))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            self.source = "nvml"
+            return
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.Q}",
@@ -79,38 +110,45 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            self.source = "nvidia-smi"
         except Exception:
             self.proc = None
 
     def _read(self):
-        for line in self.proc.stdout:
-            f = [x.strip() for x in line.split(",")]
-            if len(f) >= 8:
-                self.samples.append((time.time(), f))
-
-    def mark(self, t0, t1):
-        self.window = (t0, t1)
-
-    def summary(self):
-        if self.proc:
-            time.sleep(0.25)
-            self.proc.terminate()
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        inwin = [f for t, f in self.samples if self.window and self.window[0] - 0.15 <= t <= self.window[1] + 0.15]
-        use = inwin or [f for _, f in self.samples]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for f in use for n, v in zip(names, f[4:8]) if v.lower() == "active"})
 
         def num(v):
             try:
                 return float(v)
             except ValueError:
                 return None
-        sm = [num(f[0]) for f in use if num(f[0]) is not None]
-        mx = [num(f[1]) for f in use if num(f[1]) is not None]
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8 and num(f[0]) is not None:
+                self.samples.append((time.time(), num(f[0]), num(f[1]),
+                                     [n for n, v in zip(names, f[4:8]) if v.lower() == "active"]))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def summary(self):
+        if self.source == "nvml":
+            time.sleep(0.01)
+            self.stop = True
+        elif self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        tol = 0.0 if self.source == "nvml" else 0.15
+        inwin = [x for x in self.samples if self.window and self.window[0] - tol <= x[0] <= self.window[1] + tol]
+        use = inwin or self.samples
+        sm = [x[1] for x in use if x[1] is not None]
+        mx = [x[2] for x in use if x[2] is not None]
+        reasons = sorted({n for x in use for n in x[3]})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(use), "in_timed_region": bool(inwin)}
+                "reasons": reasons, "samples": len(use), "in_timed_region": bool(inwin),
+                "source": self.source}
 
 
 def cpu_baseline(s, budget):
