@@ -1217,7 +1217,10 @@ constexpr int TINY_AREA = PIKO_TINY_AREA;  // clipped rect area a thread rasteri
 #endif
 constexpr int QSEG = PIKO_QSEG; // queued triangles: pixels of a row per work item (amortises
                                 // the item search and the evaluator loads)
-constexpr int NSTAGE = 3;       // setup-record pipeline depth (rounds in flight per warp)
+#ifndef PIKO_NSTAGE
+#define PIKO_NSTAGE 2
+#endif
+constexpr int NSTAGE = PIKO_NSTAGE;  // setup-record pipeline depth (rounds in flight per warp)
 constexpr int TQ = NSTAGE + 2;  // primIDs are fetched two rounds before their records
 
 // Queue of larger triangles of the current bin (structure of arrays of the
