@@ -44,7 +44,10 @@ constexpr unsigned long long MAX_PAIRS = 1ull << 31;  // bin_start is int32
 constexpr int SIZE_CLASSES = 4;
 constexpr int NLIST = 2 + SIZE_CLASSES;
 constexpr int LIST_EMPTY = NLIST - 1;
-constexpr int FRAG_ROUNDS = 4;   // fragment = FRAG_ROUNDS * threads-per-CTA pairs
+#ifndef PIKO_FRAG_ROUNDS
+#define PIKO_FRAG_ROUNDS 4
+#endif
+constexpr int FRAG_ROUNDS = PIKO_FRAG_ROUNDS;  // fragment = FRAG_ROUNDS * threads-per-CTA pairs
 constexpr int EMPTY_GROUP = 8;   // empty bins per k_tile queue ticket
 constexpr int OVQ_CAP = 1024;    // k_tile: spilled large-triangle entries per CTA (96 B each)
 
