@@ -73,7 +73,7 @@ __device__ __forceinline__ u64 gtimer_ns();
 // Spin until *p >= want (signed compare); after P2P_TIMEOUT_NS a peer is
 // presumed dead: flag the frame (host reports PIKO_ENCCL) instead of hanging.
 constexpr unsigned long long P2P_TIMEOUT_NS = 10ull * 1000 * 1000 * 1000;
-__device__ __noinline__ void p2p_wait_geq(const u64* p, long long want, unsigned* timeout_flag) {
+static __device__ __noinline__ void p2p_wait_geq(const u64* p, long long want, unsigned* timeout_flag) {
   const u64 t0 = gtimer_ns();
   while ((long long)ld_acquire_sys64(p) < want) {
     __nanosleep(256);
@@ -106,6 +106,8 @@ __device__ u64 g_k1_times[4][8192][8];
 __device__ __forceinline__ void g_tl_extra(int job, int n, int cta) { g_k1_times[3][job][3] = n; g_k1_times[3][job][4] = cta; }
 #define TL_CTA(i) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_k1_times[0][7000 + blockIdx.x][i] = gtimer(); } while (0)
 #define SCAN_MARK(tile, i) do { if (threadIdx.x == 0 && (tile) < 64 && a.pass < 2) g_k1_times[1 + a.pass][8100 + (tile)][i] = gtimer(); } while (0)
+// count-matrix kernels reuse the radix slots: [1] k_cm_scan CTA j, [2] k_cm_scatter CTA
+#define CM_MARK(k, slot, i) do { if (threadIdx.x == 0 && (slot) < 8000) g_k1_times[k][slot][i] = gtimer(); } while (0)
 // look-back detail of radix passes 0/1 (thread 0 = digit 0): [pass][chunk]
 // {level-1 end time, level-1 probes, level-2 probes, group-aggregate publish time}
 __device__ u64 g_rx_lb[2][8192][8];
@@ -126,6 +128,7 @@ namespace piko {
 #define g_tl_extra(a, b, c) do { } while (0)
 #define TL_CTA(i) do { } while (0)
 #define SCAN_MARK(tile, i) do { } while (0)
+#define CM_MARK(k, slot, i) do { } while (0)
 #endif
 
 // Look-back status word: tag (frame+1, 20 bits) | flag (2 bits) | value (42 bits)
@@ -142,8 +145,11 @@ __device__ __forceinline__ unsigned frame_tag(u64 frame) { return (unsigned)((fr
 // predecessors back to the nearest inclusive prefix, 128 per probe (4 per lane,
 // lane-major: entry q = hi - 32*j - lane); publish the inclusive prefix.
 // Returns the exclusive prefix.
+static // Status words carry their own payload (tag, flag and value in one 64-bit
+// word), so relaxed atomic loads/stores suffice: an acquire load per probe
+// entry would add a fence per load to the chain.
 __device__ u64 lookback_warp(u64* status, long long chunk, u64 agg, unsigned tag, int lane) {
-  if (lane == 0) st_release64(&status[chunk], lb_pack(tag, chunk == 0 ? LB_INC : LB_AGG, agg));
+  if (lane == 0) st_relaxed64(&status[chunk], lb_pack(tag, chunk == 0 ? LB_INC : LB_AGG, agg));
   if (chunk == 0) return 0;
   u64 excl = 0;
   long long hi = chunk - 1;
@@ -152,7 +158,7 @@ __device__ u64 lookback_warp(u64* status, long long chunk, u64 agg, unsigned tag
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const long long i = hi - 32 * j - lane;
-      sv[j] = (i >= 0) ? ld_acquire64(&status[i]) : lb_pack(tag, LB_INC, 0);
+      sv[j] = (i >= 0) ? ld_relaxed64(&status[i]) : lb_pack(tag, LB_INC, 0);
     }
     // walk the 4 groups of 32 in order (nearest predecessors first)
     bool retry = false, done = false;
@@ -176,7 +182,7 @@ __device__ u64 lookback_warp(u64* status, long long chunk, u64 agg, unsigned tag
     excl += add;   // groups consumed before a retry stay consumed (hi advanced)
     if (done) break;
   }
-  if (lane == 0) st_release64(&status[chunk], lb_pack(tag, LB_INC, excl + agg));
+  if (lane == 0) st_relaxed64(&status[chunk], lb_pack(tag, LB_INC, excl + agg));
   return excl;
 }
 
@@ -266,12 +272,12 @@ __device__ __forceinline__ bool setup_tri(int4 c0, int4 c1, int4 c2, int i0, int
 }
 
 // number of bins b in tile rect [tx0,tx1]x[ty0,ty1] with b % R == r
-__device__ __noinline__ unsigned owned_in_rect_r(int tx0, int ty0, int tx1, int ty1, const Grid g);
+static __device__ __noinline__ unsigned owned_in_rect_r(int tx0, int ty0, int tx1, int ty1, const Grid g);
 __device__ __forceinline__ unsigned owned_in_rect(int tx0, int ty0, int tx1, int ty1, const Grid& g) {
   if (g.nranks == 1) return (unsigned)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
   return owned_in_rect_r(tx0, ty0, tx1, ty1, g);
 }
-__device__ __noinline__ unsigned owned_in_rect_r(int tx0, int ty0, int tx1, int ty1, const Grid g) {
+static __device__ __noinline__ unsigned owned_in_rect_r(int tx0, int ty0, int tx1, int ty1, const Grid g) {
   unsigned n = 0;
   const int w = tx1 - tx0 + 1;
   for (int ty = ty0; ty <= ty1; ++ty) {
@@ -283,13 +289,13 @@ __device__ __noinline__ unsigned owned_in_rect_r(int tx0, int ty0, int tx1, int 
 }
 
 // r-th owned bin of the rect, row-major (inverse of owned_in_rect's order)
-__device__ __noinline__ int owned_bin_at_r(int tx0, int ty0, int tx1, int ty1, unsigned r, const Grid g);
+static __device__ __noinline__ int owned_bin_at_r(int tx0, int ty0, int tx1, int ty1, unsigned r, const Grid g);
 __device__ __forceinline__ int owned_bin_at(int tx0, int ty0, int tx1, int ty1, unsigned r, const Grid& g) {
   const int w = tx1 - tx0 + 1;
   if (g.nranks == 1) return (ty0 + (int)(r / w)) * g.binsX + tx0 + (int)(r % w);
   return owned_bin_at_r(tx0, ty0, tx1, ty1, r, g);
 }
-__device__ __noinline__ int owned_bin_at_r(int tx0, int ty0, int tx1, int ty1, unsigned r, const Grid g) {
+static __device__ __noinline__ int owned_bin_at_r(int tx0, int ty0, int tx1, int ty1, unsigned r, const Grid g) {
   const int w = tx1 - tx0 + 1;
   for (int ty = ty0; ty <= ty1; ++ty) {
     const int base = ty * g.binsX + tx0;
@@ -301,6 +307,7 @@ __device__ __noinline__ int owned_bin_at_r(int tx0, int ty0, int tx1, int ty1, u
   return -1;  // unreachable for r < owned_in_rect
 }
 
+#ifndef PIKO_TILE_TU  // ---- main TU only: every kernel but k_tile ----
 // ---------------------------------------------------------------------------
 // K0: vertex stage -- each vertex transformed and snapped exactly once
 // ---------------------------------------------------------------------------
@@ -374,9 +381,10 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
   pdl_trigger();
   // every CTA takes one ticket per frame: frame = ticket / gridDim.x (the
   // triangle chunk is simply blockIdx.x -- nothing here depends on CTA order)
-  if (tid == 0) { s_tk = atomicAdd(&a.ctl->k1_ticket, 1ull); s_live = 0; s_nbig = 0; }
+  if (tid == 0) { s_tk = atomicAdd(&a.ctl->k1_ticket, 1ull) / gridDim.x; s_live = 0; s_nbig = 0; }
   for (int i = tid; i < MAX_PASSES * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
-  __syncthreads();  // histogram cleared before any thread adds to it
+  __syncthreads();  // histogram cleared before any thread adds to it; frame known
+  const u64 frame = s_tk;
   const long long chunk = blockIdx.x;
   const long long t0 = chunk * K1_CHUNK;
   K1_MARK(0);
@@ -417,8 +425,13 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
 
   // ---- setup, record + rect write (coalesced: consecutive threads, t) -------
   unsigned live = 0;
+  // count-matrix mode: the CTA's triangles all lie in row t0 >> cm_shift
+  // (K1_CHUNK divides the row size); one-bin triangles are warp-aggregated
+  uint32_t* cmrow = a.cm ? a.cm + (size_t)(t0 >> a.cm_shift) * g.NB : nullptr;
+  int bin1[K1_TPT];
 #pragma unroll
   for (int k = 0; k < K1_TPT; ++k) {
+    bin1[k] = -1;
     const long long t = t0 + tid + k * K1_THREADS;
     if (t >= a.n_tris) continue;
     uint2 rr = make_uint2(1u, 0u);  // empty rect: tx0 = 1 > tx1 = 0
@@ -427,6 +440,15 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
       const int tx0 = o.px0 >> g.bw_log2, tx1 = o.px1 >> g.bw_log2;
       const int ty0 = o.py0 >> g.bh_log2, ty1 = o.py1 >> g.bh_log2;
       const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
+      if (c == 1 && cmrow) bin1[k] = owned_bin_at(tx0, ty0, tx1, ty1, 0u, g);
+      else if (c > 1 && c <= (unsigned)K1_BIG && cmrow) {
+        for (int ty = ty0; ty <= ty1; ++ty)
+          for (int tx = tx0; tx <= tx1; ++tx) {
+            const int b = ty * g.binsX + tx;
+            if (g.nranks > 1 && b % g.nranks != g.rank) continue;
+            atomicAdd(&cmrow[b], 1u);
+          }
+      }
       if (c > 0) {
         rr = make_uint2((unsigned)tx0 | ((unsigned)ty0 << 16), (unsigned)tx1 | ((unsigned)ty1 << 16));
         ++live;
@@ -443,7 +465,9 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
         r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
                          o.small ? REC_SMALL : 0);
         // digit histograms of the radix passes over this triangle's pairs
-        if (c <= (unsigned)K1_BIG) {
+        if (a.npass == 0 && c <= (unsigned)K1_BIG) {
+          // count-matrix mode: no digit histograms
+        } else if (c <= (unsigned)K1_BIG) {
           for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx) {
               const int b = ty * g.binsX + tx;
@@ -457,10 +481,16 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
     }
     a.rect[t] = rr;
   }
+  if (cmrow) {
+#pragma unroll
+    for (int k = 0; k < K1_TPT; ++k) {
+      const unsigned peers = __match_any_sync(0xffffffffu, bin1[k]);
+      if (bin1[k] >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cmrow[bin1[k]], (unsigned)__popc(peers));
+    }
+  }
   K1_MARK(2);
   if (live) atomicAdd(&s_live, live);
   __syncthreads();
-  const u64 frame = s_tk / gridDim.x;
   if (chunk == 0 && tid == 0) {
     a.ctl->frame = frame; a.ctl->tile_next = 0; a.ctl->vmax = 0;
     for (int k = 0; k < NLIST; ++k) a.ctl->list_n[k] = 0;
@@ -476,6 +506,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
     for (unsigned j = tid; j < c; j += K1_THREADS) {
       const int b = owned_bin_at(tx0, ty0, tx1, ty1, j, g);
       for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], 1u);
+      if (cmrow) atomicAdd(&cmrow[b], 1u);
     }
   }
   __syncthreads();
@@ -490,7 +521,8 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
 // ---------------------------------------------------------------------------
 // Bin scan (run by extra CTAs of radix pass 0): bin_count -> bin_start
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, unsigned tag) {
+static __device__ __noinline__ void schedule_bins(const RadixArgs& a, long long b0, const unsigned (&c)[SCAN_ITEMS], bool active = true);
+static __device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, unsigned tag) {
   __shared__ unsigned s_wsum[SCAN_THREADS / 32];
   __shared__ u64 s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -533,6 +565,13 @@ __device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, u
     run += c[k];
   }
   if (b0 < a.NB && b0 + SCAN_ITEMS >= a.NB) a.bin_start[a.NB] = (int32_t)run;
+  schedule_bins(a, b0, c);
+}
+
+// Schedule (a6) for the SCAN_ITEMS bins b0.. of this thread with pair counts
+// c[]: owned bins into k_tile's work lists (every thread of the CTA calls it).
+static __device__ __noinline__ void schedule_bins(const RadixArgs& a, long long b0, const unsigned (&c)[SCAN_ITEMS], bool active) {
+  const int tid = threadIdx.x, lane = tid & 31;
   // Schedule: owned bins into k_tile's work lists (the order inside a list
   // does not affect the result).  Bins with more than a.frag pairs become
   // fragments (their global key tiles are CLEAR: k_tile's last fragment resets
@@ -548,7 +587,7 @@ __device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, u
 #pragma unroll
   for (int k = 0; k < SCAN_ITEMS; ++k) {
     const long long b = b0 + k;
-    const bool own = b < a.NB && (a.nranks == 1 || (int)(b % a.nranks) == a.rank);
+    const bool own = active && b < a.NB && (a.nranks == 1 || (int)(b % a.nranks) == a.rank);
     const unsigned cnt = own ? c[k] : 0u;
     const unsigned nf = (own && cnt > (unsigned)a.frag) ? (cnt + a.frag - 1) / a.frag : 0u;
     // list 0: fragments of split bins; 1..SIZE_CLASSES: single-fragment bins by
@@ -567,13 +606,11 @@ __device__ __noinline__ void bin_scan_tile(const RadixArgs& a, long long tile, u
     kd[k] = kind; loc[k] = l; nfk[k] = nf;
   }
   __syncthreads();
-  SCAN_MARK(tile, 4);
   if (tid < NLIST) {
     const unsigned n = s_ln[tid];
     s_ln[tid] = n ? atomicAdd(&a.ctl->list_n[tid], n) : 0u;
   }
   __syncthreads();
-  SCAN_MARK(tile, 5);
 #pragma unroll
   for (int k = 0; k < SCAN_ITEMS; ++k) {
     const int b = (int)(b0 + k);
@@ -638,7 +675,7 @@ __device__ __forceinline__ void rank_items(const unsigned (&key)[RX_ITEMS], unsi
 // ranked twice -- first to count (publish), then to scatter with running
 // offsets.  phase 0: count into sm.run[d] and the bin counts; phase 1: scatter
 // from sm.gstart.
-__device__ __noinline__ void expand_slow(const RadixArgs& a, RadixSmem& sm, const ExpandSmem& ex,
+static __device__ __noinline__ void expand_slow(const RadixArgs& a, RadixSmem& sm, const ExpandSmem& ex,
                                          int ntri, long long t0, unsigned n, int phase) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool dig = tid < RX_RADIX;  // thread tid owns digit tid
@@ -1057,6 +1094,381 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_bin_scan(RadixArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Count-matrix AssignBin (a4 exclusive scans + a5 stable scatter, DESIGN.md
+// sec. 6) for NB <= CM_MAX_NB.  k_setup has added every triangle's owned bins
+// into row r = t >> cm_shift of M.  The bin lists in primitive order
+// then need only
+//   pos(t, b) = bin_start[b] + sum_{r' < r} M[r'][b] + #{t' < t in row r : b in t'}
+// k_cm_scan forms the first two terms for every (row, bin) -- a column scan,
+// plus one decoupled look-back over its CTAs for bin_start -- and
+// k_cm_scatter the last term inside one CTA per row: no look-back per pair
+// chunk and no second sort pass.
+// ---------------------------------------------------------------------------
+constexpr int CM_GROUPS = 256 / CM_COLS;  // row groups per k_cm_scan CTA
+constexpr int CM_RPT = 16;                // rows per thread kept in registers
+__global__ void __launch_bounds__(256) k_cm_scan(const __grid_constant__ CmArgs a) {
+  __shared__ u64 s_tk;
+  __shared__ unsigned s_part[CM_GROUPS][CM_COLS];
+  __shared__ unsigned s_tot[CM_COLS];
+  __shared__ u64 s_base;
+  const int tid = threadIdx.x, lane = tid & 31, col = tid % CM_COLS, grp = tid / CM_COLS;
+  pdl_wait();   // k_setup's counts
+  pdl_trigger();
+  if (tid == 0) s_tk = atomicAdd(&a.ctl->cm_ticket, 1ull);
+  __syncthreads();
+  const u64 frame = s_tk / gridDim.x;
+  const long long j = (long long)(s_tk % gridDim.x);  // ticket order: look-back never waits on an unstarted CTA
+  const unsigned tag = frame_tag(frame);
+  CM_MARK(1, j, 0);
+  const int NB = a.g.NB;
+  const long long b = j * CM_COLS + col;
+  const long long rpg = (a.rows + CM_GROUPS - 1) / CM_GROUPS;
+  const long long r0 = grp * rpg, r1 = min(a.rows, r0 + rpg);
+  // the column slice stays in registers between the two sweeps when it is
+  // short (rows <= CM_GROUPS x CM_RPT, the usual case); otherwise re-read
+  unsigned sum = 0, v[CM_RPT];
+  const bool cached = rpg <= CM_RPT;
+  if (b < NB) {
+    for (long long r = r0; r < r1; r += CM_RPT) {  // CM_RPT loads in flight
+#pragma unroll
+      for (int u = 0; u < CM_RPT; ++u) v[u] = (r + u < r1) ? __ldcg(a.cm + (size_t)(r + u) * NB + b) : 0u;
+#pragma unroll
+      for (int u = 0; u < CM_RPT; ++u) sum += v[u];
+    }
+  }
+  s_part[grp][col] = sum;
+  __syncthreads();
+  CM_MARK(1, j, 1);
+  if (tid < CM_COLS) {  // exclusive over the row groups of column tid
+    unsigned run = 0;
+#pragma unroll
+    for (int q = 0; q < CM_GROUPS; ++q) {
+      const unsigned c = s_part[q][tid];
+      s_part[q][tid] = run;
+      run += c;
+    }
+    s_tot[tid] = run;
+  }
+  __syncthreads();
+  if (tid < 32) {  // bin totals of this CTA's columns -> bin_start (look-back over CTAs)
+    const unsigned c = lane < CM_COLS ? s_tot[lane] : 0u;
+    unsigned inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const unsigned agg = __shfl_sync(0xffffffffu, inc, 31);
+    const u64 ex = lookback_warp(a.status, j, agg, tag, lane);
+    if (lane < CM_COLS) s_tot[lane] = inc - c;
+    if (lane == 0) {
+      s_base = ex;
+      if (j == (long long)gridDim.x - 1) {  // last columns: P = the whole list length
+        const u64 P = ex + agg;
+        a.ctl->n_pairs = P;
+        a.sched.bin_start[NB] = (int32_t)(P < MAX_PAIRS ? P : MAX_PAIRS - 1);
+        if (P > a.cap) atomicMax(&a.ctl->overflow_tag, frame + 1);
+      }
+    }
+  }
+  __syncthreads();
+  CM_MARK(1, j, 2);
+  if (b >= NB) return;
+  const u64 bstart = s_base + s_tot[col];
+  if (grp == 0) a.sched.bin_start[b] = (int32_t)bstart;
+  u64 run = bstart + s_part[grp][col];
+  // second sweep: prefixes out, counts reset to zero for the next frame
+  for (long long r = r0; r < r1; r += CM_RPT) {
+    if (!cached) {
+#pragma unroll
+      for (int u = 0; u < CM_RPT; ++u) v[u] = (r + u < r1) ? __ldcg(a.cm + (size_t)(r + u) * NB + b) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < CM_RPT; ++u) {
+      if (r + u >= r1) break;
+      const size_t o = (size_t)(r + u) * NB + b;
+      a.cp[o] = (uint32_t)run;
+      run += v[u];
+      if (v[u]) a.cm[o] = 0u;
+    }
+  }
+  CM_MARK(1, j, 3);
+}
+
+// Stable rank by an 8-bit digit (RX_RADIX = invalid) of the items held by
+// this thread: item j of warp w, lane l is number w*ipw + 32*j + l, so
+// (warp, j, lane) is the items' order; per-warp digit counters in shared memory.
+template <int NI>
+__device__ __forceinline__ void rank_digits(const unsigned (&d)[NI], int nj,
+                                            unsigned short (*whist)[RX_RADIX], int warp, int lane,
+                                            unsigned (&rank)[NI]) {
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < NI; ++j) {
+    if (j >= nj) break;  // warp-uniform
+    const bool valid = d[j] < RX_RADIX;
+    const unsigned peers = __match_any_sync(0xffffffffu, d[j]);
+    unsigned prev = 0;
+    if (valid) prev = whist[warp][d[j]];
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) whist[warp][d[j]] = (unsigned short)(prev + __popc(peers));
+    __syncwarp();
+    rank[j] = prev + __popc(peers & lanemask_lt);
+  }
+}
+
+constexpr int CM_THREADS = 512;                  // k_cm_scatter CTA (2 per SM: 32 warps)
+constexpr int CM_WARPS = CM_THREADS / 32;
+constexpr int CM_ITEMS = RX_CHUNK / CM_THREADS;  // pairs of a window per thread
+struct CmSmem {
+  unsigned short whist[CM_WARPS][RX_RADIX];    // per-warp digit counters
+  unsigned keys[RX_CHUNK];                      // window of pairs in pair order: bin
+  int vals[RX_CHUNK];                           //   ... and primID
+  unsigned cur[RX_CHUNK];                       // cursors: by bin (NB <= RX_CHUNK) or by local digit
+  unsigned short tb[RX_CHUNK];                  // touched bin of each local digit
+  unsigned bm[CM_MAX_NB / 32];                  // bins touched by the window
+  unsigned short wpre[CM_MAX_NB / 32];          // exclusive popcount prefix of bm
+  unsigned dtot[RX_RADIX];
+  unsigned wsum[CM_WARPS];
+  unsigned n, U;
+};
+
+// One CTA per count-matrix row (plus schedule CTAs).  The row's triangles are
+// processed CM_SUB at a time, held in registers in warp-major order (triangle
+// l = warp*TPW + 32k + lane), so (warp, k, lane) is triangle order; their
+// pairs are laid out in pair order through an exclusive scan in that order
+// and ranked stably per bin through dense local digits (<= 256 per ranking
+// window).  Cursors start at CP[row][b] (bin_start + earlier rows).
+__global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_constant__ CmArgs a) {
+  extern __shared__ __align__(16) unsigned char cm_smem[];
+  CmSmem& sm = *reinterpret_cast<CmSmem*>(cm_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NB = a.g.NB, NBW = (NB + 31) >> 5;
+  const bool sched = (long long)blockIdx.x >= a.rows;
+  const bool cur_by_bin = NB <= RX_CHUNK;  // the whole cursor row lives in shared memory
+  const long long row = blockIdx.x;
+  const long long tbeg = row << a.cm_shift, tend = sched ? tbeg : min(a.n_tris, tbeg + (1ll << a.cm_shift));
+  constexpr int TPT = CM_SUB / CM_THREADS;
+  constexpr int TPW = CM_SUB / CM_WARPS;   // triangles per warp
+  CM_MARK(2, blockIdx.x, 0);
+  // the first sub-chunk's rects (k_setup's output) are loaded before the wait
+  // on k_cm_scan
+  uint2 rr[TPT];
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const long long t = tbeg + warp * TPW + k * 32 + lane;
+    rr[k] = t < tend ? __ldcg(a.rect + t) : make_uint2(1u, 0u);
+  }
+  pdl_wait();   // k_cm_scan's prefixes and bin_start
+  pdl_trigger();
+  CM_MARK(2, blockIdx.x, 1);
+  if (sched) {  // extra CTAs: k_tile's work lists (bin_start is final)
+    const long long b0 = ((long long)blockIdx.x - a.rows) * SCAN_CHUNK + (long long)tid * SCAN_ITEMS;
+    const bool active = tid < SCAN_THREADS;  // SCAN_CHUNK bins per schedule CTA
+    unsigned c[SCAN_ITEMS];
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k)
+      c[k] = (active && b0 + k < NB) ? (unsigned)(a.sched.bin_start[b0 + k + 1] - a.sched.bin_start[b0 + k]) : 0u;
+    schedule_bins(a.sched, b0, c, active);
+    return;
+  }
+  if (a.ctl->overflow_tag == a.ctl->frame + 1) return;  // P > capacity: k_tile renders background
+  uint32_t* cprow = a.cp + (size_t)row * NB;
+  if (cur_by_bin) {  // all loads in flight together, then the stores
+    constexpr int CPT = RX_CHUNK / CM_THREADS;
+    unsigned cv[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) cv[k] = tid + k * CM_THREADS < NB ? __ldcg(cprow + tid + k * CM_THREADS) : 0u;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) if (tid + k * CM_THREADS < NB) sm.cur[tid + k * CM_THREADS] = cv[k];
+  }
+  for (int w = tid; w < NBW; w += CM_THREADS) sm.bm[w] = 0u;
+  auto block_excl = [&](unsigned v) -> unsigned {  // every thread must call it
+    unsigned inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) sm.wsum[warp] = inc;
+    __syncthreads();
+    unsigned base = 0;
+    for (int w = 0; w < warp; ++w) base += sm.wsum[w];
+    __syncthreads();
+    return base + inc - v;
+  };
+  for (long long sub = tbeg; sub < tend; sub += CM_SUB) {
+    const bool last_sub = sub + CM_SUB >= tend;
+    if (sub != tbeg) {
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const long long t = sub + warp * TPW + k * 32 + lane;
+        rr[k] = t < tend ? __ldcg(a.rect + t) : make_uint2(1u, 0u);
+      }
+    }
+    // owned-bin counts and their exclusive prefix in (warp, k, lane) order
+    unsigned off[TPT], wrun = 0;
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+      const unsigned c = owned_in_rect(rr[k].x & 0xffff, rr[k].x >> 16, rr[k].y & 0xffff, rr[k].y >> 16, a.g);
+      unsigned inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      off[k] = wrun + inc - c;   // within the warp; the count is off-delta
+      wrun += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) sm.wsum[warp] = wrun;  // warp totals (wrun is warp-uniform)
+    __syncthreads();
+    unsigned wbase = 0, n = 0;
+#pragma unroll
+    for (int w = 0; w < CM_WARPS; ++w) {
+      const unsigned c = sm.wsum[w];
+      wbase += (w < warp) ? c : 0u;
+      n += c;
+    }
+    CM_MARK(2, blockIdx.x, 3);
+    for (unsigned lo = 0; lo < n; lo += RX_CHUNK) {
+      const unsigned m = min((unsigned)RX_CHUNK, n - lo);
+      const bool last_round = last_sub && lo + RX_CHUNK >= n;
+      // expand this thread's triangles' pairs inside the window [lo, lo + m)
+      // into shared memory at their pair positions
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const int tx0 = rr[k].x & 0xffff, ty0 = rr[k].x >> 16, tx1 = rr[k].y & 0xffff, ty1 = rr[k].y >> 16;
+        if (tx0 > tx1 || ty0 > ty1) continue;
+        const unsigned o = wbase + off[k];
+        const int val = (int)(sub + warp * TPW + k * 32 + lane);
+        if (a.g.nranks == 1) {  // row-major walk of the rect part inside the window
+          const int w = tx1 - tx0 + 1;
+          const unsigned c = (unsigned)(w * (ty1 - ty0 + 1));
+          const unsigned j0 = max(o, lo), j1 = min(o + c, lo + m);
+          if (j0 >= j1) continue;
+          int ty = ty0, tx = tx0;
+          if (j0 > o) { ty += (int)((j0 - o) / w); tx += (int)((j0 - o) % w); }
+          for (unsigned q = j0; q < j1; ++q) {
+            const int b = ty * a.g.binsX + tx;
+            sm.keys[q - lo] = (unsigned)b;
+            sm.vals[q - lo] = val;
+            if (++tx > tx1) { tx = tx0; ++ty; }
+          }
+        } else {
+          const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, a.g);
+          const unsigned j0 = max(o, lo), j1 = min(o + c, lo + m);
+          for (unsigned q = j0; q < j1; ++q) {
+            const int b = owned_bin_at(tx0, ty0, tx1, ty1, q - o, a.g);
+            sm.keys[q - lo] = (unsigned)b;
+            sm.vals[q - lo] = val;
+          }
+        }
+      }
+      __syncthreads();
+      // the window's items, spread evenly over the warps (warp w holds pairs
+      // [w*ipw, w*ipw + ipw)); touched-bin bitmap from the heads of runs of
+      // equal bins (consecutive pairs of a coherent mesh share their bin: one
+      // shared-memory atomic per run instead of a 32-way conflict per pair)
+      const int ipw = (int)((m + CM_WARPS * 32 - 1) / (CM_WARPS * 32)) * 32;
+      const int nj = ipw / 32;
+      unsigned kb[CM_ITEMS];
+#pragma unroll
+      for (int j = 0; j < CM_ITEMS; ++j) {
+        const unsigned pos = (unsigned)warp * ipw + j * 32 + lane;
+        kb[j] = (j < nj && pos < m) ? sm.keys[pos] : 0xFFFFFFFFu;
+        const unsigned prev = __shfl_up_sync(0xffffffffu, kb[j], 1);
+        if (kb[j] != 0xFFFFFFFFu && (lane == 0 || prev != kb[j])) atomicOr(&sm.bm[kb[j] >> 5], 1u << (kb[j] & 31));
+      }
+      __syncthreads();
+      if (lo == 0) CM_MARK(2, blockIdx.x, 4);
+      // touched bins -> dense local digits: popcount prefix of the bitmap
+      constexpr int WPT = CM_MAX_NB / 32 / CM_THREADS;  // bitmap words per thread
+      unsigned wc[WPT], ws = 0;
+#pragma unroll
+      for (int k = 0; k < WPT; ++k) {
+        const int w = tid * WPT + k;
+        wc[k] = w < NBW ? sm.bm[w] : 0u;
+        ws += __popc(wc[k]);
+      }
+      unsigned drun = block_excl(ws);
+      if (tid == CM_THREADS - 1) sm.U = drun + ws;
+#pragma unroll
+      for (int k = 0; k < WPT; ++k) {
+        const int w = tid * WPT + k;
+        if (w < NBW) sm.wpre[w] = (unsigned short)drun;
+        unsigned bits = wc[k];
+        while (bits) {
+          const int bit = __ffs(bits) - 1;
+          bits &= bits - 1;
+          sm.tb[drun++] = (unsigned short)(w * 32 + bit);
+        }
+      }
+      __syncthreads();
+      const unsigned U = sm.U;
+#ifdef PIKO_K1_TIMING
+      if (threadIdx.x == 0 && lo == 0 && blockIdx.x < 8000) g_k1_times[2][blockIdx.x][7] = U;
+#endif
+      if (!cur_by_bin)
+        for (unsigned d = tid; d < U; d += CM_THREADS) sm.cur[d] = __ldcg(cprow + sm.tb[d]);
+      unsigned ld[CM_ITEMS];
+      int val[CM_ITEMS];
+#pragma unroll
+      for (int j = 0; j < CM_ITEMS; ++j) {
+        const unsigned pos = (unsigned)warp * ipw + j * 32 + lane;
+        ld[j] = 0xFFFFFFFFu;
+        val[j] = 0;
+        if (kb[j] != 0xFFFFFFFFu) {
+          val[j] = sm.vals[pos];
+          ld[j] = sm.wpre[kb[j] >> 5] + __popc(sm.bm[kb[j] >> 5] & ((1u << (kb[j] & 31)) - 1u));
+        }
+      }
+      __syncthreads();  // window and bitmap consumed (cursors loaded)
+      if (lo == 0) CM_MARK(2, blockIdx.x, 5);
+      for (int w = tid; w < NBW; w += CM_THREADS) sm.bm[w] = 0u;  // for the next window
+      for (unsigned w0 = 0; w0 < U; w0 += RX_RADIX) {  // ranking windows of 256 local digits
+        for (int i = tid; i < CM_WARPS * RX_RADIX; i += CM_THREADS) (&sm.whist[0][0])[i] = 0;
+        __syncthreads();
+        unsigned d[CM_ITEMS], rank[CM_ITEMS];
+#pragma unroll
+        for (int j = 0; j < CM_ITEMS; ++j) d[j] = (ld[j] >= w0 && ld[j] < w0 + RX_RADIX) ? ld[j] - w0 : RX_RADIX;
+        rank_digits(d, nj, sm.whist, warp, lane, rank);
+        __syncthreads();
+        if (tid < RX_RADIX) {  // exclusive over warps (thread tid owns local digit w0 + tid)
+          unsigned tot = 0;
+#pragma unroll
+          for (int w = 0; w < CM_WARPS; ++w) {
+            const unsigned c = sm.whist[w][tid];
+            sm.whist[w][tid] = (unsigned short)tot;
+            tot += c;
+          }
+          sm.dtot[tid] = tot;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < CM_ITEMS; ++j)
+          if (j < nj && d[j] < RX_RADIX) {
+            const unsigned cu = cur_by_bin ? sm.cur[sm.tb[w0 + d[j]]] : sm.cur[w0 + d[j]];
+            a.bin_prims[cu + sm.whist[warp][d[j]] + rank[j]] = val[j];
+          }
+        __syncthreads();
+        if (tid < RX_RADIX && w0 + tid < U) {
+          if (cur_by_bin) sm.cur[sm.tb[w0 + tid]] += sm.dtot[tid];
+          else sm.cur[w0 + tid] += sm.dtot[tid];
+        }
+      }
+      if (lo == 0) CM_MARK(2, blockIdx.x, 6);
+      if (!cur_by_bin && !last_round) {  // row cursors of the bins this row touches again
+        __syncthreads();
+        for (unsigned q = tid; q < U; q += CM_THREADS) cprow[sm.tb[q]] = sm.cur[q];
+      }
+      __syncthreads();
+    }
+  }
+  CM_MARK(2, blockIdx.x, 2);
+}
+
+#endif  // PIKO_TILE_TU
+// ---------------------------------------------------------------------------
 // K6: per-bin Process -- raster + depth test + shade + write-back
 // ---------------------------------------------------------------------------
 struct RecView {
@@ -1157,25 +1569,12 @@ __device__ __forceinline__ u64 eval_pre(const TriEval& e, int Px, int Py, int t,
   return ((u64)(__float_as_uint(z) & 0x7FFFFFFFu) << 32) | (unsigned)t;
 }
 
-// O7 shade of pixel sample (Px, Py) by triangle t (recomputes O2 from the
-// vertex-stage records; normals from the caller's vertex buffer).
-__device__ __noinline__ float4 shade(const float* __restrict__ verts, const int4* __restrict__ xv,
-                                        const Mat4* M, const int32_t* __restrict__ idx, int W, int H,
-                                        const float L[3], int t, int Px, int Py) {
+// O7 shade arithmetic of pixel sample (Px, Py) given triangle t's transformed
+// corners (vertex-stage records) and the normals of its vertices i0..i2.
+__device__ __forceinline__ float4 shade_math(int4 c0, int4 c1, int4 c2, float4 m0, float4 m1, float4 m2,
+                                             int i0, int i1, int i2, int W, int H, const float L[3],
+                                             int Px, int Py) {
   Tri o;
-  const int i0 = __ldg(idx + 3ll * t), i1 = __ldg(idx + 3ll * t + 1), i2 = __ldg(idx + 3ll * t + 2);
-  int4 c0, c1, c2;
-  if (xv) {
-    c0 = __ldg(xv + i0); c1 = __ldg(xv + i1); c2 = __ldg(xv + i2);
-  } else {  // fused vertex stage: the same O1 transform, recomputed
-    const float4 p0 = load_pos(verts, i0), p1 = load_pos(verts, i1), p2 = load_pos(verts, i2);
-    c0 = transform_vertex(p0, *M, W, H);
-    c1 = transform_vertex(p1, *M, W, H);
-    c2 = transform_vertex(p2, *M, W, H);
-  }
-  const float4 m0 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i0 + 4));
-  const float4 m1 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i1 + 4));
-  const float4 m2 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i2 + 4));
   setup_tri(c0, c1, c2, i0, i1, i2, W, H, o);      // live: t won a pixel
   const bool swapped = o.X1 != c1.x || o.Y1 != c1.y;  // O2 swapped corners 1 and 2?
   const float4 n0 = m0;
@@ -1199,6 +1598,68 @@ __device__ __noinline__ float4 shade(const float* __restrict__ verts, const int4
     lam = (q > 0.0f) ? q : 0.0f;
   }
   return make_float4(__fmul_rn(0.80f, lam), __fmul_rn(0.75f, lam), __fmul_rn(0.65f, lam), 1.0f);
+}
+
+// O7 shade of pixel sample (Px, Py) by triangle t (recomputes O2 from the
+// vertex-stage records; normals from the caller's vertex buffer).
+static __device__ __noinline__ float4 shade(const float* __restrict__ verts, const int4* __restrict__ xv,
+                                        const Mat4* M, const int32_t* __restrict__ idx, int W, int H,
+                                        const float L[3], int t, int Px, int Py) {
+  const int i0 = __ldg(idx + 3ll * t), i1 = __ldg(idx + 3ll * t + 1), i2 = __ldg(idx + 3ll * t + 2);
+  int4 c0, c1, c2;
+  if (xv) {
+    c0 = __ldg(xv + i0); c1 = __ldg(xv + i1); c2 = __ldg(xv + i2);
+  } else {  // fused vertex stage: the same O1 transform, recomputed
+    const float4 p0 = load_pos(verts, i0), p1 = load_pos(verts, i1), p2 = load_pos(verts, i2);
+    c0 = transform_vertex(p0, *M, W, H);
+    c1 = transform_vertex(p1, *M, W, H);
+    c2 = transform_vertex(p2, *M, W, H);
+  }
+  const float4 m0 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i0 + 4));
+  const float4 m1 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i1 + 4));
+  const float4 m2 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i2 + 4));
+  return shade_math(c0, c1, c2, m0, m1, m2, i0, i1, i2, W, H, L, Px, Py);
+}
+
+// Deferred shade of N pixels of one row with every load of the dependent
+// chain key -> idx -> vertex records / normals issued for all N at once
+// (one chain of round trips per N pixels instead of per pixel).
+template <int N>
+__device__ __forceinline__ void shade_batch(const float* __restrict__ verts, const int4* __restrict__ xv,
+                                            const Mat4& M, const int32_t* __restrict__ idx, int W, int H,
+                                            const float L[3], const int (&t)[N], const int (&Px)[N], int Py,
+                                            float4 (&c)[N]) {
+  int vi[N][3];
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) vi[k][j] = t[k] >= 0 ? __ldg(idx + 3ll * t[k] + j) : 0;
+  int4 cv[N][3];
+  float4 nm[N][3];
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (t[k] < 0) continue;
+      if (xv) cv[k][j] = __ldg(xv + vi[k][j]);
+      else {
+        const float4 p = load_pos(verts, vi[k][j]);
+        cv[k][j] = make_int4(__float_as_int(p.x), __float_as_int(p.y), __float_as_int(p.z), __float_as_int(p.w));
+      }
+      nm[k][j] = __ldg(reinterpret_cast<const float4*>(verts + 8ll * vi[k][j] + 4));
+    }
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    c[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t[k] < 0) continue;
+    if (!xv)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        cv[k][j] = transform_vertex(make_float4(__int_as_float(cv[k][j].x), __int_as_float(cv[k][j].y),
+                                                __int_as_float(cv[k][j].z), __int_as_float(cv[k][j].w)), M, W, H);
+    c[k] = shade_math(cv[k][0], cv[k][1], cv[k][2], nm[k][0], nm[k][1], nm[k][2], vi[k][0], vi[k][1],
+                      vi[k][2], W, H, L, Px[k], Py);
+  }
 }
 
 __device__ __forceinline__ void normalise_light(const float in[3], float L[3]) {
@@ -1775,6 +2236,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   }
 }
 
+#ifndef PIKO_TILE_TU
 // ---------------------------------------------------------------------------
 // FreePipe (NEXT-3 design alternative): the whole pipeline fused
 // into one kernel with static (DirectMap) triangle -> thread mapping; fragments
@@ -2005,6 +2467,8 @@ __global__ void __launch_bounds__(256) k_bl_clear(BaselineArgs a) {
 // K7 (multi-GPU rank 0): resolve gathered tile keys -> shaded frame
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_resolve(const __grid_constant__ ResolveArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const Grid g = a.g;
   const int x = blockIdx.x * 32 + (threadIdx.x & 31);
   const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -2044,10 +2508,72 @@ __global__ void __launch_bounds__(256) k_resolve(const __grid_constant__ Resolve
     prim = (int)(unsigned)(key & 0xFFFFFFFFu);
     depth = __uint_as_float((unsigned)(key >> 32));
     c = shade(a.verts, a.xv, &a.M, a.idx, g.W, g.H, L, prim, 256 * x + 128, 256 * y + 128);
+    if (a.sc.iters && !a.sc.forward) shader_sink(a.sc, shader_work(a.sc.iters, depth));
   }
   reinterpret_cast<float4*>(a.out_rgba)[o] = c;
   a.out_depth[o] = depth;
   a.out_primid[o] = prim;
+}
+
+// ---------------------------------------------------------------------------
+// k_shade: single-GPU deferred resolve (Composite + Fragment Shader of the
+// winners).  k_tile left the packed (depth, primID) key of every
+// pixel in bin-major tiles; each thread shades a quad of 4 pixels of a row
+// with the loads of all 4 in flight together, then writes RGBA, depth and
+// primID with vector stores.  Full occupancy (no shared memory): the
+// dependent gathers of shading are hidden across warps instead of sitting on
+// k_tile's per-bin critical path.
+// ---------------------------------------------------------------------------
+constexpr int SHADE_QUAD = 4;
+__global__ void __launch_bounds__(256) k_shade(const __grid_constant__ ResolveArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const Grid g = a.g;
+  const int qx = (g.W + SHADE_QUAD - 1) / SHADE_QUAD;
+  const long long q = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (q >= (long long)qx * g.H) return;
+  const int y = (int)(q / qx), x0 = (int)(q % qx) * SHADE_QUAD;
+  const int bw = 1 << g.bw_log2, bh = 1 << g.bh_log2;
+  const int b = (y >> g.bh_log2) * g.binsX + (x0 >> g.bw_log2);
+  const int p = (y & (bh - 1)) * bw + (x0 & (bw - 1));
+  // bins are >= 8 px wide and x0 % 4 == 0: the quad is 4 consecutive keys of one bin row
+  const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(a.all_keys + (size_t)b * (size_t)(bw * bh) + p);
+  const ulonglong2 k01 = __ldcs(kp), k23 = __ldcs(kp + 1);
+  const u64 key[SHADE_QUAD] = {k01.x, k01.y, k23.x, k23.y};
+  float L[3];
+  normalise_light(a.light, L);
+  int t[SHADE_QUAD], Px[SHADE_QUAD];
+#pragma unroll
+  for (int k = 0; k < SHADE_QUAD; ++k) {
+    t[k] = (key[k] != CLEAR_KEY && x0 + k < g.W) ? (int)(unsigned)(key[k] & 0xFFFFFFFFu) : -1;
+    Px[k] = 256 * (x0 + k) + 128;
+  }
+  float4 c[SHADE_QUAD];
+  shade_batch<SHADE_QUAD>(a.verts, a.xv, a.M, a.idx, g.W, g.H, L, t, Px, 256 * y + 128, c);
+  float dep[SHADE_QUAD];
+  int prim[SHADE_QUAD];
+#pragma unroll
+  for (int k = 0; k < SHADE_QUAD; ++k) {
+    dep[k] = t[k] >= 0 ? key_depth(key[k]) : 1.0f;
+    prim[k] = t[k];
+    if (t[k] >= 0 && a.sc.iters && !a.sc.forward) shader_sink(a.sc, shader_work(a.sc.iters, dep[k]));
+  }
+  const size_t o = (size_t)y * g.W + x0;
+  if (x0 + SHADE_QUAD <= g.W && (o & 3) == 0) {
+    float4* rp = reinterpret_cast<float4*>(a.out_rgba) + o;
+#pragma unroll
+    for (int k = 0; k < SHADE_QUAD; ++k) __stcs(rp + k, c[k]);
+    __stcs(reinterpret_cast<float4*>(a.out_depth + o), make_float4(dep[0], dep[1], dep[2], dep[3]));
+    __stcs(reinterpret_cast<int4*>(a.out_primid + o), make_int4(prim[0], prim[1], prim[2], prim[3]));
+  } else {
+#pragma unroll
+    for (int k = 0; k < SHADE_QUAD; ++k) {
+      if (x0 + k >= g.W) break;
+      reinterpret_cast<float4*>(a.out_rgba)[o + k] = c[k];
+      a.out_depth[o + k] = dep[k];
+      a.out_primid[o + k] = prim[k];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -2069,15 +2595,11 @@ static cudaError_t launch_ex(Kern kern, int grid, int threads, size_t smem, bool
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-static int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
+static int sm_count() {  // of the current device (contexts may live on different GPUs)
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
 }
 
 cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s) {
@@ -2109,13 +2631,22 @@ cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream
 cudaError_t launch_bin_scan(const RadixArgs& a, int grid, bool pdl, cudaStream_t s) {
   return launch_ex(k_bin_scan, grid, SCAN_THREADS, 0, pdl, s, a);
 }
+cudaError_t launch_cm_scan(const CmArgs& a, int grid, bool pdl, cudaStream_t s) {
+  return launch_ex(k_cm_scan, grid, 256, 0, pdl, s, a);
+}
+cudaError_t launch_cm_scatter(const CmArgs& a, int grid, bool pdl, cudaStream_t s) {
+  const size_t smem = sizeof(CmSmem);
+  cudaError_t e = cudaFuncSetAttribute(k_cm_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_ex(k_cm_scatter, grid, CM_THREADS, smem, pdl, s, a);
+}
 
-struct TileKernel {
-  void (*fn)(TileArgs) = nullptr;
-  int threads = 0;
-  size_t smem = 0;
-};
+#endif  // PIKO_TILE_TU
 
+// k_tile instantiations (16 bin shapes x coverage x keys-only): with
+// -DPIKO_SPLIT_TILES they are compiled in four extra translation units
+// (-DPIKO_TILE_TU=8/16/32/64, one per bin width) in parallel with this one.
+#if !defined(PIKO_SPLIT_TILES) || defined(PIKO_TILE_TU)
 template <int BW, int BH>
 static TileKernel tile_kernel_t(bool cov, bool keys_only) {
   constexpr int NPX = BW * BH;
@@ -2127,15 +2658,36 @@ static TileKernel tile_kernel_t(bool cov, bool keys_only) {
   else k.fn = cov ? k_tile<BW, BH, THREADS, true, false> : k_tile<BW, BH, THREADS, false, false>;
   return k;
 }
+#define PIKO_TILE_BW(W_)                                                              \
+  TileKernel tile_kernel_bw##W_(int bh, bool cov, bool keys_only) {                   \
+    if (bh == 8) return tile_kernel_t<W_, 8>(cov, keys_only);                        \
+    if (bh == 16) return tile_kernel_t<W_, 16>(cov, keys_only);                      \
+    if (bh == 32) return tile_kernel_t<W_, 32>(cov, keys_only);                      \
+    if (bh == 64) return tile_kernel_t<W_, 64>(cov, keys_only);                      \
+    return TileKernel{};                                                              \
+  }
+#if !defined(PIKO_TILE_TU) || PIKO_TILE_TU == 8
+PIKO_TILE_BW(8)
+#endif
+#if !defined(PIKO_TILE_TU) || PIKO_TILE_TU == 16
+PIKO_TILE_BW(16)
+#endif
+#if !defined(PIKO_TILE_TU) || PIKO_TILE_TU == 32
+PIKO_TILE_BW(32)
+#endif
+#if !defined(PIKO_TILE_TU) || PIKO_TILE_TU == 64
+PIKO_TILE_BW(64)
+#endif
+#endif
 
-#define PIKO_TILE_CASE(W_, H_) \
-  if (bw == W_ && bh == H_) return tile_kernel_t<W_, H_>(cov, keys_only);
-
+#ifndef PIKO_TILE_TU
 static TileKernel tile_kernel(int bw, int bh, bool cov, bool keys_only) {
-  PIKO_TILE_CASE(8, 8) PIKO_TILE_CASE(8, 16) PIKO_TILE_CASE(8, 32) PIKO_TILE_CASE(8, 64)
-  PIKO_TILE_CASE(16, 8) PIKO_TILE_CASE(16, 16) PIKO_TILE_CASE(16, 32) PIKO_TILE_CASE(16, 64)
-  PIKO_TILE_CASE(32, 8) PIKO_TILE_CASE(32, 16) PIKO_TILE_CASE(32, 32) PIKO_TILE_CASE(32, 64)
-  PIKO_TILE_CASE(64, 8) PIKO_TILE_CASE(64, 16) PIKO_TILE_CASE(64, 32) PIKO_TILE_CASE(64, 64)
+  switch (bw) {
+    case 8: return tile_kernel_bw8(bh, cov, keys_only);
+    case 16: return tile_kernel_bw16(bh, cov, keys_only);
+    case 32: return tile_kernel_bw32(bh, cov, keys_only);
+    case 64: return tile_kernel_bw64(bh, cov, keys_only);
+  }
   return TileKernel{};
 }
 
@@ -2185,10 +2737,23 @@ cudaError_t launch_baseline(const BaselineArgs& a, int stage, bool pdl, cudaStre
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s) {
-  dim3 grid((a.g.W + 31) / 32, (a.g.H + 7) / 8);
-  k_resolve<<<grid, 256, 0, s>>>(a);
-  return cudaGetLastError();
+cudaError_t launch_shade(const ResolveArgs& a, bool pdl, cudaStream_t s) {
+  const long long nq = (long long)((a.g.W + SHADE_QUAD - 1) / SHADE_QUAD) * a.g.H;
+  return launch_ex(k_shade, (int)((nq + 255) / 256), 256, 0, pdl, s, a);
 }
+cudaError_t launch_resolve(const ResolveArgs& a, bool pdl, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((a.g.W + 31) / 32, (a.g.H + 7) / 8);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_resolve, a);
+}
+
+#endif  // PIKO_TILE_TU
 
 }  // namespace piko

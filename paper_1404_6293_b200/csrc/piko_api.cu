@@ -67,6 +67,7 @@ bool pow2_in(int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1))
 
 struct piko_ctx {
   int device = 0;
+  int sms = 148;            // multiprocessors of this context's device
   Grid g{};
   int bw = 0, bh = 0;
   int npass = 0;
@@ -112,7 +113,7 @@ struct piko_ctx {
   long long gcap = 0;
   // grid sizes of the last frame: the ticket/tag scheme of Control needs them
   // constant, so a change forces a reset of the control block + status words
-  long long last_grids[4] = {-1, -1, -1, -1};
+  long long last_grids[6] = {-1, -1, -1, -1, -1, -1};
   bool need_reset = true;
   bool pdl = true;
   int vs_mode = -1;        // vertex stage: -1 auto, 0 fused into k_setup, 1 separate k_vertex
@@ -137,6 +138,18 @@ struct piko_ctx {
   unsigned long long* all_keys = nullptr;   // rank 0: [nranks][owned_max][bw*bh]
   int owned_max = 0;
   bool keys_mode = false;                   // inside piko_draw_tile_keys
+  // single GPU: k_tile writes packed keys only and a separate full-occupancy
+  // k_resolve shades the frame (removes the per-pixel dependent shading
+  // gathers from the per-bin critical path of k_tile)
+  int deferred = 0;
+  // count-matrix AssignBin (NB <= CM_MAX_NB; radix passes otherwise)
+  int cm_mode = -1;                         // -1 auto, 0 radix, 1 count matrix
+  int cm_tc_log2 = 0;                       // forced log2 triangles per row (0: auto)
+  uint32_t* cm = nullptr; uint32_t* cp = nullptr; long long cm_cap = 0;  // [rows][NB]
+  unsigned long long* cm_status = nullptr;  // [cm_scan_grid]
+  bool last_cm = false;                     // the last frame used the count matrix
+  int32_t* prims_out = nullptr;             // CSR bin_prims of the last frame
+  unsigned long long* def_keys = nullptr;   // [NB][bw*bh]
   int pipeline = PIKO_PIPE_BINNED;
   unsigned long long* fp_keys = nullptr;    // FreePipe full-screen key buffer
   ShaderCost sc{};                          // pixel-shader complexity knob (NEXT-3)
@@ -224,6 +237,8 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   piko_ctx* ctx = new (std::nothrow) piko_ctx();
   if (!ctx) { g_create_error = "out of host memory"; return nullptr; }
   cudaGetDevice(&ctx->device);
+  if (cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess || ctx->sms <= 0)
+    ctx->sms = 148;
   ctx->bw = bin_w; ctx->bh = bin_h;
   Grid& g = ctx->g;
   g.W = width; g.H = height;
@@ -259,6 +274,9 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   memset(ctx->h_ctl, 0, sizeof(Control));
   if (const char* e = getenv("PIKO_NO_PDL")) ctx->pdl = e[0] == '0';
   if (const char* e = getenv("PIKO_SEPARATE_VS")) ctx->vs_mode = e[0] == '0' ? 0 : 1;
+  if (const char* e = getenv("PIKO_DEFERRED")) ctx->deferred = e[0] == '0' ? 0 : 1;
+  if (const char* e = getenv("PIKO_CM")) ctx->cm_mode = e[0] == '0' ? 0 : 1;
+  if (const char* e = getenv("PIKO_CM_TC_LOG2")) ctx->cm_tc_log2 = atoi(e);
   return ctx;
 }
 
@@ -276,7 +294,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   }
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
                   ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
-                  ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys,
+                  ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys, ctx->def_keys, ctx->cm, ctx->cp, ctx->cm_status,
                   ctx->all_keys, ctx->fp_keys, ctx->ovq, ctx->sc.sink, ctx->bl_keys, ctx->frag_key,
                   ctx->frag_px, ctx->frag_rgba};
   for (void* p : bufs)
@@ -311,15 +329,8 @@ static int ensure_tris(piko_ctx* ctx, long long T) {
 
 // look-back status words: enough chunks for the expand pass (>= 256 triangles
 // per chunk) and for the pair passes
-static long long rx_slots() {  // radix CTAs resident at once
-  static long long slots = 0;
-  if (!slots) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    slots = (long long)RX_MIN_CTAS * (sms > 0 ? sms : 148);
-  }
-  return slots;
+static long long rx_slots(const piko_ctx* ctx) {  // radix CTAs resident at once
+  return (long long)RX_MIN_CTAS * ctx->sms;
 }
 
 static int alloc_rx_status(piko_ctx* ctx) {
@@ -524,6 +535,38 @@ static int enqueue_baseline(piko_ctx* ctx, const float* verts, long long V, cons
   return PIKO_OK;
 }
 
+// Count-matrix AssignBin for this frame?  Rows of 2^cm_shift triangles (a
+// multiple of K1_CHUNK): enough rows for about two resident scatter CTAs per
+// SM, fewer (longer) rows when rows x NB would exceed CM_MAX_ENTRIES.
+static bool use_cm(const piko_ctx* ctx, long long T, int& shift, long long& rows) {
+  if (ctx->cm_mode == 0 || ctx->npass < 1 || ctx->g.NB > CM_MAX_NB) return false;
+  shift = 10;  // K1_CHUNK
+  if (ctx->cm_tc_log2 >= 10) shift = ctx->cm_tc_log2;
+  else
+    while ((T >> shift) > 2ll * ctx->sms) ++shift;
+  rows = std::max<long long>((T + (1ll << shift) - 1) >> shift, 1);
+  while (rows * ctx->g.NB > CM_MAX_ENTRIES && shift < 30) {
+    ++shift;
+    rows = std::max<long long>((T + (1ll << shift) - 1) >> shift, 1);
+  }
+  return rows * ctx->g.NB <= CM_MAX_ENTRIES;
+}
+
+static int ensure_cm(piko_ctx* ctx, long long rows) {
+  const long long need = rows * ctx->g.NB;
+  if (need > ctx->cm_cap) {
+    if (ctx->cm) cudaFree(ctx->cm);
+    if (ctx->cp) cudaFree(ctx->cp);
+    ctx->cm = nullptr; ctx->cp = nullptr; ctx->cm_cap = 0;
+    CK(cudaMalloc(&ctx->cm, sizeof(uint32_t) * need));
+    CK(cudaMalloc(&ctx->cp, sizeof(uint32_t) * need));
+    ctx->cm_cap = need;
+    ctx->need_reset = true;  // the matrix is zeroed by the reset
+  }
+  if (!ctx->cm_status) CK(cudaMalloc(&ctx->cm_status, sizeof(unsigned long long) * cm_scan_grid(ctx->g.NB)));
+  return PIKO_OK;
+}
+
 static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
                          long long T, const Mat4& M, const float L[3], float* rgba, float* depth,
                          cudaStream_t s, unsigned long long* keys_out = nullptr) {
@@ -538,7 +581,12 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   // P2P: this frame's key slot (epoch parity) at rank 0
   unsigned long long* p2p_slot = p2p ? ctx->p2p_keys + (size_t)(ctx->epoch & 1) * ctx->mnranks * ctx->owned_max * tile_px
                                      : nullptr;
-  const bool keys_only = gather || keys_out != nullptr;
+  // single GPU, no debug coverage: keys-only tile kernel + k_resolve
+  const bool defer = !gather && keys_out == nullptr && ctx->deferred && ctx->mnranks == 1 &&
+                     !(ctx->debug & PIKO_DEBUG_COVERAGE_COUNT);
+  if (defer && !ctx->def_keys)
+    CK(cudaMalloc(&ctx->def_keys, sizeof(unsigned long long) * (size_t)ctx->g.NB * tile_px));
+  const bool keys_only = gather || keys_out != nullptr || defer;
   cudaEvent_t* ev = ctx->prof ? ctx->frame_events() : nullptr;
   if (ctx->prof && !ev) return ctx->fail(PIKO_ECUDA, "cannot create profiling events");
   auto mark = [&](int stage) -> cudaError_t { return ev ? cudaEventRecord(ev[stage], s) : cudaSuccess; };
@@ -546,11 +594,17 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   const long long ntiles = (ctx->g.NB + SCAN_CHUNK - 1) / SCAN_CHUNK;
   const long long gx = std::max<long long>((T + ctx->tri_chunk - 1) / ctx->tri_chunk, 1);  // pass 0
   const long long gp = (long long)((ctx->pair_cap + RX_CHUNK - 1) / RX_CHUNK);              // passes >= 1
-  const long long grids[4] = {g1, gx, gp + ntiles, ntiles};
+  int cm_shift = 0;
+  long long cm_rows = 0;
+  const bool cm = use_cm(ctx, T, cm_shift, cm_rows);
+  if (cm && ensure_cm(ctx, cm_rows) != PIKO_OK) return PIKO_ECUDA;
+  const long long grids[6] = {g1, gx, gp + ntiles, ntiles, cm ? 1 : 0, cm ? cm_rows : 0};
   CK(mark(0));
   bool changed = ctx->need_reset;
-  for (int k = 0; k < 4; ++k) changed |= grids[k] != ctx->last_grids[k];
+  for (int k = 0; k < 6; ++k) changed |= grids[k] != ctx->last_grids[k];
   if (changed) {
+    if (ctx->cm) CK(cudaMemsetAsync(ctx->cm, 0, sizeof(uint32_t) * ctx->cm_cap, s));
+    if (ctx->cm_status) CK(cudaMemsetAsync(ctx->cm_status, 0, sizeof(unsigned long long) * cm_scan_grid(ctx->g.NB), s));
     // tickets restart at 0, so every tag-carrying status word must be cleared
     CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s));
     CK(cudaMemsetAsync(ctx->st_scan, 0, sizeof(unsigned long long) * ctx->st_scan_n, s));
@@ -561,13 +615,13 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     CK(cudaMemsetAsync(ctx->arrive, 0, sizeof(uint32_t) * ctx->g.NB, s));
     CK(cudaMemsetAsync(ctx->gkey, 0xFF, sizeof(unsigned long long) * ctx->g.NB * ctx->bw * ctx->bh, s));
     if (ctx->gcov) CK(cudaMemsetAsync(ctx->gcov, 0, sizeof(uint32_t) * ctx->g.NB * ctx->bw * ctx->bh, s));
-    for (int k = 0; k < 4; ++k) ctx->last_grids[k] = grids[k];
+    for (int k = 0; k < 6; ++k) ctx->last_grids[k] = grids[k];
     ctx->need_reset = false;
   }
   CK(mark(1 + PIKO_STAGE_CLEAR));
   const bool sep = separate_vs(ctx, V, T);
-  ctx->last_kernels = 2 + ctx->npass + (ctx->npass == 1 ? 1 : 0) +
-                      (sep ? 1 + (V < 0 && T > 0 ? 1 : 0) : 0) + (gather && ctx->mrank == 0 ? 1 : 0);
+  ctx->last_kernels = 2 + (cm ? 2 : ctx->npass + (ctx->npass == 1 ? 1 : 0)) +
+                      (sep ? 1 + (V < 0 && T > 0 ? 1 : 0) : 0) + (gather && ctx->mrank == 0 ? 1 : 0) + (defer ? 1 : 0);
   if (sep) {
     if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
     VertexArgs a{};
@@ -580,11 +634,14 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     SetupArgs a{};
     a.xv = sep ? ctx->xv : nullptr; a.xv_cap = ctx->xv_cap; a.verts = verts; a.M = M;
     a.idx = idx; a.n_tris = T; a.g = ctx->g;
-    a.npass = ctx->npass; a.rec = ctx->rec; a.rect = ctx->rect; a.ctl = ctx->ctl;
+    a.npass = cm ? 0 : ctx->npass; a.rec = ctx->rec; a.rect = ctx->rect; a.ctl = ctx->ctl;
+    a.cm = cm ? ctx->cm : nullptr; a.cm_shift = cm_shift;
     CK(launch_setup(a, (int)g1, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_SETUP));
-  for (int p = 0; p < ctx->npass; ++p) {
+  ctx->prims_out = cm ? ctx->vals[0] : ctx->vals[ctx->npass & 1];
+  ctx->last_cm = cm;
+  for (int p = 0; p < (cm ? 0 : ctx->npass); ++p) {
     RadixArgs a{};
     a.expand = p == 0; a.rect = ctx->rect; a.n_tris = T; a.tri_chunk = ctx->tri_chunk;
     a.g = ctx->g; a.cap = ctx->pair_cap; a.scan_here = p == 1;
@@ -606,6 +663,20 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     if (p == 0 && ctx->npass == 1) CK(launch_bin_scan(a, (int)ntiles, ctx->pdl, s));
     if (p == 0) CK(mark(1 + PIKO_STAGE_EXPAND));
   }
+  if (cm) {
+    CmArgs c{};
+    c.cm = ctx->cm; c.cp = ctx->cp; c.rows = cm_rows; c.cm_shift = cm_shift; c.status = ctx->cm_status;
+    c.rect = ctx->rect; c.n_tris = T; c.g = ctx->g; c.cap = ctx->pair_cap; c.bin_prims = ctx->prims_out;
+    c.ctl = ctx->ctl;
+    RadixArgs& a = c.sched;
+    a.g = ctx->g; a.ctl = ctx->ctl; a.bin_start = ctx->bin_start; a.NB = ctx->g.NB;
+    a.rank = ctx->g.rank; a.nranks = ctx->g.nranks;
+    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
+    a.frag = tile_frag(ctx->bw, ctx->bh); a.npx = ctx->bw * ctx->bh;
+    CK(launch_cm_scan(c, cm_scan_grid(ctx->g.NB), ctx->pdl, s));
+    CK(mark(1 + PIKO_STAGE_EXPAND));
+    CK(launch_cm_scatter(c, (int)(cm_rows + ntiles), ctx->pdl, s));
+  }
   if (ctx->npass == 0) CK(mark(1 + PIKO_STAGE_EXPAND));
   CK(mark(1 + PIKO_STAGE_SORT));
   {
@@ -614,12 +685,13 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.verts = verts; a.xv = sep ? ctx->xv : nullptr; a.M = M; a.idx = idx;
     a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
     a.g = ctx->g; a.npass = ctx->npass; a.rec = ctx->rec; a.bin_start = ctx->bin_start;
-    a.bin_prims = ctx->vals[ctx->npass & 1]; a.ctl = ctx->ctl;
+    a.bin_prims = ctx->prims_out; a.ctl = ctx->ctl;
     a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
     a.out_cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
     a.tile_keys = keys_out ? keys_out
                 : p2p    ? p2p_slot + (size_t)ctx->mrank * ctx->owned_max * tile_px
-                : gather ? ctx->tile_keys : nullptr;
+                : gather ? ctx->tile_keys
+                : defer  ? ctx->def_keys : nullptr;
     if (p2p) {
       a.p2p_flag = ctx->p2p_sync + ctx->mrank;
       a.p2p_done = ctx->p2p_sync + ctx->mnranks;
@@ -690,10 +762,19 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
         a.p2p_timeout = &ctx->ctl->p2p_timeout;
         a.epoch = ctx->epoch;
       }
-      CK(launch_resolve(a, s));
+      CK(launch_resolve(a, false, s));
     }
   } else {
     CK(mark(1 + PIKO_STAGE_GATHER));
+    if (defer) {
+      ResolveArgs a{};
+      a.verts = verts; a.xv = sep ? ctx->xv : nullptr; a.M = M; a.idx = idx;
+      a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
+      a.g = ctx->g; a.all_keys = ctx->def_keys; a.owned_max = ctx->owned;
+      a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
+      a.sc = ctx->sc;
+      CK(launch_shade(a, ctx->pdl, s));
+    }
   }
   CK(mark(1 + PIKO_STAGE_RESOLVE));
   if (ev) ++ctx->prof_frames;
@@ -720,7 +801,7 @@ static void adapt_tri_chunk(piko_ctx* ctx) {
   // one wave of resident radix CTAs.  Smaller chunks finish sooner and are
   // less likely to exceed RX_CHUNK where the pairs per triangle vary a lot
   // (c2: near spheres' triangles cover several bins, far ones one).
-  const long long slots = rx_slots();
+  const long long slots = rx_slots(ctx);
   const long long per_wave = ((long long)T + slots - 1) / slots;
   tc = std::min<long long>(tc, (per_wave + RX_THREADS - 1) / RX_THREADS * RX_THREADS);
 #endif
@@ -914,7 +995,7 @@ extern "C" int piko_get_bins(const piko_ctx* cctx, const int32_t** d_bin_start,
   int rc = check_frame(ctx);
   if (rc != PIKO_OK) return rc;
   *d_bin_start = ctx->bin_start;
-  *d_bin_prims = ctx->vals[ctx->npass & 1];
+  *d_bin_prims = ctx->prims_out ? ctx->prims_out : ctx->vals[ctx->npass & 1];
   *n_pairs = (int64_t)ctx->h_ctl->n_pairs;
   return PIKO_OK;
 }
@@ -1179,7 +1260,7 @@ extern "C" int piko_resolve_keys(piko_ctx* ctx, const float* verts, int64_t n_ve
   a.all_keys = reinterpret_cast<const unsigned long long*>(d_all_keys);
   a.owned_max = (ctx->g.NB + nranks - 1) / nranks;
   a.out_rgba = out_rgba; a.out_depth = out_depth; a.out_primid = ctx->primid;
-  CK(launch_resolve(a, s));
+  CK(launch_resolve(a, false, s));
   return PIKO_OK;
 }
 

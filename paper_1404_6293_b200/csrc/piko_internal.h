@@ -49,7 +49,13 @@ constexpr int LIST_EMPTY = NLIST - 1;
 #endif
 constexpr int FRAG_ROUNDS = PIKO_FRAG_ROUNDS;  // fragment = FRAG_ROUNDS * threads-per-CTA pairs
 constexpr int EMPTY_GROUP = 8;   // empty bins per k_tile queue ticket
-constexpr int OVQ_CAP = 1024;    // k_tile: spilled large-triangle entries per CTA (96 B each)
+constexpr int OVQ_CAP = 1024;
+// Count-matrix AssignBin: used when NB <= CM_MAX_NB and the
+// matrix of rows x NB per-row bin counts stays below CM_MAX_ENTRIES.
+constexpr int CM_MAX_NB = 32768;                 // touched-bin bitmap in shared memory
+constexpr long long CM_MAX_ENTRIES = 1ll << 24;  // rows * NB
+constexpr int CM_SUB = 4096;                     // triangles per scatter sub-chunk (registers)
+constexpr int CM_COLS = 16;                      // k_cm_scan: bins per CTA (x 16 row groups)    // k_tile: spilled large-triangle entries per CTA (96 B each)
 
 // ---- persistent device control block ----------------------------------------
 // Never memset per frame: every kernel of a frame takes exactly gridDim.x
@@ -62,6 +68,7 @@ struct Control {
   unsigned long long k1_ticket;
   unsigned long long rx_ticket[MAX_PASSES];
   unsigned long long scan_ticket;      // standalone bin-scan kernel (single-pass grids)
+  unsigned long long cm_ticket;        // k_cm_scan CTA tickets (count-matrix AssignBin)
   unsigned long long frame;            // written by K1 chunk 0
   unsigned int tile_next;              // dynamic bin queue of k_tile (reset by K1 chunk 0)
   unsigned int list_n[NLIST];          // work-list sizes (reset by K1 chunk 0)
@@ -124,7 +131,9 @@ struct SetupArgs {
   const int32_t* idx;
   long long n_tris;
   Grid g;
-  int npass;
+  int npass;                    // radix digit histograms to build (0 in count-matrix mode)
+  uint32_t* cm;                 // count-matrix AssignBin: M[n_tris >> cm_shift][NB] (null: radix mode)
+  int cm_shift;                 // log2 triangles per count-matrix row
   int4* rec;                    // [n_tris][3]
   uint2* rect;                  // [n_tris] tile rect {tx0|ty0<<16, tx1|ty1<<16}; empty if culled
   Control* ctl;
@@ -163,6 +172,27 @@ struct RadixArgs {
   uint32_t* gcov;               // [NB][bw*bh] coverage tiles (debug) or null
   int frag;                     // pairs per fragment
   int npx;                      // pixels per bin
+};
+
+// Count-matrix AssignBin (a3-a6 for NB <= CM_MAX_NB): k_setup adds each
+// triangle's owned bins into row t >> cm_shift of M; k_cm_scan turns M into
+// per-row exclusive column prefixes CP[r][b] = bin_start[b] + sum_{r' < r}
+// M[r'][b] (and bin_start, P); k_cm_scatter writes every row's pairs at
+// CP[r][b] + (stable rank inside the row).  The bin scan work lists reuse
+// RadixArgs (extra CTAs of k_cm_scatter).
+struct CmArgs {
+  uint32_t* cm;                 // [rows][NB] counts (zeroed again by k_cm_scan)
+  uint32_t* cp;                 // [rows][NB] column prefixes / running cursors
+  long long rows;
+  int cm_shift;
+  unsigned long long* status;   // [k_cm_scan grid] look-back words
+  const uint2* rect;
+  long long n_tris;
+  Grid g;
+  unsigned long long cap;       // pair capacity
+  int32_t* bin_prims;           // [P] output CSR values
+  Control* ctl;
+  RadixArgs sched;              // bin_start, work lists (schedule CTAs)
 };
 
 // Pixel-shader complexity: `iters` extra
@@ -230,6 +260,7 @@ struct ResolveArgs {            // rank 0 after the NCCL gather
   unsigned long long* p2p_count;        // CTA ticket (self-resetting modulo grid)
   unsigned* p2p_timeout;
   unsigned long long epoch;
+  ShaderCost sc;                         // deferred shader cost (single-GPU deferred resolve)
 };
 
 // FreePipe variant (sec. 7.2.1): one fused
@@ -287,12 +318,25 @@ cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s);
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s);
 cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream_t s);
 cudaError_t launch_bin_scan(const RadixArgs& a, int grid, bool pdl, cudaStream_t s);
+cudaError_t launch_cm_scan(const CmArgs& a, int grid, bool pdl, cudaStream_t s);
+cudaError_t launch_cm_scatter(const CmArgs& a, int grid, bool pdl, cudaStream_t s);
+inline int cm_scan_grid(int NB) { return (NB + CM_COLS - 1) / CM_COLS; }
 cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
                         bool pdl, cudaStream_t s);
 int tile_grid(int bw, int bh, bool cov, bool keys_only);  // persistent grid size
+struct TileKernel {
+  void (*fn)(TileArgs) = nullptr;
+  int threads = 0;
+  size_t smem = 0;
+};
+TileKernel tile_kernel_bw8(int bh, bool cov, bool keys_only);   // k_tile instantiation of a bin shape
+TileKernel tile_kernel_bw16(int bh, bool cov, bool keys_only);
+TileKernel tile_kernel_bw32(int bh, bool cov, bool keys_only);
+TileKernel tile_kernel_bw64(int bh, bool cov, bool keys_only);
 constexpr int TILE_THREADS = 256;  // k_tile CTA size cap
 inline int tile_threads(int bw, int bh) { return bw * bh < TILE_THREADS ? bw * bh : TILE_THREADS; }
 inline int tile_frag(int bw, int bh) { return FRAG_ROUNDS * tile_threads(bw, bh); }
-cudaError_t launch_resolve(const ResolveArgs& a, cudaStream_t s);
+cudaError_t launch_resolve(const ResolveArgs& a, bool pdl, cudaStream_t s);
+cudaError_t launch_shade(const ResolveArgs& a, bool pdl, cudaStream_t s);  // single-GPU deferred resolve
 
 }  // namespace piko

@@ -15,7 +15,7 @@ def build(name, flags, alt=None):
     import __graft_entry__ as ge
     lib = f"/tmp/libpiko_ab_{name}.so"
     objs = []
-    for src in ge.SOURCES:
+    for src in sorted({src for src, _, _ in ge.SOURCES}):  # one TU per source (no tile split)
         o = f"/tmp/{src}.ab_{name}.o"
         path = alt if (alt and src == "kernels.cu") else os.path.join(ge.CSRC, src)
         subprocess.check_call([ge._nvcc(), *ge.NVCC_FLAGS, *flags, "-I", ge.CSRC, "-c", path, "-o", o])

@@ -1,0 +1,67 @@
+#!/usr/bin/env python
+"""Per-CTA phase timelines (globaltimer ns) of the count-matrix AssignBin
+kernels: builds a -DPIKO_K1_TIMING libpiko, renders frames, prints phases."""
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import __graft_entry__ as ge
+
+lib = f"/tmp/libpiko_cmt{os.getpid()}.so"
+objs = []
+for src in sorted({src for src, _, _ in ge.SOURCES}):
+    o = f"/tmp/{src}.cmt.o"
+    subprocess.check_call([ge._nvcc(), *ge.NVCC_FLAGS, "-DPIKO_K1_TIMING", "-c", os.path.join(ge.CSRC, src), "-o", o])
+    objs.append(o)
+subprocess.check_call([ge._nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib, "-ldl", "-lcudart"])
+import paper_1404_6293_b200 as piko  # noqa: E402
+piko.LIB_PATH = lib
+piko._lib = piko.lib = piko._load()
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import scenes  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
+s = scenes.make(cfg)
+v = torch.from_numpy(s.verts).cuda()
+i = torch.from_numpy(s.idx).cuda()
+r = piko.Renderer(s.W, s.H, 16)
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+for k in range(4):
+    flush.fill_(float(k))
+    r.draw(v, i, s.mvp, s.light)
+torch.cuda.synchronize()
+buf = np.zeros((4, 8192, 8), np.uint64)
+h = ctypes.CDLL(lib)
+assert h.piko_dbg_k1_times(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes)) == 0
+T0 = int(buf[0, 0, 0])
+n1 = (s.n_tris + 1023) // 1024
+kk = buf[0, :n1].astype(np.int64) - T0
+print(f"k_setup: CTAs {n1}, start..end {kk[:,0].min()}..{kk[:,5].max()}, start p50 {np.median(kk[:,0]):.0f}; "
+      f"loads {np.median(kk[:,1]-kk[:,0]):.0f} setup {np.median(kk[:,2]-kk[:,1]):.0f} rest {np.median(kk[:,5]-kk[:,2]):.0f}")
+def rows(k, n):
+    t = buf[k, :n].astype(np.int64)
+    return t[t[:, 0] > T0] - T0
+cs = rows(1, 8000)
+print(f"k_cm_scan: CTAs {len(cs)}, start {cs[:,0].min()}..{cs[:,0].max()}, end max {cs[:,3].max()}; "
+      f"sweep1 {np.median(cs[:,1]-cs[:,0]):.0f} (p90 {np.percentile(cs[:,1]-cs[:,0],90):.0f}), "
+      f"lookback {np.median(cs[:,2]-cs[:,1]):.0f} (p90 {np.percentile(cs[:,2]-cs[:,1],90):.0f}), "
+      f"sweep2 {np.median(cs[:,3]-cs[:,2]):.0f}")
+sc = rows(2, 8000)
+print(f"k_cm_scatter: CTAs {len(sc)}, start {sc[:,0].min()}..{sc[:,0].max()} (p50 {np.median(sc[:,0]):.0f}), "
+      f"pdl-wait done {sc[:,1].min()}..{sc[:,1].max()}")
+names = {1: "pdl wait done", 3: "counts+offsets", 4: "expanded", 5: "digits+cursors", 6: "ranked+written", 2: "end"}
+for k in (1, 3, 4, 5, 6, 2):
+    m = sc[:, k] > 0
+    if m.any():
+        print(f"   {names[k]:16s}: {m.sum()} CTAs, time p50 {np.median(sc[m,k]):.0f} (min {sc[m,k].min()}, max {sc[m,k].max()})")
+u = buf[2, :8000, 7].astype(np.int64)
+u = u[u > 0]
+if len(u):
+    print(f"   U (touched bins per window): p50 {np.median(u):.0f} max {u.max()}")
+t = buf[3, :8192].astype(np.int64)
+t = t[(t[:, 0] > T0) & (t[:, 2] >= t[:, 0])] - T0
+print(f"k_tile bins: first start {t[:,0].min()}, last end {t[:,2].max()}")

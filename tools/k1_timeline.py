@@ -13,7 +13,7 @@ import __graft_entry__ as ge
 extra = [f for f in os.environ.get("PIKO_EXP", "").split() if f]
 lib = f"/tmp/libpiko_timing{os.getpid()}.so"
 objs = []
-for src in ge.SOURCES:
+for src in sorted({src for src, _, _ in ge.SOURCES}):  # one TU per source (no tile split)
     o = f"/tmp/{src}.timing.o"
     subprocess.check_call([ge._nvcc(), *ge.NVCC_FLAGS, "-DPIKO_K1_TIMING", *extra, "-c",
                            os.path.join(ge.CSRC, src), "-o", o])
