@@ -322,12 +322,20 @@ def piko_get_profile(ctx):
 class Renderer:
     """Owns a piko_ctx plus torch output buffers for one framebuffer shape."""
 
-    def __init__(self, width, height, bin_w=16, bin_h=None, device=None):
+    def __init__(self, width, height, bin_w=16, bin_h=None, device=None, sync="checked"):
+        """sync="checked" (this wrapper's default): every draw waits for its
+        frame and regrows + re-issues on a capacity miss, so the frame read
+        afterwards is always valid; "async" keeps the C ABI default
+        (piko_draw only enqueues; errors surface at a later draw or finish)."""
         import torch
         bin_h = bin_w if bin_h is None else bin_h
         self.device = torch.device(device or "cuda")
         with torch.cuda.device(self.device):
             self.ctx = piko_create(width, height, bin_w, bin_h)
+        if sync == "checked":
+            piko_set_sync(self.ctx, PIKO_SYNC_CHECKED)
+        elif sync != "async":
+            raise ValueError("sync must be 'checked' or 'async'")
         self.W, self.H, self.bin_w, self.bin_h = width, height, bin_w, bin_h
         self.rgba = torch.empty((height, width, 4), dtype=torch.float32, device=self.device)
         self.depth = torch.empty((height, width), dtype=torch.float32, device=self.device)

@@ -1774,6 +1774,8 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     __syncthreads();
   }
   TL_CTA(0);
+  if (a.status_word && blockIdx.x == 0 && tid == 0)  // multi-GPU: overflow travels with the keys
+    *a.status_word = ovf ? 0ull : a.status_ok;
   if (blockIdx.x == 0) {  // reset the next frame's double-buffered accumulators
     unsigned* h = &a.ctl->digit_hist[(frame + 1) & 1][0][0];
     for (int i = tid; i < MAX_PASSES * RX_RADIX; i += THREADS) h[i] = 0;
@@ -2485,8 +2487,16 @@ __global__ void __launch_bounds__(256) k_resolve(const __grid_constant__ Resolve
     const int b = (y >> g.bh_log2) * g.binsX + (x >> g.bw_log2);
     const int r = b % g.nranks, k = b / g.nranks;
     const int p = (y & (bh - 1)) * bw + (x & (bw - 1));
+    const size_t rs = a.rank_stride ? (size_t)a.rank_stride : (size_t)a.owned_max * (size_t)(bw * bh);
     // written by peers: bypass L1
-    key = __ldcg(&a.all_keys[((size_t)r * a.owned_max + k) * (size_t)(bw * bh) + p]);
+    key = __ldcg(&a.all_keys[(size_t)r * rs + (size_t)k * (size_t)(bw * bh) + p]);
+  }
+  if (a.status && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    // a rank that overflowed its pair capacity sent empty bins: rank 0's
+    // frame is incomplete and its host reports PIKO_ECAPACITY
+    bool bad = false;
+    for (int q = 0; q < a.nstatus; ++q) bad |= __ldcg(a.status + (size_t)q * a.status_stride) != a.status_ok;
+    if (bad) a.ctl->peer_overflow = a.ctl->frame + 1;
   }
   if (a.p2p_flags) {  // this CTA's keys are read: the last CTA releases the slot
     __syncthreads();

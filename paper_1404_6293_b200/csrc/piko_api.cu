@@ -73,7 +73,7 @@ struct piko_ctx {
   int npass = 0;
   int owned = 0;            // bins owned by this rank
   unsigned debug = 0;
-  int sync_mode = PIKO_SYNC_CHECKED;
+  int sync_mode = PIKO_SYNC_ASYNC;   // piko_draw returns once enqueued
   bool virt = false;        // virtual rank (partition without communicator)
   int multi = PIKO_MULTI_SORT_FIRST;
   int mrank = 0, mnranks = 1;  // multi-GPU rank / size (sort-last: g.rank = 0, g.nranks = 1)
@@ -119,10 +119,19 @@ struct piko_ctx {
   int vs_mode = -1;        // vertex stage: -1 auto, 0 fused into k_setup, 1 separate k_vertex
   int32_t* primid = nullptr;
   uint32_t* cov = nullptr;
-  Control* h_ctl = nullptr;          // pinned mirror of the control block
-  cudaEvent_t done = nullptr;
-  bool pending = false;              // a frame's status not yet checked
-  int last_status = PIKO_OK;
+  // Asynchronous frames (piko_draw returns once enqueued).  Each
+  // enqueued frame copies its control block into a pinned mirror of a ring
+  // slot and records an event; a frame's status is evaluated when its event
+  // has completed -- polled without blocking at the next draw, waited for
+  // only when the ring is full, at piko_finish, or by an inspection call.
+  static constexpr int NRING = 8;
+  struct Slot { Control* h = nullptr; cudaEvent_t ev = nullptr; long long T = 0; };
+  Slot ring[NRING];
+  int ring_head = 0, ring_n = 0;     // next slot to fill; frames in flight
+  Control* h_ctl = nullptr;          // mirror of the last evaluated frame
+  bool pending = false;              // ring_n > 0
+  int last_status = PIKO_OK;         // status of the last evaluated frame
+  int sticky = PIKO_OK;              // first error of an async frame not yet returned
   long long last_T = 0;
   int last_kernels = 0;                // kernels launched by the last frame
 
@@ -195,6 +204,8 @@ struct piko_ctx {
 
 extern "C" int64_t piko_owned_bins(int, int, int, int, int, int, int32_t*, int64_t);
 
+constexpr int P2P_STATUS = 128;  // p2p_sync words of rank 0 where rank r's frame status lands: [128 + 2r + parity] (R <= 127)
+
 // ranks exchange keys with rank 0 (NCCL communicator or P2P buffers)
 static bool exchanging(const piko_ctx* ctx) {
   return (ctx->comm != nullptr || ctx->p2p_keys != nullptr) && ctx->mnranks > 1;
@@ -259,8 +270,10 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
             cudaMalloc(&ctx->ctl, sizeof(Control)) == cudaSuccess &&
             cudaMalloc(&ctx->primid, sizeof(int32_t) * npx) == cudaSuccess &&
             cudaMalloc(&ctx->sc.sink, 16) == cudaSuccess &&
-            cudaMallocHost(&ctx->h_ctl, sizeof(Control)) == cudaSuccess &&
-            cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming) == cudaSuccess;
+            cudaMallocHost(&ctx->h_ctl, sizeof(Control)) == cudaSuccess;
+  for (int k = 0; k < piko_ctx::NRING && ok; ++k)
+    ok = cudaMallocHost(&ctx->ring[k].h, sizeof(Control)) == cudaSuccess &&
+         cudaEventCreateWithFlags(&ctx->ring[k].ev, cudaEventDisableTiming) == cudaSuccess;
   ctx->st_scan_n = (g.NB + SCAN_CHUNK - 1) / SCAN_CHUNK;
   ok = ok && cudaMalloc(&ctx->st_scan, sizeof(unsigned long long) * ctx->st_scan_n) == cudaSuccess;
   ok = ok && cudaMemset(ctx->bin_count, 0, sizeof(uint32_t) * g.NB) == cudaSuccess &&
@@ -283,7 +296,8 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
 extern "C" void piko_destroy(piko_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  cudaDeviceSynchronize();
+  for (int k = 0; k < ctx->ring_n; ++k)  // this context's frames in flight (not the whole device)
+    cudaEventSynchronize(ctx->ring[(ctx->ring_head - ctx->ring_n + k + piko_ctx::NRING) % piko_ctx::NRING].ev);
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   if (ctx->p2p_ipc) {
     cudaIpcCloseMemHandle(ctx->p2p_keys);
@@ -300,8 +314,11 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+  for (auto& sl : ctx->ring) {
+    if (sl.h) cudaFreeHost(sl.h);
+    if (sl.ev) cudaEventDestroy(sl.ev);
+  }
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
-  if (ctx->done) cudaEventDestroy(ctx->done);
   delete ctx;
 }
 
@@ -407,6 +424,52 @@ static int ensure_cov(piko_ctx* ctx) {
   return PIKO_OK;
 }
 
+// ---- frame status ring --------------------------------------------------------
+static int eval_frame(piko_ctx* ctx, piko_ctx::Slot& sl);
+
+// Evaluate finished frames in order; block only if `block` (all of them) --
+// otherwise stop at the first frame still running.  Errors of async frames
+// accumulate in ctx->sticky (the first one wins).
+static int poll_frames(piko_ctx* ctx, bool block) {
+  while (ctx->ring_n > 0) {
+    piko_ctx::Slot& sl = ctx->ring[(ctx->ring_head - ctx->ring_n + piko_ctx::NRING) % piko_ctx::NRING];
+    if (block) {
+      CK(cudaEventSynchronize(sl.ev));
+    } else {
+      const cudaError_t q = cudaEventQuery(sl.ev);
+      if (q == cudaErrorNotReady) break;
+      if (q != cudaSuccess) CK(q);
+    }
+    --ctx->ring_n;
+    const int rc = eval_frame(ctx, sl);
+    if (rc != PIKO_OK && ctx->sticky == PIKO_OK) ctx->sticky = rc;
+  }
+  ctx->pending = ctx->ring_n > 0;
+  return PIKO_OK;
+}
+
+// Queue the end of a frame: its control block into the next ring slot's
+// pinned mirror and an event.  A full ring waits for its oldest frame.
+static cudaError_t record_frame_end(piko_ctx* ctx, cudaStream_t s, long long T) {
+  if (ctx->ring_n == piko_ctx::NRING && poll_frames(ctx, false) == PIKO_OK && ctx->ring_n == piko_ctx::NRING) {
+    piko_ctx::Slot& old = ctx->ring[ctx->ring_head];  // == oldest when full
+    cudaError_t e = cudaEventSynchronize(old.ev);
+    if (e != cudaSuccess) return e;
+    --ctx->ring_n;
+    const int rc = eval_frame(ctx, old);
+    if (rc != PIKO_OK && ctx->sticky == PIKO_OK) ctx->sticky = rc;
+  }
+  piko_ctx::Slot& sl = ctx->ring[ctx->ring_head];
+  cudaError_t e = cudaMemcpyAsync(sl.h, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaEventRecord(sl.ev, s);
+  if (e != cudaSuccess) return e;
+  sl.T = T;
+  ctx->ring_head = (ctx->ring_head + 1) % piko_ctx::NRING;
+  ++ctx->ring_n;
+  ctx->pending = true;
+  return cudaSuccess;
+}
+
 // ---- one frame ---------------------------------------------------------------
 static int enqueue_freepipe(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
                             long long T, const Mat4& M, const float L[3], float* rgba, float* depth,
@@ -454,9 +517,7 @@ static int enqueue_freepipe(piko_ctx* ctx, const float* verts, long long V, cons
   // a vertex-capacity overflow of k_vertex (vx_overflow / vx_need kept)
   CK(cudaMemsetAsync(ctx->ctl, 0, offsetof(Control, vx_overflow), s));
   CK(cudaMemsetAsync(&ctx->ctl->n_pairs, 0, sizeof(unsigned long long) * 2, s));
-  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s));
-  CK(cudaEventRecord(ctx->done, s));
-  ctx->pending = true;
+  CK(record_frame_end(ctx, s, T));
   ctx->last_T = T;
   ctx->need_reset = true;  // the binned path must not trust tickets touched here
   return PIKO_OK;
@@ -527,9 +588,7 @@ static int enqueue_baseline(piko_ctx* ctx, const float* verts, long long V, cons
   CK(mark(1 + PIKO_STAGE_GATHER));
   CK(mark(1 + PIKO_STAGE_RESOLVE));
   if (ev) ++ctx->prof_frames;
-  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s));
-  CK(cudaEventRecord(ctx->done, s));
-  ctx->pending = true;
+  CK(record_frame_end(ctx, s, T));
   ctx->last_T = T;
   ctx->need_reset = true;  // the binned path must not trust tickets touched here
   return PIKO_OK;
@@ -696,6 +755,12 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
       a.p2p_flag = ctx->p2p_sync + ctx->mrank;
       a.p2p_done = ctx->p2p_sync + ctx->mnranks;
       a.epoch = ctx->epoch;
+      // by epoch parity, like the key slots: a rank may run one frame ahead
+      a.status_word = ctx->p2p_sync + P2P_STATUS + 2 * ctx->mrank + (ctx->epoch & 1);  // ok: the epoch
+      a.status_ok = ctx->epoch;
+    } else if (gather) {
+      a.status_word = ctx->tile_keys + (size_t)ctx->owned_max * tile_px;
+      a.status_ok = 1;
     }
     a.owned = ctx->owned;
     a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
@@ -723,22 +788,22 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
       // keys already at rank 0 (stored by k_tile over NVLink); nothing to send
     } else if (ctx->multi == PIKO_MULTI_SORT_LAST) {
       // element-wise (depth, primID) minimum of the full key images on rank 0
+      // (+ the status word: the minimum is 0 if any rank overflowed)
       rc = g_nccl.Reduce(ctx->tile_keys, ctx->mrank == 0 ? ctx->all_keys : nullptr,
-                         (size_t)ctx->owned * ctx->bw * ctx->bh, ncclUint64_, ncclMin_, 0, ctx->comm, s);
+                         (size_t)ctx->owned * ctx->bw * ctx->bh + 1, ncclUint64_, ncclMin_, 0, ctx->comm, s);
       if (rc != 0) return ctx->fail(PIKO_ENCCL, "ncclReduce failed: %s", g_nccl.GetErrorString(rc));
     } else {
     if (g_nccl.GroupStart() != 0) return ctx->fail(PIKO_ENCCL, "ncclGroupStart failed");
     if (ctx->g.rank == 0) {
-      CK(cudaMemcpyAsync(ctx->all_keys, ctx->tile_keys, tile_bytes * ctx->owned,
-                         cudaMemcpyDeviceToDevice, s));
-      for (int r = 1; r < ctx->g.nranks && rc == 0; ++r) {
-        const int owned_r = r < ctx->g.NB ? (ctx->g.NB - r + ctx->g.nranks - 1) / ctx->g.nranks : 0;
-        if (owned_r > 0)
-          rc = g_nccl.Recv(ctx->all_keys + (size_t)r * ctx->owned_max * ctx->bw * ctx->bh,
-                           tile_bytes * owned_r, ncclUint8_, r, ctx->comm, s);
-      }
-    } else if (ctx->owned > 0) {
-      rc = g_nccl.Send(ctx->tile_keys, tile_bytes * ctx->owned, ncclUint8_, 0, ctx->comm, s);
+      // every rank's block is owned_max tiles + its status word
+      const size_t blk = sizeof(unsigned long long) * ((size_t)ctx->owned_max * tile_px + 1);
+      CK(cudaMemcpyAsync(ctx->all_keys, ctx->tile_keys, blk, cudaMemcpyDeviceToDevice, s));
+      for (int r = 1; r < ctx->g.nranks && rc == 0; ++r)
+        rc = g_nccl.Recv(reinterpret_cast<unsigned char*>(ctx->all_keys) + (size_t)r * blk, blk, ncclUint8_, r,
+                         ctx->comm, s);
+    } else {
+      rc = g_nccl.Send(ctx->tile_keys, sizeof(unsigned long long) * ((size_t)ctx->owned_max * tile_px + 1),
+                       ncclUint8_, 0, ctx->comm, s);
     }
     const int rc2 = g_nccl.GroupEnd();
     if (rc != 0 || rc2 != 0)
@@ -754,6 +819,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
       a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
       a.g = ctx->g; a.all_keys = ctx->all_keys; a.owned_max = ctx->owned_max;
       a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
+      a.ctl = ctx->ctl;
       if (p2p) {
         a.all_keys = p2p_slot;
         a.p2p_flags = ctx->p2p_sync;
@@ -761,6 +827,14 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
         a.p2p_count = &ctx->ctl->p2p_count;
         a.p2p_timeout = &ctx->ctl->p2p_timeout;
         a.epoch = ctx->epoch;
+        a.status = ctx->p2p_sync + P2P_STATUS + (ctx->epoch & 1); a.status_stride = 2; a.nstatus = ctx->mnranks;
+        a.status_ok = ctx->epoch;
+      } else if (ctx->multi == PIKO_MULTI_SORT_LAST) {
+        a.status = ctx->all_keys + (size_t)ctx->owned * tile_px; a.nstatus = 1; a.status_ok = 1;
+      } else {
+        a.rank_stride = (long long)ctx->owned_max * tile_px + 1;
+        a.status = ctx->all_keys + (size_t)ctx->owned_max * tile_px;
+        a.status_stride = a.rank_stride; a.nstatus = ctx->mnranks; a.status_ok = 1;
       }
       CK(launch_resolve(a, false, s));
     }
@@ -778,9 +852,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   }
   CK(mark(1 + PIKO_STAGE_RESOLVE));
   if (ev) ++ctx->prof_frames;
-  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s));
-  CK(cudaEventRecord(ctx->done, s));
-  ctx->pending = true;
+  CK(record_frame_end(ctx, s, T));
   ctx->last_T = T;
   return PIKO_OK;
 }
@@ -808,11 +880,11 @@ static void adapt_tri_chunk(piko_ctx* ctx) {
   ctx->tri_chunk = (int)std::max<long long>(RX_THREADS, std::min<long long>(EX_MAX_TRIS, tc));
 }
 
-// Wait for the pending frame; PIKO_ECAPACITY (and grown capacity) on overflow.
-static int check_frame(piko_ctx* ctx) {
-  if (!ctx->pending) return ctx->last_status;
-  ctx->pending = false;
-  CK(cudaEventSynchronize(ctx->done));
+// Status of one completed frame from its mirror; PIKO_ECAPACITY (and grown
+// capacity) on overflow.  The mirror becomes ctx->h_ctl (stats, chunk sizes).
+static int eval_frame(piko_ctx* ctx, piko_ctx::Slot& sl) {
+  memcpy(ctx->h_ctl, sl.h, offsetof(Control, digit_hist));
+  ctx->last_T = sl.T;
   if (ctx->h_ctl->p2p_timeout) {
     CK(cudaMemsetAsync(&ctx->ctl->p2p_timeout, 0, sizeof(unsigned), 0));
     CK(cudaDeviceSynchronize());
@@ -828,11 +900,15 @@ static int check_frame(piko_ctx* ctx) {
     if (rc == PIKO_OK) ctx->fail(PIKO_ECAPACITY, "fragment capacity exceeded (%llu); grown", ctx->h_ctl->n_pairs);
     return ctx->last_status;
   }
-  if (ctx->h_ctl->overflow_tag == ctx->h_ctl->frame + 1 || ctx->h_ctl->vx_overflow) {
+  if (ctx->h_ctl->overflow_tag == ctx->h_ctl->frame + 1 || ctx->h_ctl->vx_overflow ||
+      ctx->h_ctl->peer_overflow == ctx->h_ctl->frame + 1) {
     int rc = ensure_pairs(ctx, ctx->h_ctl->n_pairs);
     if (rc == PIKO_OK) rc = ensure_verts(ctx, (long long)ctx->h_ctl->vx_need);
     ctx->last_status = rc != PIKO_OK ? rc : PIKO_ECAPACITY;
-    if (rc == PIKO_OK) ctx->fail(PIKO_ECAPACITY, "pair capacity exceeded (P=%llu); grown", ctx->h_ctl->n_pairs);
+    if (rc == PIKO_OK)
+      ctx->fail(PIKO_ECAPACITY, ctx->h_ctl->peer_overflow == ctx->h_ctl->frame + 1
+                                    ? "a peer rank's pair capacity was exceeded; its bins are empty"
+                                    : "pair capacity exceeded (P=%llu); grown", ctx->h_ctl->n_pairs);
     return ctx->last_status;
   }
   ctx->last_status = PIKO_OK;
@@ -840,10 +916,17 @@ static int check_frame(piko_ctx* ctx) {
   return PIKO_OK;
 }
 
+// Wait for every frame in flight; the status of the newest one.
+static int check_frame(piko_ctx* ctx) {
+  const bool had = ctx->ring_n > 0;
+  const int rc = poll_frames(ctx, true);
+  if (rc != PIKO_OK) return rc;
+  return had ? ctx->last_status : ctx->last_status;
+}
+
 // A failed CUDA call may leave tickets mid-frame: reset before the next frame.
 static int frame_failed(piko_ctx* ctx, int rc) {
   ctx->need_reset = true;
-  ctx->pending = false;
   return rc;
 }
 
@@ -882,10 +965,10 @@ static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32
     n_tris = (int32_t)(t1 - t0);
     ctx->prim_base = t0;
   }
-  // status of a previous asynchronous frame (grows capacity if it overflowed)
-  int prev = PIKO_OK;
-  if (ctx->pending) prev = check_frame(ctx);
-  if (prev == PIKO_ECUDA) return prev;
+  // statuses of earlier asynchronous frames that have finished (never waits;
+  // an overflowed one has grown the capacity before this frame is enqueued)
+  if (ctx->pending && (rc = poll_frames(ctx, false)) != PIKO_OK) return rc;
+  if (ctx->sticky == PIKO_ECUDA) { ctx->sticky = PIKO_OK; return PIKO_ECUDA; }
   Mat4 M;
   memcpy(M.m, mvp, sizeof M.m);
   if ((rc = ensure_tris(ctx, n_tris)) != PIKO_OK) return rc;
@@ -898,8 +981,14 @@ static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32
   for (int attempt = 0; attempt < 3; ++attempt) {
     if ((rc = enqueue_frame(ctx, verts, V, idx, n_tris, M, L, rgba, depth, s, keys_out)) != PIKO_OK)
       return frame_failed(ctx, rc);
-    if (ctx->sync_mode == PIKO_SYNC_ASYNC && !force_check) return prev == PIKO_ECAPACITY ? PIKO_OK : prev;
+    if (ctx->sync_mode == PIKO_SYNC_ASYNC && !force_check) {
+      // enqueued; report (once) an error of an earlier frame
+      const int st = ctx->sticky;
+      ctx->sticky = PIKO_OK;
+      return st;
+    }
     rc = check_frame(ctx);
+    ctx->sticky = PIKO_OK;  // checked: this frame's status is the answer
     if (rc == PIKO_ECUDA) return frame_failed(ctx, rc);
     if (rc != PIKO_ECAPACITY) return rc;
     // multi-rank: every rank must re-issue together; a capacity miss is
@@ -971,7 +1060,11 @@ extern "C" int piko_draw_host(piko_ctx* ctx, const float* h_verts, int64_t n_ver
 
 extern "C" int piko_finish(piko_ctx* ctx) {
   if (!ctx) return PIKO_EINVAL;
-  return check_frame(ctx);
+  int rc = poll_frames(ctx, true);
+  if (rc != PIKO_OK) return rc;
+  rc = ctx->sticky;  // the first error of any frame since the last report
+  ctx->sticky = PIKO_OK;
+  return rc;
 }
 
 extern "C" int piko_set_sync(piko_ctx* ctx, int mode) {
@@ -1161,11 +1254,13 @@ extern "C" int piko_attach_comm(piko_ctx* ctx, const void* uid, int rank, int nr
     CK(cudaFree(d));
     return rank == 0 ? PIKO_OK : p2p_import(ctx, h, rank, nranks);
   }
-  const size_t tile_bytes = sizeof(unsigned long long) * ctx->bw * ctx->bh;
-  CK(cudaMalloc(&ctx->tile_keys, tile_bytes * std::max(ctx->owned_max, 1)));
+  // keys of the owned bins + one status word (1: no overflow) that travels
+  // with them, so rank 0 learns of a peer's capacity miss
+  const size_t words = (size_t)ctx->bw * ctx->bh * std::max(ctx->owned_max, 1) + 1;
+  CK(cudaMalloc(&ctx->tile_keys, sizeof(unsigned long long) * words));
   // rank 0's receive buffer: every rank's tiles (sort-first), or one reduced image (sort-last)
   const size_t slots = ctx->multi == PIKO_MULTI_SORT_LAST ? 1 : (size_t)nranks;
-  if (rank == 0) CK(cudaMalloc(&ctx->all_keys, tile_bytes * ctx->owned_max * slots));
+  if (rank == 0) CK(cudaMalloc(&ctx->all_keys, sizeof(unsigned long long) * words * slots));
   return PIKO_OK;
 }
 

@@ -82,6 +82,7 @@ struct Control {
   unsigned long long p2p_arrive;       // k_tile CTA tickets (P2P arrival, modulo grid)
   unsigned long long p2p_count;        // k_resolve CTA tickets (P2P slot release)
   unsigned int p2p_timeout;            // a peer flag wait timed out (sticky)
+  unsigned long long peer_overflow;    // rank 0: frame+1 of a frame in which a peer rank overflowed
   unsigned int digit_hist[2][MAX_PASSES][RX_RADIX];  // parity double buffer
 };
 
@@ -240,6 +241,8 @@ struct TileArgs {
   const unsigned long long* p2p_done;   // rank 0's last resolved epoch
   unsigned long long epoch;             // this frame's exchange epoch (1, 2, ...)
   ShaderCost sc;
+  unsigned long long* status_word;      // multi-GPU: this rank's frame status next to its keys (null: none)
+  unsigned long long status_ok;         //   value meaning "no overflow" (NCCL: 1; P2P: the epoch)
 };
 
 struct ResolveArgs {            // rank 0 after the NCCL gather
@@ -261,6 +264,12 @@ struct ResolveArgs {            // rank 0 after the NCCL gather
   unsigned* p2p_timeout;
   unsigned long long epoch;
   ShaderCost sc;                         // deferred shader cost (single-GPU deferred resolve)
+  long long rank_stride;                 // words between ranks' key blocks (0: owned_max*bw*bh)
+  const unsigned long long* status;      // ranks' status words (null: none), status_stride apart
+  long long status_stride;
+  int nstatus;
+  unsigned long long status_ok;
+  Control* ctl;                          // rank 0: peer_overflow is raised here
 };
 
 // FreePipe variant (sec. 7.2.1): one fused

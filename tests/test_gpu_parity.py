@@ -478,3 +478,108 @@ def test_baseline_fragment_overflow_regrows(env):
     got = gpu_render(env, s, 8, pipeline=piko.PIKO_PIPE_BASELINE)
     assert got["stats"]["n_pairs"] == 64 * 64 * 64  # both triangles cover every pixel centre
     assert_frame_equal(got, oracle_frame(env, s))
+
+
+# ---- round 2: the exact benchmarked instantiation and the oracle-pin scenes --
+@pytest.mark.parametrize("assign", ["count-matrix", "radix"])
+def test_c3_b16_cov_off_bench_variant(env, assign, monkeypatch):
+    """The instantiation bench.py times: c3, 16x16 bins, coverage counting off
+    (k_tile<16,16,256,COV=0,KEYS=0>), the separate vertex stage (c3 shares
+    vertices: chosen automatically), AssignBin as configured (count matrix by
+    default; the radix passes forced) -- bit-exact vs the oracle."""
+    monkeypatch.setenv("PIKO_CM", "1" if assign == "count-matrix" else "0")
+    monkeypatch.delenv("PIKO_SEPARATE_VS", raising=False)
+    s = scenes.scene_c3()
+    got = gpu_render(env, s, 16, cov=False, frames=3)
+    assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
+    assert_bins_equal(got, env, s, 16)
+    assert got["stats"]["kernels_per_frame"] == 5
+
+
+def _pin_scenes():
+    """The scenes of the round-2 oracle pins (tests/test_oracle_pins.py):
+    snap ties, guard band, near epsilon, zero area with a non-empty rect,
+    zero depth at the range boundary."""
+    from tests.helpers import pixel_scene
+    W = H = 64
+    out = []
+    tris, zw = [], []
+    for x in (10 + 1 / 512, 11 + 3 / 512, -1 / 512):
+        tris.append([(x, 0.5), (x + 20.0, 0.5), (x, 20.5)])
+    for x in (16383.75, 16384.0, 16384.5):
+        tris.append([(0.5, 0.5), (x, 0.5), (0.5, 16.5)])
+    tris.append([(-16384.5, 0.5), (40.5, 0.5), (40.5, 16.5)])
+    tris += [[(0.5, 0.5), (5.5, 0.5), (10.5, 0.5)], [(0.5, 0.5), (10.5, 0.5), (10.5, 0.5)]]
+    zw = [[0.5] * 3] * len(tris)
+    tris += [[(0.5, 0.5), (40.5, 0.5), (0.5, 40.5)], [(0.5, 0.5), (32.5, 0.5), (0.5, 32.5)]]
+    zw += [[2.0 ** -25] * 3, [-0.125, 0.375, -0.125]]
+    v, i, m = pixel_scene(tris, np.array(zw), W, H)
+    out.append(scenes.Scene("pins", W, H, (8,), v, i, m))
+    for w0 in (2e-6, 1.0000001e-6, 5e-7):
+        M = np.zeros(16, np.float32)
+        M[0] = M[5] = 1.0
+        M[15] = np.float32(w0)
+        ndc = np.array([[-0.5, -0.5], [0.5, -0.5], [0.0, 0.5]])
+        pos = np.concatenate([ndc * np.float32(w0), np.zeros((3, 1))], 1).astype(np.float32)
+        verts = scenes.pack_verts(pos, np.tile([0, 0, 1.0], (3, 1)).astype(np.float32))
+        out.append(scenes.Scene(f"weps{w0}", W, H, (8,), verts, np.arange(3, dtype=np.int32).reshape(1, 3), M))
+    return out
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_oracle_pin_scenes_match(env, k, vs):
+    s = _pin_scenes()[k]
+    got = gpu_render(env, s, 8)
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, 8)
+
+
+def test_piko_draw_is_asynchronous(env):
+    """piko_draw returns once the frame is enqueued.  The stream
+    is held by a long device sleep; 8 c3 frames through the north-star
+    piko_draw (C default: async) all return while the first frame's end event
+    is still pending (cudaEventQuery), then piko_finish reports OK and the
+    last frame is exact."""
+    piko, _, torch = env
+    s = scenes.scene_c3()
+    dev = torch.device("cuda:0")
+    v, i = torch.from_numpy(s.verts).to(dev), torch.from_numpy(s.idx).to(dev)
+    r = piko.Renderer(s.W, s.H, 16, device=dev, sync="async")
+    r.draw(v, i, s.mvp, s.light, indexed=False)  # warm-up (allocations)
+    assert piko.piko_finish(r.ctx) == piko.PIKO_OK
+    st = torch.cuda.current_stream()
+    torch.cuda._sleep(2_000_000_000)  # ~1 s of device time ahead of the frames
+    ev = torch.cuda.Event()
+    for k in range(8):
+        assert r.draw(v, i, s.mvp, s.light, indexed=False) == piko.PIKO_OK
+        if k == 0:
+            ev.record(st)
+    assert not ev.query(), "a piko_draw call waited for the device"
+    assert piko.piko_finish(r.ctx) == piko.PIKO_OK
+    assert ev.query()
+    ref = oracle_frame(env, s, cov=False)
+    got = {"rgba": r.rgba.cpu().numpy(), "depth": r.depth.cpu().numpy(), "primid": r.primid().cpu().numpy()}
+    assert_frame_equal(got, ref, cov=False)
+    r.close()
+
+
+def test_async_overflow_reported_by_next_draw(env):
+    """an async frame that overflows is reported (once) by the next
+    piko_draw, which was enqueued with the grown capacity; that frame is exact."""
+    piko, _, torch = env
+    from tests.helpers import pixel_scene
+    tris = [[(-10.0, -10.0), (3000.0, -10.0), (-10.0, 3000.0)]] * 40
+    zs = np.linspace(0.1, 0.9, 40)[:, None].repeat(3, 1)
+    v, i, m = pixel_scene(tris, zs, 1024, 768)
+    s = scenes.Scene("cap", 1024, 768, (8,), v, i, m)
+    dev = torch.device("cuda:0")
+    vt, it = torch.from_numpy(v).to(dev), torch.from_numpy(i).to(dev)
+    r = piko.Renderer(1024, 768, 8, device=dev, sync="async")
+    assert r.draw(vt, it, m, s.light, check=False) == piko.PIKO_OK  # enqueued (overflows)
+    torch.cuda.synchronize()
+    assert r.draw(vt, it, m, s.light, check=False) == piko.PIKO_ECAPACITY  # frame 1's status
+    assert piko.piko_finish(r.ctx) == piko.PIKO_OK
+    ref = oracle_frame(env, s, cov=False)
+    got = {"rgba": r.rgba.cpu().numpy(), "depth": r.depth.cpu().numpy(), "primid": r.primid().cpu().numpy()}
+    assert_frame_equal(got, ref, cov=False)
+    r.close()

@@ -187,14 +187,16 @@ def test_perspective_transform_vs_float64(oracle_lib):
 
 
 def test_culls(oracle_lib):
-    """O1/O2/O4 culls: behind the eye (w <= eps), NaN, outside the guard band,
-    zero area, and a sliver missing every pixel centre -> no coverage, no bins."""
+    """O1/O2/O4 culls: behind the eye (w < 0), NaN, w below the near epsilon,
+    zero area, and a sliver missing every pixel centre -> no coverage, no bins.
+    (The guard band, the epsilon's value and the zero-area cull with a
+    non-empty sample rect are isolated in the tests below.)"""
     W = H = 64
     M = scenes.perspective_mvp(aspect=1.0)
     pos = np.array([
         [0, 0, 1], [1, 0, 1], [0, 1, 1],               # behind the camera (w < 0)
         [0, 0, -5], [np.nan, 0, -5], [0, 1, -5],       # NaN
-        [0, 0, -1e-9], [1e-3, 0, -1e-9], [0, 1e-3, -1e-9],  # far outside guard band
+        [0, 0, -1e-9], [1e-3, 0, -1e-9], [0, 1e-3, -1e-9],  # w = 1e-9 <= W_EPS (near plane)
         [0, 0, -5], [1, 0, -5], [2, 0, -5],            # zero area
         [0.0, 0.0, -5], [0.0001, 0.0, -5], [0.0, 0.0001, -5],  # misses all centres
     ], np.float32)
@@ -206,6 +208,96 @@ def test_culls(oracle_lib):
     assert r["covcount"].sum() == 0 and (r["primid"] == -1).all()
     start, prims = oracle_lib.bins(verts, idx, M, W, H, 8, 8)
     assert len(prims) == 0
+
+
+def _live_and_bins(oracle_lib, verts, idx, mvp, W, H):
+    oi, _ = oracle_lib.setup(verts, idx, mvp, W, H)
+    _, prims = oracle_lib.bins(verts, idx, mvp, W, H, 8, 8)
+    return oi, prims
+
+
+def test_snap_rounds_half_to_even(oracle_lib):
+    """R2 (SURVEY 8(c) ledger row 2: `rint`, ties to even): under the exact
+    ortho pixel matrix a corner at x = 10 + 1/512 px is 2560.5 subpixels and
+    snaps to 2560 (ties away from zero would give 2561); x = 11 + 3/512 ->
+    2817.5 -> 2818; x = -1/512 -> -0.5 -> 0 (not -1)."""
+    W = H = 64
+    for x, want in ((10 + 1 / 512, 2560), (11 + 3 / 512, 2818), (-1 / 512, 0)):
+        v, i, m = pixel_scene([[(x, 0.5), (x + 20.0, 0.5), (x, 20.5)]], 0.5, W, H)
+        oi, _ = oracle_lib.setup(v, i, m, W, H)
+        assert oi[0, 0] == 1 and oi[0, 1] == want, (x, oi[0])
+        # the other corners sit exactly on the lattice
+        assert sorted([oi[0, 3], oi[0, 5]]) == sorted([want + 5120, want])
+
+
+def test_guard_band_cull(oracle_lib):
+    """R2/R3 guard band (SURVEY 8(c) ledger rows 2-3: cull outside +-2^22
+    subpixels = 16384 px, boundary inclusive).  w is exactly 1 under the
+    ortho pixel matrix, so the corner's x is exact: x = 16383.75 and x = 16384
+    px are kept (the triangle covers centres near the origin and enters bins);
+    x = 16384.5 px (4194432 subpixels) culls the triangle.  A 2^24 band or no
+    test at all would keep it."""
+    W = H = 64
+    for x, live in ((16383.75, 1), (16384.0, 1), (16384.5, 0), (-16384.5, 0)):
+        v, i, m = pixel_scene([[(0.5, 0.5), (x, 0.5), (0.5, 16.5)]] if x > 0 else
+                              [[(x, 0.5), (40.5, 0.5), (40.5, 16.5)]], 0.5, W, H)
+        oi, prims = _live_and_bins(oracle_lib, v, i, m, W, H)
+        assert oi[0, 0] == live, (x, oi[0])
+        assert (len(prims) > 0) == bool(live)
+
+
+def test_near_plane_epsilon(oracle_lib):
+    """R3 ("w <= epsilon ... culled"; SURVEY 8(c) W_EPS = 1e-6):
+    a triangle whose clip w is 2e-6 is kept, one at w = 5e-7 is culled, with
+    the same NDC footprint (clip = (x, y, 0, w0): xn = x / w0)."""
+    W = H = 64
+    for w0, live in ((2e-6, 1), (1.0000001e-6, 1), (5e-7, 0), (1e-7, 0)):
+        M = np.zeros(16, np.float32)
+        M[0] = 1.0
+        M[5] = 1.0
+        M[15] = np.float32(w0)
+        ndc = np.array([[-0.5, -0.5], [0.5, -0.5], [0.0, 0.5]], np.float64)
+        pos = np.concatenate([ndc * np.float32(w0), np.zeros((3, 1))], 1).astype(np.float32)
+        verts = scenes.pack_verts(pos, np.tile([0, 0, 1.0], (3, 1)).astype(np.float32))
+        idx = np.arange(3, dtype=np.int32).reshape(1, 3)
+        oi, prims = _live_and_bins(oracle_lib, verts, idx, M, W, H)
+        assert oi[0, 0] == live, (w0, oi[0])
+        assert (len(prims) > 0) == bool(live)
+        r = render(oracle_lib, verts, idx, M, W, H)
+        assert (r["covcount"].sum() > 0) == bool(live)
+
+
+def test_zero_area_with_nonempty_rect_is_culled(oracle_lib):
+    """R7 ("degenerate t emits nothing"): collinear corners on the
+    pixel-centre row y = 0.5 have a non-empty sample rect (row 0, x 0..10) but
+    area2 == 0, so the triangle is culled: no coverage, no bin entry -- also
+    when a corner is repeated."""
+    W = H = 64
+    for tri in ([(0.5, 0.5), (5.5, 0.5), (10.5, 0.5)], [(0.5, 0.5), (10.5, 0.5), (10.5, 0.5)]):
+        v, i, m = pixel_scene([tri], 0.5, W, H)
+        oi, prims = _live_and_bins(oracle_lib, v, i, m, W, H)
+        assert oi[0, 0] == 0 and len(prims) == 0
+        assert render(oracle_lib, v, i, m, W, H)["covcount"].sum() == 0
+
+
+def test_zero_depth_at_range_boundary(oracle_lib):
+    """O6 range test is inclusive at 0 and the key of depth 0 is the smallest
+    (R4, R5): the plane z = x/64 - 1/8 (power-of-two slopes: exact) is 0.0
+    exactly at the centres of column x = 8, where it beats an opaque earlier
+    triangle at z = 2^-25 (primID 0); the depth written is +0.0 (sign bit clear;
+    with IEEE round-to-nearest the plane cannot produce -0.0, so the key's
+    0x7FFFFFFF mask is a guard that no input reaches).  Columns x < 8 are
+    discarded (z < 0); at x = 9 z = 1/64 loses to 2^-25."""
+    W = H = 64
+    tris = [[(0.5, 0.5), (40.5, 0.5), (0.5, 40.5)], [(0.5, 0.5), (32.5, 0.5), (0.5, 32.5)]]
+    zw = np.array([[2.0 ** -25] * 3, [-0.125, 0.375, -0.125]])
+    v, i, m = pixel_scene(tris, zw, W, H)
+    r = render(oracle_lib, v, i, m, W, H)
+    d = r["depth"].view(np.uint32)
+    for y in range(0, 20):
+        assert r["primid"][y, 8] == 1 and d[y, 8] == 0, (y, r["primid"][y, 8], hex(d[y, 8]))
+        assert r["primid"][y, 9] == 0 and r["depth"][y, 9] == np.float32(2.0 ** -25)
+        assert (r["primid"][y, :8] == 0).all()  # B discarded there (z < 0)
 
 
 # ------------------------------------------------------------------- depth ---

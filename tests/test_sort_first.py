@@ -232,3 +232,50 @@ def test_gpu_p2p_transport_two_processes(oracle_lib):
         assert np.array_equal(prim, ref["primid"]), f"frame {f}"
         assert np.array_equal(depth.view(np.uint32), ref["depth"].view(np.uint32)), f"frame {f}"
         assert np.abs(rgba - ref["rgba"]).max() <= 1e-5
+
+
+@pytest.mark.gpu
+def test_gpu_peer_overflow_reaches_rank0(oracle_lib):
+    """A rank whose pair capacity overflows sends empty bins; its status word
+    travels with its keys (P2P: next to its arrival flag, by slot parity), so
+    rank 0 reports PIKO_ECAPACITY for that frame too instead of returning a
+    frame with holes.  Scene: 300 tall thin triangles inside odd 8-px bin
+    columns only (binsX = 128 is even, so with R = 2 every pair belongs to
+    rank 1: 28800 pairs against an initial capacity of ~10^4)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1404_6293_b200 as piko
+    from tests.helpers import pixel_scene
+    R = 2
+    tris, zs = [], []
+    for k in range(300):
+        tx = 2 * (k % 64) + 1
+        tris.append([(8 * tx + 1.0, 0.0), (8 * tx + 7.0, 0.0), (8 * tx + 4.0, 767.0)])
+        zs.append(0.1 + 0.8 * k / 300)
+    v, i, m = pixel_scene(tris, np.array(zs), 1024, 768)
+    s = scenes.Scene("odd", 1024, 768, (8,), v, i, m)
+    dev = torch.device("cuda:0")
+    vt, it = torch.from_numpy(v).to(dev), torch.from_numpy(i).to(dev)
+    rds = [piko.Renderer(s.W, s.H, 8, device=dev) for _ in range(R)]
+    piko.piko_attach_local_peers(rds[0].ctx, rds[0].ctx, 0, R)
+    for r in range(1, R):
+        piko.piko_attach_local_peers(rds[r].ctx, rds[0].ctx, r, R)
+    ref = oracle_lib.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
+    try:
+        for f in range(3):
+            rcs = {r: rds[r].draw(vt, it, m, s.light, check=False) for r in list(range(1, R)) + [0]}
+            torch.cuda.synchronize()
+            if f == 0:  # rank 1 holds every pair: it overflows, and rank 0 must say so
+                assert rcs[1] == piko.PIKO_ECAPACITY
+                assert rcs[0] == piko.PIKO_ECAPACITY, piko.piko_last_error(rds[0].ctx)
+            else:
+                assert all(rc == piko.PIKO_OK for rc in rcs.values()), rcs
+                r0 = rds[0]
+                assert np.array_equal(r0.primid().cpu().numpy(), ref["primid"])
+                assert np.array_equal(r0.depth.cpu().numpy().view(np.uint32), ref["depth"].view(np.uint32))
+    finally:
+        for rd in rds[1:] + rds[:1]:
+            rd.close()
