@@ -151,36 +151,102 @@ class ClockSampler:
                 "source": self.source}
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(s, budget):
+    """SURVEY 8(d) CPU oracle baseline on the GPU box's host: (i) the
+    single-threaded oracle pinned to one core (sched_setaffinity, as
+    `taskset -c 0`), (ii) the same source with OpenMP over row bands on all
+    cores (oracle.render_mt, byte-identical frames).  Each leg renders whole
+    frames of the benchmarked scene for about `budget` seconds.  Returns the
+    baseline dict and the last single-threaded frame (for the parity check)."""
     import oracle
+    aff = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    if aff:
+        os.sched_setaffinity(0, {min(aff)})
     t0 = time.perf_counter()
     frames = 0
-    while True:
-        oracle.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
-        frames += 1
-        if time.perf_counter() - t0 >= budget:
-            break
+    ref = None
+    try:
+        while True:
+            ref = oracle.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
+            frames += 1
+            if time.perf_counter() - t0 >= budget:
+                break
+    finally:
+        if aff:
+            os.sched_setaffinity(0, aff)
     dt = time.perf_counter() - t0
-    return {"value": s.n_tris * frames / dt / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{frames} full frame(s) of the same scene, single-threaded C oracle "
-                      f"(gcc -O2), {dt:.1f} s", "ms_per_frame": 1e3 * dt / frames}
+    out = {"value": s.n_tris * frames / dt / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"{frames} full frame(s) of the benchmarked scene, single-threaded C oracle "
+                     f"(gcc -O2) pinned to one core, {dt:.1f} s", "ms_per_frame": 1e3 * dt / frames,
+           "cpu_model": cpu_model(), "host_cpus": os.cpu_count()}
+    try:
+        oracle.render_mt(s.verts, s.idx, s.mvp, s.light, s.W, s.H)  # thread pool + pages warm
+        t0 = time.perf_counter()
+        mf, nthreads = 0, 0
+        while True:
+            _, nthreads = oracle.render_mt(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
+            mf += 1
+            if time.perf_counter() - t0 >= budget:
+                break
+        dm = time.perf_counter() - t0
+        out["all_cores"] = {"value": s.n_tris * mf / dm / 1e6, "unit": UNIT, "cores": nthreads,
+                            "kind": "oracle (OpenMP row bands)", "ms_per_frame": 1e3 * dm / mf,
+                            "sample": f"{mf} full frame(s), {dm:.1f} s, {nthreads} threads"}
+    except Exception as e:  # noqa: BLE001
+        out["all_cores"] = {"unavailable": str(e)}
+    return out, ref
 
 
-def algorithmic_bytes(stage, T, V, L, P, NB, npx, ncov, npass):
-    """Bytes the method must move per launch of a stage."""
+def algorithmic_bytes(stage, T, V, L, P, NB, npx, ncov, npass, cm_rows=0):
+    """Bytes the method must move per launch of a stage (DESIGN.md section 6;
+    SURVEY 8(d): 48 B per covered pixel for the winner's attributes)."""
     if stage == "vertex":     # 16 B positions in, 16 B vertex record out
         return 16 * V + 16 * V
     if stage == "setup":      # idx + vertex records in; setup records (live) + tile rects out
         return 12 * T + 16 * V + 48 * L + 8 * T
-    if stage == "expand":     # radix pass 0: rects in, (key, primID) pairs out, bin counts
+    if stage == "expand":
+        if cm_rows:           # k_cm_scan: count matrix read, prefixes written, counts reset
+            return 12 * cm_rows * NB + 4 * NB
+        # radix pass 0: rects in, (key, primID) pairs out, bin counts
         return 8 * T + (8 * P if npass > 1 else 4 * P) + 4 * NB + (12 * NB if npass == 1 else 0)
-    if stage == "sort":       # passes >= 1: 8 B in / 8 B out (last: primIDs only) + CSR scan
+    if stage == "sort":
+        if cm_rows:           # k_cm_scatter: rects + cursor rows in, CSR values out, lists
+            return 8 * T + 4 * cm_rows * NB + 4 * P + 8 * NB
+        # passes >= 1: 8 B in / 8 B out (last: primIDs only) + CSR scan
         return (npass - 1) * 16 * P - 4 * P + 12 * NB if npass > 1 else 0
-    if stage == "tile":       # CSR + records in; 24 B/px out; winner re-gather
-        return 4 * (NB + 1) + 4 * P + 48 * P + 24 * npx + (12 + 3 * 32) * ncov
+    if stage == "tile":       # CSR + records in; 24 B/px out; winner attributes (SURVEY 8(d))
+        return 4 * (NB + 1) + 4 * P + 48 * P + 24 * npx + 48 * ncov
     if stage == "resolve":
-        return 8 * npx + 24 * npx + (12 + 3 * 32) * ncov
+        return 8 * npx + 24 * npx + 48 * ncov
     return 0
+
+
+def parity_check(g, s, bw, ref):
+    """Compare the GPU frame of the benchmarked configuration (and its bin
+    lists) with the oracle's frame of the same scene: primID and depth bits
+    bit-exact, RGB within 1e-5, CSR bin lists bit-exact."""
+    import numpy as np
+    import oracle
+    ok_p = bool(np.array_equal(g["primid"], ref["primid"]))
+    ok_d = bool(np.array_equal(g["depth"].view(np.uint32), ref["depth"].view(np.uint32)))
+    err = float(np.abs(g["rgba"] - ref["rgba"]).max())
+    ost, opr = oracle.bins(s.verts, s.idx, s.mvp, s.W, s.H, bw, bw)
+    ok_b = bool(np.array_equal(g["bin_start"], ost) and np.array_equal(g["bin_prims"], opr))
+    return {"ok": ok_p and ok_d and err <= 1e-5 and ok_b, "primid": ok_p, "depth_bits": ok_d,
+            "max_rgb_err": err, "bin_lists": ok_b,
+            "what": "a frame of the timed configuration (piko_draw, async) vs the CPU oracle's frame "
+                    "of the same scene (cpu_baseline)"}
 
 
 def run_piko(args):
@@ -215,7 +281,7 @@ def run_piko(args):
     bw = args.bin
     verts = torch.from_numpy(s.verts).to(dev)
     idx = torch.from_numpy(s.idx).to(dev)
-    r = piko.Renderer(s.W, s.H, bw, device=dev)
+    r = piko.Renderer(s.W, s.H, bw, device=dev, sync="checked")
     transport = None
     if world > 1:
         def attach(rd, xport):
@@ -262,9 +328,12 @@ def run_piko(args):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
-    # warm-up in checked mode (capacity settles), then asynchronous draws
+    # the north-star call piko_draw (no vertex count) is the headline;
+    # piko_draw_indexed is timed beside it.  Warm-up in checked mode
+    # (capacity settles), then the default asynchronous mode.
+    indexed = False
     for _ in range(max(args.warmup, 3)):
-        r.draw(verts, idx, s.mvp, s.light, stream)
+        r.draw(verts, idx, s.mvp, s.light, stream, indexed=indexed)
     piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
     stats = r.stats()
     ncov = int((r.primid() >= 0).sum().item()) if rank == 0 else 0
@@ -279,7 +348,7 @@ def run_piko(args):
     for k in range(args.steps):
         flush.fill_(float(k))                       # L2 flush, outside the step's events
         ev[k][0].record(stream)
-        r.draw(verts, idx, s.mvp, s.light, stream)
+        r.draw(verts, idx, s.mvp, s.light, stream, indexed=indexed)
         ev[k][1].record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -295,10 +364,45 @@ def run_piko(args):
     piko.piko_set_profiling(r.ctx, 1)
     for k in range(args.steps):
         flush.fill_(float(k))
-        r.draw(verts, idx, s.mvp, s.light, stream)
+        r.draw(verts, idx, s.mvp, s.light, stream, indexed=indexed)
     torch.cuda.synchronize(dev)
     prof, nprof = piko.piko_get_profile(r.ctx)
     piko.piko_set_profiling(r.ctx, 0)
+    if piko.piko_finish(r.ctx) != piko.PIKO_OK:
+        raise SystemExit(f"frame status: {piko.piko_last_error(r.ctx)}")
+    # the frame the parity check compares (rank 0 holds the full frame)
+    gpu_frame = None
+    if rank == 0 and world == 1:
+        r.draw(verts, idx, s.mvp, s.light, stream, indexed=indexed)
+        piko.piko_finish(r.ctx)
+        st_, pr_ = r.bins()
+        gpu_frame = {"primid": r.primid().cpu().numpy(), "depth": r.depth.cpu().numpy().copy(),
+                     "rgba": r.rgba.cpu().numpy().copy(), "bin_start": st_.cpu().numpy(),
+                     "bin_prims": pr_.cpu().numpy()}
+    # piko_draw_indexed (vertex count given: each vertex transformed once when
+    # the mesh shares vertices), same protocol
+    ie = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for _ in range(3):
+        r.draw(verts, idx, s.mvp, s.light, stream, indexed=True)
+    torch.cuda.synchronize(dev)
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        ie[k][0].record(stream)
+        r.draw(verts, idx, s.mvp, s.light, stream, indexed=True)
+        ie[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if piko.piko_finish(r.ctx) != piko.PIKO_OK:
+        raise SystemExit(f"frame status: {piko.piko_last_error(r.ctx)}")
+    idx_ms = sum(a.elapsed_time(b) for a, b in ie)
+    if world > 1:
+        t = torch.tensor([idx_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        idx_ms = float(t.item())
+    indexed_line = {"ms_per_step": idx_ms / args.steps, "value": s.n_tris * args.steps / (idx_ms / 1e3) / 1e6,
+                    "unit": UNIT, "kernels_per_frame": r.stats()["kernels_per_frame"],
+                    "what": "piko_draw_indexed: vertex count given (separate once-per-vertex stage on "
+                            "shared-vertex meshes)"}
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -308,7 +412,7 @@ def run_piko(args):
 
     # design alternative of sec. 7.2.1 (FreePipe: one fused kernel, no bins),
     # same protocol; reported beside the binned headline (1 GPU only)
-    variants = {}
+    variants = {"piko_draw_indexed": indexed_line}
     if world == 1:
         what = {piko.PIKO_PIPE_FREEPIPE: ("freepipe", "sec. 7.2.1 FreePipe: 1 fused kernel, thread per triangle, "
                                                       "global 64-bit atomicMin + resolve; no bins"),
@@ -381,7 +485,8 @@ def run_piko(args):
     per_frame = {k: v / max(nprof, 1) for k, v in prof.items()}
     cand = {k: per_frame[k] for k in ("vertex", "setup", "expand", "sort", "tile", "resolve") if per_frame[k] > 0}
     dom = max(cand, key=cand.get)
-    nb = algorithmic_bytes(dom, T, V, L, P, NB, npx, ncov, stats["radix_passes"])
+    cm_rows = stats.get("cm_rows", 0) if stats.get("assign_mode", 0) == 1 else 0
+    nb = algorithmic_bytes(dom, T, V, L, P, NB, npx, ncov, stats["radix_passes"], cm_rows)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -393,17 +498,18 @@ def run_piko(args):
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}_b{bw}.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get(dom)
-    kname = {"vertex": "k_vertex", "setup": "k_setup", "expand": "k_radix_pass<EXPAND=true> (pass 0)",
-             "sort": "k_radix_pass<EXPAND=false> (passes >= 1)", "tile": "k_tile",
-             "resolve": "k_resolve"}[dom]
+    kname = {"vertex": "k_vertex / k_index_max", "setup": "k_setup",
+             "expand": "k_cm_scan" if cm_rows else "k_radix_pass<EXPAND=true> (pass 0)",
+             "sort": "k_cm_scatter" if cm_rows else "k_radix_pass<EXPAND=false> (passes >= 1)",
+             "tile": "k_tile", "resolve": "k_resolve / k_shade"}[dom]
     roofline = {"bound": "hbm", "kernel": kname, "stage": dom,
                 "launches_per_step": max(stats["radix_passes"] - 1, 1) if dom == "sort" else 1,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": nb,
                 "ms_per_launch": per_frame[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
-    frame_bytes = sum(algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"])
-                      for k in ("vertex", "setup", "expand", "sort", "tile"))
+    frame_bytes = sum(algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"], cm_rows)
+                      for k in ("vertex", "setup", "expand", "sort", "tile") if per_frame.get(k, 0) > 0.004)
     # BASELINE.md's frame metric: ncu-measured DRAM bytes of the frame's kernels
     measured = None
     if os.path.exists(tf):
@@ -420,6 +526,7 @@ def run_piko(args):
         "config": {"workload": workload_name(args.config, s, bw), "config": args.config,
                    "width": s.W, "height": s.H, "bin": bw, "n_tris": T, "n_verts": V,
                    "n_pairs": P, "n_live": L, "covered_px": ncov, "l2": "flushed (256 MiB) before every step",
+                   "assign": "count matrix" if cm_rows else f"radix x{stats['radix_passes']}",
                    "parallelism": f"{args.multi} x{world} ({transport})" if world > 1 else "1 GPU"},
         "fps": 1e3 / ms,
         "ms_p10_p50_p90": [float(x) for x in np.percentile(step_ms, [10, 50, 90])],
@@ -430,7 +537,7 @@ def run_piko(args):
                                             "(profiles/traffic_*.json; ncu replays each kernel cold)"},
         "kernel_ms": per_frame,
         "kernel_ms_note": "per-stage CUDA-event times from a second K-step pass (events between kernels)",
-        "api": "piko_draw_indexed (C ABI via ctypes)",
+        "api": "piko_draw (north-star C ABI call via ctypes, PIKO_SYNC_ASYNC)",
         "roofline": roofline,
         "variants": variants,
         "gpu_launches": stats["kernels_per_frame"] * args.steps,
@@ -438,7 +545,8 @@ def run_piko(args):
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(s, args.cpu_budget)
+        out["cpu_baseline"], ref = cpu_baseline(s, args.cpu_budget)
+        out["parity"] = parity_check(gpu_frame, s, bw, ref)
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -72,13 +72,19 @@ enum {
                                 bin lists, one GPU.                           */
 
 /* piko_set_sync modes */
-#define PIKO_SYNC_CHECKED 0 /* default: piko_draw waits for the frame, checks
-                               the pair capacity, regrows and re-issues on
-                               overflow; returns after the frame completed.   */
-#define PIKO_SYNC_ASYNC 1   /* piko_draw only enqueues; an overflow of the
-                               frame is reported by the next piko_draw or by
-                               piko_finish (the frame's outputs are then invalid
-                               and the capacity has been grown).              */
+#define PIKO_SYNC_CHECKED 0 /* piko_draw waits for the frame, checks the pair
+                               capacity, regrows and re-issues on overflow;
+                               returns after the frame completed.             */
+#define PIKO_SYNC_ASYNC 1   /* default: piko_draw only enqueues
+                               and returns; up to 8 frames are in flight per
+                               context (the 9th draw waits for the oldest).
+                               A finished frame's status is read without
+                               blocking at the next piko_draw: an error of an
+                               earlier frame (PIKO_ECAPACITY -- that frame's
+                               outputs are invalid and the capacity has grown
+                               before this draw was enqueued -- or PIKO_ECUDA)
+                               is returned once, by the next piko_draw or by
+                               piko_finish.                                   */
 
 /* Create a context for a width x height framebuffer binned into bin_w x bin_h
  * pixel tiles (AssignToBoundingBox bins; Listing 1 uses 8x8).
@@ -90,7 +96,10 @@ enum {
  * Returns NULL on error (message via piko_last_error(NULL)).                 */
 piko_ctx *piko_create(int width, int height, int bin_w, int bin_h);
 
-/* Render one frame (asynchronous on `stream` in PIKO_SYNC_ASYNC mode).
+/* Render one frame: asynchronous on `stream` (the default PIKO_SYNC_ASYNC
+ * mode returns PIKO_OK once the frame is enqueued; see piko_set_sync).
+ * Multi-GPU: a rank that overflowed its pair capacity sends empty bins and a
+ * status word with its keys; rank 0 then reports PIKO_ECAPACITY for the frame.
  *   verts     device, f32[n_verts][8] = {px,py,pz,pad, nx,ny,nz,pad}
  *             (object-space position and normal, R15)
  *   idx       device, i32[n_tris][3]; caller guarantees 0 <= idx < n_verts
@@ -127,12 +136,12 @@ int piko_draw_host(piko_ctx *ctx, const float *h_verts, int64_t n_verts, const i
                    int32_t n_tris, const float mvp[16], const float light[3], float *h_rgba,
                    float *h_depth, void *stream);
 
-/* Wait for the last enqueued frame; returns its status (PIKO_ECAPACITY if its
- * pair lists overflowed -- the capacity has then been grown for the next
- * frame).                                                                     */
+/* Wait for every frame in flight; returns the first error of any frame not
+ * yet reported (PIKO_ECAPACITY if its pair lists overflowed -- the capacity
+ * has then been grown for the next frame), else PIKO_OK.                      */
 int piko_finish(piko_ctx *ctx);
 
-/* Select PIKO_SYNC_CHECKED (default) or PIKO_SYNC_ASYNC.                      */
+/* Select PIKO_SYNC_ASYNC (default) or PIKO_SYNC_CHECKED.                      */
 int piko_set_sync(piko_ctx *ctx, int mode);
 
 /* Select the pipeline (PIKO_PIPE_BINNED, _FREEPIPE or _BASELINE).  Outputs
@@ -285,8 +294,12 @@ typedef struct {
   int64_t n_bins;       /* bins in the grid, NB                               */
   int64_t owned_bins;   /* bins rasterized by this rank                        */
   int64_t pair_capacity;/* current pair-list capacity                          */
-  int32_t radix_passes; /* LSD passes of the stable scatter                    */
+  int32_t radix_passes; /* LSD passes the radix AssignBin would take          */
   int32_t kernels_per_frame; /* kernels launched per frame (this rank)        */
+  int32_t assign_mode;  /* AssignBin of the last frame: 0 stable LSD radix passes,
+                           1 count matrix (k_cm_scan + k_cm_scatter)           */
+  int32_t reserved;
+  int64_t cm_rows;      /* count-matrix rows (triangle chunks), 0 in radix mode */
 } piko_stats;
 int piko_get_stats(const piko_ctx *ctx, piko_stats *out);
 
@@ -301,8 +314,12 @@ int piko_nccl_unique_id(void *out_id128);
 #define PIKO_STAGE_VERTEX 1  /* k_index_max (piko_draw only) + k_vertex      */
 #define PIKO_STAGE_SETUP 2   /* k_setup: setup, count, scan, pairs           */
 #define PIKO_STAGE_EXPAND 3  /* k_radix_pass pass 0: expand pairs + digit-0 rank
-                                (+ k_bin_scan when radix_passes == 1)           */
-#define PIKO_STAGE_SORT 4    /* k_radix_pass passes >= 1 (+ CSR bin scan CTAs)  */
+                                (+ k_bin_scan when radix_passes == 1);
+                                count-matrix mode: k_cm_scan (column prefixes,
+                                bin_start)                                      */
+#define PIKO_STAGE_SORT 4    /* k_radix_pass passes >= 1 (+ CSR bin scan CTAs);
+                                count-matrix mode: k_cm_scatter (stable scatter
+                                of every row's pairs + work lists)              */
 #define PIKO_STAGE_TILE 5    /* k_tile: per-bin raster, depth, shade, store   */
 #define PIKO_STAGE_GATHER 6  /* tile-key gather (multi-GPU: NCCL, or nothing for P2P) */
 #define PIKO_STAGE_RESOLVE 7 /* k_resolve: rank-0 shade of gathered keys      */

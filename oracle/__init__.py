@@ -19,6 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "piko_oracle.c")
 _LIB = os.path.join(_HERE, "libpiko_oracle.so")
+_LIB_OMP = os.path.join(_HERE, "libpiko_oracle_omp.so")  # same source, -fopenmp (all host cores)
 
 # -ffp-contract=off is mandatory: the op order (fmaf vs separate mul/add) is
 # part of the definition the GPU path must reproduce bit for bit.
@@ -32,10 +33,11 @@ def build(force: bool = False) -> str:
     ORACLE_LIB overrides the library path (tools/oracle_mutations.py only)."""
     if os.environ.get("ORACLE_LIB"):
         return os.environ["ORACLE_LIB"]
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lm"])
-        os.replace(tmp, _LIB)
+    for lib, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(_SRC):
+            tmp = lib + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", *CFLAGS, *extra, _SRC, "-o", tmp, "-lm"])
+            os.replace(tmp, lib)
     return _LIB
 
 
@@ -105,6 +107,32 @@ def render(verts, idx, mvp, light, W, H, want_covcount=False, want_keys=False):
     if want_keys:
         out["keys"] = keys
     return out
+
+
+_lib_omp = None
+
+
+def render_mt(verts, idx, mvp, light, W, H):
+    """render() on all host cores (OpenMP over row bands; byte-identical).
+    Returns (frame dict, threads used)."""
+    global _lib_omp
+    if _lib_omp is None:
+        build()
+        lib = ctypes.CDLL(_LIB_OMP)
+        P = ctypes.c_void_p
+        lib.oracle_render_mt.argtypes = [ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int64, P, P, P, P, P]
+        lib.oracle_render_mt.restype = ctypes.c_int
+        _lib_omp = lib
+    verts, idx, mvp = _check_scene(verts, idx, mvp)
+    light = np.ascontiguousarray(np.asarray(light, np.float32).reshape(3))
+    rgba = np.empty((H, W, 4), np.float32)
+    depth = np.empty((H, W), np.float32)
+    primid = np.empty((H, W), np.int32)
+    n = _lib_omp.oracle_render_mt(W, H, _ptr(verts), _ptr(idx), idx.shape[0], _ptr(mvp), _ptr(light),
+                                  _ptr(rgba), _ptr(depth), _ptr(primid))
+    if n < 0:
+        raise ValueError(f"oracle_render_mt failed rc={n}")
+    return {"rgba": rgba, "depth": depth, "primid": primid}, n
 
 
 def bins(verts, idx, mvp, W, H, bin_w, bin_h, rank=0, nranks=1):

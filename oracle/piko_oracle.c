@@ -319,6 +319,75 @@ int oracle_render(int W, int H, const float *verts, const int32_t *idx,
   return 0;
 }
 
+#ifdef _OPENMP
+#include <omp.h>
+/* The same frame on all host cores ("the same source with
+ * OpenMP over image row bands"): O1..O4 for every triangle in parallel (each
+ * triangle independent), then row bands (4 per thread) in parallel, each running
+ * the single-threaded loop above restricted to its rows (for t ascending ...
+ * K = min(K, key)) -- every pixel is owned by exactly one band, so the min
+ * merge and hence K, depth, primID and RGB are identical to oracle_render's.
+ * Compiled only into the -fopenmp build (libpiko_oracle_omp.so); the default
+ * oracle build is unchanged.  Returns the thread count used, or < 0.        */
+int oracle_render_mt(int W, int H, const float *verts, const int32_t *idx,
+                     int64_t n_tris, const float *mvp, const float *light,
+                     float *out_rgba, float *out_depth, int32_t *out_primid) {
+  float L[3];
+  if (!normalise_light(light, L)) return -1;
+  int64_t npx = (int64_t)W * H;
+  uint64_t *K = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)npx);
+  otri *tri = (otri *)malloc(sizeof(otri) * (size_t)(n_tris > 0 ? n_tris : 1));
+  if (!K || !tri) { free(K); free(tri); return -2; }
+  int nthreads = 1;
+#pragma omp parallel
+  {
+#pragma omp single
+    nthreads = omp_get_num_threads();
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < npx; ++i) K[i] = CLEAR_KEY;
+#pragma omp for schedule(static)
+    for (int64_t t = 0; t < n_tris; ++t) setup_triangle(verts, idx, t, mvp, W, H, &tri[t]);
+    /* 4 bands per thread (each band scans the triangle list once) */
+    const int BAND = (H + 4 * nthreads - 1) / (4 * nthreads);
+#pragma omp for schedule(dynamic, 1)
+    for (int y0 = 0; y0 < H; y0 += BAND) {
+      int y1 = y0 + BAND - 1 < H - 1 ? y0 + BAND - 1 : H - 1;
+      for (int64_t t = 0; t < n_tris; ++t) {
+        const otri *o = &tri[t];
+        if (!o->live || o->py1 < y0 || o->py0 > y1) continue;
+        int ya = o->py0 > y0 ? o->py0 : y0, yb = o->py1 < y1 ? o->py1 : y1;
+        for (int y = ya; y <= yb; ++y)
+          for (int x = o->px0; x <= o->px1; ++x) {
+            if (!covers(o, x, y)) continue;
+            float z = plane_depth(o, x, y);
+            if (!(z >= 0.0f && z <= 1.0f)) continue;
+            uint64_t key = ((uint64_t)(float_bits(z) & 0x7FFFFFFFu) << 32) | (uint32_t)t;
+            int64_t p = (int64_t)y * W + x;
+            if (key < K[p]) K[p] = key;
+          }
+      }
+    }
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t p = 0; p < npx; ++p) {
+      float *c = out_rgba + 4 * p;
+      if (K[p] == CLEAR_KEY) {
+        c[0] = c[1] = c[2] = c[3] = 0.0f;
+        out_depth[p] = 1.0f;
+        out_primid[p] = -1;
+        continue;
+      }
+      int64_t t = (int64_t)(K[p] & 0xFFFFFFFFu);
+      shade_pixel(verts, &tri[t], (int)(p % W), (int)(p / W), L, c);
+      out_depth[p] = bits_float((uint32_t)(K[p] >> 32));
+      out_primid[p] = (int32_t)t;
+    }
+  }
+  free(tri);
+  free(K);
+  return nthreads;
+}
+#endif
+
 /* Bin lists (O4, P:684 AssignToBoundingBox + P:1081-1084 primitive order):
  * bins are bin_w x bin_h pixels, grid ceil(W/bin_w) x ceil(H/bin_h),
  * bin = ty * binsX + tx (row-major).  For t ascending, for ty, for tx of the

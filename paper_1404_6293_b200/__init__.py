@@ -45,7 +45,8 @@ class piko_stats(ctypes.Structure):
     _fields_ = [("n_tris", ctypes.c_int64), ("n_live", ctypes.c_int64),
                 ("n_pairs", ctypes.c_int64), ("n_bins", ctypes.c_int64),
                 ("owned_bins", ctypes.c_int64), ("pair_capacity", ctypes.c_int64),
-                ("radix_passes", ctypes.c_int32), ("kernels_per_frame", ctypes.c_int32)]
+                ("radix_passes", ctypes.c_int32), ("kernels_per_frame", ctypes.c_int32),
+                ("assign_mode", ctypes.c_int32), ("reserved", ctypes.c_int32), ("cm_rows", ctypes.c_int64)]
 
 
 def _load():

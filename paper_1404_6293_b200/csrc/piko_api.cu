@@ -157,6 +157,7 @@ struct piko_ctx {
   uint32_t* cm = nullptr; uint32_t* cp = nullptr; long long cm_cap = 0;  // [rows][NB]
   unsigned long long* cm_status = nullptr;  // [cm_scan_grid]
   bool last_cm = false;                     // the last frame used the count matrix
+  long long last_cm_rows = 0;
   int32_t* prims_out = nullptr;             // CSR bin_prims of the last frame
   unsigned long long* def_keys = nullptr;   // [NB][bw*bh]
   int pipeline = PIKO_PIPE_BINNED;
@@ -700,6 +701,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   CK(mark(1 + PIKO_STAGE_SETUP));
   ctx->prims_out = cm ? ctx->vals[0] : ctx->vals[ctx->npass & 1];
   ctx->last_cm = cm;
+  ctx->last_cm_rows = cm ? cm_rows : 0;
   for (int p = 0; p < (cm ? 0 : ctx->npass); ++p) {
     RadixArgs a{};
     a.expand = p == 0; a.rect = ctx->rect; a.n_tris = T; a.tri_chunk = ctx->tri_chunk;
@@ -1277,6 +1279,9 @@ extern "C" int piko_get_stats(const piko_ctx* cctx, piko_stats* out) {
   out->pair_capacity = (int64_t)ctx->pair_cap;
   out->radix_passes = ctx->npass;
   out->kernels_per_frame = ctx->last_kernels;
+  out->assign_mode = ctx->last_cm ? 1 : 0;
+  out->reserved = 0;
+  out->cm_rows = ctx->last_cm ? ctx->last_cm_rows : 0;
   return PIKO_OK;
 }
 
