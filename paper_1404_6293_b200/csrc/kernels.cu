@@ -1107,18 +1107,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_bin_scan(RadixArgs a) {
 constexpr int CM_GROUPS = 256 / CM_COLS;  // row groups per k_cm_scan CTA
 constexpr int CM_RPT = 16;                // rows per thread kept in registers
 __global__ void __launch_bounds__(256) k_cm_scan(const __grid_constant__ CmArgs a) {
-  __shared__ u64 s_tk;
   __shared__ unsigned s_part[CM_GROUPS][CM_COLS];
-  __shared__ unsigned s_tot[CM_COLS];
-  __shared__ u64 s_base;
-  const int tid = threadIdx.x, lane = tid & 31, col = tid % CM_COLS, grp = tid / CM_COLS;
+  __shared__ int s_last;
+  __shared__ u64 s_w[256 / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, col = tid % CM_COLS, grp = tid / CM_COLS;
   pdl_wait();   // k_setup's counts
   pdl_trigger();
-  if (tid == 0) s_tk = atomicAdd(&a.ctl->cm_ticket, 1ull);
-  __syncthreads();
-  const u64 frame = s_tk / gridDim.x;
-  const long long j = (long long)(s_tk % gridDim.x);  // ticket order: look-back never waits on an unstarted CTA
-  const unsigned tag = frame_tag(frame);
+  const long long j = blockIdx.x;
   CM_MARK(1, j, 0);
   const int NB = a.g.NB;
   const long long b = j * CM_COLS + col;
@@ -1139,7 +1134,7 @@ __global__ void __launch_bounds__(256) k_cm_scan(const __grid_constant__ CmArgs 
   s_part[grp][col] = sum;
   __syncthreads();
   CM_MARK(1, j, 1);
-  if (tid < CM_COLS) {  // exclusive over the row groups of column tid
+  if (tid < CM_COLS) {  // exclusive over the row groups of column tid; the bin total
     unsigned run = 0;
 #pragma unroll
     for (int q = 0; q < CM_GROUPS; ++q) {
@@ -1147,50 +1142,82 @@ __global__ void __launch_bounds__(256) k_cm_scan(const __grid_constant__ CmArgs 
       s_part[q][tid] = run;
       run += c;
     }
-    s_tot[tid] = run;
+    if (j * CM_COLS + tid < NB) a.sched.bin_count[j * CM_COLS + tid] = run;
   }
   __syncthreads();
-  if (tid < 32) {  // bin totals of this CTA's columns -> bin_start (look-back over CTAs)
-    const unsigned c = lane < CM_COLS ? s_tot[lane] : 0u;
-    unsigned inc = c;
+  if (b < NB) {
+    // second sweep: column prefixes out (bin_start is added by the scatter),
+    // counts reset to zero for the next frame
+    unsigned run = s_part[grp][col];
+    for (long long r = r0; r < r1; r += CM_RPT) {
+      if (!cached) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    const unsigned agg = __shfl_sync(0xffffffffu, inc, 31);
-    const u64 ex = lookback_warp(a.status, j, agg, tag, lane);
-    if (lane < CM_COLS) s_tot[lane] = inc - c;
-    if (lane == 0) {
-      s_base = ex;
-      if (j == (long long)gridDim.x - 1) {  // last columns: P = the whole list length
-        const u64 P = ex + agg;
-        a.ctl->n_pairs = P;
-        a.sched.bin_start[NB] = (int32_t)(P < MAX_PAIRS ? P : MAX_PAIRS - 1);
-        if (P > a.cap) atomicMax(&a.ctl->overflow_tag, frame + 1);
+        for (int u = 0; u < CM_RPT; ++u) v[u] = (r + u < r1) ? __ldcg(a.cm + (size_t)(r + u) * NB + b) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < CM_RPT; ++u) {
+        if (r + u >= r1) break;
+        const size_t o = (size_t)(r + u) * NB + b;
+        a.cp[o] = run;
+        run += v[u];
+        if (v[u]) a.cm[o] = 0u;
       }
     }
   }
-  __syncthreads();
   CM_MARK(1, j, 2);
-  if (b >= NB) return;
-  const u64 bstart = s_base + s_tot[col];
-  if (grp == 0) a.sched.bin_start[b] = (int32_t)bstart;
-  u64 run = bstart + s_part[grp][col];
-  // second sweep: prefixes out, counts reset to zero for the next frame
-  for (long long r = r0; r < r1; r += CM_RPT) {
-    if (!cached) {
+  // the last CTA to finish scans the bin totals into bin_start (no chain
+  // between CTAs: every other CTA is done after its own sweeps)
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const u64 t = atomicAdd(&a.ctl->cm_done, 1ull);
+    s_last = (t + 1) % gridDim.x == 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  u64 carry = 0;
+  // steps of 256 * BPT bins, BPT consecutive per thread (all loads of a step in flight)
+  constexpr int BPT = 16;
+  for (int b0 = 0; b0 < NB; b0 += 256 * BPT) {
+    unsigned c[BPT];
+    u64 cs = 0;
 #pragma unroll
-      for (int u = 0; u < CM_RPT; ++u) v[u] = (r + u < r1) ? __ldcg(a.cm + (size_t)(r + u) * NB + b) : 0u;
+    for (int k = 0; k < BPT; ++k) {
+      const int bb = b0 + tid * BPT + k;
+      c[k] = bb < NB ? __ldcg(a.sched.bin_count + bb) : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < CM_RPT; ++u) {
-      if (r + u >= r1) break;
-      const size_t o = (size_t)(r + u) * NB + b;
-      a.cp[o] = (uint32_t)run;
-      run += v[u];
-      if (v[u]) a.cm[o] = 0u;
+    for (int k = 0; k < BPT; ++k) cs += c[k];
+    u64 inc = cs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
     }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    u64 base = carry, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 256 / 32; ++w) {
+      base += w < warp ? s_w[w] : 0ull;
+      tot += s_w[w];
+    }
+    u64 run = base + inc - cs;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+      const int bb = b0 + tid * BPT + k;
+      if (bb < NB) a.sched.bin_start[bb] = (int32_t)(run < MAX_PAIRS ? run : MAX_PAIRS - 1);
+      run += c[k];
+    }
+    carry += tot;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const u64 P = carry;
+    a.ctl->n_pairs = P;
+    a.sched.bin_start[NB] = (int32_t)(P < MAX_PAIRS ? P : MAX_PAIRS - 1);
+    if (P > a.cap) atomicMax(&a.ctl->overflow_tag, a.ctl->frame + 1);
   }
   CM_MARK(1, j, 3);
 }
@@ -1274,13 +1301,17 @@ __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_const
   }
   if (a.ctl->overflow_tag == a.ctl->frame + 1) return;  // P > capacity: k_tile renders background
   uint32_t* cprow = a.cp + (size_t)row * NB;
-  if (cur_by_bin) {  // all loads in flight together, then the stores
+  if (cur_by_bin) {  // cursor = bin_start + column prefix; all loads in flight, then the stores
     constexpr int CPT = RX_CHUNK / CM_THREADS;
-    unsigned cv[CPT];
+    unsigned cv[CPT], bv[CPT];
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) cv[k] = tid + k * CM_THREADS < NB ? __ldcg(cprow + tid + k * CM_THREADS) : 0u;
+    for (int k = 0; k < CPT; ++k) {
+      const int bb = tid + k * CM_THREADS;
+      cv[k] = bb < NB ? __ldcg(cprow + bb) : 0u;
+      bv[k] = bb < NB ? (unsigned)__ldcg(a.sched.bin_start + bb) : 0u;
+    }
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) if (tid + k * CM_THREADS < NB) sm.cur[tid + k * CM_THREADS] = cv[k];
+    for (int k = 0; k < CPT; ++k) if (tid + k * CM_THREADS < NB) sm.cur[tid + k * CM_THREADS] = cv[k] + bv[k];
   }
   for (int w = tid; w < NBW; w += CM_THREADS) sm.bm[w] = 0u;
   auto block_excl = [&](unsigned v) -> unsigned {  // every thread must call it
@@ -1409,7 +1440,8 @@ __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_const
       if (threadIdx.x == 0 && lo == 0 && blockIdx.x < 8000) g_k1_times[2][blockIdx.x][7] = U;
 #endif
       if (!cur_by_bin)
-        for (unsigned d = tid; d < U; d += CM_THREADS) sm.cur[d] = __ldcg(cprow + sm.tb[d]);
+        for (unsigned d = tid; d < U; d += CM_THREADS)
+          sm.cur[d] = __ldcg(cprow + sm.tb[d]) + (unsigned)__ldcg(a.sched.bin_start + sm.tb[d]);
       unsigned ld[CM_ITEMS];
       int val[CM_ITEMS];
 #pragma unroll
@@ -1459,7 +1491,8 @@ __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_const
       if (lo == 0) CM_MARK(2, blockIdx.x, 6);
       if (!cur_by_bin && !last_round) {  // row cursors of the bins this row touches again
         __syncthreads();
-        for (unsigned q = tid; q < U; q += CM_THREADS) cprow[sm.tb[q]] = sm.cur[q];
+        for (unsigned q = tid; q < U; q += CM_THREADS)
+          cprow[sm.tb[q]] = sm.cur[q] - (unsigned)__ldcg(a.sched.bin_start + sm.tb[q]);
       }
       __syncthreads();
     }

@@ -155,7 +155,6 @@ struct piko_ctx {
   int cm_mode = -1;                         // -1 auto, 0 radix, 1 count matrix
   int cm_tc_log2 = 0;                       // forced log2 triangles per row (0: auto)
   uint32_t* cm = nullptr; uint32_t* cp = nullptr; long long cm_cap = 0;  // [rows][NB]
-  unsigned long long* cm_status = nullptr;  // [cm_scan_grid]
   bool last_cm = false;                     // the last frame used the count matrix
   long long last_cm_rows = 0;
   int32_t* prims_out = nullptr;             // CSR bin_prims of the last frame
@@ -309,7 +308,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   }
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
                   ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
-                  ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys, ctx->def_keys, ctx->cm, ctx->cp, ctx->cm_status,
+                  ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys, ctx->def_keys, ctx->cm, ctx->cp,
                   ctx->all_keys, ctx->fp_keys, ctx->ovq, ctx->sc.sink, ctx->bl_keys, ctx->frag_key,
                   ctx->frag_px, ctx->frag_rgba};
   for (void* p : bufs)
@@ -623,7 +622,6 @@ static int ensure_cm(piko_ctx* ctx, long long rows) {
     ctx->cm_cap = need;
     ctx->need_reset = true;  // the matrix is zeroed by the reset
   }
-  if (!ctx->cm_status) CK(cudaMalloc(&ctx->cm_status, sizeof(unsigned long long) * cm_scan_grid(ctx->g.NB)));
   return PIKO_OK;
 }
 
@@ -664,7 +662,6 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   for (int k = 0; k < 6; ++k) changed |= grids[k] != ctx->last_grids[k];
   if (changed) {
     if (ctx->cm) CK(cudaMemsetAsync(ctx->cm, 0, sizeof(uint32_t) * ctx->cm_cap, s));
-    if (ctx->cm_status) CK(cudaMemsetAsync(ctx->cm_status, 0, sizeof(unsigned long long) * cm_scan_grid(ctx->g.NB), s));
     // tickets restart at 0, so every tag-carrying status word must be cleared
     CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s));
     CK(cudaMemsetAsync(ctx->st_scan, 0, sizeof(unsigned long long) * ctx->st_scan_n, s));
@@ -726,11 +723,11 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   }
   if (cm) {
     CmArgs c{};
-    c.cm = ctx->cm; c.cp = ctx->cp; c.rows = cm_rows; c.cm_shift = cm_shift; c.status = ctx->cm_status;
+    c.cm = ctx->cm; c.cp = ctx->cp; c.rows = cm_rows; c.cm_shift = cm_shift;
     c.rect = ctx->rect; c.n_tris = T; c.g = ctx->g; c.cap = ctx->pair_cap; c.bin_prims = ctx->prims_out;
     c.ctl = ctx->ctl;
     RadixArgs& a = c.sched;
-    a.g = ctx->g; a.ctl = ctx->ctl; a.bin_start = ctx->bin_start; a.NB = ctx->g.NB;
+    a.g = ctx->g; a.ctl = ctx->ctl; a.bin_start = ctx->bin_start; a.bin_count = ctx->bin_count; a.NB = ctx->g.NB;
     a.rank = ctx->g.rank; a.nranks = ctx->g.nranks;
     a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
     a.frag = tile_frag(ctx->bw, ctx->bh); a.npx = ctx->bw * ctx->bh;

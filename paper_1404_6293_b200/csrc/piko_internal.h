@@ -68,7 +68,7 @@ struct Control {
   unsigned long long k1_ticket;
   unsigned long long rx_ticket[MAX_PASSES];
   unsigned long long scan_ticket;      // standalone bin-scan kernel (single-pass grids)
-  unsigned long long cm_ticket;        // k_cm_scan CTA tickets (count-matrix AssignBin)
+  unsigned long long cm_done;          // k_cm_scan CTAs finished (modulo grid: the last scans bin_start)
   unsigned long long frame;            // written by K1 chunk 0
   unsigned int tile_next;              // dynamic bin queue of k_tile (reset by K1 chunk 0)
   unsigned int list_n[NLIST];          // work-list sizes (reset by K1 chunk 0)
@@ -178,15 +178,15 @@ struct RadixArgs {
 // Count-matrix AssignBin (a3-a6 for NB <= CM_MAX_NB): k_setup adds each
 // triangle's owned bins into row t >> cm_shift of M; k_cm_scan turns M into
 // per-row exclusive column prefixes CP[r][b] = bin_start[b] + sum_{r' < r}
-// M[r'][b] (and bin_start, P); k_cm_scatter writes every row's pairs at
-// CP[r][b] + (stable rank inside the row).  The bin scan work lists reuse
+// M[r'][b] and the bin totals, its last CTA bin_start and P; k_cm_scatter
+// writes every row's pairs at bin_start[b] + CP[r][b] + (stable rank inside
+// the row).  The bin scan work lists reuse
 // RadixArgs (extra CTAs of k_cm_scatter).
 struct CmArgs {
   uint32_t* cm;                 // [rows][NB] counts (zeroed again by k_cm_scan)
   uint32_t* cp;                 // [rows][NB] column prefixes / running cursors
   long long rows;
   int cm_shift;
-  unsigned long long* status;   // [k_cm_scan grid] look-back words
   const uint2* rect;
   long long n_tris;
   Grid g;

@@ -46,10 +46,10 @@ def rows(k, n):
     t = buf[k, :n].astype(np.int64)
     return t[t[:, 0] > T0] - T0
 cs = rows(1, 8000)
-print(f"k_cm_scan: CTAs {len(cs)}, start {cs[:,0].min()}..{cs[:,0].max()}, end max {cs[:,3].max()}; "
+last = cs[cs[:, 3] > 0]
+print(f"k_cm_scan: CTAs {len(cs)}, start {cs[:,0].min()}..{cs[:,0].max()}, sweeps end max {cs[:,2].max()}; "
       f"sweep1 {np.median(cs[:,1]-cs[:,0]):.0f} (p90 {np.percentile(cs[:,1]-cs[:,0],90):.0f}), "
-      f"lookback {np.median(cs[:,2]-cs[:,1]):.0f} (p90 {np.percentile(cs[:,2]-cs[:,1],90):.0f}), "
-      f"sweep2 {np.median(cs[:,3]-cs[:,2]):.0f}")
+      f"sweep2 {np.median(cs[:,2]-cs[:,1]):.0f}; last CTA bin scan end {last[:,3].max() if len(last) else -1}")
 sc = rows(2, 8000)
 print(f"k_cm_scatter: CTAs {len(sc)}, start {sc[:,0].min()}..{sc[:,0].max()} (p50 {np.median(sc[:,0]):.0f}), "
       f"pdl-wait done {sc[:,1].min()}..{sc[:,1].max()}")
@@ -65,3 +65,23 @@ if len(u):
 t = buf[3, :8192].astype(np.int64)
 t = t[(t[:, 0] > T0) & (t[:, 2] >= t[:, 0])] - T0
 print(f"k_tile bins: first start {t[:,0].min()}, last end {t[:,2].max()}")
+st = r.stats()
+nb = st["owned_bins"]
+t = buf[3, :min(nb, 8192)].astype(np.int64)
+t = t[(t[:, 0] > T0) & (t[:, 2] >= t[:, 0])]
+base = t[:, 0].min()
+ne = t[:, 3]
+for lo, hi in ((0, 0), (1, 64), (65, 256), (257, 1024), (1025, 1 << 30)):
+    m = (ne >= lo) & (ne <= hi)
+    if m.any():
+        r1 = t[m, 1] - t[m, 0]
+        r2 = t[m, 2] - t[m, 1]
+        print(f"   bins with {lo}-{hi} pairs: {m.sum():5d}  raster median {np.median(r1):7.0f} p90 {np.percentile(r1,90):7.0f}"
+              f"  writeback median {np.median(r2):7.0f} p90 {np.percentile(r2,90):7.0f}")
+cta = t[:, 4]
+per = np.bincount(cta.astype(np.int64))
+print(f"   bins per CTA: min {per[per>0].min()} max {per.max()} CTAs {np.count_nonzero(per)}")
+c = buf[0, 7000:7000 + 1024].astype(np.int64)
+c = c[c[:, 0] > T0] - T0
+print(f"   k_tile CTAs: resident first {c[:,3].min()} p50 {np.median(c[:,3]):.0f}; past pdl wait {c[:,0].min()}..{c[:,0].max()};"
+      f" bin loop end p50 {np.median(c[:,1]):.0f} max {c[:,1].max()}; CTA end p50 {np.median(c[:,2]):.0f} max {c[:,2].max()}")
