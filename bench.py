@@ -58,7 +58,9 @@ def parse():
 
 def workload_name(cfg, s, bw):
     return {"c2": "c2: 100 UV spheres, 100K tris", "c3": "c3: UV sphere 500x1000, 1M tris",
-            "c4": "c4: random soup, 4M tris", "c5": "c5: jittered grid, 16M tris"}.get(cfg, cfg) + \
+            "c4": "c4: random soup, 4M tris", "c5": "c5: jittered grid, 16M tris",
+            "c6": "c6: Reyes, 256 bicubic patches split/diced on the device into ~1.1M micropolygon "
+                  "tris"}.get(cfg, cfg) + \
         f", {s.W}x{s.H}, {bw}x{bw} bins"
 
 
@@ -170,6 +172,20 @@ def cpu_baseline(s, budget):
     frames of the benchmarked scene for about `budget` seconds.  Returns the
     baseline dict and the last single-threaded frame (for the parity check)."""
     import oracle
+    import scenes
+    patch = isinstance(s, scenes.PatchScene)
+
+    def frame1():  # Reyes: the oracle's Split/Dice is part of the frame
+        if patch:
+            _, v, i = oracle.dice(s.patches, s.mvp, s.W, s.H, s.dice_px, s.max_grid)
+            return oracle.render(v, i, s.mvp, s.light, s.W, s.H), i.shape[0]
+        return oracle.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H), s.n_tris
+
+    def frame_mt():
+        if patch:
+            _, v, i = oracle.dice(s.patches, s.mvp, s.W, s.H, s.dice_px, s.max_grid)
+            return oracle.render_mt(v, i, s.mvp, s.light, s.W, s.H)[1], i.shape[0]
+        return oracle.render_mt(s.verts, s.idx, s.mvp, s.light, s.W, s.H)[1], s.n_tris
     aff = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
     if aff:
         os.sched_setaffinity(0, {min(aff)})
@@ -178,7 +194,7 @@ def cpu_baseline(s, budget):
     ref = None
     try:
         while True:
-            ref = oracle.render(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
+            ref, T = frame1()
             frames += 1
             if time.perf_counter() - t0 >= budget:
                 break
@@ -186,21 +202,21 @@ def cpu_baseline(s, budget):
         if aff:
             os.sched_setaffinity(0, aff)
     dt = time.perf_counter() - t0
-    out = {"value": s.n_tris * frames / dt / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
+    out = {"value": T * frames / dt / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
            "sample": f"{frames} full frame(s) of the benchmarked scene, single-threaded C oracle "
                      f"(gcc -O2) pinned to one core, {dt:.1f} s", "ms_per_frame": 1e3 * dt / frames,
            "cpu_model": cpu_model(), "host_cpus": os.cpu_count()}
     try:
-        oracle.render_mt(s.verts, s.idx, s.mvp, s.light, s.W, s.H)  # thread pool + pages warm
+        frame_mt()  # thread pool + pages warm
         t0 = time.perf_counter()
         mf, nthreads = 0, 0
         while True:
-            _, nthreads = oracle.render_mt(s.verts, s.idx, s.mvp, s.light, s.W, s.H)
+            nthreads, T = frame_mt()
             mf += 1
             if time.perf_counter() - t0 >= budget:
                 break
         dm = time.perf_counter() - t0
-        out["all_cores"] = {"value": s.n_tris * mf / dm / 1e6, "unit": UNIT, "cores": nthreads,
+        out["all_cores"] = {"value": T * mf / dm / 1e6, "unit": UNIT, "cores": nthreads,
                             "kind": "oracle (OpenMP row bands)", "ms_per_frame": 1e3 * dm / mf,
                             "sample": f"{mf} full frame(s), {dm:.1f} s, {nthreads} threads"}
     except Exception as e:  # noqa: BLE001
@@ -241,7 +257,12 @@ def parity_check(g, s, bw, ref):
     ok_p = bool(np.array_equal(g["primid"], ref["primid"]))
     ok_d = bool(np.array_equal(g["depth"].view(np.uint32), ref["depth"].view(np.uint32)))
     err = float(np.abs(g["rgba"] - ref["rgba"]).max())
-    ost, opr = oracle.bins(s.verts, s.idx, s.mvp, s.W, s.H, bw, bw)
+    import scenes
+    if isinstance(s, scenes.PatchScene):
+        _, v, i = oracle.dice(s.patches, s.mvp, s.W, s.H, s.dice_px, s.max_grid)
+        ost, opr = oracle.bins(v, i, s.mvp, s.W, s.H, bw, bw)
+    else:
+        ost, opr = oracle.bins(s.verts, s.idx, s.mvp, s.W, s.H, bw, bw)
     ok_b = bool(np.array_equal(g["bin_start"], ost) and np.array_equal(g["bin_prims"], opr))
     return {"ok": ok_p and ok_d and err <= 1e-5 and ok_b, "primid": ok_p, "depth_bits": ok_d,
             "max_rgb_err": err, "bin_lists": ok_b,
@@ -278,9 +299,21 @@ def run_piko(args):
             dist.init_process_group("nccl", device_id=dev)
 
     s = scenes.make(args.config)
+    patch = isinstance(s, scenes.PatchScene)  # Reyes (c6): Split/Dice on the device each frame
     bw = args.bin
-    verts = torch.from_numpy(s.verts).to(dev)
-    idx = torch.from_numpy(s.idx).to(dev)
+    if patch:
+        if world > 1:
+            raise SystemExit("the Reyes config (c6) runs on one GPU")
+        pt = torch.from_numpy(s.patches).to(dev)
+        verts = idx = None
+    else:
+        verts = torch.from_numpy(s.verts).to(dev)
+        idx = torch.from_numpy(s.idx).to(dev)
+
+    def frame(indexed=False):
+        if patch:
+            return r.draw_patches(pt, s.mvp, s.light, s.dice_px, s.max_grid, stream)
+        return r.draw(verts, idx, s.mvp, s.light, stream, indexed=indexed)
     r = piko.Renderer(s.W, s.H, bw, device=dev, sync="checked")
     transport = None
     if world > 1:
@@ -333,7 +366,7 @@ def run_piko(args):
     # (capacity settles), then the default asynchronous mode.
     indexed = False
     for _ in range(max(args.warmup, 3)):
-        r.draw(verts, idx, s.mvp, s.light, stream, indexed=indexed)
+        frame(indexed)
     piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
     stats = r.stats()
     ncov = int((r.primid() >= 0).sum().item()) if rank == 0 else 0
@@ -348,7 +381,7 @@ def run_piko(args):
     for k in range(args.steps):
         flush.fill_(float(k))                       # L2 flush, outside the step's events
         ev[k][0].record(stream)
-        r.draw(verts, idx, s.mvp, s.light, stream, indexed=indexed)
+        frame(indexed)
         ev[k][1].record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -364,7 +397,7 @@ def run_piko(args):
     piko.piko_set_profiling(r.ctx, 1)
     for k in range(args.steps):
         flush.fill_(float(k))
-        r.draw(verts, idx, s.mvp, s.light, stream, indexed=indexed)
+        frame(indexed)
     torch.cuda.synchronize(dev)
     prof, nprof = piko.piko_get_profile(r.ctx)
     piko.piko_set_profiling(r.ctx, 0)
@@ -373,7 +406,7 @@ def run_piko(args):
     # the frame the parity check compares (rank 0 holds the full frame)
     gpu_frame = None
     if rank == 0 and world == 1:
-        r.draw(verts, idx, s.mvp, s.light, stream, indexed=indexed)
+        frame(indexed)
         piko.piko_finish(r.ctx)
         st_, pr_ = r.bins()
         gpu_frame = {"primid": r.primid().cpu().numpy(), "depth": r.depth.cpu().numpy().copy(),
@@ -382,24 +415,25 @@ def run_piko(args):
     # piko_draw_indexed (vertex count given: each vertex transformed once when
     # the mesh shares vertices), same protocol
     ie = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    for _ in range(3):
-        r.draw(verts, idx, s.mvp, s.light, stream, indexed=True)
+          for _ in range(args.steps if not patch else 0)]
+    for _ in range(3 if not patch else 0):
+        frame(True)
     torch.cuda.synchronize(dev)
-    for k in range(args.steps):
+    for k in range(len(ie)):
         flush.fill_(float(k))
         ie[k][0].record(stream)
-        r.draw(verts, idx, s.mvp, s.light, stream, indexed=True)
+        frame(True)
         ie[k][1].record(stream)
     torch.cuda.synchronize(dev)
     if piko.piko_finish(r.ctx) != piko.PIKO_OK:
         raise SystemExit(f"frame status: {piko.piko_last_error(r.ctx)}")
-    idx_ms = sum(a.elapsed_time(b) for a, b in ie)
+    idx_ms = sum(a.elapsed_time(b) for a, b in ie) if ie else float("nan")
+    T = r.stats()["n_tris"] if patch else s.n_tris  # Reyes: the diced micropolygon triangles
     if world > 1:
         t = torch.tensor([idx_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         idx_ms = float(t.item())
-    indexed_line = {"ms_per_step": idx_ms / args.steps, "value": s.n_tris * args.steps / (idx_ms / 1e3) / 1e6,
+    indexed_line = {"ms_per_step": idx_ms / args.steps, "value": T * args.steps / (idx_ms / 1e3) / 1e6,
                     "unit": UNIT, "kernels_per_frame": r.stats()["kernels_per_frame"],
                     "what": "piko_draw_indexed: vertex count given (separate once-per-vertex stage on "
                             "shared-vertex meshes)"}
@@ -412,8 +446,8 @@ def run_piko(args):
 
     # design alternative of sec. 7.2.1 (FreePipe: one fused kernel, no bins),
     # same protocol; reported beside the binned headline (1 GPU only)
-    variants = {"piko_draw_indexed": indexed_line}
-    if world == 1:
+    variants = {"piko_draw_indexed": indexed_line} if not patch else {}
+    if world == 1 and not patch:
         what = {piko.PIKO_PIPE_FREEPIPE: ("freepipe", "sec. 7.2.1 FreePipe: 1 fused kernel, thread per triangle, "
                                                       "global 64-bit atomicMin + resolve; no bins"),
                 piko.PIKO_PIPE_BASELINE: ("baseline", "sec. 7.1 Baseline: VS, Rasterizer, Fragment Shader, Depth "
@@ -422,7 +456,7 @@ def run_piko(args):
             piko.piko_set_pipeline(r.ctx, pipe)
             piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_CHECKED)
             for _ in range(max(args.warmup, 3)):
-                r.draw(verts, idx, s.mvp, s.light, stream)
+                frame(False)
             piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
             fe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in range(args.steps)]
@@ -430,11 +464,11 @@ def run_piko(args):
             for k in range(args.steps):
                 flush.fill_(float(k))
                 fe[k][0].record(stream)
-                r.draw(verts, idx, s.mvp, s.light, stream)
+                frame(False)
                 fe[k][1].record(stream)
             torch.cuda.synchronize(dev)
             fms = sum(a.elapsed_time(b) for a, b in fe) / args.steps
-            variants[name] = {"ms_per_step": fms, "value": s.n_tris / (fms / 1e3) / 1e6, "unit": UNIT,
+            variants[name] = {"ms_per_step": fms, "value": T / (fms / 1e3) / 1e6, "unit": UNIT,
                               "what": desc}
             piko.piko_finish(r.ctx)
         piko.piko_set_pipeline(r.ctx, piko.PIKO_PIPE_BINNED)
@@ -442,7 +476,7 @@ def run_piko(args):
 
     # end-to-end through the public host-buffer call (H2D + frame + D2H per step)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not patch:
         piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_CHECKED)
         hv = torch.from_numpy(s.verts).pin_memory()
         hi = torch.from_numpy(s.idx).pin_memory()
@@ -466,7 +500,7 @@ def run_piko(args):
             t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": s.n_tris * ke / (e_ms / 1e3) / 1e6, "unit": UNIT,
+        e2e = {"value": T * ke / (e_ms / 1e3) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": int(hv.numel() * 4 + hi.numel() * 4),
                "d2h_bytes_per_step": int((hrgba.numel() + hdepth.numel()) * 4) if rank == 0 else 0,
                "ms_per_step": e_ms / ke, "steps": ke}
@@ -479,7 +513,7 @@ def run_piko(args):
         return
 
     clocks = sampler.summary()
-    T, V = s.n_tris, s.verts.shape[0]
+    V = piko.piko_get_diced(r.ctx)[1] if patch else s.verts.shape[0]
     P, L, NB = stats["n_pairs"], stats["n_live"], stats["n_bins"]
     npx = s.W * s.H
     per_frame = {k: v / max(nprof, 1) for k, v in prof.items()}

@@ -136,6 +136,31 @@ int piko_draw_host(piko_ctx *ctx, const float *h_verts, int64_t n_verts, const i
                    int32_t n_tris, const float mvp[16], const float light[3], float *h_rgba,
                    float *h_depth, void *stream);
 
+/* Reyes micropolygon pipeline (sec. 5
+ * "Reyes": Split -> Dice -> Sample -> Shade).  Draws n_patches bicubic Bezier
+ * patches: Split/Dice on the device into a micropolygon mesh (DESIGN.md
+ * R19-R21: per-patch rates Gu x Gv = the smallest powers of two <= max_grid
+ * with the projected control-polyline length <= dice_px * G; quads split into
+ * two triangles), then the binned Sample stage (AssignBin + per-bin raster;
+ * the paper uses 32x32 bins, P:1199-1201 -- create the context with 32x32) and
+ * Shade, exactly as piko_draw draws the mesh.
+ *   patches  device, f32[n_patches][16][4] = (x, y, z, pad); control point
+ *            a*4 + b, a along u, b along v; 16-byte aligned
+ *   dice_px  > 0, target micropolygon edge (screen pixels, L-inf)
+ *   max_grid power of two in [1, 1024] (caps Gu, Gv)
+ * Other arguments as piko_draw.  The mesh lives in the context (see
+ * piko_get_diced) until the next call; the call synchronises `stream` once
+ * (mesh size readback between the rate and mesh kernels).  PIKO_ESTATE after
+ * piko_attach_comm or with the FreePipe/Baseline pipelines.                  */
+int piko_draw_patches(piko_ctx *ctx, const float *patches, int32_t n_patches, const float mvp[16],
+                      const float light[3], float dice_px, int32_t max_grid, float *out_rgba,
+                      float *out_depth, void *stream);
+
+/* The micropolygon mesh of the last piko_draw_patches (device pointers owned
+ * by the context: verts f32[n_verts][8], idx i32[n_tris][3]).               */
+int piko_get_diced(const piko_ctx *ctx, const float **d_verts, int64_t *n_verts,
+                   const int32_t **d_idx, int64_t *n_tris);
+
 /* Wait for every frame in flight; returns the first error of any frame not
  * yet reported (PIKO_ECAPACITY if its pair lists overflowed -- the capacity
  * has then been grown for the next frame), else PIKO_OK.                      */

@@ -57,6 +57,11 @@ def _load():
         lib.oracle_bins.argtypes = [ctypes.c_int] * 6 + [P, P, ctypes.c_int64, P, P, P,
                                                           ctypes.c_int64]
         lib.oracle_bins.restype = ctypes.c_int64
+        lib.oracle_dice_grid.argtypes = [P, ctypes.c_int64, P, ctypes.c_int, ctypes.c_int, ctypes.c_float,
+                                         ctypes.c_int, P]
+        lib.oracle_dice_grid.restype = ctypes.c_int
+        lib.oracle_dice_mesh.argtypes = [P, ctypes.c_int64, P, P, P]
+        lib.oracle_dice_mesh.restype = ctypes.c_int64
         _lib = lib
     return _lib
 
@@ -107,6 +112,25 @@ def render(verts, idx, mvp, light, W, H, want_covcount=False, want_keys=False):
     if want_keys:
         out["keys"] = keys
     return out
+
+
+def dice(patches, mvp, W, H, dice_px, max_grid):
+    """Reyes Split + Dice (R19-R21): per-patch dice rates G i32[P][2]
+    = (Gu, Gv) and the micropolygon mesh (verts f32[V][8], idx i32[T][3]) in
+    patch order."""
+    patches = np.ascontiguousarray(patches, dtype=np.float32).reshape(-1, 16, 4)
+    mvp = np.ascontiguousarray(np.asarray(mvp, dtype=np.float32).reshape(16))
+    n = patches.shape[0]
+    G = np.zeros((n, 2), np.int32)
+    lib = _load()
+    lib.oracle_dice_grid(_ptr(patches), n, _ptr(mvp), W, H, float(dice_px), int(max_grid), _ptr(G))
+    g = G.astype(np.int64)
+    V, T = int(((g[:, 0] + 1) * (g[:, 1] + 1)).sum()), int((2 * g[:, 0] * g[:, 1]).sum())
+    verts = np.zeros((V, 8), np.float32)
+    idx = np.zeros((T, 3), np.int32)
+    got = lib.oracle_dice_mesh(_ptr(patches), n, _ptr(G), _ptr(verts), _ptr(idx))
+    assert got == T
+    return G, verts, idx
 
 
 _lib_omp = None

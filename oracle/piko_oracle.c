@@ -319,6 +319,139 @@ int oracle_render(int W, int H, const float *verts, const int32_t *idx,
   return 0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Reyes Split + Dice (sec. 5 "Reyes":
+ * Split -> Dice -> Sample -> Shade).  The paper's Split is adaptive ("Bezier
+ * patches may go through an unbounded number of splits") and Dice follows
+ * Patney et al.; the readings (R19-R21):
+ *  R19 Split decision per bicubic patch from its projected control hull:
+ *      Lu = max over the 4 control rows along u of the polyline length
+ *      sum_a max(|dsx|, |dsy|) between consecutive projected control points
+ *      (likewise Lv along v; the polyline bounds the curve's length).  The
+ *      patch is split into Gu x Gv sub-patches, each diced into one
+ *      micropolygon quad -- i.e. a uniform Gu x Gv dice -- with Gu the
+ *      smallest power of two (<= max_grid) such that Lu <= dice_px * Gu
+ *      (Gv likewise); a control point behind the near plane (or non-finite):
+ *      Gu = Gv = max_grid.  Deterministic split tree and micropolygons.
+ *  R20 Micropolygon quad (i, j) -> triangles (v00, v10, v11), (v00, v11, v01);
+ *      vertices row-major in u (i) then v (j), patches in input order, so the
+ *      primitive order (tie-break, bin order) is fixed.
+ *  R21 Position = tensor-product cubic Bernstein evaluation, normal = Pv x Pu,
+ *      with the pinned op order below (fma where written).               */
+
+/* Bernstein weights and derivatives at u (u = i / G, exact for G = 2^k). */
+static void bernstein(float u, float B[4], float dB[4]) {
+  float s = 1.0f - u;
+  B[0] = (s * s) * s;
+  B[1] = ((3.0f * u) * s) * s;
+  B[2] = ((3.0f * u) * u) * s;
+  B[3] = (u * u) * u;
+  dB[0] = -((3.0f * s) * s);
+  dB[1] = (3.0f * s) * (s - 2.0f * u);
+  dB[2] = (3.0f * u) * (2.0f * s - u);
+  dB[3] = (3.0f * u) * u;
+}
+/* sum_k w[k] * p[k] with the pinned order fma(w3,p3, fma(w2,p2, fma(w1,p1, w0*p0))) */
+static float comb4(const float w[4], float p0, float p1, float p2, float p3) {
+  return fmaf(w[3], p3, fmaf(w[2], p2, fmaf(w[1], p1, w[0] * p0)));
+}
+static int pow2_rate(float len, float dice_px, int max_grid) {
+  int g = 1;
+  while (g < max_grid && len > dice_px * (float)g) g *= 2;
+  return g;
+}
+
+/* R19: dice rates of every patch.  patches f32[n][16][4] (control point
+ * a*4+b, a along u, b along v).  G[2p] = Gu, G[2p+1] = Gv.  Returns 0.      */
+int oracle_dice_grid(const float *patches, int64_t n, const float *M, int W, int H,
+                     float dice_px, int max_grid, int32_t *G) {
+  float hw = 0.5f * (float)W, hh = 0.5f * (float)H;
+  for (int64_t p = 0; p < n; ++p) {
+    const float *cp = patches + 64 * p;
+    float sx[16], sy[16];
+    int behind = 0;
+    for (int k = 0; k < 16; ++k) {
+      float x = cp[4 * k], y = cp[4 * k + 1], z = cp[4 * k + 2];
+      float cx = fmaf(M[0], x, fmaf(M[1], y, fmaf(M[2], z, M[3])));
+      float cy = fmaf(M[4], x, fmaf(M[5], y, fmaf(M[6], z, M[7])));
+      float cw = fmaf(M[12], x, fmaf(M[13], y, fmaf(M[14], z, M[15])));
+      if (!isfinite(cx) || !isfinite(cy) || !isfinite(cw) || !(cw > W_EPS)) { behind = 1; break; }
+      float r = 1.0f / cw;
+      sx[k] = fmaf(cx * r, hw, hw);
+      sy[k] = fmaf(-(cy * r), hh, hh);
+    }
+    if (behind) { G[2 * p] = G[2 * p + 1] = max_grid; continue; }
+    float Lu = 0.0f, Lv = 0.0f;
+    for (int b = 0; b < 4; ++b) {          /* rows along u: points a*4+b, a = 0..3 */
+      float l = 0.0f;
+      for (int a = 0; a < 3; ++a) {
+        float dx = fabsf(sx[4 * (a + 1) + b] - sx[4 * a + b]), dy = fabsf(sy[4 * (a + 1) + b] - sy[4 * a + b]);
+        l = l + (dx > dy ? dx : dy);
+      }
+      if (l > Lu) Lu = l;
+    }
+    for (int a = 0; a < 4; ++a) {          /* rows along v: points a*4+b, b = 0..3 */
+      float l = 0.0f;
+      for (int b = 0; b < 3; ++b) {
+        float dx = fabsf(sx[4 * a + b + 1] - sx[4 * a + b]), dy = fabsf(sy[4 * a + b + 1] - sy[4 * a + b]);
+        l = l + (dx > dy ? dx : dy);
+      }
+      if (l > Lv) Lv = l;
+    }
+    G[2 * p] = pow2_rate(Lu, dice_px, max_grid);
+    G[2 * p + 1] = pow2_rate(Lv, dice_px, max_grid);
+  }
+  return 0;
+}
+
+/* R20/R21: the micropolygon mesh.  verts f32[sum (Gu+1)(Gv+1)][8], idx
+ * i32[sum 2 Gu Gv][3], patches in order.  Returns the triangle count.       */
+int64_t oracle_dice_mesh(const float *patches, int64_t n, const int32_t *G, float *verts,
+                         int32_t *idx) {
+  int64_t vb = 0, tb = 0;
+  for (int64_t p = 0; p < n; ++p) {
+    const float *cp = patches + 64 * p;
+    int gu = G[2 * p], gv = G[2 * p + 1];
+    for (int i = 0; i <= gu; ++i) {
+      float Bu[4], dBu[4];
+      bernstein((float)i / (float)gu, Bu, dBu);
+      for (int j = 0; j <= gv; ++j) {
+        float Bv[4], dBv[4];
+        bernstein((float)j / (float)gv, Bv, dBv);
+        float P[3], Pu[3], Pv[3];
+        for (int c = 0; c < 3; ++c) {
+          float Q[4], QV[4];
+          for (int a = 0; a < 4; ++a) {
+            const float *row = cp + 16 * a + c; /* control points a*4+0..3, component c */
+            Q[a] = comb4(Bv, row[0], row[4], row[8], row[12]);
+            QV[a] = comb4(dBv, row[0], row[4], row[8], row[12]);
+          }
+          P[c] = comb4(Bu, Q[0], Q[1], Q[2], Q[3]);
+          Pu[c] = comb4(dBu, Q[0], Q[1], Q[2], Q[3]);
+          Pv[c] = comb4(Bu, QV[0], QV[1], QV[2], QV[3]);
+        }
+        float *v = verts + 8 * (vb + (int64_t)i * (gv + 1) + j);
+        v[0] = P[0]; v[1] = P[1]; v[2] = P[2]; v[3] = 0.0f;
+        v[4] = fmaf(Pv[1], Pu[2], -(Pv[2] * Pu[1]));
+        v[5] = fmaf(Pv[2], Pu[0], -(Pv[0] * Pu[2]));
+        v[6] = fmaf(Pv[0], Pu[1], -(Pv[1] * Pu[0]));
+        v[7] = 0.0f;
+      }
+    }
+    for (int i = 0; i < gu; ++i)
+      for (int j = 0; j < gv; ++j) {
+        int32_t v00 = (int32_t)(vb + (int64_t)i * (gv + 1) + j), v01 = v00 + 1;
+        int32_t v10 = v00 + (gv + 1), v11 = v10 + 1;
+        int32_t *t = idx + 3 * (tb + 2 * ((int64_t)i * gv + j));
+        t[0] = v00; t[1] = v10; t[2] = v11;
+        t[3] = v00; t[4] = v11; t[5] = v01;
+      }
+    vb += (int64_t)(gu + 1) * (gv + 1);
+    tb += 2 * (int64_t)gu * gv;
+  }
+  return tb;
+}
+
 #ifdef _OPENMP
 #include <omp.h>
 /* The same frame on all host cores ("the same source with

@@ -31,7 +31,8 @@ EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_se
            "piko_draw_tile_keys", "piko_resolve_keys", "piko_tile_keys_count", "piko_owned_bins",
            "piko_set_pipeline", "piko_set_profiling", "piko_get_profile", "piko_set_multi",
            "piko_triangle_range", "piko_set_transport", "piko_attach_local_peers",
-           "piko_p2p_export", "piko_p2p_import", "piko_set_shader_cost")
+           "piko_p2p_export", "piko_p2p_import", "piko_set_shader_cost", "piko_draw_patches",
+           "piko_get_diced")
 STAGES = ("clear", "vertex", "setup", "expand", "sort", "tile", "gather", "resolve")
 
 
@@ -86,6 +87,8 @@ def _load():
         "piko_nccl_unique_id": ([P], I),
         "piko_set_profiling": ([P, I], I),
         "piko_get_profile": ([P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)], I),
+        "piko_draw_patches": ([P, P, ctypes.c_int32, P, P, ctypes.c_float, ctypes.c_int32, P, P, P], I),
+        "piko_get_diced": ([P, ctypes.POINTER(P), ctypes.POINTER(I64), ctypes.POINTER(P), ctypes.POINTER(I64)], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -129,14 +132,40 @@ def _check(ctx, rc):
 
 
 # ---- the C ABI, one Python function per entry point -------------------------
+_dims = {}  # ctx handle -> (width, height): shape checks of the output buffers
+
+
 def piko_create(width, height, bin_w, bin_h):
     h = _lib.piko_create(width, height, bin_w, bin_h)
     if not h:
         raise PikoError(PIKO_EINVAL, _lib.piko_last_error(None).decode())
+    _dims[h] = (width, height)
     return ctypes.c_void_p(h)
 
 
+def _check_scene(verts, idx, n_tris=None):
+    """verts f32[V][8], idx i32[T][3] (n_tris <= T): the C ABI reads them raw."""
+    if verts is not None and (verts.dim() != 2 or verts.shape[1] != 8):
+        raise ValueError(f"verts must be [V][8], got {tuple(verts.shape)}")
+    if idx is not None:
+        if idx.dim() != 2 or idx.shape[1] != 3:
+            raise ValueError(f"idx must be [T][3], got {tuple(idx.shape)}")
+        if n_tris is not None and int(n_tris) > idx.shape[0]:
+            raise ValueError(f"n_tris {n_tris} > idx rows {idx.shape[0]}")
+
+
+def _check_outputs(ctx, rgba, depth):
+    W, H = _dims.get(ctx.value, (None, None))
+    if W is None:
+        return
+    if rgba is not None and rgba.numel() < 4 * W * H:
+        raise ValueError(f"out_rgba holds {rgba.numel()} floats, need {4 * W * H} (H x W x 4)")
+    if depth is not None and depth.numel() < W * H:
+        raise ValueError(f"out_depth holds {depth.numel()} floats, need {W * H} (H x W)")
+
+
 def piko_destroy(ctx):
+    _dims.pop(ctx.value, None)
     _lib.piko_destroy(ctx)
 
 
@@ -147,6 +176,8 @@ def piko_last_error(ctx):
 
 def piko_draw(ctx, verts, idx, n_tris, mvp, light, out_rgba, out_depth, stream=None, check=True):
     import torch
+    _check_scene(verts, idx, n_tris)
+    _check_outputs(ctx, out_rgba, out_depth)
     rc = _lib.piko_draw(ctx, _dev_ptr(verts, torch.float32, "verts"),
                         _dev_ptr(idx, torch.int32, "idx"), int(n_tris), _f32x(mvp, 16),
                         _f32x(light, 3), _dev_ptr(out_rgba, torch.float32, "out_rgba"),
@@ -157,6 +188,10 @@ def piko_draw(ctx, verts, idx, n_tris, mvp, light, out_rgba, out_depth, stream=N
 def piko_draw_indexed(ctx, verts, n_verts, idx, n_tris, mvp, light, out_rgba, out_depth,
                       stream=None, check=True):
     import torch
+    _check_scene(verts, idx, n_tris)
+    if verts is not None and int(n_verts) > verts.shape[0]:
+        raise ValueError(f"n_verts {n_verts} > verts rows {verts.shape[0]}")
+    _check_outputs(ctx, out_rgba, out_depth)
     rc = _lib.piko_draw_indexed(ctx, _dev_ptr(verts, torch.float32, "verts"), int(n_verts),
                                 _dev_ptr(idx, torch.int32, "idx"), int(n_tris), _f32x(mvp, 16),
                                 _f32x(light, 3), _dev_ptr(out_rgba, torch.float32, "out_rgba"),
@@ -204,14 +239,44 @@ def piko_resolve_keys(ctx, verts, idx, mvp, light, nranks, all_keys, out_rgba, o
 
 def piko_draw_host(ctx, verts, idx, mvp, light, out_rgba, out_depth, stream=None):
     """verts/idx/out_* are CPU torch tensors (pinned for full bandwidth)."""
+    import torch
     for t in (verts, idx, out_rgba, out_depth):
         if t.is_cuda or not t.is_contiguous():
             raise ValueError("piko_draw_host takes contiguous CPU tensors")
+    for t, dt, name in ((verts, torch.float32, "verts"), (idx, torch.int32, "idx"),
+                        (out_rgba, torch.float32, "out_rgba"), (out_depth, torch.float32, "out_depth")):
+        if t.dtype != dt:
+            raise ValueError(f"{name} must be {dt}")
+    _check_scene(verts, idx)
+    _check_outputs(ctx, out_rgba, out_depth)
     rc = _lib.piko_draw_host(ctx, ctypes.c_void_p(verts.data_ptr()), verts.shape[0],
                              ctypes.c_void_p(idx.data_ptr()), idx.shape[0], _f32x(mvp, 16),
                              _f32x(light, 3), ctypes.c_void_p(out_rgba.data_ptr()),
                              ctypes.c_void_p(out_depth.data_ptr()), _stream_ptr(stream))
     return _check(ctx, rc)
+
+
+def piko_draw_patches(ctx, patches, mvp, light, dice_px, max_grid, out_rgba, out_depth, stream=None,
+                      check=True):
+    """Reyes: Split/Dice the bicubic patches (f32[P][16][4] CUDA tensor) on the
+    device and draw the micropolygons (NEXT-4)."""
+    import torch
+    if patches.dim() != 3 or tuple(patches.shape[1:]) != (16, 4):
+        raise ValueError(f"patches must be [P][16][4], got {tuple(patches.shape)}")
+    _check_outputs(ctx, out_rgba, out_depth)
+    rc = _lib.piko_draw_patches(ctx, _dev_ptr(patches, torch.float32, "patches"), int(patches.shape[0]),
+                                _f32x(mvp, 16), _f32x(light, 3), ctypes.c_float(dice_px), int(max_grid),
+                                _dev_ptr(out_rgba, torch.float32, "out_rgba"),
+                                _dev_ptr(out_depth, torch.float32, "out_depth"), _stream_ptr(stream))
+    return _check(ctx, rc) if check else rc
+
+
+def piko_get_diced(ctx):
+    """(verts ptr, n_verts, idx ptr, n_tris) of the last piko_draw_patches mesh."""
+    v, i = ctypes.c_void_p(), ctypes.c_void_p()
+    nv, nt = ctypes.c_int64(), ctypes.c_int64()
+    _check(ctx, _lib.piko_get_diced(ctx, ctypes.byref(v), ctypes.byref(nv), ctypes.byref(i), ctypes.byref(nt)))
+    return v.value, nv.value, i.value, nt.value
 
 
 def piko_finish(ctx):
@@ -353,6 +418,17 @@ class Renderer:
                                      self.rgba, self.depth, stream, check)
         return piko_draw(self.ctx, verts, idx, idx.shape[0], mvp, light, self.rgba, self.depth,
                          stream, check)
+
+    def draw_patches(self, patches, mvp, light, dice_px=2.0, max_grid=128, stream=None, check=True):
+        return piko_draw_patches(self.ctx, patches, mvp, light, dice_px, max_grid, self.rgba, self.depth,
+                                 stream, check)
+
+    def diced(self):
+        """(verts f32[V][8], idx i32[T][3]) of the last draw_patches, as torch copies."""
+        import torch
+        v, nv, i, nt = piko_get_diced(self.ctx)
+        return (_wrap_device(v, (nv, 8), torch.float32, self.device),
+                _wrap_device(i, (nt, 3), torch.int32, self.device))
 
     def primid(self):
         import torch

@@ -1500,6 +1500,154 @@ __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_const
   CM_MARK(2, blockIdx.x, 2);
 }
 
+// ---------------------------------------------------------------------------
+// Reyes Split + Dice (R19-R21).
+// k_dice_rate: one CTA; each thread decides the split/dice rate (Gu, Gv) of
+// patches from their projected control hull, then a block scan over the
+// patches gives every patch its first vertex and first triangle (primitive
+// order = patch order, then quad (i, j), then half).  k_dice: one CTA per
+// patch evaluates its (Gu+1)(Gv+1) vertices (position + Pv x Pu normal) and
+// writes its 2 Gu Gv triangles.  Same pinned op order as the oracle.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int pow2_rate(float len, float dice_px, int max_grid) {
+  int g = 1;
+  while (g < max_grid && len > __fmul_rn(dice_px, (float)g)) g *= 2;
+  return g;
+}
+__device__ int2 dice_rate(const float* __restrict__ cp, const Mat4& M, int W, int H, float dice_px,
+                          int max_grid) {
+  const float hw = __fmul_rn(0.5f, (float)W), hh = __fmul_rn(0.5f, (float)H);
+  float sx[16], sy[16];
+  for (int k = 0; k < 16; ++k) {
+    const float x = cp[4 * k], y = cp[4 * k + 1], z = cp[4 * k + 2];
+    const float cx = __fmaf_rn(M.m[0], x, __fmaf_rn(M.m[1], y, __fmaf_rn(M.m[2], z, M.m[3])));
+    const float cy = __fmaf_rn(M.m[4], x, __fmaf_rn(M.m[5], y, __fmaf_rn(M.m[6], z, M.m[7])));
+    const float cw = __fmaf_rn(M.m[12], x, __fmaf_rn(M.m[13], y, __fmaf_rn(M.m[14], z, M.m[15])));
+    if (!(isfinite(cx) && isfinite(cy) && isfinite(cw)) || !(cw > W_EPS)) return make_int2(max_grid, max_grid);
+    const float r = __frcp_rn(cw);
+    sx[k] = __fmaf_rn(__fmul_rn(cx, r), hw, hw);
+    sy[k] = __fmaf_rn(-__fmul_rn(cy, r), hh, hh);
+  }
+  float Lu = 0.0f, Lv = 0.0f;
+  for (int b = 0; b < 4; ++b) {  // control rows along u: points a*4+b
+    float l = 0.0f;
+    for (int a = 0; a < 3; ++a) {
+      const float dx = fabsf(__fsub_rn(sx[4 * (a + 1) + b], sx[4 * a + b]));
+      const float dy = fabsf(__fsub_rn(sy[4 * (a + 1) + b], sy[4 * a + b]));
+      l = __fadd_rn(l, dx > dy ? dx : dy);
+    }
+    if (l > Lu) Lu = l;
+  }
+  for (int a = 0; a < 4; ++a) {  // control rows along v: points a*4+b
+    float l = 0.0f;
+    for (int b = 0; b < 3; ++b) {
+      const float dx = fabsf(__fsub_rn(sx[4 * a + b + 1], sx[4 * a + b]));
+      const float dy = fabsf(__fsub_rn(sy[4 * a + b + 1], sy[4 * a + b]));
+      l = __fadd_rn(l, dx > dy ? dx : dy);
+    }
+    if (l > Lv) Lv = l;
+  }
+  return make_int2(pow2_rate(Lu, dice_px, max_grid), pow2_rate(Lv, dice_px, max_grid));
+}
+
+__global__ void __launch_bounds__(1024) k_dice_rate(const __grid_constant__ DiceArgs a) {
+  __shared__ unsigned long long s_w[2][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long carry_v = 0, carry_t = 0;
+  for (long long p0 = 0; p0 < a.n; p0 += 1024) {
+    const long long p = p0 + tid;
+    unsigned long long nv = 0, nt = 0;
+    if (p < a.n) {
+      const int2 g = dice_rate(a.patches + 64 * p, a.M, a.W, a.H, a.dice_px, a.max_grid);
+      a.rate[p] = g;
+      nv = (unsigned long long)(g.x + 1) * (g.y + 1);
+      nt = 2ull * g.x * g.y;
+    }
+    unsigned long long iv = nv, it = nt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long tv = __shfl_up_sync(0xffffffffu, iv, o), tt = __shfl_up_sync(0xffffffffu, it, o);
+      if (lane >= o) { iv += tv; it += tt; }
+    }
+    if (lane == 31) { s_w[0][warp] = iv; s_w[1][warp] = it; }
+    __syncthreads();
+    unsigned long long bv = carry_v, bt = carry_t, sv = 0, st = 0;
+    for (int w = 0; w < 32; ++w) {
+      if (w < warp) { bv += s_w[0][w]; bt += s_w[1][w]; }
+      sv += s_w[0][w];
+      st += s_w[1][w];
+    }
+    if (p < a.n) {
+      a.base[2 * p] = (long long)(bv + iv - nv);
+      a.base[2 * p + 1] = (long long)(bt + it - nt);
+    }
+    carry_v += sv;
+    carry_t += st;
+    __syncthreads();
+  }
+  if (tid == 0) { a.total[0] = (long long)carry_v; a.total[1] = (long long)carry_t; }
+}
+
+__device__ __forceinline__ void bernstein(float u, float B[4], float dB[4]) {
+  const float s = __fsub_rn(1.0f, u);
+  B[0] = __fmul_rn(__fmul_rn(s, s), s);
+  B[1] = __fmul_rn(__fmul_rn(__fmul_rn(3.0f, u), s), s);
+  B[2] = __fmul_rn(__fmul_rn(__fmul_rn(3.0f, u), u), s);
+  B[3] = __fmul_rn(__fmul_rn(u, u), u);
+  dB[0] = -__fmul_rn(__fmul_rn(3.0f, s), s);
+  dB[1] = __fmul_rn(__fmul_rn(3.0f, s), __fsub_rn(s, __fmul_rn(2.0f, u)));
+  dB[2] = __fmul_rn(__fmul_rn(3.0f, u), __fsub_rn(__fmul_rn(2.0f, s), u));
+  dB[3] = __fmul_rn(__fmul_rn(3.0f, u), u);
+}
+__device__ __forceinline__ float comb4(const float w[4], float p0, float p1, float p2, float p3) {
+  return __fmaf_rn(w[3], p3, __fmaf_rn(w[2], p2, __fmaf_rn(w[1], p1, __fmul_rn(w[0], p0))));
+}
+
+__global__ void __launch_bounds__(256) k_dice(const __grid_constant__ DiceArgs a) {
+  __shared__ float s_cp[64];
+  const long long p = blockIdx.x;
+  if (threadIdx.x < 64) s_cp[threadIdx.x] = a.patches[64 * p + threadIdx.x];
+  __syncthreads();
+  const int2 g = a.rate[p];
+  const int gu = g.x, gv = g.y;
+  const long long vb = a.base[2 * p], tb = a.base[2 * p + 1];
+  const int nvv = (gu + 1) * (gv + 1);
+  for (int k = threadIdx.x; k < nvv; k += blockDim.x) {
+    const int i = k / (gv + 1), j = k - i * (gv + 1);
+    float Bu[4], dBu[4], Bv[4], dBv[4];
+    bernstein(__fdiv_rn((float)i, (float)gu), Bu, dBu);
+    bernstein(__fdiv_rn((float)j, (float)gv), Bv, dBv);
+    float P[3], Pu[3], Pv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float Q[4], QV[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float* row = s_cp + 16 * r + c;  // control points r*4 + 0..3, component c
+        Q[r] = comb4(Bv, row[0], row[4], row[8], row[12]);
+        QV[r] = comb4(dBv, row[0], row[4], row[8], row[12]);
+      }
+      P[c] = comb4(Bu, Q[0], Q[1], Q[2], Q[3]);
+      Pu[c] = comb4(dBu, Q[0], Q[1], Q[2], Q[3]);
+      Pv[c] = comb4(Bu, QV[0], QV[1], QV[2], QV[3]);
+    }
+    float4* v = reinterpret_cast<float4*>(a.verts + 8 * (vb + k));
+    v[0] = make_float4(P[0], P[1], P[2], 0.0f);
+    v[1] = make_float4(__fmaf_rn(Pv[1], Pu[2], -__fmul_rn(Pv[2], Pu[1])),
+                       __fmaf_rn(Pv[2], Pu[0], -__fmul_rn(Pv[0], Pu[2])),
+                       __fmaf_rn(Pv[0], Pu[1], -__fmul_rn(Pv[1], Pu[0])), 0.0f);
+  }
+  const int nq = gu * gv;
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    const int i = q / gv, j = q - i * gv;
+    const int v00 = (int)(vb + (long long)i * (gv + 1) + j), v01 = v00 + 1;
+    const int v10 = v00 + (gv + 1), v11 = v10 + 1;
+    int32_t* t = a.idx + 3 * (tb + 2ll * q);
+    t[0] = v00; t[1] = v10; t[2] = v11;
+    t[3] = v00; t[4] = v11; t[5] = v01;
+  }
+}
+
 #endif  // PIKO_TILE_TU
 // ---------------------------------------------------------------------------
 // K6: per-bin Process -- raster + depth test + shade + write-back
@@ -2673,6 +2821,14 @@ cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream
 }
 cudaError_t launch_bin_scan(const RadixArgs& a, int grid, bool pdl, cudaStream_t s) {
   return launch_ex(k_bin_scan, grid, SCAN_THREADS, 0, pdl, s, a);
+}
+cudaError_t launch_dice_rate(const DiceArgs& a, cudaStream_t s) {
+  k_dice_rate<<<1, 1024, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_dice(const DiceArgs& a, cudaStream_t s) {
+  if (a.n > 0) k_dice<<<(unsigned)a.n, 256, 0, s>>>(a);
+  return cudaGetLastError();
 }
 cudaError_t launch_cm_scan(const CmArgs& a, int grid, bool pdl, cudaStream_t s) {
   return launch_ex(k_cm_scan, grid, 256, 0, pdl, s, a);

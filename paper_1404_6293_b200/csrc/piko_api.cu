@@ -136,6 +136,14 @@ struct piko_ctx {
   int last_kernels = 0;                // kernels launched by the last frame
 
 
+  // Reyes Split/Dice output (piko_draw_patches): the micropolygon mesh
+  float* dice_verts = nullptr; long long dice_vcap = 0;
+  int32_t* dice_idx = nullptr; long long dice_tcap = 0;
+  int2* dice_rate = nullptr; long long* dice_base = nullptr; long long dice_pcap = 0;
+  long long* dice_total = nullptr;        // device [2]
+  long long* h_dice_total = nullptr;      // pinned [2]
+  long long dice_V = 0, dice_T = 0;
+
   // end-to-end staging
   float* d_verts = nullptr; long long d_verts_cap = 0;
   int32_t* d_idx = nullptr; long long d_idx_cap = 0;
@@ -308,12 +316,13 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   }
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
                   ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
-                  ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys, ctx->def_keys, ctx->cm, ctx->cp,
+                  ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys, ctx->def_keys, ctx->cm, ctx->cp, ctx->dice_verts, ctx->dice_idx, ctx->dice_rate, ctx->dice_base, ctx->dice_total,
                   ctx->all_keys, ctx->fp_keys, ctx->ovq, ctx->sc.sink, ctx->bl_keys, ctx->frag_key,
                   ctx->frag_px, ctx->frag_rgba};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+  if (ctx->h_dice_total) cudaFreeHost(ctx->h_dice_total);
   for (auto& sl : ctx->ring) {
     if (sl.h) cudaFreeHost(sl.h);
     if (sl.ev) cudaEventDestroy(sl.ev);
@@ -1054,6 +1063,73 @@ extern "C" int piko_draw_host(piko_ctx* ctx, const float* h_verts, int64_t n_ver
     CK(cudaMemcpyAsync(h_depth, ctx->d_depth, sizeof(float) * npx, cudaMemcpyDeviceToHost, s));
   }
   CK(cudaStreamSynchronize(s));
+  return PIKO_OK;
+}
+
+// Reyes: Split + Dice on the device into
+// context-owned mesh buffers, then the binned pipeline samples the
+// micropolygons (the Sample stage: AssignBin + per-bin raster; 32x32 bins in
+// the paper) and shades them.  The one host synchronisation is
+// the readback of the mesh size between Dice's rate/scan kernel and the mesh
+// kernel (the pipeline's grids are sized from the triangle count).
+extern "C" int piko_draw_patches(piko_ctx* ctx, const float* patches, int32_t n_patches,
+                                 const float mvp[16], const float light[3], float dice_px,
+                                 int32_t max_grid, float* out_rgba, float* out_depth, void* stream) {
+  if (!ctx) return PIKO_EINVAL;
+  if (n_patches < 0 || (n_patches > 0 && !patches) || !mvp || !light)
+    return ctx->fail(PIKO_EINVAL, "bad patch arguments");
+  if (!(dice_px > 0.0f) || !std::isfinite(dice_px)) return ctx->fail(PIKO_EINVAL, "dice_px must be > 0");
+  if (max_grid < 1 || max_grid > 1024 || (max_grid & (max_grid - 1)))
+    return ctx->fail(PIKO_EINVAL, "max_grid must be a power of two in [1, 1024]");
+  if (reinterpret_cast<uintptr_t>(patches) & 15u) return ctx->fail(PIKO_EINVAL, "patches must be 16-byte aligned");
+  if (ctx->pipeline != PIKO_PIPE_BINNED || exchanging(ctx))
+    return ctx->fail(PIKO_ESTATE, "piko_draw_patches runs the binned pipeline on one GPU");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  if (n_patches > ctx->dice_pcap) {
+    if (ctx->dice_rate) cudaFree(ctx->dice_rate);
+    if (ctx->dice_base) cudaFree(ctx->dice_base);
+    ctx->dice_rate = nullptr; ctx->dice_base = nullptr; ctx->dice_pcap = 0;
+    CK(cudaMalloc(&ctx->dice_rate, sizeof(int2) * n_patches));
+    CK(cudaMalloc(&ctx->dice_base, sizeof(long long) * 2 * n_patches));
+    ctx->dice_pcap = n_patches;
+  }
+  if (!ctx->dice_total) {
+    CK(cudaMalloc(&ctx->dice_total, sizeof(long long) * 2));
+    CK(cudaMallocHost(&ctx->h_dice_total, sizeof(long long) * 2));
+  }
+  DiceArgs d{};
+  d.patches = patches; d.n = n_patches; memcpy(d.M.m, mvp, sizeof d.M.m);
+  d.W = ctx->g.W; d.H = ctx->g.H; d.dice_px = dice_px; d.max_grid = max_grid;
+  d.rate = ctx->dice_rate; d.base = ctx->dice_base; d.total = ctx->dice_total;
+  CK(launch_dice_rate(d, s));
+  CK(cudaMemcpyAsync(ctx->h_dice_total, ctx->dice_total, sizeof(long long) * 2, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const long long V = ctx->h_dice_total[0], T = ctx->h_dice_total[1];
+  if (T > INT32_MAX || V > INT32_MAX) return ctx->fail(PIKO_ECAPACITY, "diced mesh too large (%lld triangles)", T);
+  if (V > ctx->dice_vcap) {
+    if (ctx->dice_verts) cudaFree(ctx->dice_verts);
+    ctx->dice_verts = nullptr; ctx->dice_vcap = 0;
+    CK(cudaMalloc(&ctx->dice_verts, sizeof(float) * 8 * std::max<long long>(V, 1)));
+    ctx->dice_vcap = std::max<long long>(V, 1);
+  }
+  if (T > ctx->dice_tcap) {
+    if (ctx->dice_idx) cudaFree(ctx->dice_idx);
+    ctx->dice_idx = nullptr; ctx->dice_tcap = 0;
+    CK(cudaMalloc(&ctx->dice_idx, sizeof(int32_t) * 3 * std::max<long long>(T, 1)));
+    ctx->dice_tcap = std::max<long long>(T, 1);
+  }
+  d.verts = ctx->dice_verts; d.idx = ctx->dice_idx;
+  CK(launch_dice(d, s));
+  ctx->dice_V = V; ctx->dice_T = T;
+  return draw_impl(ctx, ctx->dice_verts, V, ctx->dice_idx, (int32_t)T, mvp, light, out_rgba, out_depth, s, false);
+}
+
+extern "C" int piko_get_diced(const piko_ctx* ctx, const float** d_verts, int64_t* n_verts,
+                              const int32_t** d_idx, int64_t* n_tris) {
+  if (!ctx || !d_verts || !n_verts || !d_idx || !n_tris) return PIKO_EINVAL;
+  *d_verts = ctx->dice_verts; *n_verts = ctx->dice_V;
+  *d_idx = ctx->dice_idx; *n_tris = ctx->dice_T;
   return PIKO_OK;
 }
 

@@ -318,7 +318,26 @@ struct BaselineArgs {
   ShaderCost sc;
 };
 
+// Reyes Split + Dice (R19-R21): bicubic Bezier
+// patches -> micropolygon mesh that the binned pipeline then samples (32x32
+// bins).
+struct DiceArgs {
+  const float* patches;          // f32[n][16][4] (x, y, z, pad), control point a*4+b
+  long long n;
+  Mat4 M;
+  int W, H;
+  float dice_px;
+  int max_grid;
+  int2* rate;                    // [n] (Gu, Gv)
+  long long* base;               // [n][2] first vertex, first triangle
+  long long* total;              // [2] vertices, triangles (device; copied to the host)
+  float* verts;                  // [V][8] out
+  int32_t* idx;                  // [T][3] out
+};
+
 // ---- launchers (kernels.cu); pdl = programmatic dependent launch -----------
+cudaError_t launch_dice_rate(const DiceArgs& a, cudaStream_t s);
+cudaError_t launch_dice(const DiceArgs& a, cudaStream_t s);
 cudaError_t launch_baseline(const BaselineArgs& a, int stage, bool pdl, cudaStream_t s);
 cudaError_t launch_freepipe(const FreePipeArgs& a, bool pdl, cudaStream_t s);
 cudaError_t launch_fp_resolve(const FreePipeArgs& a, bool pdl, cudaStream_t s);

@@ -13,6 +13,9 @@ triangles", Buddha 1.1M "very small triangles", all at 1024x768):
   c3  1024x768, bins 8/16/32/64, one 1M-tri UV sphere    (Buddha scale)
   c4  1920x1080, 16x16 bins, 4M-tri random soup in NDC
   c5  3840x2160, 16x16 / 8x8 bins, 16M-tri jittered grid (micropolygon density)
+  c6  1024x768, 32x32 bins, 256 bicubic Bezier patches (a bumpy height field in
+      perspective) for the Reyes Split/Dice/Sample pipeline (PAPER.md:1172-1206;
+      SURVEY 8(f) NEXT-4); diced on the device into micropolygon quads (edge bound 2 px)
 
 Layout: verts f32[V][8] = {px,py,pz,0, nx,ny,nz,0},
 idx i32[T][3], mvp f32[16] row-major with clip = M * (x,y,z,1), light f32[3].
@@ -302,7 +305,62 @@ def scene_c5() -> Scene:
     return scene_grid(4000, 2000, 3840, 2160, 5, "c5", (16, 8))
 
 
-CONFIGS = {"c1": scene_c1, "c2": scene_c2, "c3": scene_c3, "c4": scene_c4, "c5": scene_c5}
+@dataclass
+class PatchScene:
+    """Bicubic Bezier patches: f32[P][16][4], control point k = a*4 + b with a
+    along u and b along v, (x, y, z, 0).  Diced on the device (Split/Dice)."""
+    name: str
+    W: int
+    H: int
+    bin_sizes: tuple
+    patches: np.ndarray
+    mvp: np.ndarray
+    light: np.ndarray = field(default_factory=lambda: LIGHT.copy())
+    dice_px: float = 2.0
+    max_grid: int = 128
+
+    @property
+    def n_patches(self) -> int:
+        return int(self.patches.shape[0])
+
+
+def view_mvp(pitch_deg=25.0, eye_y=3.0, **persp) -> np.ndarray:
+    """Perspective * view (camera at (0, eye_y, 0) pitched down), row-major."""
+    c, s_ = math.cos(math.radians(pitch_deg)), math.sin(math.radians(pitch_deg))
+    R = np.array([[1, 0, 0, 0], [0, c, -s_, 0], [0, s_, c, 0], [0, 0, 0, 1]], np.float64)
+    T = np.eye(4)
+    T[1, 3] = -eye_y
+    P = perspective_mvp(**persp).astype(np.float64).reshape(4, 4)
+    return (P @ R @ T).astype(np.float32).reshape(16)
+
+
+def scene_patches(n: int = 16, seed: int = 6, W: int = 1024, H: int = 768, name: str = "c6",
+                  x_range=(-6.0, 6.0), z_range=(-18.0, -3.0), dice_px: float = 2.0,
+                  max_grid: int = 128) -> PatchScene:
+    """n x n bicubic patches on a shared (3n+1)^2 control lattice (C0 across
+    patch borders) over a bumpy height field y = h(x, z) in front of a
+    camera pitched down (PAPER.md:1222-1225 Teapot/Bigguy are not shipped)."""
+    rng = np.random.default_rng(seed)
+    m = 3 * n + 1
+    xs = np.linspace(*x_range, m)
+    zs = np.linspace(*z_range, m)
+    X, Z = np.meshgrid(xs, zs, indexing="ij")
+    Y = 0.6 * np.sin(0.9 * X) * np.cos(0.7 * Z) + 0.3 * np.sin(2.1 * X + 1.3 * Z) + \
+        rng.uniform(-0.15, 0.15, X.shape)
+    lat = np.stack([X, Y, Z, np.zeros_like(X)], -1).astype(np.float32)
+    patches = np.empty((n * n, 16, 4), np.float32)
+    for pi in range(n):
+        for pj in range(n):
+            blk = lat[3 * pi:3 * pi + 4, 3 * pj:3 * pj + 4]   # [a (u)][b (v)]
+            patches[pi * n + pj] = blk.reshape(16, 4)
+    return PatchScene(name, W, H, (32,), patches, view_mvp(), dice_px=dice_px, max_grid=max_grid)
+
+
+def scene_c6() -> PatchScene:
+    return scene_patches()
+
+
+CONFIGS = {"c1": scene_c1, "c2": scene_c2, "c3": scene_c3, "c4": scene_c4, "c5": scene_c5, "c6": scene_c6}
 
 
 def make(name: str) -> Scene:
