@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
   // every CTA takes one ticket per frame: frame = ticket / gridDim.x (the
   // triangle chunk is simply blockIdx.x -- nothing here depends on CTA order)
   if (tid == 0) { s_tk = atomicAdd(&a.ctl->k1_ticket, 1ull) / gridDim.x; s_live = 0; s_nbig = 0; }
-  for (int i = tid; i < MAX_PASSES * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
+  for (int i = tid; i < a.npass * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
   __syncthreads();  // histogram cleared before any thread adds to it; frame known
   const u64 frame = s_tk;
   const long long chunk = blockIdx.x;
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
       const int tx0 = o.px0 >> g.bw_log2, tx1 = o.px1 >> g.bw_log2;
       const int ty0 = o.py0 >> g.bh_log2, ty1 = o.py1 >> g.bh_log2;
       const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
-      if (c == 1 && cmrow) bin1[k] = owned_bin_at(tx0, ty0, tx1, ty1, 0u, g);
+      if (c == 1 && cmrow) bin1[k] = g.nranks == 1 ? ty0 * g.binsX + tx0 : owned_bin_at(tx0, ty0, tx1, ty1, 0u, g);
       else if (c > 1 && c <= (unsigned)K1_BIG && cmrow) {
         for (int ty = ty0; ty <= ty1; ++ty)
           for (int tx = tx0; tx <= tx1; ++tx) {
@@ -1933,7 +1933,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   TileSmem<BW, BH, THREADS>& sm = *reinterpret_cast<TileSmem<BW, BH, THREADS>*>(smem_raw);
   unsigned* s_cov = reinterpret_cast<unsigned*>(smem_raw + sizeof(TileSmem<BW, BH, THREADS>));
   __shared__ int s_bin;     // current bin (-1: work list exhausted)
-  __shared__ int s_rng[3];  // its CSR sub-range [s, e) and fragment count (0: whole bin)
+  __shared__ int s_rng[4];  // its CSR sub-range [s, e), fragment count (0: whole bin), first fragment slot
   __shared__ int s_nbig;    // large triangles queued for the pixel-parallel pass
   __shared__ unsigned s_ln[NLIST];
   __shared__ int s_last;
@@ -1966,8 +1966,9 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
       a.bin_start[1] = ovf ? 0 : (int32_t)a.ctl->n_pairs;
     }
   }
-  // next frame's look-back group arrival counters (every CTA a slice)
-  for (int p = 0; p < a.npass; ++p) {
+  // next frame's look-back group arrival counters (every CTA a slice; only
+  // the radix AssignBin uses them)
+  for (int p = 0; p < (a.radix ? a.npass : 0); ++p) {
     uint32_t* ga = a.garrive + ((size_t)p * 2 + ((frame + 1) & 1)) * a.gcap;
     for (long long i = (long long)blockIdx.x * THREADS + tid; i < a.gcap; i += (long long)gridDim.x * THREADS)
       ga[i] = 0u;
@@ -1994,7 +1995,10 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     re = a.bin_start[b + 1];
   };
   // work item w -> bin, CSR sub-range, number of fragments of the bin (0: unsplit)
-  auto work_item = [&](unsigned w, int& b, int& rs, int& re, int& nf) {
+  // (fragments of a bin are consecutive in the list: fragment j of item w
+  // keeps its key tile in slot w, the bin's first slot is w - j)
+  auto work_item = [&](unsigned w, int& b, int& rs, int& re, int& nf, int& fs) {
+    fs = -1;
     if (w < n_frag) {
       const int2 it = a.frag_list[w];
       b = it.x;
@@ -2003,6 +2007,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
       nf = (e0 - s0 + a.frag - 1) / a.frag;
       rs = s0 + it.y * a.frag;
       re = min(rs + a.frag, e0);
+      fs = (int)w - it.y;
     } else if (w < n_work) {
       if (a.npass == 0) {
         b = 0;
@@ -2026,14 +2031,14 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
 
   // ---- LoadBalance schedule over the work list ----------------
   // thread 0 keeps the next item in registers one item ahead
-  int q_bin = -1, q_s = 0, q_e = 0, q_nf = 0;
+  int q_bin = -1, q_s = 0, q_e = 0, q_nf = 0, q_fs = -1;
   unsigned q_tk = 0;
   if (tid == 0) {
     const unsigned t0 = atomicAdd(&a.ctl->tile_next, 1u);
     q_tk = atomicAdd(&a.ctl->tile_next, 1u);
-    int b0 = -1, s0 = 0, e0 = 0, nf0 = 0;
-    work_item(t0, b0, s0, e0, nf0);
-    s_bin = b0; s_rng[0] = s0; s_rng[1] = e0; s_rng[2] = nf0;
+    int b0 = -1, s0 = 0, e0 = 0, nf0 = 0, fs0 = -1;
+    work_item(t0, b0, s0, e0, nf0, fs0);
+    s_bin = b0; s_rng[0] = s0; s_rng[1] = e0; s_rng[2] = nf0; s_rng[3] = fs0;
   }
   __syncthreads();
   // Pipeline prologue of an item: primIDs of the first TQ rounds and the
@@ -2061,10 +2066,10 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   for (;;) {
     const int b = s_bin;
     if (b < 0) break;
-    const int s = s_rng[0], e = s_rng[1], nfrag = s_rng[2];
+    const int s = s_rng[0], e = s_rng[1], nfrag = s_rng[2], fslot0 = s_rng[3];
     TL_MARK(b, 0);
     if (tid == 0) {  // prefetch the next item
-      work_item(q_tk, q_bin, q_s, q_e, q_nf);
+      work_item(q_tk, q_bin, q_s, q_e, q_nf, q_fs);
       if (q_bin >= 0) q_tk = atomicAdd(&a.ctl->tile_next, 1u);
       s_nx[0] = q_bin; s_nx[1] = q_s; s_nx[2] = q_e;
     }
@@ -2339,14 +2344,15 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
         store_pixel<COV, KEYS_ONLY>(a, L, job, p, NPX, x, y, sm.key[p], COV ? s_cov[p] : 0u);
       }
     } else {
-      // fragment of a split bin: merge into the bin's global key tile; the
-      // last fragment to arrive writes the bin
-      u64* gk = a.gkey + (size_t)b * NPX;
+      // fragment of a split bin: its key tile goes to its own slot with plain
+      // coalesced stores (no atomics); the last fragment to arrive takes the
+      // per-pixel minimum over the bin's slots and writes the bin
+      const int myslot = fslot0 + (s - a.bin_start[b]) / a.frag;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         const int p = tid + k * THREADS;
         if (p >= NPX) continue;
-        if (sm.key[p] != CLEAR_KEY) atomicMin(&gk[p], sm.key[p]);
+        a.fkey[(size_t)myslot * NPX + p] = sm.key[p];
         if (COV && s_cov[p]) atomicAdd(&a.gcov[(size_t)b * NPX + p], s_cov[p]);
       }
       __threadfence();
@@ -2365,9 +2371,17 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
           if (p >= NPX) continue;
           const int x = x0 + (p % BW), y = y0 + (p / BW);
           if (!KEYS_ONLY && (x > x1 || y > y1)) continue;
-          const u64 key = __ldcg(&gk[p]);
+          u64 key = sm.key[p];
+          for (int f0 = 0; f0 < nfrag; f0 += 4) {  // 4 slot loads in flight
+            u64 kv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              kv[u] = (f0 + u < nfrag && fslot0 + f0 + u != myslot)
+                          ? __ldcg(&a.fkey[(size_t)(fslot0 + f0 + u) * NPX + p]) : CLEAR_KEY;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) key = kv[u] < key ? kv[u] : key;
+          }
           const unsigned cv = COV ? __ldcg(&a.gcov[(size_t)b * NPX + p]) : 0u;
-          gk[p] = CLEAR_KEY;  // ready for the next frame
           if (COV) a.gcov[(size_t)b * NPX + p] = 0u;
           store_pixel<COV, KEYS_ONLY>(a, L, job, p, NPX, x, y, key, cv);
         }
@@ -2376,7 +2390,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     TL_MARK(b, 2);
     if (tid == 0 && b < 8192) { g_tl_extra(b, e - s, blockIdx.x); }
     __syncthreads();  // keys consumed before the next bin reinitialises them
-    if (tid == 0) { s_bin = q_bin; s_rng[0] = q_s; s_rng[1] = q_e; s_rng[2] = q_nf; }
+    if (tid == 0) { s_bin = q_bin; s_rng[0] = q_s; s_rng[1] = q_e; s_rng[2] = q_nf; s_rng[3] = q_fs; }
     __syncthreads();
   }
 

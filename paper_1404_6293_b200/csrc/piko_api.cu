@@ -98,7 +98,7 @@ struct piko_ctx {
   int32_t* bin_start = nullptr;
   int2* frag_list = nullptr; long long frag_cap = 0;  // split-bin fragments
   int32_t* bin_list = nullptr;       // [NLIST-1][NB] single-fragment bins by size class, empty bins
-  unsigned long long* gkey = nullptr;  // [NB][bw*bh] key tiles of split bins
+  unsigned long long* fkey = nullptr;  // [frag_cap][bw*bh] key tile of every split-bin fragment
   uint32_t* gcov = nullptr;          // [NB][bw*bh] coverage tiles (debug)
   uint32_t* arrive = nullptr;        // [NB] fragment arrival counters
   int4* ovq = nullptr; long long ovq_ctas = 0;  // k_tile queue overflow [ctas][OVQ_CAP][6]
@@ -273,7 +273,6 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   bool ok = cudaMalloc(&ctx->bin_count, sizeof(uint32_t) * g.NB) == cudaSuccess &&
             cudaMalloc(&ctx->bin_start, sizeof(int32_t) * (g.NB + 1)) == cudaSuccess &&
             cudaMalloc(&ctx->bin_list, sizeof(int32_t) * (NLIST - 1) * (size_t)g.NB) == cudaSuccess &&
-            cudaMalloc(&ctx->gkey, sizeof(unsigned long long) * (size_t)g.NB * bin_w * bin_h) == cudaSuccess &&
             cudaMalloc(&ctx->arrive, sizeof(uint32_t) * (size_t)g.NB) == cudaSuccess &&
             cudaMalloc(&ctx->ctl, sizeof(Control)) == cudaSuccess &&
             cudaMalloc(&ctx->primid, sizeof(int32_t) * npx) == cudaSuccess &&
@@ -315,7 +314,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
     cudaFree(ctx->p2p_sync);
   }
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
-                  ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->gkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
+                  ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->fkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys, ctx->def_keys, ctx->cm, ctx->cp, ctx->dice_verts, ctx->dice_idx, ctx->dice_rate, ctx->dice_base, ctx->dice_total,
                   ctx->all_keys, ctx->fp_keys, ctx->ovq, ctx->sc.sink, ctx->bl_keys, ctx->frag_key,
                   ctx->frag_px, ctx->frag_rgba};
@@ -397,6 +396,9 @@ static int ensure_pairs(piko_ctx* ctx, unsigned long long P) {
   if (ctx->frag_list) cudaFree(ctx->frag_list);
   ctx->frag_list = nullptr;
   CK(cudaMalloc(&ctx->frag_list, sizeof(int2) * fcap));
+  if (ctx->fkey) cudaFree(ctx->fkey);
+  ctx->fkey = nullptr;
+  CK(cudaMalloc(&ctx->fkey, sizeof(unsigned long long) * (size_t)fcap * ctx->bw * ctx->bh));
   ctx->frag_cap = fcap;
   ctx->need_reset = true;
   return PIKO_OK;
@@ -679,7 +681,6 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     CK(cudaMemsetAsync(ctx->garr, 0, sizeof(uint32_t) * 2 * ctx->gcap * ctx->npass, s));
     CK(cudaMemsetAsync(ctx->bin_count, 0, sizeof(uint32_t) * ctx->g.NB, s));
     CK(cudaMemsetAsync(ctx->arrive, 0, sizeof(uint32_t) * ctx->g.NB, s));
-    CK(cudaMemsetAsync(ctx->gkey, 0xFF, sizeof(unsigned long long) * ctx->g.NB * ctx->bw * ctx->bh, s));
     if (ctx->gcov) CK(cudaMemsetAsync(ctx->gcov, 0, sizeof(uint32_t) * ctx->g.NB * ctx->bw * ctx->bh, s));
     for (int k = 0; k < 6; ++k) ctx->last_grids[k] = grids[k];
     ctx->need_reset = false;
@@ -723,7 +724,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.ctl = ctx->ctl; a.pass = p; a.shift = RX_BITS * p;
     a.bin_count = ctx->bin_count; a.bin_start = ctx->bin_start; a.scan_status = ctx->st_scan;
     a.NB = ctx->g.NB; a.rank = ctx->g.rank; a.nranks = ctx->g.nranks;
-    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
+    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list;
     a.gcov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->gcov : nullptr;
     a.frag = tile_frag(ctx->bw, ctx->bh); a.npx = ctx->bw * ctx->bh;
     CK(launch_radix_pass(a, (int)(p == 0 ? gx : gp + (p == 1 ? ntiles : 0)), ctx->pdl, s));
@@ -738,7 +739,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     RadixArgs& a = c.sched;
     a.g = ctx->g; a.ctl = ctx->ctl; a.bin_start = ctx->bin_start; a.bin_count = ctx->bin_count; a.NB = ctx->g.NB;
     a.rank = ctx->g.rank; a.nranks = ctx->g.nranks;
-    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
+    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list;
     a.frag = tile_frag(ctx->bw, ctx->bh); a.npx = ctx->bw * ctx->bh;
     CK(launch_cm_scan(c, cm_scan_grid(ctx->g.NB), ctx->pdl, s));
     CK(mark(1 + PIKO_STAGE_EXPAND));
@@ -771,10 +772,11 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
       a.status_ok = 1;
     }
     a.owned = ctx->owned;
-    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list; a.gkey = ctx->gkey;
-    a.gcov = ctx->gcov; a.arrive = ctx->arrive; a.frag = tile_frag(ctx->bw, ctx->bh);
+    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list;
+    a.fkey = ctx->fkey; a.gcov = ctx->gcov; a.arrive = ctx->arrive; a.frag = tile_frag(ctx->bw, ctx->bh);
     a.garrive = ctx->garr; a.gcap = ctx->gcap;
     a.prim_base = (unsigned)ctx->prim_base;
+    a.radix = cm ? 0 : 1;
     if (keys_only) a.out_cov = nullptr;
     const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, keys_only)));
     if (grid > ctx->ovq_ctas) {  // spill space of the per-bin large-triangle queue

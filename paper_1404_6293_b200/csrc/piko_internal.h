@@ -169,7 +169,6 @@ struct RadixArgs {
   int rank, nranks;             // only owned bins enter the work lists
   int2* frag_list;              // [frag_cap] {bin, fragment}
   int32_t* bin_list;            // [NLIST-1][NB] single-fragment bins by size class, empty bins
-  unsigned long long* gkey;     // [NB][bw*bh] key tiles of split bins
   uint32_t* gcov;               // [NB][bw*bh] coverage tiles (debug) or null
   int frag;                     // pairs per fragment
   int npx;                      // pixels per bin
@@ -228,13 +227,14 @@ struct TileArgs {
   int owned;                    // bins owned by this rank (grid may be larger)
   const int2* frag_list;
   const int32_t* bin_list;
-  unsigned long long* gkey;
+  unsigned long long* fkey;      // [frag_cap][bw*bh] key tile of every fragment item (slot = item index)
   uint32_t* gcov;
   uint32_t* arrive;             // [NB] fragments merged so far (self-resetting)
   int frag;
   uint32_t* garrive;            // [npass][2][gcap] look-back group arrival counters;
   long long gcap;               //   k_tile zeroes the next frame's parity
   unsigned prim_base;           // keys-only: added to the primID of every stored key (sort-last)
+  int radix;                    // 1: the frame used the radix AssignBin (its look-back counters)
   int4* ovq;                    // [grid][OVQ_CAP][6] overflow of the per-bin queue (null: none)
   // P2P transport (sort-first): tile_keys points into rank 0's memory
   unsigned long long* p2p_flag;         // rank 0's arrival flag of this rank (null: no P2P)

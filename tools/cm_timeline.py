@@ -85,3 +85,19 @@ c = buf[0, 7000:7000 + 1024].astype(np.int64)
 c = c[c[:, 0] > T0] - T0
 print(f"   k_tile CTAs: resident first {c[:,3].min()} p50 {np.median(c[:,3]):.0f}; past pdl wait {c[:,0].min()}..{c[:,0].max()};"
       f" bin loop end p50 {np.median(c[:,1]):.0f} max {c[:,1].max()}; CTA end p50 {np.median(c[:,2]):.0f} max {c[:,2].max()}")
+tt = buf[3, :min(nb, 8192)].astype(np.int64)
+ok = (tt[:, 0] > T0) & (tt[:, 2] >= tt[:, 0])
+rows = [(int(tt[b, 4]), b, int(tt[b, 3]), tt[b, 0] - T0, tt[b, 1] - tt[b, 0], tt[b, 2] - tt[b, 1])
+        for b in np.nonzero(ok)[0]]
+by = {}
+for cta, b, n, st_, ra, wb in rows:
+    by.setdefault(cta, []).append((st_, b, n, ra, wb))
+ends = sorted(((max(s_ + r_ + w_ for s_, _, _, r_, w_ in v), c) for c, v in by.items()), reverse=True)
+print("   slowest CTAs (end ns): bins as (start, pairs, raster, writeback)")
+for e_, cc in ends[:6]:
+    print(f"     cta {cc:4d} end {e_:6d}: " + "  ".join(f"({s_},{n},{r_},{w_})" for s_, _, n, r_, w_ in sorted(by[cc])))
+firsts = sorted(v[0][0] for v in (sorted(x) for x in by.values()))
+print(f"   first-bin start across CTAs: min {firsts[0]} p50 {np.median(firsts):.0f} max {max(firsts)}")
+seconds = sorted(sorted(x)[1][0] for x in by.values() if len(x) > 1)
+if seconds:
+    print(f"   second-bin start: min {seconds[0]} p50 {np.median(seconds):.0f} max {max(seconds)}; CTAs with 2+ bins {len(seconds)}")
