@@ -536,7 +536,21 @@ def run_piko(args):
              "expand": "k_cm_scan" if cm_rows else "k_radix_pass<EXPAND=true> (pass 0)",
              "sort": "k_cm_scatter" if cm_rows else "k_radix_pass<EXPAND=false> (passes >= 1)",
              "tile": "k_tile", "resolve": "k_resolve / k_shade"}[dom]
+    ncu_note = None  # the same kernel's ncu --set full counters (profiles/ncu_full_r2_<cfg>.txt)
+    nf = os.path.join(ROOT, "profiles", f"ncu_full_r2_{args.config}.txt")
+    if os.path.exists(nf):
+        want = {"tile": "k_tile", "setup": "k_setup", "expand": "k_cm_scan" if cm_rows else "k_radix_pass",
+                "sort": "k_cm_scatter" if cm_rows else "k_radix_pass", "vertex": "k_vertex"}.get(dom)
+        lines = [l for l in open(nf) if not l.startswith("#")]
+        hdr = [l for l in open(nf) if l.startswith("# kernel")]
+        for l in lines:
+            if want and want in l.split(",")[0]:
+                ncu_note = (hdr[0][2:].strip() if hdr else "") + " | " + l.strip()
+                break
     roofline = {"bound": "hbm", "kernel": kname, "stage": dom,
+                "limiter": ("latency: few resident warps per SM and dependent L2 round trips per bin "
+                            "(ncu issue-active / warps-active in `ncu`)") if dom == "tile" else None,
+                "ncu": ncu_note,
                 "launches_per_step": max(stats["radix_passes"] - 1, 1) if dom == "sort" else 1,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": nb,
@@ -544,13 +558,22 @@ def run_piko(args):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
     frame_bytes = sum(algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"], cm_rows)
                       for k in ("vertex", "setup", "expand", "sort", "tile") if per_frame.get(k, 0) > 0.004)
-    # BASELINE.md's frame metric: ncu-measured DRAM bytes of the frame's kernels
-    measured = None
-    if os.path.exists(tf):
+    # BASELINE.md's frame metric: ncu-measured DRAM bytes of one whole frame
+    # (range replay: all kernels in one range, L2 write-backs included --
+    # tools/frame_dram.py); else the sum of per-kernel cold replays
+    measured, measured_note = None, None
+    ff = os.path.join(ROOT, "profiles", f"traffic_frame_{args.config}_b{bw}.json")
+    if os.path.exists(ff):
+        fj = json.load(open(ff))
+        measured = int(fj["frame_bytes"])
+        measured_note = f"profiles/traffic_frame_{args.config}_b{bw}.json: " + fj.get("_note", "")
+    elif os.path.exists(tf):
         tj = json.load(open(tf))
         ran = [k for k in ("vertex", "setup", "expand", "sort", "tile") if per_frame.get(k, 0) > 0.004]
         if all(k in tj for k in ran):
             measured = int(sum(tj[k] for k in ran))
+            measured_note = ("sum of ncu dram__bytes_read+write per kernel of one frame "
+                             "(profiles/traffic_*.json; ncu replays each kernel cold)")
     ms = total_ms / args.steps
     out = {
         "metric": METRIC, "value": T * args.steps / (total_ms / 1e3) / 1e6, "unit": UNIT,
@@ -567,8 +590,7 @@ def run_piko(args):
         "frame_roofline": {"algorithmic_bytes": frame_bytes, "frac": frame_bytes / (ms / 1e3) / 1e9 / peak,
                            "measured_bytes": measured,
                            "frac_measured": measured / (ms / 1e3) / 1e9 / peak if measured else None,
-                           "measured_note": "sum of ncu dram__bytes_read+write per kernel of one frame "
-                                            "(profiles/traffic_*.json; ncu replays each kernel cold)"},
+                           "measured_note": measured_note},
         "kernel_ms": per_frame,
         "kernel_ms_note": "per-stage CUDA-event times from a second K-step pass (events between kernels)",
         "api": "piko_draw (north-star C ABI call via ctypes, PIKO_SYNC_ASYNC)",

@@ -27,7 +27,9 @@ def stage(name):
     if base == "k_radix_pass":  # template argument EXPAND: pass 0 vs passes >= 1
         return "expand" if any(t in name for t in ("<(bool)1>", "<true>", "<1>")) else "sort"
     return {"k_vertex": "vertex", "k_setup": "setup", "k_tile": "tile", "k_resolve": "resolve",
-            "k_bin_scan": "expand", "k_index_max": "vertex"}.get(base)
+            "k_bin_scan": "expand", "k_index_max": "vertex", "k_cm_scan": "expand",
+            "k_cm_scatter": "sort", "k_shade": "resolve", "k_dice_rate": "dice",
+            "k_dice": "dice"}.get(base)
 
 
 rows = [r for r in csv.reader(open(launches)) if r and not r[0].startswith("==")]
