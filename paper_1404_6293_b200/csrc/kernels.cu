@@ -25,6 +25,7 @@
 // round-to-nearest intrinsics, explicit fma); this TU is compiled with
 // --fmad=false so no other contraction can happen.
 #include <algorithm>
+#include <cstddef>
 #include <cstdint>
 
 #include "piko_internal.h"
@@ -115,6 +116,9 @@ __device__ u64 g_rx_lb[2][8192][8];
 }  // namespace piko
 extern "C" int piko_dbg_k1_times(void* host, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(host, piko::g_k1_times, bytes);
+}
+extern "C" int piko_dbg_k1_set(const void* host, size_t bytes) {
+  return (int)cudaMemcpyToSymbol(piko::g_k1_times, host, bytes);
 }
 extern "C" int piko_dbg_rx_lb(void* host, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(host, piko::g_rx_lb, bytes);
@@ -312,8 +316,18 @@ static __device__ __noinline__ int owned_bin_at_r(int tx0, int ty0, int tx1, int
 // K0: vertex stage -- each vertex transformed and snapped exactly once
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(VX_THREADS) k_vertex(VertexArgs a) {
+#ifdef PIKO_K1_TIMING
+  if (threadIdx.x == 0) {  // [0][8190]: first / last CTA start (before the wait), [0][8191]: after it
+    const u64 t = gtimer();
+    atomicMin(&g_k1_times[0][8190][0], t);
+    atomicMax(&g_k1_times[0][8190][1], t);
+  }
+#endif
   pdl_wait();   // the previous frame's kernels still read xv
   pdl_trigger();
+#ifdef PIKO_K1_TIMING
+  if (threadIdx.x == 0) atomicMin(&g_k1_times[0][8191][0], gtimer());
+#endif
   long long V = a.n_verts >= 0 ? a.n_verts : (long long)a.ctl->vmax;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.ctl->vx_need = (unsigned long long)V;
@@ -1165,6 +1179,7 @@ __global__ void __launch_bounds__(256) k_cm_scan(const __grid_constant__ CmArgs 
     }
   }
   CM_MARK(1, j, 2);
+  if (NB <= RX_CHUNK) return;  // small grids: every k_cm_scatter CTA scans the totals itself
   // the last CTA to finish scans the bin totals into bin_start (no chain
   // between CTAs: every other CTA is done after its own sweeps)
   __syncthreads();
@@ -1182,10 +1197,18 @@ __global__ void __launch_bounds__(256) k_cm_scan(const __grid_constant__ CmArgs 
   for (int b0 = 0; b0 < NB; b0 += 256 * BPT) {
     unsigned c[BPT];
     u64 cs = 0;
+    if ((NB & 3) == 0 && b0 + tid * BPT + BPT <= NB) {  // contiguous 16-byte loads (see k_cm_scatter)
 #pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-      const int bb = b0 + tid * BPT + k;
-      c[k] = bb < NB ? __ldcg(a.sched.bin_count + bb) : 0u;
+      for (int k = 0; k < BPT; k += 4) {
+        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(a.sched.bin_count + b0 + tid * BPT + k));
+        c[k] = q.x; c[k + 1] = q.y; c[k + 2] = q.z; c[k + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < BPT; ++k) {
+        const int bb = b0 + tid * BPT + k;
+        c[k] = bb < NB ? __ldcg(a.sched.bin_count + bb) : 0u;
+      }
     }
 #pragma unroll
     for (int k = 0; k < BPT; ++k) cs += c[k];
@@ -1286,33 +1309,85 @@ __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_const
     const long long t = tbeg + warp * TPW + k * 32 + lane;
     rr[k] = t < tend ? __ldcg(a.rect + t) : make_uint2(1u, 0u);
   }
-  pdl_wait();   // k_cm_scan's prefixes and bin_start
+  pdl_wait();   // k_cm_scan's column prefixes and bin totals (bin_start too when NB > RX_CHUNK)
   pdl_trigger();
   CM_MARK(2, blockIdx.x, 1);
-  if (sched) {  // extra CTAs: k_tile's work lists (bin_start is final)
+  uint32_t* cprow = a.cp + (size_t)(sched ? 0 : row) * NB;
+  if (cur_by_bin) {
+    // NB <= RX_CHUNK: every CTA scans the bin totals itself (BPT consecutive
+    // bins per thread) -- bin_start without a serial last-CTA phase -- and
+    // the cursors are bin_start + the row's column prefix, by bin
+    constexpr int BPT = RX_CHUNK / CM_THREADS;
+    static_assert(BPT % 4 == 0, "uint4 loads");
+    unsigned c[BPT], cv[BPT];
+    u64 csum = 0;
+    if ((NB & 3) == 0 && tid * BPT + BPT <= NB) {
+      // BPT consecutive words per thread as 16-byte loads: a warp reads one
+      // contiguous run (scalar loads at this stride fetch every sector BPT times)
+#pragma unroll
+      for (int k = 0; k < BPT; k += 4) {
+        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(a.sched.bin_count + tid * BPT + k));
+        c[k] = q.x; c[k + 1] = q.y; c[k + 2] = q.z; c[k + 3] = q.w;
+        const uint4 r = sched ? make_uint4(0u, 0u, 0u, 0u) : __ldcg(reinterpret_cast<const uint4*>(cprow + tid * BPT + k));
+        cv[k] = r.x; cv[k + 1] = r.y; cv[k + 2] = r.z; cv[k + 3] = r.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < BPT; ++k) {
+        const int bb = tid * BPT + k;
+        c[k] = bb < NB ? __ldcg(a.sched.bin_count + bb) : 0u;
+        cv[k] = (bb < NB && !sched) ? __ldcg(cprow + bb) : 0u;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) csum += c[k];
+    u64 inc = csum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    __shared__ u64 s_w64[CM_WARPS];
+    __shared__ u64 s_P;
+    if (lane == 31) s_w64[warp] = inc;
+    __syncthreads();
+    u64 base = 0, P = 0;
+#pragma unroll
+    for (int w = 0; w < CM_WARPS; ++w) {
+      base += w < warp ? s_w64[w] : 0ull;
+      P += s_w64[w];
+    }
+    u64 run = base + inc - csum;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+      const int bb = tid * BPT + k;
+      if (bb < NB) {
+        sm.cur[bb] = (unsigned)run + cv[k];
+        if (sched) a.sched.bin_start[bb] = (int32_t)(run < MAX_PAIRS ? run : MAX_PAIRS - 1);
+      }
+      run += c[k];
+    }
+    if (tid == 0) s_P = P;
+    __syncthreads();
+    P = s_P;
+    if (sched && blockIdx.x == a.rows && tid == 0) {  // the first schedule CTA publishes P
+      a.ctl->n_pairs = P;
+      a.sched.bin_start[NB] = (int32_t)(P < MAX_PAIRS ? P : MAX_PAIRS - 1);
+      if (P > a.cap) atomicMax(&a.ctl->overflow_tag, a.ctl->frame + 1);
+    }
+    if (P > a.cap) return;  // every CTA sees it: nothing is written, k_tile renders background
+  }
+  if (sched) {  // extra CTAs: k_tile's work lists
     const long long b0 = ((long long)blockIdx.x - a.rows) * SCAN_CHUNK + (long long)tid * SCAN_ITEMS;
     const bool active = tid < SCAN_THREADS;  // SCAN_CHUNK bins per schedule CTA
     unsigned c[SCAN_ITEMS];
 #pragma unroll
     for (int k = 0; k < SCAN_ITEMS; ++k)
-      c[k] = (active && b0 + k < NB) ? (unsigned)(a.sched.bin_start[b0 + k + 1] - a.sched.bin_start[b0 + k]) : 0u;
+      c[k] = (active && b0 + k < NB) ? __ldcg(a.sched.bin_count + b0 + k) : 0u;
     schedule_bins(a.sched, b0, c, active);
     return;
   }
-  if (a.ctl->overflow_tag == a.ctl->frame + 1) return;  // P > capacity: k_tile renders background
-  uint32_t* cprow = a.cp + (size_t)row * NB;
-  if (cur_by_bin) {  // cursor = bin_start + column prefix; all loads in flight, then the stores
-    constexpr int CPT = RX_CHUNK / CM_THREADS;
-    unsigned cv[CPT], bv[CPT];
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      const int bb = tid + k * CM_THREADS;
-      cv[k] = bb < NB ? __ldcg(cprow + bb) : 0u;
-      bv[k] = bb < NB ? (unsigned)__ldcg(a.sched.bin_start + bb) : 0u;
-    }
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) if (tid + k * CM_THREADS < NB) sm.cur[tid + k * CM_THREADS] = cv[k] + bv[k];
-  }
+  if (a.ctl->overflow_tag == a.ctl->frame + 1) return;  // P > capacity (or vertex overflow): background
   for (int w = tid; w < NBW; w += CM_THREADS) sm.bm[w] = 0u;
   auto block_excl = [&](unsigned v) -> unsigned {  // every thread must call it
     unsigned inc = v;
@@ -2091,6 +2166,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     // the bin is done.  Tiny triangles: one thread loops over its pixels;
     // larger ones: warp-cooperative (triangle, pixel) expansion.
     const int nround = (e - s + THREADS - 1) / THREADS;
+    TL_MARK(b, 5);  // tile cleared
     if (!pre) prologue(s, e);
     for (int k = 0; k < nround; ++k) {
       const int buf = k % NSTAGE;
@@ -2215,8 +2291,10 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
       }
       __syncwarp();  // round k's slots are free for round k + NSTAGE
     }
+    TL_MARK(b, 6);  // rounds issued/rasterized
     cp_async_wait<0>();
     __syncthreads();
+    TL_MARK(b, 7);  // all records consumed
     // record stages are free: start the next item's loads now
     pre = s_nx[0] >= 0;
     if (pre) prologue(s_nx[1], s_nx[2]);
@@ -2403,8 +2481,11 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     tk = __shfl_sync(0xffffffffu, tk, 0);
     const unsigned e0 = tk * EMPTY_GROUP;
     if (e0 >= n_empty) break;
+    // the group's bin ids in one round trip (lane l loads entry e0 + l), not
+    // one dependent load per bin
+    const int bl = (lane < EMPTY_GROUP && e0 + lane < n_empty) ? empty_bin(e0 + lane) : 0;
     for (unsigned e = e0; e < min(e0 + EMPTY_GROUP, n_empty); ++e) {
-      const int b = empty_bin(e);
+      const int b = __shfl_sync(0xffffffffu, bl, (int)(e - e0));
       const int x0 = (b % g.binsX) * BW, y0 = (b / g.binsX) * BH;
       const int x1 = min(x0 + BW, g.W) - 1, y1 = min(y0 + BH, g.H) - 1;
       const int job = (b - g.rank) / g.nranks;
@@ -2417,6 +2498,22 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   }
   TL_CTA(2);
   if (fwd) shader_sink(a.sc, facc);
+  if (a.status_out) {
+    // the frame's control block (P, overflow tags, statistics -- final: the
+    // kernels that write them are complete) straight into the host's pinned
+    // mirror by the last CTA: no device-to-host copy on the stream
+    __shared__ int s_mlast;
+    __syncthreads();
+    if (tid == 0) s_mlast = (atomicAdd(&a.ctl->tile_done, 1ull) + 1) % gridDim.x == 0;
+    __syncthreads();
+    if (s_mlast) {
+      __threadfence();
+      constexpr int NW = (int)(offsetof(Control, digit_hist) / sizeof(u64));
+      const volatile u64* src = reinterpret_cast<const volatile u64*>(a.ctl);
+      u64* dst = reinterpret_cast<u64*>(a.status_out);
+      for (int w = tid; w < NW; w += THREADS) dst[w] = src[w];
+    }
+  }
   if (KEYS_ONLY && a.p2p_flag) {
     // P2P: every CTA's key stores (straight into rank 0's memory over NVLink)
     // are made visible system-wide before it is counted; the last CTA counted

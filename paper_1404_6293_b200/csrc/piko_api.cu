@@ -125,7 +125,12 @@ struct piko_ctx {
   // has completed -- polled without blocking at the next draw, waited for
   // only when the ring is full, at piko_finish, or by an inspection call.
   static constexpr int NRING = 8;
-  struct Slot { Control* h = nullptr; cudaEvent_t ev = nullptr; long long T = 0; };
+  struct Slot {
+    Control* h = nullptr;   // pinned, mapped host mirror
+    Control* d = nullptr;   // its device alias: the binned frame's last kernel writes it directly
+    cudaEvent_t ev = nullptr;
+    long long T = 0;
+  };
   Slot ring[NRING];
   int ring_head = 0, ring_n = 0;     // next slot to fill; frames in flight
   Control* h_ctl = nullptr;          // mirror of the last evaluated frame
@@ -279,7 +284,8 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
             cudaMalloc(&ctx->sc.sink, 16) == cudaSuccess &&
             cudaMallocHost(&ctx->h_ctl, sizeof(Control)) == cudaSuccess;
   for (int k = 0; k < piko_ctx::NRING && ok; ++k)
-    ok = cudaMallocHost(&ctx->ring[k].h, sizeof(Control)) == cudaSuccess &&
+    ok = cudaHostAlloc(&ctx->ring[k].h, sizeof(Control), cudaHostAllocMapped) == cudaSuccess &&
+         cudaHostGetDevicePointer(&ctx->ring[k].d, ctx->ring[k].h, 0) == cudaSuccess &&
          cudaEventCreateWithFlags(&ctx->ring[k].ev, cudaEventDisableTiming) == cudaSuccess;
   ctx->st_scan_n = (g.NB + SCAN_CHUNK - 1) / SCAN_CHUNK;
   ok = ok && cudaMalloc(&ctx->st_scan, sizeof(unsigned long long) * ctx->st_scan_n) == cudaSuccess;
@@ -323,7 +329,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
   if (ctx->h_dice_total) cudaFreeHost(ctx->h_dice_total);
   for (auto& sl : ctx->ring) {
-    if (sl.h) cudaFreeHost(sl.h);
+    if (sl.h) cudaFreeHost(sl.h);  // (cudaHostAlloc'ed)
     if (sl.ev) cudaEventDestroy(sl.ev);
   }
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -459,9 +465,10 @@ static int poll_frames(piko_ctx* ctx, bool block) {
   return PIKO_OK;
 }
 
-// Queue the end of a frame: its control block into the next ring slot's
-// pinned mirror and an event.  A full ring waits for its oldest frame.
-static cudaError_t record_frame_end(piko_ctx* ctx, cudaStream_t s, long long T) {
+// Make the next ring slot free (a full ring waits for its oldest frame) and
+// return its mirror's device alias (the binned frame's tile kernel writes the
+// control block into it: no copy on the stream).
+static cudaError_t reserve_slot(piko_ctx* ctx, Control** dev_mirror) {
   if (ctx->ring_n == piko_ctx::NRING && poll_frames(ctx, false) == PIKO_OK && ctx->ring_n == piko_ctx::NRING) {
     piko_ctx::Slot& old = ctx->ring[ctx->ring_head];  // == oldest when full
     cudaError_t e = cudaEventSynchronize(old.ev);
@@ -470,8 +477,17 @@ static cudaError_t record_frame_end(piko_ctx* ctx, cudaStream_t s, long long T) 
     const int rc = eval_frame(ctx, old);
     if (rc != PIKO_OK && ctx->sticky == PIKO_OK) ctx->sticky = rc;
   }
+  if (dev_mirror) *dev_mirror = ctx->ring[ctx->ring_head].d;
+  return cudaSuccess;
+}
+
+// Queue the end of a frame: its control block into the next ring slot's
+// pinned mirror (unless the last kernel already wrote it) and an event.
+static cudaError_t record_frame_end(piko_ctx* ctx, cudaStream_t s, long long T, bool mirrored = false) {
+  cudaError_t e = reserve_slot(ctx, nullptr);
+  if (e != cudaSuccess) return e;
   piko_ctx::Slot& sl = ctx->ring[ctx->ring_head];
-  cudaError_t e = cudaMemcpyAsync(sl.h, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s);
+  if (!mirrored) e = cudaMemcpyAsync(sl.h, ctx->ctl, offsetof(Control, digit_hist), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaEventRecord(sl.ev, s);
   if (e != cudaSuccess) return e;
   sl.T = T;
@@ -777,6 +793,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.garrive = ctx->garr; a.gcap = ctx->gcap;
     a.prim_base = (unsigned)ctx->prim_base;
     a.radix = cm ? 0 : 1;
+    if (!gather) CK(reserve_slot(ctx, &a.status_out));  // the tile kernel ends the frame's control updates
     if (keys_only) a.out_cov = nullptr;
     const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, keys_only)));
     if (grid > ctx->ovq_ctas) {  // spill space of the per-bin large-triangle queue
@@ -862,7 +879,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   }
   CK(mark(1 + PIKO_STAGE_RESOLVE));
   if (ev) ++ctx->prof_frames;
-  CK(record_frame_end(ctx, s, T));
+  CK(record_frame_end(ctx, s, T, !gather));
   ctx->last_T = T;
   return PIKO_OK;
 }

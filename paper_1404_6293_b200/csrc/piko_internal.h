@@ -83,6 +83,7 @@ struct Control {
   unsigned long long p2p_count;        // k_resolve CTA tickets (P2P slot release)
   unsigned int p2p_timeout;            // a peer flag wait timed out (sticky)
   unsigned long long peer_overflow;    // rank 0: frame+1 of a frame in which a peer rank overflowed
+  unsigned long long tile_done;        // k_tile CTA tickets (modulo grid: the last one mirrors this block)
   unsigned int digit_hist[2][MAX_PASSES][RX_RADIX];  // parity double buffer
 };
 
@@ -235,6 +236,7 @@ struct TileArgs {
   long long gcap;               //   k_tile zeroes the next frame's parity
   unsigned prim_base;           // keys-only: added to the primID of every stored key (sort-last)
   int radix;                    // 1: the frame used the radix AssignBin (its look-back counters)
+  Control* status_out;          // mapped host mirror: the last CTA copies the control block (null: none)
   int4* ovq;                    // [grid][OVQ_CAP][6] overflow of the per-bin queue (null: none)
   // P2P transport (sort-first): tile_keys points into rank 0's memory
   unsigned long long* p2p_flag;         // rank 0's arrival flag of this rank (null: no P2P)
@@ -361,7 +363,10 @@ TileKernel tile_kernel_bw8(int bh, bool cov, bool keys_only);   // k_tile instan
 TileKernel tile_kernel_bw16(int bh, bool cov, bool keys_only);
 TileKernel tile_kernel_bw32(int bh, bool cov, bool keys_only);
 TileKernel tile_kernel_bw64(int bh, bool cov, bool keys_only);
-constexpr int TILE_THREADS = 256;  // k_tile CTA size cap
+#ifndef PIKO_TILE_THREADS
+#define PIKO_TILE_THREADS 256
+#endif
+constexpr int TILE_THREADS = PIKO_TILE_THREADS;  // k_tile CTA size cap
 inline int tile_threads(int bw, int bh) { return bw * bh < TILE_THREADS ? bw * bh : TILE_THREADS; }
 inline int tile_frag(int bw, int bh) { return FRAG_ROUNDS * tile_threads(bw, bh); }
 cudaError_t launch_resolve(const ResolveArgs& a, bool pdl, cudaStream_t s);

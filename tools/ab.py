@@ -44,8 +44,11 @@ def run(lib, cfg, bw):
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     st = torch.cuda.current_stream()
     ts = []
+    ahead = int(os.environ.get("AB_SLEEP", "0"))  # cycles of device sleep after the flush (host runs ahead)
     for k in range(40):
         flush.fill_(float(k))
+        if ahead:
+            torch.cuda._sleep(ahead)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         r.draw(v, i, s.mvp, s.light)

@@ -10,11 +10,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import __graft_entry__ as ge
 
+extra = [f for f in os.environ.get("PIKO_EXP", "").split() if f]
 lib = f"/tmp/libpiko_cmt{os.getpid()}.so"
 objs = []
 for src in sorted({src for src, _, _ in ge.SOURCES}):
     o = f"/tmp/{src}.cmt.o"
-    subprocess.check_call([ge._nvcc(), *ge.NVCC_FLAGS, "-DPIKO_K1_TIMING", "-c", os.path.join(ge.CSRC, src), "-o", o])
+    subprocess.check_call([ge._nvcc(), *ge.NVCC_FLAGS, "-DPIKO_K1_TIMING", *extra, "-c", os.path.join(ge.CSRC, src), "-o", o])
     objs.append(o)
 subprocess.check_call([ge._nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib, "-ldl", "-lcudart"])
 import paper_1404_6293_b200 as piko  # noqa: E402
@@ -30,14 +31,28 @@ v = torch.from_numpy(s.verts).cuda()
 i = torch.from_numpy(s.idx).cuda()
 r = piko.Renderer(s.W, s.H, 16)
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+h = ctypes.CDLL(lib)
+piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
+st = torch.cuda.current_stream()
 for k in range(4):
     flush.fill_(float(k))
+    if k == 3:  # reset the vertex-start slots (atomicMin/Max) before the measured frame
+        z = np.zeros((4, 8192, 8), np.uint64)
+        z[0, 8190, 0] = z[0, 8191, 0] = np.uint64(2**63)
+        torch.cuda.synchronize()
+        h.piko_dbg_k1_set(z.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(z.nbytes))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
     r.draw(v, i, s.mvp, s.light)
-torch.cuda.synchronize()
+    e1.record(st)
+    torch.cuda.synchronize()
+print(f"event-timed frame: {e0.elapsed_time(e1) * 1000:.1f} us")
+piko.piko_finish(r.ctx)
 buf = np.zeros((4, 8192, 8), np.uint64)
-h = ctypes.CDLL(lib)
 assert h.piko_dbg_k1_times(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes)) == 0
 T0 = int(buf[0, 0, 0])
+vs = buf[0, 8190].astype(np.int64)
+print(f"k_vertex: first CTA start {int(vs[0]) - T0} ns, last CTA start {int(vs[1]) - T0}, first past wait {int(buf[0, 8191, 0]) - T0} (rel. k_setup chunk 0)")
 n1 = (s.n_tris + 1023) // 1024
 kk = buf[0, :n1].astype(np.int64) - T0
 print(f"k_setup: CTAs {n1}, start..end {kk[:,0].min()}..{kk[:,5].max()}, start p50 {np.median(kk[:,0]):.0f}; "
@@ -78,6 +93,11 @@ for lo, hi in ((0, 0), (1, 64), (65, 256), (257, 1024), (1025, 1 << 30)):
         r2 = t[m, 2] - t[m, 1]
         print(f"   bins with {lo}-{hi} pairs: {m.sum():5d}  raster median {np.median(r1):7.0f} p90 {np.percentile(r1,90):7.0f}"
               f"  writeback median {np.median(r2):7.0f} p90 {np.percentile(r2,90):7.0f}")
+m = (ne >= 257)
+if m.any():
+    tm = t[m]
+    print(f"   heavy bins phases (median ns): clear {np.median(tm[:,5]-tm[:,0]):.0f}  rounds {np.median(tm[:,6]-tm[:,5]):.0f}"
+          f"  wait+sync {np.median(tm[:,7]-tm[:,6]):.0f}  prologue+drain {np.median(tm[:,1]-tm[:,7]):.0f}  writeback {np.median(tm[:,2]-tm[:,1]):.0f}")
 cta = t[:, 4]
 per = np.bincount(cta.astype(np.int64))
 print(f"   bins per CTA: min {per[per>0].min()} max {per.max()} CTAs {np.count_nonzero(per)}")
