@@ -395,22 +395,45 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
   pdl_trigger();
   // every CTA takes one ticket per frame: frame = ticket / gridDim.x (the
   // triangle chunk is simply blockIdx.x -- nothing here depends on CTA order)
-  if (tid == 0) { s_tk = atomicAdd(&a.ctl->k1_ticket, 1ull) / gridDim.x; s_live = 0; s_nbig = 0; }
-  for (int i = tid; i < a.npass * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
-  __syncthreads();  // histogram cleared before any thread adds to it; frame known
-  const u64 frame = s_tk;
   const long long chunk = blockIdx.x;
   const long long t0 = chunk * K1_CHUNK;
   K1_MARK(0);
-  // ---- loads first (all independent): indices, then vertex-stage records ---
+  // ---- the chunk's indices: 16-byte coalesced loads staged in shared memory
+  // (12 consecutive ints per 4 triangles; t0 is a multiple of K1_CHUNK and idx
+  // is 16-byte aligned), issued together with the frame ticket --------------
+  __shared__ int4 s_idx[K1_CHUNK * 3 / 4];
+  u64 tk = 0;
+  if (tid == 0) tk = atomicAdd(&a.ctl->k1_ticket, 1ull);
+  {
+    const long long nint = 3 * (min((long long)K1_CHUNK, a.n_tris - t0));
+    const long long n4 = nint >> 2;
+    const int4* ip = reinterpret_cast<const int4*>(a.idx + 3 * t0);
+    int4 q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int j = tid + k * K1_THREADS;
+      q[k] = j < n4 ? __ldg(ip + j) : make_int4(-1, -1, -1, -1);
+      if (j == n4 && (nint & 3)) {  // ragged tail: 1-3 ints
+        int* qi = reinterpret_cast<int*>(&q[k]);
+        for (int u = 0; u < (int)(nint & 3); ++u) qi[u] = __ldg(a.idx + 3 * t0 + 4 * n4 + u);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s_idx[tid + k * K1_THREADS] = q[k];
+  }
+  for (int i = tid; i < a.npass * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
+  if (tid == 0) { s_tk = tk / gridDim.x; s_live = 0; s_nbig = 0; }
+  __syncthreads();  // indices staged; histogram cleared; frame known
+  const u64 frame = s_tk;
   int vi[K1_TPT][3];
+  const int* sidx = reinterpret_cast<const int*>(s_idx);
 #pragma unroll
   for (int k = 0; k < K1_TPT; ++k) {
     const long long t = t0 + tid + k * K1_THREADS;
     const bool in = t < a.n_tris;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      vi[k][c] = in ? __ldg(a.idx + 3 * t + c) : -1;
+      vi[k][c] = in ? sidx[3 * (tid + k * K1_THREADS) + c] : -1;
       if (!FUSED && vi[k][c] >= a.xv_cap) vi[k][c] = -1;  // overflowed frame: stay in bounds
     }
   }
