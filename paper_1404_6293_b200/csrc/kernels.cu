@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(256) k_index_max(const int32_t* __restrict__ i
   int m = -1;
   const long long n4 = n / 4;
   const int4* p = reinterpret_cast<const int4*>(idx);
+#pragma unroll 4
   for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n4; i += (long long)gridDim.x * 256) {
     const int4 q = __ldg(p + i);
     m = max(m, max(max(q.x, q.y), max(q.z, q.w)));
@@ -367,7 +368,15 @@ __global__ void __launch_bounds__(256) k_index_max(const int32_t* __restrict__ i
     m = max(m, __ldg(idx + i));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m >= 0) atomicMax(&ctl->vmax, (unsigned)m + 1u);
+  // one global atomic per CTA (per-warp atomics on one address serialise at L2)
+  __shared__ int s_m[8];
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int mm = s_m[0];
+    for (int w = 1; w < 8; ++w) mm = max(mm, s_m[w]);
+    if (mm >= 0) atomicMax(&ctl->vmax, (unsigned)mm + 1u);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -2934,7 +2943,8 @@ cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s) {
 }
 
 cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool pdl, cudaStream_t s) {
-  const long long want = std::min<long long>((n / 4 + 255) / 256, 8ll * sm_count());
+  // a few int4 loads in flight per thread: about 2 waves of CTAs
+  const long long want = std::min<long long>((n / 4 + 255) / 256, 4ll * sm_count());
   return launch_ex(k_index_max, (int)(want > 0 ? want : 1), 256, 0, pdl, s, idx, n, ctl);
 }
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s) {

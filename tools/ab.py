@@ -51,7 +51,7 @@ def run(lib, cfg, bw):
             torch.cuda._sleep(ahead)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        r.draw(v, i, s.mvp, s.light)
+        r.draw(v, i, s.mvp, s.light, indexed=os.environ.get("AB_DRAW", "indexed") == "indexed")
         e1.record(st)
         torch.cuda.synchronize()
         if k >= 10:
