@@ -411,8 +411,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
   // (12 consecutive ints per 4 triangles; t0 is a multiple of K1_CHUNK and idx
   // is 16-byte aligned), issued together with the frame ticket --------------
   __shared__ int4 s_idx[K1_CHUNK * 3 / 4];
-  u64 tk = 0;
-  if (tid == 0) tk = atomicAdd(&a.ctl->k1_ticket, 1ull);
+  const u64 tk = a.frame * gridDim.x;  // (host frame counter: no same-address atomic burst)
   {
     const long long nint = 3 * (min((long long)K1_CHUNK, a.n_tris - t0));
     const long long n4 = nint >> 2;
@@ -2040,7 +2039,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   TileSmem<BW, BH, THREADS>& sm = *reinterpret_cast<TileSmem<BW, BH, THREADS>*>(smem_raw);
   unsigned* s_cov = reinterpret_cast<unsigned*>(smem_raw + sizeof(TileSmem<BW, BH, THREADS>));
   __shared__ int s_bin;     // current bin (-1: work list exhausted)
-  __shared__ int s_rng[4];  // its CSR sub-range [s, e), fragment count (0: whole bin), first fragment slot
+  __shared__ int s_rng[5];  // its CSR sub-range [s, e), fragment count (0: whole bin), first fragment slot, fragment index
   __shared__ int s_nbig;    // large triangles queued for the pixel-parallel pass
   __shared__ unsigned s_ln[NLIST];
   __shared__ int s_last;
@@ -2055,6 +2054,9 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   TL_CTA(3);  // resident
   pdl_wait();
   pdl_trigger();
+#ifdef PIKO_EXP_NOTILE
+  return;  // ablation: everything before the tile kernel
+#endif
   const u64 frame = a.ctl->frame;
   const bool ovf = a.ctl->overflow_tag == frame + 1;
   if (KEYS_ONLY && a.p2p_done) {  // P2P: rank 0 has finished reading this key slot
@@ -2101,27 +2103,41 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     rs = a.bin_start[b];
     re = a.bin_start[b + 1];
   };
-  // work item w -> bin, CSR sub-range, number of fragments of the bin (0: unsplit)
-  // (fragments of a bin are consecutive in the list: fragment j of item w
-  // keeps its key tile in slot w, the bin's first slot is w - j)
-  auto work_item = [&](unsigned w, int& b, int& rs, int& re, int& nf, int& fs) {
+  // work item w -> bin, CSR sub-range, number of fragments of the bin (0:
+  // unsplit), first fragment slot, fragment index.  Order (an LPT
+  // approximation without a sort): whole bins of size class 1 (> 3/4 of a
+  // fragment), then the fragments of split bins (balanced: a bin of n pairs
+  // becomes nf = ceil(n / frag) fragments of n / nf pairs, no small
+  // remainders), then size classes 2..4.  A bin's fragments are consecutive in
+  // frag_list: fragment j of list position w keeps its key tile in slot w.
+  auto work_item = [&](unsigned w, int& b, int& rs, int& re, int& nf, int& fs, int& fj) {
     fs = -1;
-    if (w < n_frag) {
-      const int2 it = a.frag_list[w];
+    fj = 0;
+    const unsigned n1 = (a.npass == 0) ? 0u : s_ln[1];
+    if (w >= n1 && w < n1 + n_frag) {
+      const unsigned wf = w - n1;
+      const int2 it = a.frag_list[wf];
       b = it.x;
       int s0, e0;
       bin_range(b, s0, e0);
-      nf = (e0 - s0 + a.frag - 1) / a.frag;
-      rs = s0 + it.y * a.frag;
-      re = min(rs + a.frag, e0);
-      fs = (int)w - it.y;
+      const long long n = e0 - s0;
+      nf = (int)((n + a.frag - 1) / a.frag);
+      rs = s0 + (int)((it.y * n) / nf);
+      re = s0 + (int)(((it.y + 1) * n) / nf);
+      fs = (int)wf - it.y;
+      fj = it.y;
     } else if (w < n_work) {
       if (a.npass == 0) {
         b = 0;
-      } else {  // size classes, largest first: list k >= 1 lives at bin_list[(k-1) NB]
-        unsigned r = w - n_frag;
-        int k = 1;
-        while (r >= s_ln[k]) r -= s_ln[k++];
+      } else {  // size classes: list k >= 1 lives at bin_list[(k-1) NB]
+        unsigned r;
+        int k;
+        if (w < n1) { r = w; k = 1; }
+        else {
+          r = w - n1 - n_frag;
+          k = 2;
+          while (r >= s_ln[k]) r -= s_ln[k++];
+        }
         b = a.bin_list[(size_t)(k - 1) * g.NB + r];
       }
       bin_range(b, rs, re);
@@ -2138,14 +2154,17 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
 
   // ---- LoadBalance schedule over the work list ----------------
   // thread 0 keeps the next item in registers one item ahead
-  int q_bin = -1, q_s = 0, q_e = 0, q_nf = 0, q_fs = -1;
+  int q_bin = -1, q_s = 0, q_e = 0, q_nf = 0, q_fs = -1, q_fj = 0;
   unsigned q_tk = 0;
   if (tid == 0) {
-    const unsigned t0 = atomicAdd(&a.ctl->tile_next, 1u);
-    q_tk = atomicAdd(&a.ctl->tile_next, 1u);
-    int b0 = -1, s0 = 0, e0 = 0, nf0 = 0, fs0 = -1;
-    work_item(t0, b0, s0, e0, nf0, fs0);
-    s_bin = b0; s_rng[0] = s0; s_rng[1] = e0; s_rng[2] = nf0; s_rng[3] = fs0;
+    // the first two items are static (blockIdx, blockIdx + grid): 2 x grid
+    // same-address atomics at kernel start serialise at L2 for ~10 us; later
+    // items come from the dynamic queue (its tickets start at 2 x grid)
+    const unsigned t0 = blockIdx.x;
+    q_tk = blockIdx.x + gridDim.x;
+    int b0 = -1, s0 = 0, e0 = 0, nf0 = 0, fs0 = -1, fj0 = 0;
+    work_item(t0, b0, s0, e0, nf0, fs0, fj0);
+    s_bin = b0; s_rng[0] = s0; s_rng[1] = e0; s_rng[2] = nf0; s_rng[3] = fs0; s_rng[4] = fj0;
   }
   __syncthreads();
   // Pipeline prologue of an item: primIDs of the first TQ rounds and the
@@ -2173,11 +2192,11 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   for (;;) {
     const int b = s_bin;
     if (b < 0) break;
-    const int s = s_rng[0], e = s_rng[1], nfrag = s_rng[2], fslot0 = s_rng[3];
+    const int s = s_rng[0], e = s_rng[1], nfrag = s_rng[2], fslot0 = s_rng[3], fidx = s_rng[4];
     TL_MARK(b, 0);
     if (tid == 0) {  // prefetch the next item
-      work_item(q_tk, q_bin, q_s, q_e, q_nf, q_fs);
-      if (q_bin >= 0) q_tk = atomicAdd(&a.ctl->tile_next, 1u);
+      work_item(q_tk, q_bin, q_s, q_e, q_nf, q_fs, q_fj);
+      if (q_bin >= 0) q_tk = 2u * gridDim.x + atomicAdd(&a.ctl->tile_next, 1u);
       s_nx[0] = q_bin; s_nx[1] = q_s; s_nx[2] = q_e;
     }
     const int bx = b % g.binsX, by = b / g.binsX;
@@ -2457,7 +2476,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
       // fragment of a split bin: its key tile goes to its own slot with plain
       // coalesced stores (no atomics); the last fragment to arrive takes the
       // per-pixel minimum over the bin's slots and writes the bin
-      const int myslot = fslot0 + (s - a.bin_start[b]) / a.frag;
+      const int myslot = fslot0 + fidx;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         const int p = tid + k * THREADS;
@@ -2500,19 +2519,25 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     TL_MARK(b, 2);
     if (tid == 0 && b < 8192) { g_tl_extra(b, e - s, blockIdx.x); }
     __syncthreads();  // keys consumed before the next bin reinitialises them
-    if (tid == 0) { s_bin = q_bin; s_rng[0] = q_s; s_rng[1] = q_e; s_rng[2] = q_nf; s_rng[3] = q_fs; }
+    if (tid == 0) { s_bin = q_bin; s_rng[0] = q_s; s_rng[1] = q_e; s_rng[2] = q_nf; s_rng[3] = q_fs; s_rng[4] = q_fj; }
     __syncthreads();
   }
 
   TL_CTA(1);
   // ---- empty bins: background only, no shared memory, no barriers ------------
   // every warp pulls groups of EMPTY_GROUP bins from a second queue
+#ifdef PIKO_EXP_NOEMPTY
+  if (false)
+#endif
+  // (one queue ticket per CTA for THREADS/32 groups: per-warp tickets on one
+  // address serialised at L2)
+  __shared__ unsigned s_etk;
   for (;;) {
-    unsigned tk = 0;
-    if (lane == 0) tk = atomicAdd(&a.ctl->empty_next, 1u);
-    tk = __shfl_sync(0xffffffffu, tk, 0);
-    const unsigned e0 = tk * EMPTY_GROUP;
-    if (e0 >= n_empty) break;
+    __syncthreads();
+    if (tid == 0) s_etk = atomicAdd(&a.ctl->empty_next, 1u);
+    __syncthreads();
+    const unsigned e0 = (s_etk * (THREADS / 32) + warp) * EMPTY_GROUP;
+    if (s_etk * (THREADS / 32) * EMPTY_GROUP >= n_empty) break;
     // the group's bin ids in one round trip (lane l loads entry e0 + l), not
     // one dependent load per bin
     const int bl = (lane < EMPTY_GROUP && e0 + lane < n_empty) ? empty_bin(e0 + lane) : 0;

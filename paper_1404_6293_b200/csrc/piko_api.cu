@@ -115,6 +115,7 @@ struct piko_ctx {
   // constant, so a change forces a reset of the control block + status words
   long long last_grids[6] = {-1, -1, -1, -1, -1, -1};
   bool need_reset = true;
+  unsigned long long frames = 0;      // binned frames enqueued since the control block was reset
   bool pdl = true;
   int vs_mode = -1;        // vertex stage: -1 auto, 0 fused into k_setup, 1 separate k_vertex
   int32_t* primid = nullptr;
@@ -168,6 +169,7 @@ struct piko_ctx {
   int cm_mode = -1;                         // -1 auto, 0 radix, 1 count matrix
   int cm_tc_log2 = 0;                       // forced log2 triangles per row (0: auto)
   uint32_t* cm = nullptr; uint32_t* cp = nullptr; long long cm_cap = 0;  // [rows][NB]
+  bool tile_items_grid = false;             // k_tile: one CTA per possible item instead of persistent
   bool last_cm = false;                     // the last frame used the count matrix
   long long last_cm_rows = 0;
   int32_t* prims_out = nullptr;             // CSR bin_prims of the last frame
@@ -302,6 +304,7 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   if (const char* e = getenv("PIKO_SEPARATE_VS")) ctx->vs_mode = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_DEFERRED")) ctx->deferred = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_CM")) ctx->cm_mode = e[0] == '0' ? 0 : 1;
+  if (const char* e = getenv("PIKO_TILE_GRID")) ctx->tile_items_grid = strcmp(e, "items") == 0;
   if (const char* e = getenv("PIKO_CM_TC_LOG2")) ctx->cm_tc_log2 = atoi(e);
   return ctx;
 }
@@ -705,6 +708,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     if (ctx->gcov) CK(cudaMemsetAsync(ctx->gcov, 0, sizeof(uint32_t) * ctx->g.NB * ctx->bw * ctx->bh, s));
     for (int k = 0; k < 6; ++k) ctx->last_grids[k] = grids[k];
     ctx->need_reset = false;
+    ctx->frames = 0;
   }
   CK(mark(1 + PIKO_STAGE_CLEAR));
   const bool sep = separate_vs(ctx, V, T);
@@ -724,6 +728,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.idx = idx; a.n_tris = T; a.g = ctx->g;
     a.npass = cm ? 0 : ctx->npass; a.rec = ctx->rec; a.rect = ctx->rect; a.ctl = ctx->ctl;
     a.cm = cm ? ctx->cm : nullptr; a.cm_shift = cm_shift;
+    a.frame = ctx->frames++;
     CK(launch_setup(a, (int)g1, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_SETUP));
@@ -800,15 +805,20 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.radix = cm ? 0 : 1;
     if (!gather) CK(reserve_slot(ctx, &a.status_out));  // the tile kernel ends the frame's control updates
     if (keys_only) a.out_cov = nullptr;
-    const int grid = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, keys_only)));
-    if (grid > ctx->ovq_ctas) {  // spill space of the per-bin large-triangle queue
+    // persistent grid (all CTAs resident, items from the queue) or, with
+    // PIKO_TILE_GRID=items, one CTA per possible work item so the hardware
+    // block scheduler balances them (the paper's LoadBalance)
+    const int pers = std::max(1, std::min(ctx->owned, tile_grid(ctx->bw, ctx->bh, a.out_cov != nullptr, keys_only)));
+    const int grid = ctx->tile_items_grid ? (int)std::max<long long>(pers, std::min<long long>(ctx->owned + ctx->frag_cap, INT32_MAX / 2))
+                                          : pers;
+    if (pers > ctx->ovq_ctas) {  // spill space of the per-bin large-triangle queue (per resident CTA)
       if (ctx->ovq) cudaFree(ctx->ovq);
       ctx->ovq = nullptr;
       ctx->ovq_ctas = 0;
-      CK(cudaMalloc(&ctx->ovq, sizeof(int4) * 6 * OVQ_CAP * (size_t)grid));
-      ctx->ovq_ctas = grid;
+      CK(cudaMalloc(&ctx->ovq, sizeof(int4) * 6 * OVQ_CAP * (size_t)pers));
+      ctx->ovq_ctas = pers;
     }
-    a.ovq = ctx->ovq;
+    a.ovq = grid == pers ? ctx->ovq : nullptr;  // item grid: overflow takes the warp-cooperative path
     CK(launch_tile(a, ctx->bw, ctx->bh, grid, a.out_cov != nullptr, keys_only, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_TILE));

@@ -136,6 +136,7 @@ struct SetupArgs {
   int npass;                    // radix digit histograms to build (0 in count-matrix mode)
   uint32_t* cm;                 // count-matrix AssignBin: M[n_tris >> cm_shift][NB] (null: radix mode)
   int cm_shift;                 // log2 triangles per count-matrix row
+  unsigned long long frame;     // frames enqueued since the control block was reset (host counter)
   int4* rec;                    // [n_tris][3]
   uint2* rect;                  // [n_tris] tile rect {tx0|ty0<<16, tx1|ty1<<16}; empty if culled
   Control* ctl;
