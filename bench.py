@@ -224,13 +224,17 @@ def cpu_baseline(s, budget):
     return out, ref
 
 
-def algorithmic_bytes(stage, T, V, L, P, NB, npx, ncov, npass, cm_rows=0):
+def algorithmic_bytes(stage, T, V, L, P, NB, npx, ncov, npass, cm_rows=0, cl_chunks=0):
     """Bytes the method must move per launch of a stage (DESIGN.md section 6;
     SURVEY 8(d): 48 B per covered pixel for the winner's attributes)."""
     if stage == "vertex":     # 16 B positions in, 16 B vertex record out
         return 16 * V + 16 * V
     if stage == "setup":      # idx + vertex records in; setup records (live) + tile rects out
+        if cl_chunks:         # chunk lists: the sorted pairs (4 B) instead of the rects
+            return 12 * T + 16 * V + 48 * L + 4 * P
         return 12 * T + 16 * V + 48 * L + 8 * T
+    if cl_chunks:             # k_cl_bins: totals, chunk bitmaps, list segments in; CSR + lists out
+        return (4 * NB + 4 * NB * ((cl_chunks + 31) // 32) + 8 * P + 8 * NB) if stage == "sort" else 0
     if stage == "expand":
         if cm_rows:           # k_cm_scan: count matrix read, prefixes written, counts reset
             return 12 * cm_rows * NB + 4 * NB
@@ -520,7 +524,8 @@ def run_piko(args):
     cand = {k: per_frame[k] for k in ("vertex", "setup", "expand", "sort", "tile", "resolve") if per_frame[k] > 0}
     dom = max(cand, key=cand.get)
     cm_rows = stats.get("cm_rows", 0) if stats.get("assign_mode", 0) == 1 else 0
-    nb = algorithmic_bytes(dom, T, V, L, P, NB, npx, ncov, stats["radix_passes"], cm_rows)
+    cl_chunks = stats.get("cm_rows", 0) if stats.get("assign_mode", 0) == 2 else 0
+    nb = algorithmic_bytes(dom, T, V, L, P, NB, npx, ncov, stats["radix_passes"], cm_rows, cl_chunks)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -534,13 +539,14 @@ def run_piko(args):
         traffic = json.load(open(tf)).get(dom)
     kname = {"vertex": "k_vertex / k_index_max", "setup": "k_setup",
              "expand": "k_cm_scan" if cm_rows else "k_radix_pass<EXPAND=true> (pass 0)",
-             "sort": "k_cm_scatter" if cm_rows else "k_radix_pass<EXPAND=false> (passes >= 1)",
+             "sort": "k_cl_bins" if cl_chunks else "k_cm_scatter" if cm_rows else "k_radix_pass<EXPAND=false> (passes >= 1)",
              "tile": "k_tile", "resolve": "k_resolve / k_shade"}[dom]
     ncu_note = None  # the same kernel's ncu --set full counters (profiles/ncu_full_r2_<cfg>.txt)
     nf = os.path.join(ROOT, "profiles", f"ncu_full_r2_{args.config}.txt")
     if os.path.exists(nf):
         want = {"tile": "k_tile", "setup": "k_setup", "expand": "k_cm_scan" if cm_rows else "k_radix_pass",
-                "sort": "k_cm_scatter" if cm_rows else "k_radix_pass", "vertex": "k_vertex"}.get(dom)
+                "sort": "k_cl_bins" if cl_chunks else "k_cm_scatter" if cm_rows else "k_radix_pass",
+                "vertex": "k_vertex"}.get(dom)
         lines = [l for l in open(nf) if not l.startswith("#")]
         hdr = [l for l in open(nf) if l.startswith("# kernel")]
         for l in lines:
@@ -551,12 +557,12 @@ def run_piko(args):
                 "limiter": ("latency: few resident warps per SM and dependent L2 round trips per bin "
                             "(ncu issue-active / warps-active in `ncu`)") if dom == "tile" else None,
                 "ncu": ncu_note,
-                "launches_per_step": max(stats["radix_passes"] - 1, 1) if dom == "sort" else 1,
+                "launches_per_step": max(stats["radix_passes"] - 1, 1) if (dom == "sort" and not (cm_rows or cl_chunks)) else 1,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": nb,
                 "ms_per_launch": per_frame[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
-    frame_bytes = sum(algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"], cm_rows)
+    frame_bytes = sum(algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"], cm_rows, cl_chunks)
                       for k in ("vertex", "setup", "expand", "sort", "tile") if per_frame.get(k, 0) > 0.004)
     # BASELINE.md's frame metric: ncu-measured DRAM bytes of one whole frame
     # (range replay: all kernels in one range, L2 write-backs included --
@@ -583,7 +589,8 @@ def run_piko(args):
         "config": {"workload": workload_name(args.config, s, bw), "config": args.config,
                    "width": s.W, "height": s.H, "bin": bw, "n_tris": T, "n_verts": V,
                    "n_pairs": P, "n_live": L, "covered_px": ncov, "l2": "flushed (256 MiB) before every step",
-                   "assign": "count matrix" if cm_rows else f"radix x{stats['radix_passes']}",
+                   "assign": ("chunk lists" if cl_chunks else "count matrix" if cm_rows
+                              else f"radix x{stats['radix_passes']}"),
                    "parallelism": f"{args.multi} x{world} ({transport})" if world > 1 else "1 GPU"},
         "fps": 1e3 / ms,
         "ms_p10_p50_p90": [float(x) for x in np.percentile(step_ms, [10, 50, 90])],

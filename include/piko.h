@@ -322,9 +322,11 @@ typedef struct {
   int32_t radix_passes; /* LSD passes the radix AssignBin would take          */
   int32_t kernels_per_frame; /* kernels launched per frame (this rank)        */
   int32_t assign_mode;  /* AssignBin of the last frame: 0 stable LSD radix passes,
-                           1 count matrix (k_cm_scan + k_cm_scatter)           */
+                           1 count matrix (k_cm_scan + k_cm_scatter),
+                           2 chunk lists (sorted in k_setup + k_cl_bins)        */
   int32_t reserved;
-  int64_t cm_rows;      /* count-matrix rows (triangle chunks), 0 in radix mode */
+  int64_t cm_rows;      /* count-matrix rows / chunk-list chunks (triangle
+                           chunks), 0 in radix mode                            */
 } piko_stats;
 int piko_get_stats(const piko_ctx *ctx, piko_stats *out);
 

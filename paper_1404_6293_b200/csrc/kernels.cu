@@ -390,10 +390,196 @@ constexpr int K1_BIG = 64;  // triangles with more owned bins go to the CTA-wide
 // positions (each shared vertex is transformed once per triangle using it --
 // same arithmetic, so the same bits -- and one kernel and its 16 B/vertex
 // round trip through HBM/L2 disappear).
+// Shared memory of k_setup (dynamic: over the 48 KB static limit): the staged
+// indices, the radix digit histograms and the large-triangle list, and the
+// chunk-list AssignBin's touched-bin bitmap and per-touched-bin arrays.
+struct K1Smem {
+  int4 idx[K1_CHUNK * 3 / 4];
+  unsigned hist[MAX_PASSES][RX_RADIX];
+  uint2 big[K1_CHUNK];
+  unsigned char bigg[K1_CHUNK];       // chunk-list mode: group of a listed triangle
+  uint2 mrect[K1_CHUNK];              // chunk-list: rect of slot k*K1_THREADS + tid if it owns 2..K1_BIG bins
+  unsigned bm[CL_MAX_NB / 32];        // chunk-list: bins touched by the chunk
+  unsigned short wpre[CL_MAX_NB / 32];  // exclusive popcount prefix of bm (local digit base)
+  unsigned short tb[CL_MAX_NB];       // local digit d -> bin
+  unsigned mask[CL_MAX_NB];           // by local digit: bit (k*8 + warp) = that group has a pair in the bin
+  unsigned cnt[CL_MAX_NB];            // by local digit: pairs of the bin in this chunk
+  unsigned wsum[K1_THREADS / 32];
+  unsigned U;
+};
+static_assert(K1_TPT * K1_THREADS / 32 <= 32, "32-triangle groups of a chunk fit one mask word");
+
+// ---------------------------------------------------------------------------
+// Chunk-list AssignBin, first half (a3 count inside k_setup).
+// The chunk's triangles form 32 groups of 32 consecutive primitives (group
+// k*8 + warp = triangles t0 + 32 (k*8 + warp) + lane).  Its pairs mark the
+// touched bins in a bitmap; the popcount prefix turns them into dense local
+// digits; the pairs then add their group bit and count per digit.  One entry
+// per touched bin b: cl_ent[b][chunk] = {group mask, pairs}, bit `chunk` of
+// b's chunk bitmap, cl_tot[b] += pairs.  Work is O(pairs + NB/32 + touched).
+// One-bin triangles arrive warp-aggregated (bin1); multi-bin ones through the
+// big list (rect + group), their pairs spread over the CTA.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned cl_digit(const K1Smem& sm, int b) {
+  return sm.wpre[b >> 5] + __popc(sm.bm[b >> 5] & ((1u << (b & 31)) - 1u));
+}
+template <int PHASE>  // 0: mark bins in the bitmap; 1: masks and counts by digit
+__device__ __forceinline__ void cl_pairs(K1Smem& sm, const int (&bin1)[K1_TPT], unsigned mflag, unsigned nbig,
+                                         const Grid& g) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int k = 0; k < K1_TPT; ++k) {
+    const unsigned peers = __match_any_sync(0xffffffffu, bin1[k]);
+    if (bin1[k] >= 0 && lane == __ffs(peers) - 1) {
+      const int b = bin1[k];
+      if (PHASE == 0) atomicOr(&sm.bm[b >> 5], 1u << (b & 31));
+      else {
+        const unsigned d = cl_digit(sm, b);
+        atomicOr(&sm.mask[d], 1u << (k * (K1_THREADS / 32) + warp));
+        atomicAdd(&sm.cnt[d], (unsigned)__popc(peers));
+      }
+    }
+  }
+  // triangles owning 2..K1_BIG bins: their own thread walks the rect
+#pragma unroll
+  for (int k = 0; k < K1_TPT; ++k) {
+    if (!(mflag >> k & 1u)) continue;
+    const uint2 rr = sm.mrect[k * K1_THREADS + tid];
+    const int tx0 = rr.x & 0xffff, ty0 = rr.x >> 16, tx1 = rr.y & 0xffff, ty1 = rr.y >> 16;
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        const int b = ty * g.binsX + tx;
+        if (g.nranks > 1 && b % g.nranks != g.rank) continue;
+        if (PHASE == 0) atomicOr(&sm.bm[b >> 5], 1u << (b & 31));
+        else {
+          const unsigned d = cl_digit(sm, b);
+          atomicOr(&sm.mask[d], 1u << (k * (K1_THREADS / 32) + warp));
+          atomicAdd(&sm.cnt[d], 1u);
+        }
+      }
+  }
+  // larger ones: the whole CTA walks their bins
+  for (unsigned q = 0; q < nbig; ++q) {
+    const uint2 rr = sm.big[q];
+    const int tx0 = rr.x & 0xffff, ty0 = rr.x >> 16, tx1 = rr.y & 0xffff, ty1 = rr.y >> 16;
+    const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
+    for (unsigned j = tid; j < c; j += K1_THREADS) {
+      const int b = owned_bin_at(tx0, ty0, tx1, ty1, j, g);
+      if (PHASE == 0) atomicOr(&sm.bm[b >> 5], 1u << (b & 31));
+      else {
+        const unsigned d = cl_digit(sm, b);
+        atomicOr(&sm.mask[d], 1u << sm.bigg[q]);
+        atomicAdd(&sm.cnt[d], 1u);
+      }
+    }
+  }
+}
+__device__ __forceinline__ void cl_publish(const SetupArgs& a, K1Smem& sm, const int (&bin1)[K1_TPT],
+                                           unsigned mflag, unsigned nbig, long long chunk, u64 frame) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Grid& g = a.g;
+  const int NBW = (g.NB + 31) >> 5;
+  // (the bitmap was zeroed before the main loop; big-list pairs are marked here)
+  cl_pairs<0>(sm, bin1, mflag, nbig, g);
+  __syncthreads();
+  // touched bins -> local digits (words: one per thread; NBW <= CL_MAX_NB/32 <= K1_THREADS)
+  static_assert(CL_MAX_NB / 32 <= K1_THREADS, "one bitmap word per thread");
+  const unsigned wv = tid < NBW ? sm.bm[tid] : 0u;
+  const unsigned pc = __popc(wv);
+  unsigned inc = pc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) sm.wsum[warp] = inc;
+  __syncthreads();
+  unsigned d = inc - pc;
+#pragma unroll
+  for (int w = 0; w < K1_THREADS / 32; ++w) d += w < warp ? sm.wsum[w] : 0u;
+  if (tid < NBW) sm.wpre[tid] = (unsigned short)d;
+  if (tid == K1_THREADS - 1) sm.U = d + pc;
+  for (unsigned bits = wv; bits; bits &= bits - 1) {
+    sm.tb[d] = (unsigned short)(tid * 32 + __ffs(bits) - 1);
+    sm.mask[d] = 0u;
+    sm.cnt[d] = 0u;
+    ++d;
+  }
+  __syncthreads();
+  cl_pairs<1>(sm, bin1, mflag, nbig, g);
+  __syncthreads();
+  // one entry per touched bin
+  const unsigned U = sm.U, cbit = 1u << (chunk & 31);
+  for (unsigned q = tid; q < U; q += K1_THREADS) {
+    const int b = sm.tb[q];
+    const unsigned c = sm.cnt[q];
+    a.cl_ent[(size_t)b * a.cl_nch + chunk] = make_uint2(sm.mask[q], c);
+    atomicOr(&a.cl_bm[(size_t)b * a.cl_nw + (chunk >> 5)], cbit);
+    atomicAdd(&a.cl_tot[b], c);
+  }
+  // the grid's last CTA scans the bin totals into bin_start (no chain between
+  // CTAs: each other CTA is done once its entries are published)
+  __shared__ int s_last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = (atomicAdd(&a.ctl->cl_done, 1ull) + 1) % gridDim.x == 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  constexpr int BPT = CL_MAX_NB / K1_THREADS;
+  static_assert(BPT % 4 == 0, "uint4 loads");
+  const int NB = g.NB;
+  unsigned c[BPT];
+#pragma unroll
+  for (int k = 0; k < BPT; k += 4) {
+    const int bb = tid * BPT + k;
+    if ((NB & 3) == 0 && bb + 4 <= NB) {
+      const uint4 q = __ldcg(reinterpret_cast<const uint4*>(a.cl_tot + bb));
+      c[k] = q.x; c[k + 1] = q.y; c[k + 2] = q.z; c[k + 3] = q.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[k + u] = bb + u < NB ? __ldcg(a.cl_tot + bb + u) : 0u;
+    }
+  }
+  u64 cs = 0;
+#pragma unroll
+  for (int k = 0; k < BPT; ++k) cs += c[k];
+  u64 inc64 = cs;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 t = __shfl_up_sync(0xffffffffu, inc64, o);
+    if (lane >= o) inc64 += t;
+  }
+  __shared__ u64 s_w64[K1_THREADS / 32];
+  if (lane == 31) s_w64[warp] = inc64;
+  __syncthreads();
+  u64 run = inc64 - cs, P = 0;
+#pragma unroll
+  for (int w = 0; w < K1_THREADS / 32; ++w) {
+    run += w < warp ? s_w64[w] : 0ull;
+    P += s_w64[w];
+  }
+#pragma unroll
+  for (int k = 0; k < BPT; ++k) {
+    const int bb = tid * BPT + k;
+    if (bb < NB) a.cl_start[bb] = (int32_t)(run < MAX_PAIRS ? run : MAX_PAIRS - 1);
+    run += c[k];
+  }
+  if (tid == 0) {
+    a.ctl->n_pairs = P;
+    a.cl_start[NB] = (int32_t)(P < MAX_PAIRS ? P : MAX_PAIRS - 1);
+    if (P > a.cl_cap) atomicMax(&a.ctl->overflow_tag, frame + 1);
+  }
+}
+
 template <bool FUSED>
 __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
-  __shared__ unsigned s_hist[MAX_PASSES][RX_RADIX];
-  __shared__ uint2 s_big[K1_CHUNK];
+  extern __shared__ __align__(16) unsigned char k1_dyn[];
+  K1Smem& sm1 = *reinterpret_cast<K1Smem*>(k1_dyn);
+  unsigned (&s_hist)[MAX_PASSES][RX_RADIX] = sm1.hist;
+  uint2 (&s_big)[K1_CHUNK] = sm1.big;
   __shared__ unsigned s_nbig;
   __shared__ u64 s_tk;
   __shared__ unsigned s_live;
@@ -410,7 +596,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
   // ---- the chunk's indices: 16-byte coalesced loads staged in shared memory
   // (12 consecutive ints per 4 triangles; t0 is a multiple of K1_CHUNK and idx
   // is 16-byte aligned), issued together with the frame ticket --------------
-  __shared__ int4 s_idx[K1_CHUNK * 3 / 4];
+  int4 (&s_idx)[K1_CHUNK * 3 / 4] = sm1.idx;
   const u64 tk = a.frame * gridDim.x;  // (host frame counter: no same-address atomic burst)
   {
     const long long nint = 3 * (min((long long)K1_CHUNK, a.n_tris - t0));
@@ -430,6 +616,9 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
     for (int k = 0; k < 3; ++k) s_idx[tid + k * K1_THREADS] = q[k];
   }
   for (int i = tid; i < a.npass * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
+  const bool cl = a.cl_ent != nullptr;  // chunk-list AssignBin (CTA-uniform)
+  if (cl)
+    for (int i = tid; i < ((g.NB + 31) >> 5); i += K1_THREADS) sm1.bm[i] = 0u;
   if (tid == 0) { s_tk = tk / gridDim.x; s_live = 0; s_nbig = 0; }
   __syncthreads();  // indices staged; histogram cleared; frame known
   const u64 frame = s_tk;
@@ -473,7 +662,9 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
   // count-matrix mode: the CTA's triangles all lie in row t0 >> cm_shift
   // (K1_CHUNK divides the row size); one-bin triangles are warp-aggregated
   uint32_t* cmrow = a.cm ? a.cm + (size_t)(t0 >> a.cm_shift) * g.NB : nullptr;
+  const int warp = tid >> 5;
   int bin1[K1_TPT];
+  unsigned mflag = 0;  // chunk-list: slots whose triangle owns 2..K1_BIG bins (rect in mrect)
 #pragma unroll
   for (int k = 0; k < K1_TPT; ++k) {
     bin1[k] = -1;
@@ -485,7 +676,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
       const int tx0 = o.px0 >> g.bw_log2, tx1 = o.px1 >> g.bw_log2;
       const int ty0 = o.py0 >> g.bh_log2, ty1 = o.py1 >> g.bh_log2;
       const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
-      if (c == 1 && cmrow) bin1[k] = g.nranks == 1 ? ty0 * g.binsX + tx0 : owned_bin_at(tx0, ty0, tx1, ty1, 0u, g);
+      if (c == 1 && (cmrow || cl)) bin1[k] = g.nranks == 1 ? ty0 * g.binsX + tx0 : owned_bin_at(tx0, ty0, tx1, ty1, 0u, g);
       else if (c > 1 && c <= (unsigned)K1_BIG && cmrow) {
         for (int ty = ty0; ty <= ty1; ++ty)
           for (int tx = tx0; tx <= tx1; ++tx) {
@@ -510,7 +701,10 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
         r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
                          o.small ? REC_SMALL : 0);
         // digit histograms of the radix passes over this triangle's pairs
-        if (a.npass == 0 && c <= (unsigned)K1_BIG) {
+        if (cl && c > 1 && c <= (unsigned)K1_BIG) {  // chunk-list: walked by this thread
+          sm1.mrect[k * K1_THREADS + tid] = rr;
+          mflag |= 1u << k;
+        } else if (a.npass == 0 && c <= (unsigned)K1_BIG) {
           // count-matrix mode: no digit histograms
         } else if (c <= (unsigned)K1_BIG) {
           for (int ty = ty0; ty <= ty1; ++ty)
@@ -520,7 +714,9 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
               for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], 1u);
             }
         } else {
-          s_big[atomicAdd(&s_nbig, 1u)] = rr;
+          const unsigned q = atomicAdd(&s_nbig, 1u);
+          s_big[q] = rr;
+          sm1.bigg[q] = (unsigned char)(k * (K1_THREADS / 32) + warp);
         }
       }
     }
@@ -544,14 +740,18 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
   }
   // large triangles: the whole CTA walks their bins
   const unsigned nbig = s_nbig;
-  for (unsigned q = 0; q < nbig; ++q) {
-    const uint2 rr = s_big[q];
-    const int tx0 = rr.x & 0xffff, ty0 = rr.x >> 16, tx1 = rr.y & 0xffff, ty1 = rr.y >> 16;
-    const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
-    for (unsigned j = tid; j < c; j += K1_THREADS) {
-      const int b = owned_bin_at(tx0, ty0, tx1, ty1, j, g);
-      for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], 1u);
-      if (cmrow) atomicAdd(&cmrow[b], 1u);
+  if (cl) {
+    cl_publish(a, sm1, bin1, mflag, nbig, chunk, frame);
+  } else {
+    for (unsigned q = 0; q < nbig; ++q) {
+      const uint2 rr = s_big[q];
+      const int tx0 = rr.x & 0xffff, ty0 = rr.x >> 16, tx1 = rr.y & 0xffff, ty1 = rr.y >> 16;
+      const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
+      for (unsigned j = tid; j < c; j += K1_THREADS) {
+        const int b = owned_bin_at(tx0, ty0, tx1, ty1, j, g);
+        for (int p = 0; p < a.npass; ++p) atomicAdd(&s_hist[p][(b >> (RX_BITS * p)) & (RX_RADIX - 1)], 1u);
+        if (cmrow) atomicAdd(&cmrow[b], 1u);
+      }
     }
   }
   __syncthreads();
@@ -1607,6 +1807,182 @@ __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_const
 }
 
 // ---------------------------------------------------------------------------
+// Chunk-list AssignBin, second half (a4 bin scan + a5 stable scatter + a6
+// schedule).  Persistent CTAs; CTA j owns bins j + k*grid.
+// Every CTA scans the NB totals (bin_start of its bins, P).  For a non-empty
+// bin: its chunk bitmap lists its chunks in ascending order and each chunk's
+// entry {group mask, pairs} its 32-triangle groups in ascending order --
+// primitive order.  Entry destinations are the exclusive scan of
+// the entries' pairs; pass A loads every group's 32 rects (several per warp in
+// flight) and ballots "rect holds b"; pass B (a warp per entry) walks the
+// entry's groups in order and writes the primIDs.  A bin over CLB_ENT chunks
+// or CLB_GRP groups flags the frame (the host falls back to the count matrix).
+// CTAs past the gather part build k_tile's work lists.
+// ---------------------------------------------------------------------------
+struct ClbSmem {
+  unsigned ch[CLB_ENT];          // entry q: chunk
+  uint2 ent[CLB_ENT];            // entry q: {group mask, first group index}
+  unsigned dst[CLB_ENT];         // entry q: exclusive pair offset in the bin
+  unsigned grp[CLB_GRP];         // group j: global group index (triangles 32 grp + lane)
+  unsigned bal[CLB_GRP];         // ballot of group j ("rect holds the bin")
+  unsigned bs[CLB_KMAX], bc[CLB_KMAX];  // this CTA's bins: start, count
+  u64 w64[CLB_THREADS / 32];
+  unsigned ne, ng;
+};
+__device__ __forceinline__ u64 clb_scan64(u64 v, u64* w64, u64& tot) {  // block exclusive scan
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u64 inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  __syncthreads();  // (w64 may still be read by an earlier scan)
+  if (lane == 31) w64[warp] = inc;
+  __syncthreads();
+  u64 base = 0;
+  tot = 0;
+#pragma unroll
+  for (int w = 0; w < CLB_THREADS / 32; ++w) {
+    const u64 c = w64[w];
+    base += w < warp ? c : 0ull;
+    tot += c;
+  }
+  return base + inc - v;
+}
+
+__global__ void __launch_bounds__(CLB_THREADS) k_cl_bins(const __grid_constant__ ClArgs a) {
+  extern __shared__ __align__(16) unsigned char clb_dyn[];
+  ClbSmem& sm = *reinterpret_cast<ClbSmem*>(clb_dyn);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARP = CLB_THREADS / 32;
+  const int NB = a.g.NB;
+  const unsigned par = (unsigned)(a.frame & 1);
+  const uint32_t* tot = a.cl_tot + (size_t)par * NB;
+  pdl_wait();   // k_setup's entries, bitmaps, totals and rects
+  pdl_trigger();
+  const bool sched = (int)blockIdx.x >= a.nbin_ctas;
+  const int G = a.nbin_ctas;
+  // bin_start (and P, the overflow tag) come from k_setup's last CTA
+  const bool ovf = a.ctl->overflow_tag == a.frame + 1;
+  if (sched) {  // k_tile's work lists (only when the frame fits)
+    if (ovf) return;  // (CTA-uniform)
+    const long long b0 = ((long long)blockIdx.x - a.nbin_ctas) * SCAN_CHUNK + (long long)tid * SCAN_ITEMS;
+    const bool active = tid < SCAN_THREADS;
+    unsigned cc[SCAN_ITEMS];
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) cc[k] = (active && b0 + k < NB) ? __ldcg(tot + b0 + k) : 0u;
+    schedule_bins(a.sched, b0, cc, active);
+    return;
+  }
+  // this CTA's bins: start and count; the other parity of the totals (read by
+  // the previous frame's scan) is zeroed for the next frame's k_setup
+  if (tid < CLB_KMAX) {
+    const long long b = blockIdx.x + (long long)tid * G;
+    if (b < NB) {
+      const int s0 = __ldcg(a.sched.bin_start + b), s1 = __ldcg(a.sched.bin_start + b + 1);
+      sm.bs[tid] = (unsigned)s0;
+      sm.bc[tid] = (unsigned)(s1 - s0);
+      a.cl_tot[(size_t)(par ^ 1u) * NB + b] = 0u;
+    }
+  }
+  __syncthreads();
+  const int wpt = (a.nw + CLB_THREADS - 1) / CLB_THREADS;
+  for (int kk = 0; (long long)blockIdx.x + (long long)kk * G < NB; ++kk) {
+    if (sm.bc[kk] == 0) continue;  // no entries, no bitmap bits (CTA-uniform)
+    const long long b = blockIdx.x + (long long)kk * G;
+    const unsigned bstart = sm.bs[kk];
+    const int bx = (int)(b % a.g.binsX), by = (int)(b / a.g.binsX);
+    // ---- the bin's chunks: bitmap words (thread tid holds words tid*wpt ..), zeroed
+    uint32_t* bm = a.cl_bm + (size_t)b * a.nw;
+    unsigned wd[CL_WPT], pc = 0;
+#pragma unroll
+    for (int i = 0; i < CL_WPT; ++i) {
+      const int w = tid * wpt + i;
+      wd[i] = (i < wpt && w < a.nw) ? __ldcg(bm + w) : 0u;
+      pc += __popc(wd[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < CL_WPT; ++i)
+      if (wd[i]) bm[tid * wpt + i] = 0u;
+    u64 nev;
+    unsigned e = (unsigned)clb_scan64(pc, sm.w64, nev);
+    const unsigned ne = (unsigned)nev;
+    if (ovf || ne > (unsigned)CLB_ENT) {  // (CTA-uniform)
+      if (!ovf && tid == 0) { a.ctl->cl_overflow = 1u; atomicMax(&a.ctl->overflow_tag, a.frame + 1); }
+      continue;
+    }
+#pragma unroll
+    for (int i = 0; i < CL_WPT; ++i)
+      for (unsigned bits = wd[i]; bits; bits &= bits - 1) sm.ch[e++] = (unsigned)((tid * wpt + i) * 32 + __ffs(bits) - 1);
+    __syncthreads();
+    // ---- entries {mask, pairs}: exclusive scans of pairs (destinations) and
+    // groups (packed: pairs << 32 | groups), EPT consecutive entries per thread
+    constexpr int EPT = CLB_ENT / CLB_THREADS;
+    uint2 en[EPT];
+    u64 es = 0;
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const unsigned q = tid * EPT + u;
+      en[u] = q < ne ? __ldcg(a.cl_ent + (size_t)b * a.nch + sm.ch[q]) : make_uint2(0u, 0u);
+      es += ((u64)en[u].y << 32) | (unsigned)__popc(en[u].x);
+    }
+    u64 esum;
+    u64 eo = clb_scan64(es, sm.w64, esum);
+    const unsigned ng = (unsigned)esum;
+    if (ng > (unsigned)CLB_GRP) {
+      if (tid == 0) { a.ctl->cl_overflow = 1u; atomicMax(&a.ctl->overflow_tag, a.frame + 1); }
+      continue;
+    }
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const unsigned q = tid * EPT + u;
+      if (q < ne) {
+        unsigned g0 = (unsigned)eo;
+        sm.ent[q] = make_uint2(en[u].x, g0);
+        sm.dst[q] = (unsigned)(eo >> 32);
+        const unsigned gbase = sm.ch[q] * 32u;
+        for (unsigned bits = en[u].x; bits; bits &= bits - 1) sm.grp[g0++] = gbase + (unsigned)(__ffs(bits) - 1);
+      }
+      eo += ((u64)en[u].y << 32) | (unsigned)__popc(en[u].x);
+    }
+    __syncthreads();
+    // ---- pass A: ballots "rect holds b", 8 groups per warp in flight
+    for (unsigned j0 = warp; j0 < ng; j0 += 8 * NWARP) {
+      uint2 rr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const unsigned j = j0 + u * NWARP;
+        const long long t = j < ng ? (long long)sm.grp[j] * 32 + lane : a.n_tris;
+        rr[u] = t < a.n_tris ? __ldcg(a.rect + t) : make_uint2(1u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const unsigned j = j0 + u * NWARP;
+        const int tx0 = rr[u].x & 0xffff, ty0 = rr[u].x >> 16, tx1 = rr[u].y & 0xffff, ty1 = rr[u].y >> 16;
+        const unsigned bal = __ballot_sync(0xffffffffu, tx0 <= bx && bx <= tx1 && ty0 <= by && by <= ty1);
+        if (j < ng && lane == 0) sm.bal[j] = bal;
+      }
+    }
+    __syncthreads();
+    // ---- pass B: a warp per entry walks its groups in order
+    const unsigned lt = (1u << lane) - 1u;
+    int32_t* out = a.bin_prims + bstart;
+    for (unsigned q = warp; q < ne; q += NWARP) {
+      const uint2 eq = sm.ent[q];
+      unsigned o = sm.dst[q];
+      const unsigned ngq = __popc(eq.x);
+      for (unsigned j = eq.y; j < eq.y + ngq; ++j) {
+        const unsigned bal = sm.bal[j];
+        if (bal >> lane & 1u) out[o + __popc(bal & lt)] = (int32_t)(sm.grp[j] * 32u + lane);
+        o += __popc(bal);
+      }
+    }
+    __syncthreads();  // shared arrays are reused by the next bin
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Reyes Split + Dice (R19-R21).
 // k_dice_rate: one CTA; each thread decides the split/dice rate (Gu, Gv) of
 // patches from their projected control hull, then a block scan over the
@@ -2526,12 +2902,12 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   TL_CTA(1);
   // ---- empty bins: background only, no shared memory, no barriers ------------
   // every warp pulls groups of EMPTY_GROUP bins from a second queue
-#ifdef PIKO_EXP_NOEMPTY
-  if (false)
-#endif
   // (one queue ticket per CTA for THREADS/32 groups: per-warp tickets on one
   // address serialised at L2)
   __shared__ unsigned s_etk;
+#ifdef PIKO_EXP_NOEMPTY
+  if (false)
+#endif
   for (;;) {
     __syncthreads();
     if (tid == 0) s_etk = atomicAdd(&a.ctl->empty_next, 1u);
@@ -2973,8 +3349,12 @@ cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool
   return launch_ex(k_index_max, (int)(want > 0 ? want : 1), 256, 0, pdl, s, idx, n, ctl);
 }
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s) {
-  if (!a.xv) return launch_ex(k_setup<true>, grid, K1_THREADS, 0, pdl, s, a);
-  return launch_ex(k_setup<false>, grid, K1_THREADS, 0, pdl, s, a);
+  // (set per launch: the attribute belongs to the current device's context)
+  cudaError_t e = a.xv ? cudaFuncSetAttribute(k_setup<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem))
+                       : cudaFuncSetAttribute(k_setup<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem));
+  if (e != cudaSuccess) return e;
+  if (!a.xv) return launch_ex(k_setup<true>, grid, K1_THREADS, sizeof(K1Smem), pdl, s, a);
+  return launch_ex(k_setup<false>, grid, K1_THREADS, sizeof(K1Smem), pdl, s, a);
 }
 cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream_t s) {
   if (a.expand) {
@@ -3007,6 +3387,12 @@ cudaError_t launch_cm_scatter(const CmArgs& a, int grid, bool pdl, cudaStream_t 
   cudaError_t e = cudaFuncSetAttribute(k_cm_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_ex(k_cm_scatter, grid, CM_THREADS, smem, pdl, s, a);
+}
+cudaError_t launch_cl_bins(const ClArgs& a, int grid, bool pdl, cudaStream_t s) {
+  const size_t smem = sizeof(ClbSmem);
+  cudaError_t e = cudaFuncSetAttribute(k_cl_bins, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_ex(k_cl_bins, grid, CLB_THREADS, smem, pdl, s, a);
 }
 
 #endif  // PIKO_TILE_TU

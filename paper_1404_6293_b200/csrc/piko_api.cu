@@ -172,6 +172,14 @@ struct piko_ctx {
   bool tile_items_grid = false;             // k_tile: one CTA per possible item instead of persistent
   bool last_cm = false;                     // the last frame used the count matrix
   long long last_cm_rows = 0;
+  // chunk-list AssignBin (NB <= CL_MAX_NB; the default where it applies)
+  int cl_mode = 0;                          // 0 off (default: slower on c2/c3), 1 on where it applies
+  bool cl_off = false;                      // a chunk overflowed CL_WIN: count matrix from now on
+  bool last_cl = false;                     // the last frame used the chunk lists
+  long long last_cl_nch = 0;
+  uint2* cl_ent = nullptr; long long cl_ent_cap = 0;      // [NB][chunks] {group mask, pairs}
+  uint32_t* cl_bm = nullptr; long long cl_bm_cap = 0;     // [NB][words]
+  uint32_t* cl_tot = nullptr;                              // [2][NB]
   int32_t* prims_out = nullptr;             // CSR bin_prims of the last frame
   unsigned long long* def_keys = nullptr;   // [NB][bw*bh]
   int pipeline = PIKO_PIPE_BINNED;
@@ -304,6 +312,7 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   if (const char* e = getenv("PIKO_SEPARATE_VS")) ctx->vs_mode = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_DEFERRED")) ctx->deferred = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_CM")) ctx->cm_mode = e[0] == '0' ? 0 : 1;
+  if (const char* e = getenv("PIKO_CL")) ctx->cl_mode = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_TILE_GRID")) ctx->tile_items_grid = strcmp(e, "items") == 0;
   if (const char* e = getenv("PIKO_CM_TC_LOG2")) ctx->cm_tc_log2 = atoi(e);
   return ctx;
@@ -326,7 +335,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
                   ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->fkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys, ctx->def_keys, ctx->cm, ctx->cp, ctx->dice_verts, ctx->dice_idx, ctx->dice_rate, ctx->dice_base, ctx->dice_total,
                   ctx->all_keys, ctx->fp_keys, ctx->ovq, ctx->sc.sink, ctx->bl_keys, ctx->frag_key,
-                  ctx->frag_px, ctx->frag_rgba};
+                  ctx->frag_px, ctx->frag_rgba, ctx->cl_ent, ctx->cl_bm, ctx->cl_tot};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -660,6 +669,40 @@ static int ensure_cm(piko_ctx* ctx, long long rows) {
   return PIKO_OK;
 }
 
+// Chunk-list AssignBin for this frame?  k_setup CTAs (chunks of K1_CHUNK
+// triangles) record per bin the mask of their 32-triangle groups with a pair
+// in it (per-bin arrays in shared memory: NB <= CL_MAX_NB) and k_cl_bins
+// compacts every bin's candidates; off after a bin had more than CLB_ENT
+// chunks or CLB_GRP groups (unordered soups: the count matrix handles them).
+static bool use_cl(const piko_ctx* ctx, long long T, long long& nch, int& nw) {
+  nch = (T + K1_CHUNK - 1) / K1_CHUNK;
+  nw = (int)((nch + 31) / 32);
+  if (ctx->cl_mode == 0 || ctx->cl_off || T <= 0 || ctx->g.NB > CL_MAX_NB) return false;
+  return nw <= CLB_THREADS * CL_WPT && nch * ctx->g.NB <= CL_MAX_ENTRIES;
+}
+
+static int ensure_cl(piko_ctx* ctx, long long nch, int nw) {
+  const long long NB = ctx->g.NB;
+  if (NB * nch > ctx->cl_ent_cap) {
+    if (ctx->cl_ent) cudaFree(ctx->cl_ent);
+    ctx->cl_ent = nullptr; ctx->cl_ent_cap = 0;
+    CK(cudaMalloc(&ctx->cl_ent, sizeof(uint2) * NB * nch));
+    ctx->cl_ent_cap = NB * nch;
+  }
+  if (NB * nw > ctx->cl_bm_cap) {
+    if (ctx->cl_bm) cudaFree(ctx->cl_bm);
+    ctx->cl_bm = nullptr; ctx->cl_bm_cap = 0;
+    CK(cudaMalloc(&ctx->cl_bm, sizeof(uint32_t) * NB * nw));
+    ctx->cl_bm_cap = NB * nw;
+    ctx->need_reset = true;  // bitmaps are zeroed by the reset
+  }
+  if (!ctx->cl_tot) {
+    CK(cudaMalloc(&ctx->cl_tot, sizeof(uint32_t) * 2 * NB));
+    ctx->need_reset = true;
+  }
+  return PIKO_OK;
+}
+
 static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
                          long long T, const Mat4& M, const float L[3], float* rgba, float* depth,
                          cudaStream_t s, unsigned long long* keys_out = nullptr) {
@@ -687,16 +730,21 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   const long long ntiles = (ctx->g.NB + SCAN_CHUNK - 1) / SCAN_CHUNK;
   const long long gx = std::max<long long>((T + ctx->tri_chunk - 1) / ctx->tri_chunk, 1);  // pass 0
   const long long gp = (long long)((ctx->pair_cap + RX_CHUNK - 1) / RX_CHUNK);              // passes >= 1
-  int cm_shift = 0;
-  long long cm_rows = 0;
-  const bool cm = use_cm(ctx, T, cm_shift, cm_rows);
+  int cm_shift = 0, cl_nw = 0;
+  long long cm_rows = 0, cl_nch = 0;
+  const bool clm = use_cl(ctx, T, cl_nch, cl_nw);
+  if (clm && ensure_cl(ctx, cl_nch, cl_nw) != PIKO_OK) return PIKO_ECUDA;
+  const bool cm = !clm && use_cm(ctx, T, cm_shift, cm_rows);
   if (cm && ensure_cm(ctx, cm_rows) != PIKO_OK) return PIKO_ECUDA;
-  const long long grids[6] = {g1, gx, gp + ntiles, ntiles, cm ? 1 : 0, cm ? cm_rows : 0};
+  const bool sorted_here = cm || clm;  // no radix passes this frame
+  const long long grids[6] = {g1, gx, gp + ntiles, ntiles, clm ? 2 : cm ? 1 : 0, cm ? cm_rows : 0};
   CK(mark(0));
   bool changed = ctx->need_reset;
   for (int k = 0; k < 6; ++k) changed |= grids[k] != ctx->last_grids[k];
   if (changed) {
     if (ctx->cm) CK(cudaMemsetAsync(ctx->cm, 0, sizeof(uint32_t) * ctx->cm_cap, s));
+    if (ctx->cl_bm) CK(cudaMemsetAsync(ctx->cl_bm, 0, sizeof(uint32_t) * ctx->cl_bm_cap, s));
+    if (ctx->cl_tot) CK(cudaMemsetAsync(ctx->cl_tot, 0, sizeof(uint32_t) * 2 * ctx->g.NB, s));
     // tickets restart at 0, so every tag-carrying status word must be cleared
     CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), s));
     CK(cudaMemsetAsync(ctx->st_scan, 0, sizeof(unsigned long long) * ctx->st_scan_n, s));
@@ -712,7 +760,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   }
   CK(mark(1 + PIKO_STAGE_CLEAR));
   const bool sep = separate_vs(ctx, V, T);
-  ctx->last_kernels = 2 + (cm ? 2 : ctx->npass + (ctx->npass == 1 ? 1 : 0)) +
+  ctx->last_kernels = 2 + (clm ? 1 : cm ? 2 : ctx->npass + (ctx->npass == 1 ? 1 : 0)) +
                       (sep ? 1 + (V < 0 && T > 0 ? 1 : 0) : 0) + (gather && ctx->mrank == 0 ? 1 : 0) + (defer ? 1 : 0);
   if (sep) {
     if (V < 0 && T > 0) CK(launch_index_max(idx, 3 * T, ctx->ctl, ctx->pdl, s));
@@ -726,16 +774,24 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     SetupArgs a{};
     a.xv = sep ? ctx->xv : nullptr; a.xv_cap = ctx->xv_cap; a.verts = verts; a.M = M;
     a.idx = idx; a.n_tris = T; a.g = ctx->g;
-    a.npass = cm ? 0 : ctx->npass; a.rec = ctx->rec; a.rect = ctx->rect; a.ctl = ctx->ctl;
+    a.npass = sorted_here ? 0 : ctx->npass; a.rec = ctx->rec; a.rect = ctx->rect; a.ctl = ctx->ctl;
     a.cm = cm ? ctx->cm : nullptr; a.cm_shift = cm_shift;
     a.frame = ctx->frames++;
+    if (clm) {
+      a.cl_ent = ctx->cl_ent; a.cl_bm = ctx->cl_bm;
+      a.cl_tot = ctx->cl_tot + (size_t)(a.frame & 1) * ctx->g.NB;
+      a.cl_nch = cl_nch; a.cl_nw = cl_nw;
+      a.cl_start = ctx->bin_start; a.cl_cap = ctx->pair_cap;
+    }
     CK(launch_setup(a, (int)g1, ctx->pdl, s));
   }
   CK(mark(1 + PIKO_STAGE_SETUP));
-  ctx->prims_out = cm ? ctx->vals[0] : ctx->vals[ctx->npass & 1];
+  ctx->prims_out = sorted_here ? ctx->vals[0] : ctx->vals[ctx->npass & 1];
   ctx->last_cm = cm;
   ctx->last_cm_rows = cm ? cm_rows : 0;
-  for (int p = 0; p < (cm ? 0 : ctx->npass); ++p) {
+  ctx->last_cl = clm;
+  ctx->last_cl_nch = clm ? cl_nch : 0;
+  for (int p = 0; p < (sorted_here ? 0 : ctx->npass); ++p) {
     RadixArgs a{};
     a.expand = p == 0; a.rect = ctx->rect; a.n_tris = T; a.tri_chunk = ctx->tri_chunk;
     a.g = ctx->g; a.cap = ctx->pair_cap; a.scan_here = p == 1;
@@ -771,6 +827,21 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     CK(mark(1 + PIKO_STAGE_EXPAND));
     CK(launch_cm_scatter(c, (int)(cm_rows + ntiles), ctx->pdl, s));
   }
+  if (clm) {
+    ClArgs c{};
+    c.cl_ent = ctx->cl_ent; c.rect = ctx->rect; c.n_tris = T; c.cl_bm = ctx->cl_bm; c.cl_tot = ctx->cl_tot;
+    c.nch = cl_nch; c.nw = cl_nw; c.frame = ctx->frames - 1;
+    // persistent: CTA j owns bins j + k * grid (<= CLB_KMAX each)
+    c.nbin_ctas = std::min(ctx->g.NB, std::max(8 * ctx->sms, (ctx->g.NB + CLB_KMAX - 1) / CLB_KMAX));
+    c.g = ctx->g; c.cap = ctx->pair_cap; c.bin_prims = ctx->prims_out; c.ctl = ctx->ctl;
+    RadixArgs& a = c.sched;
+    a.g = ctx->g; a.ctl = ctx->ctl; a.bin_start = ctx->bin_start; a.bin_count = ctx->bin_count; a.NB = ctx->g.NB;
+    a.rank = ctx->g.rank; a.nranks = ctx->g.nranks;
+    a.frag_list = ctx->frag_list; a.bin_list = ctx->bin_list;
+    a.frag = tile_frag(ctx->bw, ctx->bh); a.npx = ctx->bw * ctx->bh;
+    CK(mark(1 + PIKO_STAGE_EXPAND));
+    CK(launch_cl_bins(c, (int)(c.nbin_ctas + ntiles), ctx->pdl, s));
+  }
   if (ctx->npass == 0) CK(mark(1 + PIKO_STAGE_EXPAND));
   CK(mark(1 + PIKO_STAGE_SORT));
   {
@@ -802,7 +873,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.fkey = ctx->fkey; a.gcov = ctx->gcov; a.arrive = ctx->arrive; a.frag = tile_frag(ctx->bw, ctx->bh);
     a.garrive = ctx->garr; a.gcap = ctx->gcap;
     a.prim_base = (unsigned)ctx->prim_base;
-    a.radix = cm ? 0 : 1;
+    a.radix = sorted_here ? 0 : 1;
     if (!gather) CK(reserve_slot(ctx, &a.status_out));  // the tile kernel ends the frame's control updates
     if (keys_only) a.out_cov = nullptr;
     // persistent grid (all CTAs resident, items from the queue) or, with
@@ -942,6 +1013,7 @@ static int eval_frame(piko_ctx* ctx, piko_ctx::Slot& sl) {
     if (rc == PIKO_OK) ctx->fail(PIKO_ECAPACITY, "fragment capacity exceeded (%llu); grown", ctx->h_ctl->n_pairs);
     return ctx->last_status;
   }
+  if (ctx->h_ctl->cl_overflow) ctx->cl_off = true;  // next frames: count matrix (the reset clears the flag)
   if (ctx->h_ctl->overflow_tag == ctx->h_ctl->frame + 1 || ctx->h_ctl->vx_overflow ||
       ctx->h_ctl->peer_overflow == ctx->h_ctl->frame + 1) {
     int rc = ensure_pairs(ctx, ctx->h_ctl->n_pairs);
@@ -1386,9 +1458,9 @@ extern "C" int piko_get_stats(const piko_ctx* cctx, piko_stats* out) {
   out->pair_capacity = (int64_t)ctx->pair_cap;
   out->radix_passes = ctx->npass;
   out->kernels_per_frame = ctx->last_kernels;
-  out->assign_mode = ctx->last_cm ? 1 : 0;
+  out->assign_mode = ctx->last_cl ? 2 : ctx->last_cm ? 1 : 0;
   out->reserved = 0;
-  out->cm_rows = ctx->last_cm ? ctx->last_cm_rows : 0;
+  out->cm_rows = ctx->last_cl ? ctx->last_cl_nch : ctx->last_cm ? ctx->last_cm_rows : 0;
   return PIKO_OK;
 }
 

@@ -3,6 +3,7 @@
 // the CPU checker.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -55,7 +56,19 @@ constexpr int OVQ_CAP = 1024;
 constexpr int CM_MAX_NB = 32768;                 // touched-bin bitmap in shared memory
 constexpr long long CM_MAX_ENTRIES = 1ll << 24;  // rows * NB
 constexpr int CM_SUB = 4096;                     // triangles per scatter sub-chunk (registers)
-constexpr int CM_COLS = 16;                      // k_cm_scan: bins per CTA (x 16 row groups)    // k_tile: spilled large-triangle entries per CTA (96 B each)
+constexpr int CM_COLS = 16;                      // k_cm_scan: bins per CTA (x 16 row groups)
+// Chunk-list AssignBin (round 2): each k_setup CTA (a chunk
+// of K1_CHUNK triangles = 32 groups of 32) records per touched bin the mask of
+// its groups with a pair in the bin and the pair count; k_cl_bins walks a bin's
+// chunks (bitmap) and groups (masks) in primitive order and compacts the
+// triangles whose rect holds the bin with warp ballots.
+constexpr int CL_MAX_NB = 4096;                  // per-bin masks / counts of a chunk in shared memory
+constexpr int CL_WPT = 8;                        // bitmap words per k_cl_bins thread (chunks <= 512*32*8)
+constexpr long long CL_MAX_ENTRIES = 1ll << 26;  // NB x chunks (the entry matrix)
+constexpr int CLB_THREADS = 256;                 // k_cl_bins CTA
+constexpr int CLB_ENT = 1024;                    // entries (chunks) of one bin (more: count matrix)
+constexpr int CLB_GRP = 2048;                    // groups of one bin (more: count matrix)
+constexpr int CLB_KMAX = 32;                     // bins per persistent k_cl_bins CTA
 
 // ---- persistent device control block ----------------------------------------
 // Never memset per frame: every kernel of a frame takes exactly gridDim.x
@@ -64,11 +77,12 @@ constexpr int CM_COLS = 16;                      // k_cm_scan: bins per CTA (x 1
 // Per-frame accumulators are double-buffered by frame parity; the tile kernel
 // zeroes the next frame's copy.  The host resets the block (and the status
 // arrays) only when a grid size changes or after an error.
-struct Control {
+struct Control {  // (the mirror copies whole 8-byte words up to digit_hist: keep u32 fields paired)
   unsigned long long k1_ticket;
   unsigned long long rx_ticket[MAX_PASSES];
   unsigned long long scan_ticket;      // standalone bin-scan kernel (single-pass grids)
   unsigned long long cm_done;          // k_cm_scan CTAs finished (modulo grid: the last scans bin_start)
+  unsigned long long cl_done;          // chunk-list k_setup CTAs finished (modulo grid: the last scans bin_start)
   unsigned long long frame;            // written by K1 chunk 0
   unsigned int tile_next;              // dynamic bin queue of k_tile (reset by K1 chunk 0)
   unsigned int list_n[NLIST];          // work-list sizes (reset by K1 chunk 0)
@@ -82,10 +96,13 @@ struct Control {
   unsigned long long p2p_arrive;       // k_tile CTA tickets (P2P arrival, modulo grid)
   unsigned long long p2p_count;        // k_resolve CTA tickets (P2P slot release)
   unsigned int p2p_timeout;            // a peer flag wait timed out (sticky)
+  unsigned int cl_overflow;            // a bin had more than CLB_ENT chunks / CLB_GRP groups (host: count matrix)
   unsigned long long peer_overflow;    // rank 0: frame+1 of a frame in which a peer rank overflowed
   unsigned long long tile_done;        // k_tile CTA tickets (modulo grid: the last one mirrors this block)
   unsigned int digit_hist[2][MAX_PASSES][RX_RADIX];  // parity double buffer
 };
+
+static_assert(offsetof(Control, digit_hist) % 8 == 0, "the host mirror copies whole words");
 
 struct Mat4 {
   float m[16];
@@ -140,6 +157,16 @@ struct SetupArgs {
   int4* rec;                    // [n_tris][3]
   uint2* rect;                  // [n_tris] tile rect {tx0|ty0<<16, tx1|ty1<<16}; empty if culled
   Control* ctl;
+  // chunk-list AssignBin (null: off): per touched bin b, cl_ent[b][chunk] =
+  // {mask of the chunk's 32-triangle groups with a pair in b, pairs}, bit
+  // `chunk` of cl_bm[b][cl_nw], cl_tot[b] += pairs
+  uint2* cl_ent;
+  uint32_t* cl_bm;
+  uint32_t* cl_tot;             // this frame's parity half of [2][NB]
+  long long cl_nch;             // chunks (= grid)
+  int cl_nw;                    // bitmap words per bin
+  int32_t* cl_start;            // [NB+1] bin_start: the grid's last CTA scans the totals
+  unsigned long long cl_cap;    //   ... and checks P against the pair capacity
 };
 
 struct RadixArgs {
@@ -193,6 +220,28 @@ struct CmArgs {
   Grid g;
   unsigned long long cap;       // pair capacity
   int32_t* bin_prims;           // [P] output CSR values
+  Control* ctl;
+  RadixArgs sched;              // bin_start, work lists (schedule CTAs)
+};
+
+// Chunk-list AssignBin, second half (k_cl_bins): persistent CTAs take the
+// non-empty bins; a bin's chunk bitmap (ascending chunk) and group masks
+// (ascending group) enumerate its candidate triangles in primitive order, the
+// rect test + ballot compacts them to bin_prims[bin_start[b] ...].  Extra CTAs
+// build k_tile's work lists.
+struct ClArgs {
+  const uint2* cl_ent;
+  const uint2* rect;
+  uint32_t* cl_bm;              // words are zeroed after reading (next frame)
+  uint32_t* cl_tot;             // [2][NB]: this frame's parity read, the other zeroed
+  long long nch;
+  int nw;
+  int nbin_ctas;                // CTAs of the gather part (the rest build work lists)
+  long long n_tris;
+  unsigned long long frame;     // host frame counter (parity of cl_tot)
+  Grid g;
+  unsigned long long cap;       // pair capacity of bin_prims
+  int32_t* bin_prims;
   Control* ctl;
   RadixArgs sched;              // bin_start, work lists (schedule CTAs)
 };
@@ -351,6 +400,7 @@ cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream
 cudaError_t launch_bin_scan(const RadixArgs& a, int grid, bool pdl, cudaStream_t s);
 cudaError_t launch_cm_scan(const CmArgs& a, int grid, bool pdl, cudaStream_t s);
 cudaError_t launch_cm_scatter(const CmArgs& a, int grid, bool pdl, cudaStream_t s);
+cudaError_t launch_cl_bins(const ClArgs& a, int grid, bool pdl, cudaStream_t s);
 inline int cm_scan_grid(int NB) { return (NB + CM_COLS - 1) / CM_COLS; }
 cudaError_t launch_tile(const TileArgs& a, int bw, int bh, int grid, bool cov, bool keys_only,
                         bool pdl, cudaStream_t s);

@@ -364,8 +364,10 @@ def test_stats_and_profile(env):
     assert st["n_pairs"] == len(oprims) and st["n_bins"] == len(ostart) - 1
     oi, _ = env[1].setup(s.verts, s.idx, s.mvp, s.W, s.H)
     assert st["n_live"] == int(oi[:, 0].sum())
-    # c3 is a shared-vertex mesh (2V <= 3T): separate vertex stage, 2 radix passes
+    # c3 is a shared-vertex mesh (2V <= 3T): separate vertex stage; count-matrix
+    # AssignBin (the default): k_vertex, k_setup, k_cm_scan, k_cm_scatter, k_tile
     assert st["radix_passes"] == 2 and st["kernels_per_frame"] == 5
+    assert st["assign_mode"] == 1
     r.close()
 
 
@@ -481,19 +483,66 @@ def test_baseline_fragment_overflow_regrows(env):
 
 
 # ---- round 2: the exact benchmarked instantiation and the oracle-pin scenes --
-@pytest.mark.parametrize("assign", ["count-matrix", "radix"])
+ASSIGN_ENV = {"chunk-list": {"PIKO_CL": "1"}, "count-matrix": {"PIKO_CL": "0", "PIKO_CM": "1"},
+              "radix": {"PIKO_CL": "0", "PIKO_CM": "0"}}
+ASSIGN_MODE = {"chunk-list": 2, "count-matrix": 1, "radix": 0}
+
+
+@pytest.mark.parametrize("assign", ["chunk-list", "count-matrix", "radix"])
 def test_c3_b16_cov_off_bench_variant(env, assign, monkeypatch):
     """The instantiation bench.py times: c3, 16x16 bins, coverage counting off
     (k_tile<16,16,256,COV=0,KEYS=0>), the separate vertex stage (c3 shares
     vertices: chosen automatically), AssignBin as configured (count matrix by
-    default; the radix passes forced) -- bit-exact vs the oracle."""
-    monkeypatch.setenv("PIKO_CM", "1" if assign == "count-matrix" else "0")
+    default; the chunk lists and the radix passes forced) -- bit-exact vs the
+    oracle."""
+    for k, v in ASSIGN_ENV[assign].items():
+        monkeypatch.setenv(k, v)
     monkeypatch.delenv("PIKO_SEPARATE_VS", raising=False)
     s = scenes.scene_c3()
     got = gpu_render(env, s, 16, cov=False, frames=3)
     assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
     assert_bins_equal(got, env, s, 16)
-    assert got["stats"]["kernels_per_frame"] == 5
+    assert got["stats"]["assign_mode"] == ASSIGN_MODE[assign]
+    assert got["stats"]["kernels_per_frame"] == (4 if assign == "chunk-list" else 5)
+
+
+@pytest.mark.parametrize("assign", ["chunk-list", "count-matrix", "radix"])
+@pytest.mark.parametrize("cfg,bw", [("c2", 16), ("c2", 8), ("c1", 8)])
+def test_assign_modes_agree(env, assign, cfg, bw, monkeypatch):
+    """Every AssignBin mode gives the oracle's bin lists and frame (c2: many
+    chunks, 2.2 pairs per triangle; 8-px bins: NB = 12288 > CL_MAX_NB, so the
+    chunk-list request falls through to the count matrix)."""
+    for k, v in ASSIGN_ENV[assign].items():
+        monkeypatch.setenv(k, v)
+    s = scenes.make(cfg)
+    got = gpu_render(env, s, bw, frames=2)
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, bw)
+    NB = ((s.W + bw - 1) // bw) * ((s.H + bw - 1) // bw)
+    want = ASSIGN_MODE[assign] if not (assign == "chunk-list" and NB > 4096) else 1
+    assert got["stats"]["assign_mode"] == want
+
+
+def test_chunk_list_overflow_falls_back(env, monkeypatch):
+    """A bin that collects more than CLB_GRP = 2048 groups of 32 triangles
+    (3000 scattered one-bin triangles x 32 stride: one per group, all in bin 0,
+    plus fill): the frame reports the overflow, the context switches to the
+    count matrix, and the checked draw re-issues it -- frame and bin lists exact."""
+    from tests.helpers import pixel_scene
+    tris = []
+    for k in range(2100 * 32):
+        if k % 32 == 0:
+            tris.append([(1.5, 1.5), (5.5, 1.5), (1.5, 5.5)])  # bin 0 (8-px bins)
+        else:
+            tris.append([(300.5, 300.5), (300.5, 300.5), (300.5, 300.5)])  # degenerate: culled
+    verts, idx, mvp = pixel_scene(tris, 0.5, 512, 512)
+    s = scenes.Scene("cl_overflow", 512, 512, (8,), verts, idx, mvp)
+    monkeypatch.setenv("PIKO_CL", "1")
+    got = gpu_render(env, s, 8, frames=2)
+    assert got["stats"]["n_pairs"] == 2100
+    assert got["stats"]["assign_mode"] == 1
+    assert_frame_equal(got, oracle_frame(env, s))
+    assert_bins_equal(got, env, s, 8)
 
 
 def _pin_scenes():
