@@ -2473,7 +2473,8 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   unsigned n_work = 0;
 #pragma unroll
   for (int k = 0; k < LIST_EMPTY; ++k) n_work += s_ln[k];
-  const unsigned n_frag = s_ln[0], n_empty = s_ln[LIST_EMPTY];
+  const unsigned n_frag = s_ln[0];
+  const unsigned n_empty = a.skip_empty ? 0u : s_ln[LIST_EMPTY];  // (deferred resolve: background from the CSR)
   auto bin_range = [&](int b, int& rs, int& re) {
     if (a.npass == 0) { rs = 0; re = (int)a.ctl->n_pairs; return; }
     rs = a.bin_start[b];
@@ -3259,7 +3260,10 @@ __global__ void __launch_bounds__(256) k_resolve(const __grid_constant__ Resolve
 // dependent gathers of shading are hidden across warps instead of sitting on
 // k_tile's per-bin critical path.
 // ---------------------------------------------------------------------------
-constexpr int SHADE_QUAD = 4;
+#ifndef PIKO_SHADE_QUAD
+#define PIKO_SHADE_QUAD 4
+#endif
+constexpr int SHADE_QUAD = PIKO_SHADE_QUAD;  // pixels of a row per k_shade thread (1 or 4)
 __global__ void __launch_bounds__(256) k_shade(const __grid_constant__ ResolveArgs a) {
   pdl_wait();
   pdl_trigger();
@@ -3272,9 +3276,15 @@ __global__ void __launch_bounds__(256) k_shade(const __grid_constant__ ResolveAr
   const int b = (y >> g.bh_log2) * g.binsX + (x0 >> g.bw_log2);
   const int p = (y & (bh - 1)) * bw + (x0 & (bw - 1));
   // bins are >= 8 px wide and x0 % 4 == 0: the quad is 4 consecutive keys of one bin row
-  const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(a.all_keys + (size_t)b * (size_t)(bw * bh) + p);
-  const ulonglong2 k01 = __ldcs(kp), k23 = __ldcs(kp + 1);
-  const u64 key[SHADE_QUAD] = {k01.x, k01.y, k23.x, k23.y};
+  u64 key[SHADE_QUAD];
+  if constexpr (SHADE_QUAD == 4) {
+    const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(a.all_keys + (size_t)b * (size_t)(bw * bh) + p);
+    const ulonglong2 k01 = __ldcs(kp), k23 = __ldcs(kp + 1);
+    key[0] = k01.x; key[1] = k01.y; key[2] = k23.x; key[3] = k23.y;
+  } else {
+#pragma unroll
+    for (int k = 0; k < SHADE_QUAD; ++k) key[k] = __ldcs(a.all_keys + (size_t)b * (size_t)(bw * bh) + p + k);
+  }
   float L[3];
   normalise_light(a.light, L);
   int t[SHADE_QUAD], Px[SHADE_QUAD];
@@ -3294,12 +3304,12 @@ __global__ void __launch_bounds__(256) k_shade(const __grid_constant__ ResolveAr
     if (t[k] >= 0 && a.sc.iters && !a.sc.forward) shader_sink(a.sc, shader_work(a.sc.iters, dep[k]));
   }
   const size_t o = (size_t)y * g.W + x0;
-  if (x0 + SHADE_QUAD <= g.W && (o & 3) == 0) {
+  if (SHADE_QUAD == 4 && x0 + SHADE_QUAD <= g.W && (o & 3) == 0) {
     float4* rp = reinterpret_cast<float4*>(a.out_rgba) + o;
 #pragma unroll
     for (int k = 0; k < SHADE_QUAD; ++k) __stcs(rp + k, c[k]);
-    __stcs(reinterpret_cast<float4*>(a.out_depth + o), make_float4(dep[0], dep[1], dep[2], dep[3]));
-    __stcs(reinterpret_cast<int4*>(a.out_primid + o), make_int4(prim[0], prim[1], prim[2], prim[3]));
+    __stcs(reinterpret_cast<float4*>(a.out_depth + o), make_float4(dep[0], dep[SHADE_QUAD > 1 ? 1 : 0], dep[SHADE_QUAD > 2 ? 2 : 0], dep[SHADE_QUAD > 3 ? 3 : 0]));
+    __stcs(reinterpret_cast<int4*>(a.out_primid + o), make_int4(prim[0], prim[SHADE_QUAD > 1 ? 1 : 0], prim[SHADE_QUAD > 2 ? 2 : 0], prim[SHADE_QUAD > 3 ? 3 : 0]));
   } else {
 #pragma unroll
     for (int k = 0; k < SHADE_QUAD; ++k) {
@@ -3309,6 +3319,86 @@ __global__ void __launch_bounds__(256) k_shade(const __grid_constant__ ResolveAr
       a.out_primid[o + k] = prim[k];
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// k_shade1: the deferred resolve with one pixel per thread (row-major, so the
+// output stores are coalesced) and no per-pixel setup: the winner's
+// orientation comes from its snapped corners' area sign alone (the O2 swap of
+// corners 1 and 2), then the O7 arithmetic of shade_math in the same order.
+// Pixels of bins without pairs (k_tile skipped them) and of overflowed frames
+// are background without a key load.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 shade_lean(const float* __restrict__ verts, const int4* __restrict__ xv,
+                                             const Mat4& M, const int32_t* __restrict__ idx, int W, int H,
+                                             const float L[3], int t, int Px, int Py) {
+  const int i0 = __ldg(idx + 3ll * t), i1 = __ldg(idx + 3ll * t + 1), i2 = __ldg(idx + 3ll * t + 2);
+  int4 c0, c1, c2;
+  if (xv) {
+    c0 = __ldg(xv + i0); c1 = __ldg(xv + i1); c2 = __ldg(xv + i2);
+  } else {
+    const float4 p0 = load_pos(verts, i0), p1 = load_pos(verts, i1), p2 = load_pos(verts, i2);
+    c0 = transform_vertex(p0, M, W, H);
+    c1 = transform_vertex(p1, M, W, H);
+    c2 = transform_vertex(p2, M, W, H);
+  }
+  float4 m0 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i0 + 4));
+  float4 m1 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i1 + 4));
+  float4 m2 = __ldg(reinterpret_cast<const float4*>(verts + 8ll * i2 + 4));
+  long long area2 = (long long)(c1.x - c0.x) * (long long)(c2.y - c0.y) -
+                    (long long)(c1.y - c0.y) * (long long)(c2.x - c0.x);
+  if (area2 < 0) {  // O2 orientation normalisation (as setup_tri)
+    const int4 ti = c1; c1 = c2; c2 = ti;
+    const float4 tm = m1; m1 = m2; m2 = tm;
+    area2 = -area2;
+  }
+  const float rw0 = __int_as_float(c0.w), rw1 = __int_as_float(c1.w), rw2 = __int_as_float(c2.w);
+  const long long w0 = (long long)(c2.x - c1.x) * (Py - c1.y) - (long long)(c2.y - c1.y) * (Px - c1.x);
+  const long long w1 = (long long)(c0.x - c2.x) * (Py - c2.y) - (long long)(c0.y - c2.y) * (Px - c2.x);
+  const long long w2 = (long long)(c1.x - c0.x) * (Py - c0.y) - (long long)(c1.y - c0.y) * (Px - c0.x);
+  const float inv = __frcp_rn(__ll2float_rn(area2));
+  const float l0 = __fmul_rn(__fmul_rn(__ll2float_rn(w0), inv), rw0);
+  const float l1 = __fmul_rn(__fmul_rn(__ll2float_rn(w1), inv), rw1);
+  const float l2 = __fmul_rn(__fmul_rn(__ll2float_rn(w2), inv), rw2);
+  const float vx = __fmaf_rn(l2, m2.x, __fmaf_rn(l1, m1.x, __fmul_rn(l0, m0.x)));
+  const float vy = __fmaf_rn(l2, m2.y, __fmaf_rn(l1, m1.y, __fmul_rn(l0, m0.y)));
+  const float vz = __fmaf_rn(l2, m2.z, __fmaf_rn(l1, m1.z, __fmul_rn(l0, m0.z)));
+  const float d2 = __fmaf_rn(vx, vx, __fmaf_rn(vy, vy, __fmul_rn(vz, vz)));
+  float lam = 0.0f;
+  if (d2 != 0.0f) {
+    const float q = __fdiv_rn(__fmaf_rn(vx, L[0], __fmaf_rn(vy, L[1], __fmul_rn(vz, L[2]))), __fsqrt_rn(d2));
+    lam = (q > 0.0f) ? q : 0.0f;
+  }
+  return make_float4(__fmul_rn(0.80f, lam), __fmul_rn(0.75f, lam), __fmul_rn(0.65f, lam), 1.0f);
+}
+
+__global__ void __launch_bounds__(256) k_shade1(const __grid_constant__ ResolveArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const Grid g = a.g;
+  const long long o = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (o >= (long long)g.W * g.H) return;
+  const int y = (int)(o / g.W), x = (int)(o % g.W);
+  const int bw = 1 << g.bw_log2, bh = 1 << g.bh_log2;
+  const int b = (y >> g.bh_log2) * g.binsX + (x >> g.bw_log2);
+  const bool empty = a.bin_start == nullptr ? false
+                     : (a.ctl->overflow_tag == a.ctl->frame + 1 || __ldg(a.bin_start + b + 1) == __ldg(a.bin_start + b));
+  const u64 key = empty ? CLEAR_KEY
+                        : __ldcs(a.all_keys + (size_t)b * (size_t)(bw * bh) + (y & (bh - 1)) * bw + (x & (bw - 1)));
+  float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+  float dep = 1.0f;
+  int prim = -1;
+  if (key != CLEAR_KEY) {
+    float L[3];
+    normalise_light(a.light, L);
+    prim = (int)(unsigned)(key & 0xFFFFFFFFu);
+    dep = key_depth(key);
+    c = shade_lean(a.verts, a.xv, a.M, a.idx, g.W, g.H, L, prim, 256 * x + 128, 256 * y + 128);
+    if (a.sc.iters && !a.sc.forward) shader_sink(a.sc, shader_work(a.sc.iters, dep));
+  }
+  __stcs(reinterpret_cast<float4*>(a.out_rgba) + o, c);
+  __stcs(a.out_depth + o, dep);
+  __stcs(a.out_primid + o, prim);
 }
 
 // ---------------------------------------------------------------------------
@@ -3492,6 +3582,10 @@ cudaError_t launch_baseline(const BaselineArgs& a, int stage, bool pdl, cudaStre
 }
 
 cudaError_t launch_shade(const ResolveArgs& a, bool pdl, cudaStream_t s) {
+  if (a.bin_start) {  // one pixel per thread, empty bins known from the CSR (k_tile skipped them)
+    const long long n = (long long)a.g.W * a.g.H;
+    return launch_ex(k_shade1, (int)((n + 255) / 256), 256, 0, pdl, s, a);
+  }
   const long long nq = (long long)((a.g.W + SHADE_QUAD - 1) / SHADE_QUAD) * a.g.H;
   return launch_ex(k_shade, (int)((nq + 255) / 256), 256, 0, pdl, s, a);
 }

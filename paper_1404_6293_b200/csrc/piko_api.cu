@@ -874,6 +874,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.garrive = ctx->garr; a.gcap = ctx->gcap;
     a.prim_base = (unsigned)ctx->prim_base;
     a.radix = sorted_here ? 0 : 1;
+    a.skip_empty = defer && ctx->g.NB > 1 ? 1 : 0;
     if (!gather) CK(reserve_slot(ctx, &a.status_out));  // the tile kernel ends the frame's control updates
     if (keys_only) a.out_cov = nullptr;
     // persistent grid (all CTAs resident, items from the queue) or, with
@@ -960,6 +961,8 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
       a.g = ctx->g; a.all_keys = ctx->def_keys; a.owned_max = ctx->owned;
       a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
       a.sc = ctx->sc;
+      a.ctl = ctx->ctl;
+      if (ctx->g.NB > 1) a.bin_start = ctx->bin_start;
       CK(launch_shade(a, ctx->pdl, s));
     }
   }

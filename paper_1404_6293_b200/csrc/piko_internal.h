@@ -286,6 +286,7 @@ struct TileArgs {
   long long gcap;               //   k_tile zeroes the next frame's parity
   unsigned prim_base;           // keys-only: added to the primID of every stored key (sort-last)
   int radix;                    // 1: the frame used the radix AssignBin (its look-back counters)
+  int skip_empty;               // 1: bins without pairs are not written (the deferred resolve knows them)
   Control* status_out;          // mapped host mirror: the last CTA copies the control block (null: none)
   int4* ovq;                    // [grid][OVQ_CAP][6] overflow of the per-bin queue (null: none)
   // P2P transport (sort-first): tile_keys points into rank 0's memory
@@ -322,6 +323,7 @@ struct ResolveArgs {            // rank 0 after the NCCL gather
   int nstatus;
   unsigned long long status_ok;
   Control* ctl;                          // rank 0: peer_overflow is raised here
+  const int32_t* bin_start;              // single-GPU deferred resolve: [NB+1] (empty bins: background) or null
 };
 
 // FreePipe variant (sec. 7.2.1): one fused

@@ -632,3 +632,26 @@ def test_async_overflow_reported_by_next_draw(env):
     got = {"rgba": r.rgba.cpu().numpy(), "depth": r.depth.cpu().numpy(), "primid": r.primid().cpu().numpy()}
     assert_frame_equal(got, ref, cov=False)
     r.close()
+
+
+@pytest.mark.parametrize("deferred", ["1", "0"])
+@pytest.mark.parametrize("cfg,bw", [("c1", 8), ("c2", 16), ("c3", 16), ("c2", 32)])
+def test_deferred_resolve_matches_oracle(env, cfg, bw, deferred, monkeypatch):
+    """Keys-only k_tile (empty bins skipped) + the one-pixel-per-thread deferred
+    resolve k_shade1 (background of empty bins from the CSR, lean O2 orientation
+    from the snapped corners) against the oracle, and the immediate write-back
+    beside it."""
+    monkeypatch.setenv("PIKO_DEFERRED", deferred)
+    s = scenes.make(cfg)
+    got = gpu_render(env, s, bw, cov=False, frames=2)
+    assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
+    assert_bins_equal(got, env, s, bw)
+
+
+def test_deferred_overflow_frame_is_background_then_exact(env, monkeypatch):
+    """An overflowing deferred frame (pair capacity) is reported and re-issued;
+    the final frame is exact."""
+    monkeypatch.setenv("PIKO_DEFERRED", "1")
+    s = scenes.scene_c2()
+    got = gpu_render(env, s, 8, cov=False, frames=1)  # 8-px bins: P = 418504 > the initial capacity
+    assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
