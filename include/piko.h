@@ -136,6 +136,23 @@ int piko_draw_host(piko_ctx *ctx, const float *h_verts, int64_t n_verts, const i
                    int32_t n_tris, const float mvp[16], const float light[3], float *h_rgba,
                    float *h_depth, void *stream);
 
+/* Pipelined end-to-end variant of piko_draw_host: returns once the frame's
+ * upload, draw and download are enqueued.  Two context-owned device staging
+ * slots alternate: the upload of frame k+1 (on an internal copy stream) runs
+ * while frame k draws on `stream` and frame k-1 downloads (on a second copy
+ * stream), so a sequence of calls is bound by the slowest of H2D, draw and
+ * D2H instead of their sum.  `stream` is ordered after this frame's download:
+ * synchronising it (or piko_finish) completes the frame.  The host buffers
+ * must stay valid, h_verts / h_idx unmodified and h_rgba / h_depth unread,
+ * until then; they must be pinned (cudaHostAlloc / cudaHostRegister / torch
+ * pin_memory) for the copies to be asynchronous (pageable memory still gives
+ * the right frame, synchronously).  Errors of the draw are asynchronous as
+ * for piko_draw in PIKO_SYNC_ASYNC mode (an overflowed frame is reported by a
+ * later call or by piko_finish; its staged image is the background).       */
+int piko_draw_host_async(piko_ctx *ctx, const float *h_verts, int64_t n_verts,
+                         const int32_t *h_idx, int32_t n_tris, const float mvp[16],
+                         const float light[3], float *h_rgba, float *h_depth, void *stream);
+
 /* Reyes micropolygon pipeline (sec. 5
  * "Reyes": Split -> Dice -> Sample -> Shade).  Draws n_patches bicubic Bezier
  * patches: Split/Dice on the device into a micropolygon mesh (DESIGN.md

@@ -24,7 +24,7 @@ PIKO_MULTI_SORT_FIRST, PIKO_MULTI_SORT_LAST = 0, 1
 PIKO_XPORT_NCCL, PIKO_XPORT_P2P = 0, 1
 
 # names of every symbol include/piko.h declares (checked by tests)
-EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_finish", "piko_set_sync",
+EXPORTS = ("piko_create", "piko_draw", "piko_draw_host", "piko_draw_host_async", "piko_finish", "piko_set_sync",
            "piko_destroy", "piko_last_error", "piko_get_primid", "piko_get_bins",
            "piko_set_debug", "piko_get_coverage", "piko_set_partition", "piko_attach_comm",
            "piko_get_stats", "piko_nccl_unique_id", "piko_draw_indexed",
@@ -60,6 +60,7 @@ def _load():
         "piko_create": ([I, I, I, I], P),
         "piko_draw": ([P, P, P, ctypes.c_int32, P, P, P, P, P], I),
         "piko_draw_host": ([P, P, I64, P, ctypes.c_int32, P, P, P, P, P], I),
+        "piko_draw_host_async": ([P, P, I64, P, ctypes.c_int32, P, P, P, P, P], I),
         "piko_draw_indexed": ([P, P, I64, P, ctypes.c_int32, P, P, P, P, P], I),
         "piko_draw_tile_keys": ([P, P, I64, P, ctypes.c_int32, P, P, P, P], I),
         "piko_resolve_keys": ([P, P, I64, P, ctypes.c_int32, P, P, I, P, P, P, P], I),
@@ -253,6 +254,27 @@ def piko_draw_host(ctx, verts, idx, mvp, light, out_rgba, out_depth, stream=None
                              ctypes.c_void_p(idx.data_ptr()), idx.shape[0], _f32x(mvp, 16),
                              _f32x(light, 3), ctypes.c_void_p(out_rgba.data_ptr()),
                              ctypes.c_void_p(out_depth.data_ptr()), _stream_ptr(stream))
+    return _check(ctx, rc)
+
+
+def piko_draw_host_async(ctx, verts, idx, mvp, light, out_rgba, out_depth, stream=None):
+    """Pipelined piko_draw_host: enqueues upload, draw and download and returns
+    (pinned CPU tensors; read the outputs after synchronising `stream` or
+    piko_finish).  Errors are asynchronous (reported by a later call / finish)."""
+    import torch
+    for t in (verts, idx, out_rgba, out_depth):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("piko_draw_host_async takes contiguous CPU tensors")
+    for t, dt, name in ((verts, torch.float32, "verts"), (idx, torch.int32, "idx"),
+                        (out_rgba, torch.float32, "out_rgba"), (out_depth, torch.float32, "out_depth")):
+        if t.dtype != dt:
+            raise ValueError(f"{name} must be {dt}")
+    _check_scene(verts, idx)
+    _check_outputs(ctx, out_rgba, out_depth)
+    rc = _lib.piko_draw_host_async(ctx, ctypes.c_void_p(verts.data_ptr()), verts.shape[0],
+                                   ctypes.c_void_p(idx.data_ptr()), idx.shape[0], _f32x(mvp, 16),
+                                   _f32x(light, 3), ctypes.c_void_p(out_rgba.data_ptr()),
+                                   ctypes.c_void_p(out_depth.data_ptr()), _stream_ptr(stream))
     return _check(ctx, rc)
 
 

@@ -575,7 +575,10 @@ __device__ __forceinline__ void cl_publish(const SetupArgs& a, K1Smem& sm, const
 }
 
 template <bool FUSED>
-__global__ void __launch_bounds__(K1_THREADS, 3) k_setup(SetupArgs a) {
+#ifndef PIKO_K1_MINB
+#define PIKO_K1_MINB 3
+#endif
+__global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a) {
   extern __shared__ __align__(16) unsigned char k1_dyn[];
   K1Smem& sm1 = *reinterpret_cast<K1Smem*>(k1_dyn);
   unsigned (&s_hist)[MAX_PASSES][RX_RADIX] = sm1.hist;

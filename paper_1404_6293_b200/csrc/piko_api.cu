@@ -150,6 +150,18 @@ struct piko_ctx {
   long long* h_dice_total = nullptr;      // pinned [2]
   long long dice_V = 0, dice_T = 0;
 
+  // pipelined end-to-end staging (piko_draw_host_async): two slots, an upload
+  // and a download stream; a slot is reused once its previous frame is drawn
+  struct HostSlot {
+    float* verts = nullptr; long long vcap = 0;
+    int32_t* idx = nullptr; long long icap = 0;
+    float* rgba = nullptr; float* depth = nullptr;
+    cudaEvent_t in_done = nullptr, frame_done = nullptr, out_done = nullptr;
+    bool used = false;
+  };
+  HostSlot hs[2];
+  int hs_next = 0;
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
   // end-to-end staging
   float* d_verts = nullptr; long long d_verts_cap = 0;
   int32_t* d_idx = nullptr; long long d_idx_cap = 0;
@@ -345,6 +357,16 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
     if (sl.ev) cudaEventDestroy(sl.ev);
   }
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto& h : ctx->hs) {
+    if (h.out_done) cudaEventSynchronize(h.out_done);
+    void* hb[] = {h.verts, h.idx, h.rgba, h.depth};
+    for (void* p : hb)
+      if (p) cudaFree(p);
+    for (cudaEvent_t e : {h.in_done, h.frame_done, h.out_done})
+      if (e) cudaEventDestroy(e);
+  }
+  if (ctx->cs_in) cudaStreamDestroy(ctx->cs_in);
+  if (ctx->cs_out) cudaStreamDestroy(ctx->cs_out);
   delete ctx;
 }
 
@@ -1068,7 +1090,7 @@ static int validate_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, 
 
 static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32_t* idx,
                      int32_t n_tris, const float mvp[16], const float light[3], float* rgba,
-                     float* depth, cudaStream_t s, bool force_check,
+                     float* depth, cudaStream_t s, bool force_check, bool force_async,
                      unsigned long long* keys_out = nullptr) {
   float L[3] = {0.0f, 0.0f, 0.0f};
   int rc = validate_draw(ctx, verts, idx, n_tris, mvp, light, rgba, depth, L);
@@ -1098,7 +1120,7 @@ static int draw_impl(piko_ctx* ctx, const float* verts, long long V, const int32
   for (int attempt = 0; attempt < 3; ++attempt) {
     if ((rc = enqueue_frame(ctx, verts, V, idx, n_tris, M, L, rgba, depth, s, keys_out)) != PIKO_OK)
       return frame_failed(ctx, rc);
-    if (ctx->sync_mode == PIKO_SYNC_ASYNC && !force_check) {
+    if ((ctx->sync_mode == PIKO_SYNC_ASYNC || force_async) && !force_check) {
       // enqueued; report (once) an error of an earlier frame
       const int st = ctx->sticky;
       ctx->sticky = PIKO_OK;
@@ -1120,7 +1142,7 @@ extern "C" int piko_draw(piko_ctx* ctx, const float* verts, const int32_t* idx, 
                          float* out_depth, void* stream) {
   if (!ctx) return PIKO_EINVAL;
   return draw_impl(ctx, verts, -1, idx, n_tris, mvp, light, out_rgba, out_depth,
-                   static_cast<cudaStream_t>(stream), false);
+                   static_cast<cudaStream_t>(stream), false, false);
 }
 
 extern "C" int piko_draw_indexed(piko_ctx* ctx, const float* verts, int64_t n_verts,
@@ -1130,7 +1152,7 @@ extern "C" int piko_draw_indexed(piko_ctx* ctx, const float* verts, int64_t n_ve
   if (!ctx) return PIKO_EINVAL;
   if (n_verts < 0 || (n_tris > 0 && n_verts < 1)) return ctx->fail(PIKO_EINVAL, "bad n_verts");
   return draw_impl(ctx, verts, n_verts, idx, n_tris, mvp, light, out_rgba, out_depth,
-                   static_cast<cudaStream_t>(stream), false);
+                   static_cast<cudaStream_t>(stream), false, false);
 }
 
 extern "C" int piko_draw_host(piko_ctx* ctx, const float* h_verts, int64_t n_verts,
@@ -1164,7 +1186,7 @@ extern "C" int piko_draw_host(piko_ctx* ctx, const float* h_verts, int64_t n_ver
   if (n_tris > 0)
     CK(cudaMemcpyAsync(ctx->d_idx, h_idx, sizeof(int32_t) * 3 * (size_t)n_tris, cudaMemcpyHostToDevice, s));
   int rc = draw_impl(ctx, ctx->d_verts, n_verts, ctx->d_idx, n_tris, mvp, light, ctx->d_rgba,
-                     ctx->d_depth, s, true);
+                     ctx->d_depth, s, true, false);
   if (rc != PIKO_OK) return rc;
   const bool has_out = !(exchanging(ctx) && ctx->mrank != 0);
   if (has_out) {
@@ -1173,6 +1195,68 @@ extern "C" int piko_draw_host(piko_ctx* ctx, const float* h_verts, int64_t n_ver
   }
   CK(cudaStreamSynchronize(s));
   return PIKO_OK;
+}
+
+extern "C" int piko_draw_host_async(piko_ctx* ctx, const float* h_verts, int64_t n_verts,
+                                    const int32_t* h_idx, int32_t n_tris, const float mvp[16],
+                                    const float light[3], float* h_rgba, float* h_depth, void* stream) {
+  if (!ctx) return PIKO_EINVAL;
+  if (n_verts < 0 || n_tris < 0) return ctx->fail(PIKO_EINVAL, "negative size");
+  if (n_tris > 0 && (!h_verts || !h_idx)) return ctx->fail(PIKO_EINVAL, "null host scene buffer");
+  if (!h_rgba || !h_depth) return ctx->fail(PIKO_EINVAL, "null host output buffer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->cs_in) {
+    CK(cudaStreamCreateWithFlags(&ctx->cs_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->cs_out, cudaStreamNonBlocking));
+  }
+  piko_ctx::HostSlot& h = ctx->hs[ctx->hs_next];
+  ctx->hs_next ^= 1;
+  const size_t npx = (size_t)ctx->g.W * ctx->g.H;
+  if (!h.in_done) {
+    CK(cudaEventCreateWithFlags(&h.in_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h.frame_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h.out_done, cudaEventDisableTiming));
+    CK(cudaMalloc(&h.rgba, sizeof(float) * 4 * npx));
+    CK(cudaMalloc(&h.depth, sizeof(float) * npx));
+  }
+  if (n_verts > h.vcap || n_tris > h.icap) {  // grow: the slot's last frame must be done with it
+    if (h.used) CK(cudaEventSynchronize(h.out_done));
+    if (n_verts > h.vcap) {
+      if (h.verts) cudaFree(h.verts);
+      h.verts = nullptr;
+      CK(cudaMalloc(&h.verts, sizeof(float) * 8 * std::max<int64_t>(n_verts, 1)));
+      h.vcap = n_verts;
+    }
+    if (n_tris > h.icap) {
+      if (h.idx) cudaFree(h.idx);
+      h.idx = nullptr;
+      CK(cudaMalloc(&h.idx, sizeof(int32_t) * 3 * std::max<int32_t>(n_tris, 1)));
+      h.icap = n_tris;
+    }
+  }
+  // upload (after the slot's previous frame has read its inputs)
+  if (h.used) CK(cudaStreamWaitEvent(ctx->cs_in, h.frame_done, 0));
+  if (n_verts > 0)
+    CK(cudaMemcpyAsync(h.verts, h_verts, sizeof(float) * 8 * n_verts, cudaMemcpyHostToDevice, ctx->cs_in));
+  if (n_tris > 0)
+    CK(cudaMemcpyAsync(h.idx, h_idx, sizeof(int32_t) * 3 * (size_t)n_tris, cudaMemcpyHostToDevice, ctx->cs_in));
+  CK(cudaEventRecord(h.in_done, ctx->cs_in));
+  // draw on the caller's stream (enqueue only)
+  CK(cudaStreamWaitEvent(s, h.in_done, 0));
+  const int rc = draw_impl(ctx, h.verts, n_verts, h.idx, n_tris, mvp, light, h.rgba, h.depth, s, false, true);
+  CK(cudaEventRecord(h.frame_done, s));
+  // download; the caller's stream then orders after it (its sync covers the frame)
+  const bool has_out = !(exchanging(ctx) && ctx->mrank != 0);
+  CK(cudaStreamWaitEvent(ctx->cs_out, h.frame_done, 0));
+  if (has_out) {
+    CK(cudaMemcpyAsync(h_rgba, h.rgba, sizeof(float) * 4 * npx, cudaMemcpyDeviceToHost, ctx->cs_out));
+    CK(cudaMemcpyAsync(h_depth, h.depth, sizeof(float) * npx, cudaMemcpyDeviceToHost, ctx->cs_out));
+  }
+  CK(cudaEventRecord(h.out_done, ctx->cs_out));
+  CK(cudaStreamWaitEvent(s, h.out_done, 0));
+  h.used = true;
+  return rc;
 }
 
 // Reyes: Split + Dice on the device into
@@ -1231,7 +1315,7 @@ extern "C" int piko_draw_patches(piko_ctx* ctx, const float* patches, int32_t n_
   d.verts = ctx->dice_verts; d.idx = ctx->dice_idx;
   CK(launch_dice(d, s));
   ctx->dice_V = V; ctx->dice_T = T;
-  return draw_impl(ctx, ctx->dice_verts, V, ctx->dice_idx, (int32_t)T, mvp, light, out_rgba, out_depth, s, false);
+  return draw_impl(ctx, ctx->dice_verts, V, ctx->dice_idx, (int32_t)T, mvp, light, out_rgba, out_depth, s, false, false);
 }
 
 extern "C" int piko_get_diced(const piko_ctx* ctx, const float** d_verts, int64_t* n_verts,
@@ -1514,7 +1598,7 @@ extern "C" int piko_draw_tile_keys(piko_ctx* ctx, const float* verts, int64_t n_
   if (n_verts < 0 || (n_tris > 0 && n_verts < 1)) return ctx->fail(PIKO_EINVAL, "bad n_verts");
   ctx->keys_mode = true;
   const int rc = draw_impl(ctx, verts, n_verts, idx, n_tris, mvp, light, nullptr, nullptr,
-                           static_cast<cudaStream_t>(stream), false,
+                           static_cast<cudaStream_t>(stream), false, false,
                            reinterpret_cast<unsigned long long*>(d_tile_keys));
   ctx->keys_mode = false;
   return rc;

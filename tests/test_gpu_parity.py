@@ -296,6 +296,37 @@ def test_draw_host_e2e_matches_device_path(env):
     r.close()
 
 
+def test_draw_host_async_pipelined_frames(env):
+    """piko_draw_host_async: six frames of two alternating views (so a slot or
+    stream mix-up shows) enqueued back to back into six pinned host buffers,
+    then one synchronisation -- every frame bit-exact vs the oracle (c2 first
+    draws once synchronously so the pair capacity is settled)."""
+    piko, _, torch = env
+    s = scenes.scene_c2()
+    views = [s.mvp, (np.asarray(s.mvp, np.float32).reshape(4, 4) @ np.diag([1.0, 1.0, 1.0, 1.0]).astype(np.float32)
+                     @ np.array([[1, 0, 0, 0.3], [0, 1, 0, 0], [0, 0, 1, 0], [0, 0, 0, 1]], np.float32)).reshape(-1)]
+    r = piko.Renderer(s.W, s.H, 16)
+    hv = torch.from_numpy(s.verts).pin_memory()
+    hi = torch.from_numpy(s.idx).pin_memory()
+    rgba0 = torch.empty((s.H, s.W, 4), dtype=torch.float32).pin_memory()
+    depth0 = torch.empty((s.H, s.W), dtype=torch.float32).pin_memory()
+    piko.piko_draw_host(r.ctx, hv, hi, s.mvp, s.light, rgba0, depth0)
+    outs = [(torch.empty((s.H, s.W, 4), dtype=torch.float32).pin_memory(),
+             torch.empty((s.H, s.W), dtype=torch.float32).pin_memory()) for _ in range(6)]
+    st = torch.cuda.current_stream()
+    for k, (rgba, depth) in enumerate(outs):
+        assert piko.piko_draw_host_async(r.ctx, hv, hi, views[k % 2], s.light, rgba, depth, st) == 0
+    st.synchronize()
+    assert piko.piko_finish(r.ctx) == 0
+    for v in range(2):
+        ref = env[1].render(s.verts, s.idx, np.asarray(views[v], np.float32), s.light, s.W, s.H)
+        for k in range(v, 6, 2):
+            rgba, depth = outs[k]
+            assert np.array_equal(depth.numpy().view(np.uint32), ref["depth"].view(np.uint32)), (v, k)
+            assert np.abs(rgba.numpy() - ref["rgba"]).max() <= RGB_TOL
+    r.close()
+
+
 def test_argument_validation(env):
     piko, _, torch = env
     s = scenes.scene_c1()
