@@ -632,31 +632,28 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
     const long long t = t0 + tid + k * K1_THREADS;
     const bool in = t < a.n_tris;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      vi[k][c] = in ? sidx[3 * (tid + k * K1_THREADS) + c] : -1;
-      if (!FUSED && vi[k][c] >= a.xv_cap) vi[k][c] = -1;  // overflowed frame: stay in bounds
-    }
+    for (int c = 0; c < 3; ++c) vi[k][c] = in ? sidx[3 * (tid + k * K1_THREADS) + c] : 0;
   }
+  // corner loads without predication: slots past n_tris (skipped below) load
+  // vertex 0; an index past the vertex records (an overflowed frame, reported
+  // and discarded) is clamped in bounds
   int4 cv[K1_TPT][3];
   if constexpr (FUSED) {
     float4 pp[K1_TPT][3];
 #pragma unroll
     for (int k = 0; k < K1_TPT; ++k)
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        pp[k][c] = vi[k][c] >= 0 ? load_pos(a.verts, vi[k][c]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < 3; ++c) pp[k][c] = load_pos(a.verts, max(vi[k][c], 0));
 #pragma unroll
     for (int k = 0; k < K1_TPT; ++k)
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        cv[k][c] = vi[k][c] >= 0 ? transform_vertex(pp[k][c], a.M, g.W, g.H)
-                                 : make_int4(VX_CULLED, 0, 0, 0);
+      for (int c = 0; c < 3; ++c) cv[k][c] = transform_vertex(pp[k][c], a.M, g.W, g.H);
   } else {
+    const unsigned vlast = (unsigned)(a.xv_cap - 1);
 #pragma unroll
     for (int k = 0; k < K1_TPT; ++k)
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        cv[k][c] = vi[k][c] >= 0 ? __ldg(a.xv + vi[k][c]) : make_int4(VX_CULLED, 0, 0, 0);
+      for (int c = 0; c < 3; ++c) cv[k][c] = __ldg(a.xv + min((unsigned)vi[k][c], vlast));
   }
   K1_MARK(1);
 
