@@ -634,16 +634,18 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
 #pragma unroll
     for (int c = 0; c < 3; ++c) vi[k][c] = in ? sidx[3 * (tid + k * K1_THREADS) + c] : 0;
   }
-  // corner loads without predication: slots past n_tris (skipped below) load
-  // vertex 0; an index past the vertex records (an overflowed frame, reported
+  // corner loads predicated per slot only (slots past n_tris are skipped
+  // below); an index past the vertex records (an overflowed frame, reported
   // and discarded) is clamped in bounds
   int4 cv[K1_TPT][3];
   if constexpr (FUSED) {
     float4 pp[K1_TPT][3];
 #pragma unroll
-    for (int k = 0; k < K1_TPT; ++k)
+    for (int k = 0; k < K1_TPT; ++k) {
+      const bool in = t0 + tid + k * K1_THREADS < a.n_tris;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) pp[k][c] = load_pos(a.verts, max(vi[k][c], 0));
+      for (int c = 0; c < 3; ++c) pp[k][c] = in ? load_pos(a.verts, vi[k][c]) : make_float4(0.f, 0.f, 0.f, 1.f);
+    }
 #pragma unroll
     for (int k = 0; k < K1_TPT; ++k)
 #pragma unroll
@@ -651,9 +653,12 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
   } else {
     const unsigned vlast = (unsigned)(a.xv_cap - 1);
 #pragma unroll
-    for (int k = 0; k < K1_TPT; ++k)
+    for (int k = 0; k < K1_TPT; ++k) {
+      const bool in = t0 + tid + k * K1_THREADS < a.n_tris;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) cv[k][c] = __ldg(a.xv + min((unsigned)vi[k][c], vlast));
+      for (int c = 0; c < 3; ++c)
+        cv[k][c] = in ? __ldg(a.xv + min((unsigned)vi[k][c], vlast)) : make_int4(VX_CULLED, 0, 0, 0);
+    }
   }
   K1_MARK(1);
 
@@ -735,7 +740,7 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
   if (chunk == 0 && tid == 0) {
     a.ctl->frame = frame; a.ctl->tile_next = 0; a.ctl->vmax = 0;
     for (int k = 0; k < NLIST; ++k) a.ctl->list_n[k] = 0;
-    a.ctl->empty_next = 0;
+    a.ctl->empty_next = 0; a.ctl->eq_next = 0;
     if (a.ctl->vx_overflow) { a.ctl->vx_overflow = 0; atomicMax(&a.ctl->overflow_tag, frame + 1); }
   }
   // large triangles: the whole CTA walks their bins
@@ -2428,6 +2433,44 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   const int fwd = a.sc.forward ? a.sc.iters : 0;  // forward shader cost per fragment
   float facc = 0.0f;
   TL_CTA(3);  // resident
+  // ---- bins without pairs: background.  One ticket queue over all bins
+  // (EMPTY_TICKET bins per CTA ticket, a warp takes EMPTY_TICKET/warps of
+  // them); a bin is written iff it is owned and its pair count is 0.  With
+  // early_empty the CTAs resident before the dependency wait already drain it:
+  // the counts are final (k_cm_scan, two launches back, completed before the
+  // scatter passed its own wait and triggered this launch), the empty bins are
+  // never touched by the pair items, and the previous frame's k_tile is
+  // complete -- so the background overlaps the scatter instead of trailing
+  // the heavy bins.
+  constexpr int EB_WARP = 4;                        // bins per warp per ticket
+  constexpr int EMPTY_TICKET = EB_WARP * (THREADS / 32);
+  __shared__ unsigned s_etk;
+  auto empty_pass = [&]() {
+    for (;;) {
+      if (tid == 0) s_etk = atomicAdd(&a.ctl->eq_next, 1u);
+      __syncthreads();
+      const long long b0 = (long long)s_etk * EMPTY_TICKET + warp * EB_WARP;
+      const bool done = (long long)s_etk * EMPTY_TICKET >= g.NB;
+      __syncthreads();
+      if (done) break;
+      const long long bl = b0 + (lane & (EB_WARP - 1));
+      const bool mine = lane < EB_WARP && bl < g.NB && (g.nranks == 1 || (int)(bl % g.nranks) == g.rank) &&
+                        __ldcg(a.bin_count + bl) == 0u;
+      const unsigned em = __ballot_sync(0xffffffffu, mine);
+      for (unsigned m = em; m; m &= m - 1) {
+        const int b = (int)(b0 + __ffs(m) - 1);
+        const int x0 = (b % g.binsX) * BW, y0 = (b / g.binsX) * BH;
+        const int x1 = min(x0 + BW, g.W) - 1, y1 = min(y0 + BH, g.H) - 1;
+        const int job = (b - g.rank) / g.nranks;
+        for (int p = lane; p < NPX; p += 32) {
+          const int x = x0 + (p % BW), y = y0 + (p / BW);
+          if (!KEYS_ONLY && (x > x1 || y > y1)) continue;
+          store_pixel<COV, KEYS_ONLY>(a, L, job, p, NPX, x, y, CLEAR_KEY, 0u);
+        }
+      }
+    }
+  };
+  if (a.early_empty) empty_pass();
   pdl_wait();
   pdl_trigger();
 #ifdef PIKO_EXP_NOTILE
@@ -2905,10 +2948,11 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   // every warp pulls groups of EMPTY_GROUP bins from a second queue
   // (one queue ticket per CTA for THREADS/32 groups: per-warp tickets on one
   // address serialised at L2)
-  __shared__ unsigned s_etk;
 #ifdef PIKO_EXP_NOEMPTY
   if (false)
 #endif
+  if (a.early_empty && !ovf) empty_pass();  // what the early CTAs left of the same queue
+  else
   for (;;) {
     __syncthreads();
     if (tid == 0) s_etk = atomicAdd(&a.ctl->empty_next, 1u);

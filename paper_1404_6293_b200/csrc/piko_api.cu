@@ -185,6 +185,7 @@ struct piko_ctx {
   bool last_cm = false;                     // the last frame used the count matrix
   long long last_cm_rows = 0;
   // chunk-list AssignBin (NB <= CL_MAX_NB; the default where it applies)
+  int early_empty = 1;                      // PIKO_EARLY_EMPTY=0: empty bins after the pair items
   int cl_mode = 0;                          // 0 off (default: slower on c2/c3), 1 on where it applies
   bool cl_off = false;                      // a chunk overflowed CL_WIN: count matrix from now on
   bool last_cl = false;                     // the last frame used the chunk lists
@@ -325,6 +326,7 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   if (const char* e = getenv("PIKO_DEFERRED")) ctx->deferred = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_CM")) ctx->cm_mode = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_CL")) ctx->cl_mode = e[0] == '0' ? 0 : 1;
+  if (const char* e = getenv("PIKO_EARLY_EMPTY")) ctx->early_empty = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_TILE_GRID")) ctx->tile_items_grid = strcmp(e, "items") == 0;
   if (const char* e = getenv("PIKO_CM_TC_LOG2")) ctx->cm_tc_log2 = atoi(e);
   return ctx;
@@ -897,6 +899,9 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.prim_base = (unsigned)ctx->prim_base;
     a.radix = sorted_here ? 0 : 1;
     a.skip_empty = defer && ctx->g.NB > 1 ? 1 : 0;
+    // the counts are final two launches before k_tile in count-matrix frames
+    a.early_empty = cm && !keys_only && ctx->early_empty ? 1 : 0;
+    a.bin_count = ctx->bin_count;
     if (!gather) CK(reserve_slot(ctx, &a.status_out));  // the tile kernel ends the frame's control updates
     if (keys_only) a.out_cov = nullptr;
     // persistent grid (all CTAs resident, items from the queue) or, with

@@ -87,6 +87,7 @@ struct Control {  // (the mirror copies whole 8-byte words up to digit_hist: kee
   unsigned int tile_next;              // dynamic bin queue of k_tile (reset by K1 chunk 0)
   unsigned int list_n[NLIST];          // work-list sizes (reset by K1 chunk 0)
   unsigned int empty_next;             // k_tile queue of empty-bin groups (reset by K1 chunk 0)
+  unsigned int eq_next;                // k_tile ticket queue over all bins for the empty ones (reset by K1 chunk 0)
   unsigned int vmax;                   // max(idx)+1 from k_index_max (zeroed by K1 chunk 0)
   unsigned int vx_overflow;            // k_vertex: vmax > xv capacity (K1 turns it into overflow_tag)
   unsigned long long vx_need;          // vertex count the last frame needed
@@ -287,6 +288,9 @@ struct TileArgs {
   unsigned prim_base;           // keys-only: added to the primID of every stored key (sort-last)
   int radix;                    // 1: the frame used the radix AssignBin (its look-back counters)
   int skip_empty;               // 1: bins without pairs are not written (the deferred resolve knows them)
+  int early_empty;              // 1: empty bins (bin_count == 0) from one ticket queue, drained first by
+                                //    the CTAs resident before the dependency wait (count-matrix frames)
+  const uint32_t* bin_count;    // [NB] pair counts (early_empty)
   Control* status_out;          // mapped host mirror: the last CTA copies the control block (null: none)
   int4* ovq;                    // [grid][OVQ_CAP][6] overflow of the per-bin queue (null: none)
   // P2P transport (sort-first): tile_keys points into rank 0's memory
