@@ -589,8 +589,8 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
   const int tid = threadIdx.x;
   const Grid g = a.g;
 
-  pdl_wait();   // k_vertex output; the previous frame's kernels read rec / rect
-  pdl_trigger();
+  // (the index loads below read only the caller's input: they are issued
+  // before the dependency wait, so CTAs resident early overlap k_vertex)
   // every CTA takes one ticket per frame: frame = ticket / gridDim.x (the
   // triangle chunk is simply blockIdx.x -- nothing here depends on CTA order)
   const long long chunk = blockIdx.x;
@@ -623,6 +623,8 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
   if (cl)
     for (int i = tid; i < ((g.NB + 31) >> 5); i += K1_THREADS) sm1.bm[i] = 0u;
   if (tid == 0) { s_tk = tk / gridDim.x; s_live = 0; s_nbig = 0; }
+  pdl_wait();   // k_vertex output; the previous frame's kernels read rec / rect / the count matrix
+  pdl_trigger();
   __syncthreads();  // indices staged; histogram cleared; frame known
   const u64 frame = s_tk;
   int vi[K1_TPT][3];
