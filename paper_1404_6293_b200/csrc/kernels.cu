@@ -2480,6 +2480,17 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
 #endif
   const u64 frame = a.ctl->frame;
   const bool ovf = a.ctl->overflow_tag == frame + 1;
+  if (a.status_out && blockIdx.x == 0 && tid < 32) {
+    // the frame's control block (P, overflow tags, statistics) straight into
+    // the host's pinned mirror: every field the host reads is final once the
+    // AssignBin kernels are complete (this wait), so CTA 0 writes it here and
+    // the PCIe writes drain under the tile work instead of trailing it (no
+    // device-to-host copy on the stream, no last-CTA detection)
+    constexpr int NW = (int)(offsetof(Control, digit_hist) / sizeof(u64));
+    const volatile u64* src = reinterpret_cast<const volatile u64*>(a.ctl);
+    u64* dst = reinterpret_cast<u64*>(a.status_out);
+    for (int w = tid; w < NW; w += 32) dst[w] = src[w];
+  }
   if (KEYS_ONLY && a.p2p_done) {  // P2P: rank 0 has finished reading this key slot
     if (tid == 0) p2p_wait_geq(a.p2p_done, (long long)a.epoch - 2, &a.ctl->p2p_timeout);
     __syncthreads();
@@ -2978,22 +2989,6 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   }
   TL_CTA(2);
   if (fwd) shader_sink(a.sc, facc);
-  if (a.status_out) {
-    // the frame's control block (P, overflow tags, statistics -- final: the
-    // kernels that write them are complete) straight into the host's pinned
-    // mirror by the last CTA: no device-to-host copy on the stream
-    __shared__ int s_mlast;
-    __syncthreads();
-    if (tid == 0) s_mlast = (atomicAdd(&a.ctl->tile_done, 1ull) + 1) % gridDim.x == 0;
-    __syncthreads();
-    if (s_mlast) {
-      __threadfence();
-      constexpr int NW = (int)(offsetof(Control, digit_hist) / sizeof(u64));
-      const volatile u64* src = reinterpret_cast<const volatile u64*>(a.ctl);
-      u64* dst = reinterpret_cast<u64*>(a.status_out);
-      for (int w = tid; w < NW; w += THREADS) dst[w] = src[w];
-    }
-  }
   if (KEYS_ONLY && a.p2p_flag) {
     // P2P: every CTA's key stores (straight into rank 0's memory over NVLink)
     // are made visible system-wide before it is counted; the last CTA counted

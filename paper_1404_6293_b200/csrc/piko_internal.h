@@ -99,7 +99,7 @@ struct Control {  // (the mirror copies whole 8-byte words up to digit_hist: kee
   unsigned int p2p_timeout;            // a peer flag wait timed out (sticky)
   unsigned int cl_overflow;            // a bin had more than CLB_ENT chunks / CLB_GRP groups (host: count matrix)
   unsigned long long peer_overflow;    // rank 0: frame+1 of a frame in which a peer rank overflowed
-  unsigned long long tile_done;        // k_tile CTA tickets (modulo grid: the last one mirrors this block)
+  unsigned long long tile_done;        // (unused since k_tile CTA 0 writes the host mirror at its start)
   unsigned int digit_hist[2][MAX_PASSES][RX_RADIX];  // parity double buffer
 };
 
