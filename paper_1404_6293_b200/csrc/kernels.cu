@@ -3476,7 +3476,10 @@ cudaError_t launch_vertex(const VertexArgs& a, bool pdl, cudaStream_t s) {
 
 cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool pdl, cudaStream_t s) {
   // a few int4 loads in flight per thread: about 2 waves of CTAs
-  const long long want = std::min<long long>((n / 4 + 255) / 256, 4ll * sm_count());
+#ifndef PIKO_IMAX_CTAS_PER_SM
+#define PIKO_IMAX_CTAS_PER_SM 4
+#endif
+  const long long want = std::min<long long>((n / 4 + 255) / 256, (long long)PIKO_IMAX_CTAS_PER_SM * sm_count());
   return launch_ex(k_index_max, (int)(want > 0 ? want : 1), 256, 0, pdl, s, idx, n, ctl);
 }
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s) {
