@@ -3483,12 +3483,15 @@ cudaError_t launch_index_max(const int32_t* idx, long long n, Control* ctl, bool
   return launch_ex(k_index_max, (int)(want > 0 ? want : 1), 256, 0, pdl, s, idx, n, ctl);
 }
 cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s) {
+  // the chunk-list arrays (the tail of K1Smem from bm on) only in chunk-list
+  // frames: otherwise the smaller carve-out leaves the L1 to the corner gathers
   // (set per launch: the attribute belongs to the current device's context)
-  cudaError_t e = a.xv ? cudaFuncSetAttribute(k_setup<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem))
-                       : cudaFuncSetAttribute(k_setup<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem));
+  const size_t smem = a.cl_ent ? sizeof(K1Smem) : offsetof(K1Smem, bm);
+  cudaError_t e = a.xv ? cudaFuncSetAttribute(k_setup<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                       : cudaFuncSetAttribute(k_setup<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (!a.xv) return launch_ex(k_setup<true>, grid, K1_THREADS, sizeof(K1Smem), pdl, s, a);
-  return launch_ex(k_setup<false>, grid, K1_THREADS, sizeof(K1Smem), pdl, s, a);
+  if (!a.xv) return launch_ex(k_setup<true>, grid, K1_THREADS, smem, pdl, s, a);
+  return launch_ex(k_setup<false>, grid, K1_THREADS, smem, pdl, s, a);
 }
 cudaError_t launch_radix_pass(const RadixArgs& a, int grid, bool pdl, cudaStream_t s) {
   if (a.expand) {
