@@ -394,9 +394,15 @@ constexpr int K1_BIG = 64;  // triangles with more owned bins go to the CTA-wide
 // indices, the radix digit histograms and the large-triangle list, and the
 // chunk-list AssignBin's touched-bin bitmap and per-touched-bin arrays.
 struct K1Smem {
-  int4 idx[K1_CHUNK * 3 / 4];
-  unsigned hist[MAX_PASSES][RX_RADIX];
-  uint2 big[K1_CHUNK];
+  union {                             // the staged indices are consumed before the main loop
+    int4 idx[K1_CHUNK * 3 / 4];
+    struct {
+      uint2 big[K1_CHUNK];
+      unsigned hist[MAX_PASSES][RX_RADIX];
+    } rx;
+  } u;
+  // (launches in count-matrix / radix frames allocate only the union: the small
+  // carve-out leaves the L1 to the corner gathers)
   unsigned char bigg[K1_CHUNK];       // chunk-list mode: group of a listed triangle
   uint2 mrect[K1_CHUNK];              // chunk-list: rect of slot k*K1_THREADS + tid if it owns 2..K1_BIG bins
   unsigned bm[CL_MAX_NB / 32];        // chunk-list: bins touched by the chunk
@@ -460,7 +466,7 @@ __device__ __forceinline__ void cl_pairs(K1Smem& sm, const int (&bin1)[K1_TPT], 
   }
   // larger ones: the whole CTA walks their bins
   for (unsigned q = 0; q < nbig; ++q) {
-    const uint2 rr = sm.big[q];
+    const uint2 rr = sm.u.rx.big[q];
     const int tx0 = rr.x & 0xffff, ty0 = rr.x >> 16, tx1 = rr.y & 0xffff, ty1 = rr.y >> 16;
     const unsigned c = owned_in_rect(tx0, ty0, tx1, ty1, g);
     for (unsigned j = tid; j < c; j += K1_THREADS) {
@@ -581,8 +587,8 @@ template <bool FUSED>
 __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a) {
   extern __shared__ __align__(16) unsigned char k1_dyn[];
   K1Smem& sm1 = *reinterpret_cast<K1Smem*>(k1_dyn);
-  unsigned (&s_hist)[MAX_PASSES][RX_RADIX] = sm1.hist;
-  uint2 (&s_big)[K1_CHUNK] = sm1.big;
+  unsigned (&s_hist)[MAX_PASSES][RX_RADIX] = sm1.u.rx.hist;
+  uint2 (&s_big)[K1_CHUNK] = sm1.u.rx.big;
   __shared__ unsigned s_nbig;
   __shared__ u64 s_tk;
   __shared__ unsigned s_live;
@@ -599,7 +605,7 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
   // ---- the chunk's indices: 16-byte coalesced loads staged in shared memory
   // (12 consecutive ints per 4 triangles; t0 is a multiple of K1_CHUNK and idx
   // is 16-byte aligned), issued together with the frame ticket --------------
-  int4 (&s_idx)[K1_CHUNK * 3 / 4] = sm1.idx;
+  int4 (&s_idx)[K1_CHUNK * 3 / 4] = sm1.u.idx;
   const u64 tk = a.frame * gridDim.x;  // (host frame counter: no same-address atomic burst)
   {
     const long long nint = 3 * (min((long long)K1_CHUNK, a.n_tris - t0));
@@ -618,7 +624,6 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
 #pragma unroll
     for (int k = 0; k < 3; ++k) s_idx[tid + k * K1_THREADS] = q[k];
   }
-  for (int i = tid; i < a.npass * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
   const bool cl = a.cl_ent != nullptr;  // chunk-list AssignBin (CTA-uniform)
   if (cl)
     for (int i = tid; i < ((g.NB + 31) >> 5); i += K1_THREADS) sm1.bm[i] = 0u;
@@ -635,6 +640,12 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
     const bool in = t < a.n_tris;
 #pragma unroll
     for (int c = 0; c < 3; ++c) vi[k][c] = in ? sidx[3 * (tid + k * K1_THREADS) + c] : 0;
+  }
+  // the index space now holds the large-triangle list and the digit histograms
+  __syncthreads();
+  if (a.npass > 0) {
+    for (int i = tid; i < a.npass * RX_RADIX; i += K1_THREADS) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
   }
   // corner loads predicated per slot only (slots past n_tris are skipped
   // below); an index past the vertex records (an overflowed frame, reported
@@ -723,7 +734,7 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
         } else {
           const unsigned q = atomicAdd(&s_nbig, 1u);
           s_big[q] = rr;
-          sm1.bigg[q] = (unsigned char)(k * (K1_THREADS / 32) + warp);
+          if (cl) sm1.bigg[q] = (unsigned char)(k * (K1_THREADS / 32) + warp);  // (tail: chunk-list launches only)
         }
       }
     }
@@ -3486,7 +3497,7 @@ cudaError_t launch_setup(const SetupArgs& a, int grid, bool pdl, cudaStream_t s)
   // the chunk-list arrays (the tail of K1Smem from bm on) only in chunk-list
   // frames: otherwise the smaller carve-out leaves the L1 to the corner gathers
   // (set per launch: the attribute belongs to the current device's context)
-  const size_t smem = a.cl_ent ? sizeof(K1Smem) : offsetof(K1Smem, bm);
+  const size_t smem = a.cl_ent ? sizeof(K1Smem) : offsetof(K1Smem, bigg);
   cudaError_t e = a.xv ? cudaFuncSetAttribute(k_setup<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                        : cudaFuncSetAttribute(k_setup<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
