@@ -2381,7 +2381,10 @@ struct BigQueue {
 template <int BW, int BH, int THREADS>
 struct TileSmem {
   static constexpr int NPX = BW * BH;
-  static constexpr int BIGQ = THREADS;  // queued per bin (overflow: warp-cooperative path)
+#ifndef PIKO_BIGQ_DIV
+#define PIKO_BIGQ_DIV 1
+#endif
+  static constexpr int BIGQ = THREADS / PIKO_BIGQ_DIV;  // queued per bin (overflow: spill region, then warp-cooperative)
   u64 key[NPX];
   int4 rec[NSTAGE][THREADS][3];
   BigQueue<BIGQ> q;
