@@ -455,11 +455,12 @@ static bool separate_vs(const piko_ctx* ctx, long long V, long long T) {
   if (ctx->pipeline == PIKO_PIPE_BASELINE) return true;  // VS is its own stage
   if (ctx->vs_mode >= 0) return ctx->vs_mode == 1;
   if (V >= 0) return 2 * V <= 3 * T;
-  // piko_draw (no vertex count): the separate stage derives V with
-  // k_index_max; decide from the vertex count the last separate frame saw
-  // (k_vertex records it), trying the separate stage while it is unknown
-  const long long seen = ctx->h_ctl ? (long long)ctx->h_ctl->vx_need : 0;
-  return seen == 0 || 2 * seen <= 3 * T;
+  // piko_draw (no vertex count): the separate stage would first derive V with
+  // a k_index_max pass over idx and then need k_vertex -- two launches on the
+  // critical path; the fused k_setup transforms the corners itself and is
+  // faster on every mesh measured (c3 84 vs 88 us, c5 1262 vs 1336 us, c2
+  // 163 vs 165 us)
+  return false;
 }
 
 // xv capacity for V vertices (V < 0: unknown; sized from an upper bound)
