@@ -2384,7 +2384,11 @@ struct TileSmem {
 #ifndef PIKO_BIGQ_DIV
 #define PIKO_BIGQ_DIV 1
 #endif
+#ifdef PIKO_BIGQ
+  static constexpr int BIGQ = PIKO_BIGQ < THREADS ? PIKO_BIGQ : THREADS;
+#else
   static constexpr int BIGQ = THREADS / PIKO_BIGQ_DIV;  // queued per bin (overflow: spill region, then warp-cooperative)
+#endif
   u64 key[NPX];
   int4 rec[NSTAGE][THREADS][3];
   BigQueue<BIGQ> q;
