@@ -2,6 +2,8 @@
 """Render `--warmup` + `--frames` frames of a config for ncu captures.
 
     ncu --set full -k regex:k_ -s <warmup*kernels_per_frame> python tools/profile_frame.py
+(--api draw, the default, is the bench's piko_draw: k_setup<FUSED>, k_cm_scan,
+k_cm_scatter, k_tile per frame on c3; --api indexed adds k_vertex)
 Prints kernels_per_frame on stderr so the skip count can be derived.
 """
 from __future__ import annotations
@@ -19,6 +21,8 @@ def main():
     ap.add_argument("--bin", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--frames", type=int, default=1)
+    ap.add_argument("--api", choices=["draw", "indexed"], default="draw",
+                    help="piko_draw (the bench headline: fused vertex stage) or piko_draw_indexed")
     a = ap.parse_args()
     import torch
 
@@ -31,7 +35,7 @@ def main():
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     for k in range(a.warmup + a.frames):
         flush.fill_(float(k))
-        r.draw(v, i, s.mvp, s.light)
+        r.draw(v, i, s.mvp, s.light, indexed=a.api == "indexed")
     torch.cuda.synchronize()
     st = r.stats()
     print(f"stats {st}", file=sys.stderr)
