@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
   if (chunk == 0 && tid == 0) {
     a.ctl->frame = frame; a.ctl->tile_next = 0; a.ctl->vmax = 0;
     for (int k = 0; k < NLIST; ++k) a.ctl->list_n[k] = 0;
-    a.ctl->empty_next = 0; a.ctl->eq_next = 0;
+    a.ctl->empty_next = 0; a.ctl->eq_next = 0; a.ctl->cm_touched = 0;
     if (a.ctl->vx_overflow) { a.ctl->vx_overflow = 0; atomicMax(&a.ctl->overflow_tag, frame + 1); }
   }
   // large triangles: the whole CTA walks their bins
@@ -1760,6 +1760,7 @@ __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_const
       }
       __syncthreads();
       const unsigned U = sm.U;
+      if (threadIdx.x == 0) atomicAdd(&a.ctl->cm_touched, (u64)U);
 #ifdef PIKO_K1_TIMING
       if (threadIdx.x == 0 && lo == 0 && blockIdx.x < 8000) g_k1_times[2][blockIdx.x][7] = U;
 #endif

@@ -131,6 +131,7 @@ struct piko_ctx {
     Control* d = nullptr;   // its device alias: the binned frame's last kernel writes it directly
     cudaEvent_t ev = nullptr;
     long long T = 0;
+    bool cm = false;        // the frame used the count-matrix AssignBin
   };
   Slot ring[NRING];
   int ring_head = 0, ring_n = 0;     // next slot to fill; frames in flight
@@ -183,6 +184,7 @@ struct piko_ctx {
   uint32_t* cm = nullptr; uint32_t* cp = nullptr; long long cm_cap = 0;  // [rows][NB]
   bool tile_items_grid = false;             // k_tile: one CTA per possible item instead of persistent
   bool last_cm = false;                     // the last frame used the count matrix
+  long long cm_dense_T = -1;                 // triangle count of frames whose count matrix was dense
   long long last_cm_rows = 0;
   // chunk-list AssignBin (NB <= CL_MAX_NB; the default where it applies)
   int early_empty = 1;                      // PIKO_EARLY_EMPTY=0: empty bins after the pair items
@@ -533,6 +535,7 @@ static cudaError_t record_frame_end(piko_ctx* ctx, cudaStream_t s, long long T, 
   if (e == cudaSuccess) e = cudaEventRecord(sl.ev, s);
   if (e != cudaSuccess) return e;
   sl.T = T;
+  sl.cm = ctx->pipeline == PIKO_PIPE_BINNED && ctx->last_cm;
   ctx->ring_head = (ctx->ring_head + 1) % piko_ctx::NRING;
   ++ctx->ring_n;
   ctx->pending = true;
@@ -668,6 +671,10 @@ static int enqueue_baseline(piko_ctx* ctx, const float* verts, long long V, cons
 // SM, fewer (longer) rows when rows x NB would exceed CM_MAX_ENTRIES.
 static bool use_cm(const piko_ctx* ctx, long long T, int& shift, long long& rows) {
   if (ctx->cm_mode == 0 || ctx->npass < 1 || ctx->g.NB > CM_MAX_NB) return false;
+  // a count-matrix frame of this size showed dense rows (most of a window's
+  // pairs in distinct bins: an unordered soup) -- the radix passes rank those
+  // with less work (c4: 1179 vs 1139 us); auto mode only
+  if (ctx->cm_mode < 0 && ctx->cm_dense_T == T) return false;
   shift = 10;  // K1_CHUNK
   if (ctx->cm_tc_log2 >= 10) shift = ctx->cm_tc_log2;
   else
@@ -1057,6 +1064,11 @@ static int eval_frame(piko_ctx* ctx, piko_ctx::Slot& sl) {
     return ctx->last_status;
   }
   ctx->last_status = PIKO_OK;
+  // touched bins per pair over the scatter windows: above 1/4 the rows are
+  // dense (coherent meshes: c3 0.02) and the next frames of this size use the
+  // radix passes
+  if (sl.cm && ctx->h_ctl->n_pairs > 0 && 4 * ctx->h_ctl->cm_touched > ctx->h_ctl->n_pairs)
+    ctx->cm_dense_T = sl.T;
   adapt_tri_chunk(ctx);
   return PIKO_OK;
 }

@@ -83,6 +83,8 @@ struct Control {  // (the mirror copies whole 8-byte words up to digit_hist: kee
   unsigned long long scan_ticket;      // standalone bin-scan kernel (single-pass grids)
   unsigned long long cm_done;          // k_cm_scan CTAs finished (modulo grid: the last scans bin_start)
   unsigned long long cl_done;          // chunk-list k_setup CTAs finished (modulo grid: the last scans bin_start)
+  unsigned long long cm_touched;       // count-matrix frame: sum over scatter windows of the bins touched
+                                       //   (dense rows, e.g. unordered soups: the host switches to the radix passes)
   unsigned long long frame;            // written by K1 chunk 0
   unsigned int tile_next;              // dynamic bin queue of k_tile (reset by K1 chunk 0)
   unsigned int list_n[NLIST];          // work-list sizes (reset by K1 chunk 0)

@@ -686,3 +686,16 @@ def test_deferred_overflow_frame_is_background_then_exact(env, monkeypatch):
     s = scenes.scene_c2()
     got = gpu_render(env, s, 8, cov=False, frames=1)  # 8-px bins: P = 418504 > the initial capacity
     assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
+
+
+def test_dense_count_matrix_switches_to_radix(env, monkeypatch):
+    """Auto AssignBin: an unordered soup's count-matrix rows are dense (most of
+    a scatter window's pairs in distinct bins), so after the first frame the
+    context ranks frames of that size with the radix passes -- both frames
+    exact, the bin lists too; a coherent mesh (c3) stays on the count matrix."""
+    monkeypatch.delenv("PIKO_CM", raising=False)
+    s = scenes.scene_soup(200000, 960, 540, seed=77, name="soup", bin_sizes=(16,))
+    got = gpu_render(env, s, 16, cov=False, frames=2)
+    assert got["stats"]["assign_mode"] == 0
+    assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
+    assert_bins_equal(got, env, s, 16)
