@@ -616,6 +616,14 @@ def run_piko(args):
                            "frac_measured": measured / (ms / 1e3) / 1e9 / peak if measured else None,
                            "measured_note": measured_note},
         "kernel_ms": per_frame,
+        # every stage against the same HBM peak (algorithmic bytes per launch /
+        # its event time) -- the dominant one is `roofline`
+        "stage_roofline": {k: {"ms": per_frame[k],
+                               "algorithmic_bytes": algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"],
+                                                                      cm_rows, cl_chunks),
+                               "frac": algorithmic_bytes(k, T, V, L, P, NB, npx, ncov, stats["radix_passes"], cm_rows,
+                                                         cl_chunks) / (per_frame[k] / 1e3) / 1e9 / peak}
+                           for k in ("vertex", "setup", "expand", "sort", "tile") if per_frame.get(k, 0) > 0.004},
         "kernel_ms_note": "per-stage CUDA-event times from a second K-step pass (events between kernels)",
         "api": "piko_draw (north-star C ABI call via ctypes, PIKO_SYNC_ASYNC)",
         "roofline": roofline,
