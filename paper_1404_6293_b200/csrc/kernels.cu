@@ -2404,7 +2404,10 @@ __device__ __forceinline__ void normalise_light(const float in[3], float L[3]) {
 #ifndef PIKO_TINY_AREA
 #define PIKO_TINY_AREA 4
 #endif
-constexpr int TINY_AREA = PIKO_TINY_AREA;  // clipped rect area a thread rasterizes alone
+constexpr int TINY_AREA = PIKO_TINY_AREA;
+#ifndef PIKO_TINY32
+#define PIKO_TINY32 1  // tiny small triangles: incremental 32-bit edge functions (0: eval_pre)
+#endif  // clipped rect area a thread rasterizes alone
 #ifndef PIKO_QSEG
 #define PIKO_QSEG 4
 #endif
@@ -2684,23 +2687,16 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   __shared__ int s_list[FRAG_ROUNDS * THREADS];
   __shared__ int s_wc[THREADS / 32];
   int ncv = 0;  // compacted pairs of the item whose prologue was issued last
-  // the next item's primIDs, loaded while the current item rasterizes
-  int nxt[FRAG_ROUNDS];
-#pragma unroll
-  for (int j = 0; j < FRAG_ROUNDS; ++j) nxt[j] = -1;
-  bool have_nxt = false;
-  unsigned nxw[FRAG_ROUNDS];  // their no-coverage words, loaded after the item's first round
-  bool have_nxw = false;
   auto compact = [&](int s_, int e_) -> int {  // CTA-uniform call (two barriers)
     int tv[FRAG_ROUNDS];
 #pragma unroll
     for (int j = 0; j < FRAG_ROUNDS; ++j) {
       const int i = s_ + j * THREADS + tid;
-      tv[j] = have_nxt ? nxt[j] : i < e_ ? a.bin_prims[i] : -1;
+      tv[j] = i < e_ ? a.bin_prims[i] : -1;
     }
 #pragma unroll
     for (int j = 0; j < FRAG_ROUNDS; ++j) {
-      const unsigned wd = have_nxw ? nxw[j] : tv[j] >= 0 ? a.nocov[tv[j] >> 5] : 0u;
+      const unsigned wd = tv[j] >= 0 ? a.nocov[tv[j] >> 5] : 0u;
       if (tv[j] >= 0 && ((wd >> (tv[j] & 31)) & 1u)) tv[j] = -1;
     }
     unsigned bal[FRAG_ROUNDS];
@@ -2777,17 +2773,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     // the bin is done.  Tiny triangles: one thread loops over its pixels;
     // larger ones: warp-cooperative (triangle, pixel) expansion.
     TL_MARK(b, 5);  // tile cleared
-    if (!pre) { have_nxt = have_nxw = false; prologue(s, e); }
-    have_nxw = false;
-    if (cmode) {  // s_nx was written before the clear barrier
-      const int nb = s_nx[0], ns = s_nx[1], ne = s_nx[2];
-#pragma unroll
-      for (int j = 0; j < FRAG_ROUNDS; ++j) {
-        const int i = ns + j * THREADS + tid;
-        nxt[j] = (nb >= 0 && i < ne) ? a.bin_prims[i] : -1;
-      }
-      have_nxt = true;
-    }
+    if (!pre) prologue(s, e);
     const int nround = ((cmode ? ncv : e - s) + THREADS - 1) / THREADS;
     for (int k = 0; k < nround; ++k) {
       const int buf = k % NSTAGE;
@@ -2821,6 +2807,45 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
 #ifdef PIKO_EXP_NORASTER
           if (r.X0 == 123456789) sm.key[0] = t_cur;
 #else
+#if PIKO_TINY32
+          if (r.small) {
+            // small triangle (bbox extent < 2^15 subpixels): the three edge
+            // functions at the clipped rect's first sample, then stepped by
+            // -256 A per pixel and +256 B per row -- the same exact integer
+            // values as eval_pre (every sample lies in the bbox, so each true
+            // value fits int32 and the wrapped unsigned sums are exact) without
+            // its 64-bit constants; depth from the same fma chain
+            const int dx0 = 256 * rx0 + 128 - r.X0, dy0 = 256 * ry0 + 128 - r.Y0;
+            const unsigned A0 = (unsigned)(r.Y1 - r.Y0), B0 = (unsigned)(r.X1 - r.X0);
+            const unsigned A1 = (unsigned)(r.Y2 - r.Y1), B1 = (unsigned)(r.X2 - r.X1);
+            const unsigned A2 = (unsigned)(r.Y0 - r.Y2), B2 = (unsigned)(r.X0 - r.X2);
+            unsigned q0 = B0 * (unsigned)dy0 - A0 * (unsigned)dx0;
+            unsigned q1 = B1 * (unsigned)(dy0 + r.Y0 - r.Y1) - A1 * (unsigned)(dx0 + r.X0 - r.X1);
+            unsigned q2 = B2 * (unsigned)(dy0 + r.Y0 - r.Y2) - A2 * (unsigned)(dx0 + r.X0 - r.X2);
+            const int th0 = tl_thr(r.X0, r.Y0, r.X1, r.Y1), th1 = tl_thr(r.X1, r.Y1, r.X2, r.Y2);
+            const int th2 = tl_thr(r.X2, r.Y2, r.X0, r.Y0);
+            int p0 = (ry0 - y0) * BW + (rx0 - x0);
+            for (int yy = 0; yy < h; ++yy) {
+              unsigned e0 = q0, e1 = q1, e2 = q2;
+              for (int xx = 0; xx < w; ++xx) {
+                if ((int)e0 > th0 && (int)e1 > th1 && (int)e2 > th2) {
+                  if (COV) atomicAdd(&s_cov[p0 + xx], 1u);
+                  const float z = __fmaf_rn(r.za, __int2float_rn(dx0 + 256 * xx),
+                                            __fmaf_rn(r.zb, __int2float_rn(dy0 + 256 * yy), r.zw0));
+                  if (z >= 0.0f && z <= 1.0f) {
+                    const u64 key = ((u64)(__float_as_uint(z) & 0x7FFFFFFFu) << 32) | (unsigned)t_cur;
+                    atomicMin(&sm.key[p0 + xx], key);
+                    if (fwd) facc = __fadd_rn(facc, shader_work(fwd, key_depth(key)));
+                  }
+                }
+                e0 -= 256u * A0; e1 -= 256u * A1; e2 -= 256u * A2;
+              }
+              q0 += 256u * B0; q1 += 256u * B1; q2 += 256u * B2;
+              p0 += BW;
+            }
+          } else
+#endif
+          {
           const TriEval ev = prepare(r);
           for (int y = ry0; y < ry0 + h; ++y)
             for (int x = rx0; x < rx0 + w; ++x) {
@@ -2837,6 +2862,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
               if (key == 12345) sm.key[p] = key;
 #endif
             }
+          }
 #endif
           area = 0;
         } else {
@@ -2908,11 +2934,6 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
             }
           }
         }
-      }
-      if (cmode && k == 0) {  // CTA-uniform: the next item's primIDs have arrived by now
-#pragma unroll
-        for (int j = 0; j < FRAG_ROUNDS; ++j) nxw[j] = nxt[j] >= 0 ? a.nocov[nxt[j] >> 5] : 0u;
-        have_nxw = true;
       }
       __syncwarp();  // round k's slots are free for round k + NSTAGE
     }
