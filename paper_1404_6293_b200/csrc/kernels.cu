@@ -580,39 +580,6 @@ __device__ __forceinline__ void cl_publish(const SetupArgs& a, K1Smem& sm, const
   }
 }
 
-// Does triangle o cover any pixel sample of its sample rect?  Asked only for
-// small triangles (bbox extent < 2^15 subpixels) whose rect holds at most
-// NOCOV_AREA pixels.  The tile kernel's exact integer edge test (O3 with the
-// top-left rule R1): each edge function at the rect's first sample, then
-// stepped by +-256 x the edge's deltas per pixel.  Every sample lies inside
-// the bbox, so every true value fits int32 and the wrapped unsigned sums are
-// exact.  A triangle covering none contributes to no pixel of any bin, so
-// k_tile may drop its pairs without changing any output.
-__device__ __forceinline__ bool covers_any_sample(const Tri& o) {
-  const int w = NOCOV_AREA == 1 ? 1 : o.px1 - o.px0 + 1, h = NOCOV_AREA == 1 ? 1 : o.py1 - o.py0 + 1;
-  const unsigned dx = (unsigned)(256 * o.px0 + 128 - o.X0), dy = (unsigned)(256 * o.py0 + 128 - o.Y0);
-  const unsigned A0 = (unsigned)(o.Y1 - o.Y0), B0 = (unsigned)(o.X1 - o.X0);
-  const unsigned A1 = (unsigned)(o.Y2 - o.Y1), B1 = (unsigned)(o.X2 - o.X1);
-  const unsigned A2 = (unsigned)(o.Y0 - o.Y2), B2 = (unsigned)(o.X0 - o.X2);
-  // E_ab(P) = B_ab (Py - Ya) - A_ab (Px - Xa), with P - Va = (P - V0) + (V0 - Va)
-  const unsigned dx1 = dx + (unsigned)(o.X0 - o.X1), dy1 = dy + (unsigned)(o.Y0 - o.Y1);
-  const unsigned dx2 = dx + (unsigned)(o.X0 - o.X2), dy2 = dy + (unsigned)(o.Y0 - o.Y2);
-  unsigned r0 = B0 * dy - A0 * dx, r1 = B1 * dy1 - A1 * dx1, r2 = B2 * dy2 - A2 * dx2;
-  const int t01 = ((o.Y1 == o.Y0 && o.X1 > o.X0) || (o.Y1 < o.Y0)) ? -1 : 0;
-  const int t12 = ((o.Y2 == o.Y1 && o.X2 > o.X1) || (o.Y2 < o.Y1)) ? -1 : 0;
-  const int t20 = ((o.Y0 == o.Y2 && o.X0 > o.X2) || (o.Y0 < o.Y2)) ? -1 : 0;
-  bool any = false;
-  for (int y = 0; y < h; ++y) {
-    unsigned e0 = r0, e1 = r1, e2 = r2;
-    for (int x = 0; x < w; ++x) {
-      any |= (int)e0 > t01 && (int)e1 > t12 && (int)e2 > t20;
-      e0 -= 256u * A0; e1 -= 256u * A1; e2 -= 256u * A2;
-    }
-    r0 += 256u * B0; r1 += 256u * B1; r2 += 256u * B2;
-  }
-  return any;
-}
-
 template <bool FUSED>
 #ifndef PIKO_K1_MINB
 #define PIKO_K1_MINB 3
@@ -716,7 +683,6 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
   const int warp = tid >> 5;
   int bin1[K1_TPT];
   unsigned mflag = 0;  // chunk-list: slots whose triangle owns 2..K1_BIG bins (rect in mrect)
-  unsigned ncm = 0;    // slots whose triangle covers no sample (nocov bit)
 #pragma unroll
   for (int k = 0; k < K1_TPT; ++k) {
     bin1[k] = -1;
@@ -747,19 +713,11 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
         const float inv = __frcp_rn(__ll2float_rn(o.area2));
         const float za = __fmul_rn(__fmaf_rn(dz1, dy2, -__fmul_rn(dz2, dy1)), inv);
         const float zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
-        // tiny triangle covering no sample: flagged for k_tile, no record
-        const bool nc = a.nocov && o.small && o.px1 - o.px0 < NOCOV_AREA && o.py1 - o.py0 < NOCOV_AREA &&
-                        (NOCOV_AREA == 1 || (o.px1 - o.px0 + 1) * (o.py1 - o.py0 + 1) <= NOCOV_AREA) &&
-                        !covers_any_sample(o);
-        if (nc) {
-          ncm |= 1u << k;
-        } else {
-          int4* r = a.rec + 3 * t;
-          r[0] = make_int4(o.X0, o.Y0, o.X1, o.Y1);
-          r[1] = make_int4(o.X2, o.Y2, __float_as_int(o.zw0), __float_as_int(za));
-          r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
-                           o.small ? REC_SMALL : 0);
-        }
+        int4* r = a.rec + 3 * t;
+        r[0] = make_int4(o.X0, o.Y0, o.X1, o.Y1);
+        r[1] = make_int4(o.X2, o.Y2, __float_as_int(o.zw0), __float_as_int(za));
+        r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
+                         o.small ? REC_SMALL : 0);
         // digit histograms of the radix passes over this triangle's pairs
         if (cl && c > 1 && c <= (unsigned)K1_BIG) {  // chunk-list: walked by this thread
           sm1.mrect[k * K1_THREADS + tid] = rr;
@@ -781,14 +739,6 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
       }
     }
     a.rect[t] = rr;
-  }
-  if (a.nocov) {  // one word per warp and slot: triangles t0 + k*K1_THREADS + 32*warp + lane
-#pragma unroll
-    for (int k = 0; k < K1_TPT; ++k) {
-      const unsigned m = __ballot_sync(0xffffffffu, (ncm >> k) & 1u);
-      const long long tw = t0 + k * K1_THREADS + 32 * warp;
-      if ((threadIdx.x & 31) == 0 && tw < a.n_tris) a.nocov[tw >> 5] = m;
-    }
   }
   if (cmrow) {
 #pragma unroll
@@ -2404,10 +2354,10 @@ __device__ __forceinline__ void normalise_light(const float in[3], float L[3]) {
 #ifndef PIKO_TINY_AREA
 #define PIKO_TINY_AREA 4
 #endif
-constexpr int TINY_AREA = PIKO_TINY_AREA;
+constexpr int TINY_AREA = PIKO_TINY_AREA;  // clipped rect area a thread rasterizes alone
 #ifndef PIKO_TINY32
 #define PIKO_TINY32 1  // tiny small triangles: incremental 32-bit edge functions (0: eval_pre)
-#endif  // clipped rect area a thread rasterizes alone
+#endif
 #ifndef PIKO_QSEG
 #define PIKO_QSEG 4
 #endif
@@ -2676,62 +2626,10 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
   // records of the first NSTAGE-1 rounds (cp.async).  For every item after the
   // first it is issued as soon as the previous item's raster has freed the
   // record stages, so it overlaps that item's queue pass and write-back.
-  //
-  // With the no-coverage bits (a.nocov; every item then holds <= FRAG_ROUNDS
-  // x THREADS pairs) an item's list is first compacted into shared memory to
-  // the triangles that can cover a sample: on small-triangle meshes most pairs
-  // are tiny triangles between pixel centres, and they would otherwise take a
-  // round slot, a record fetch and a raster pass each.  The list order is
-  // irrelevant to the result (the depth test is a minimum over unique keys).
-  const bool cmode = a.nocov != nullptr;
-  __shared__ int s_list[FRAG_ROUNDS * THREADS];
-  __shared__ int s_wc[THREADS / 32];
-  int ncv = 0;  // compacted pairs of the item whose prologue was issued last
-  auto compact = [&](int s_, int e_) -> int {  // CTA-uniform call (two barriers)
-    int tv[FRAG_ROUNDS];
-#pragma unroll
-    for (int j = 0; j < FRAG_ROUNDS; ++j) {
-      const int i = s_ + j * THREADS + tid;
-      tv[j] = i < e_ ? a.bin_prims[i] : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < FRAG_ROUNDS; ++j) {
-      const unsigned wd = tv[j] >= 0 ? a.nocov[tv[j] >> 5] : 0u;
-      if (tv[j] >= 0 && ((wd >> (tv[j] & 31)) & 1u)) tv[j] = -1;
-    }
-    unsigned bal[FRAG_ROUNDS];
-    int wc = 0;
-#pragma unroll
-    for (int j = 0; j < FRAG_ROUNDS; ++j) {
-      bal[j] = __ballot_sync(0xffffffffu, tv[j] >= 0);
-      wc += __popc(bal[j]);
-    }
-    if (lane == 0) s_wc[warp] = wc;
-    __syncthreads();
-    int base = 0, tot = 0;
-#pragma unroll
-    for (int w2 = 0; w2 < THREADS / 32; ++w2) {
-      const int v = s_wc[w2];
-      base += w2 < warp ? v : 0;
-      tot += v;
-    }
-    const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int j = 0; j < FRAG_ROUNDS; ++j) {
-      if (tv[j] >= 0) s_list[base + __popc(bal[j] & lt)] = tv[j];
-      base += __popc(bal[j]);
-    }
-    __syncthreads();
-    return tot;
-  };
-  // entry i of the current item's (compacted) list, -1 past its end
-  auto prim_at = [&](int s_, int e_, int i) -> int {
-    if (cmode) return i < ncv ? s_list[i] : -1;
-    return s_ + i < e_ ? a.bin_prims[s_ + i] : -1;
-  };
+  // entry i of the current item's list, -1 past its end
+  auto prim_at = [&](int s_, int e_, int i) -> int { return s_ + i < e_ ? a.bin_prims[s_ + i] : -1; };
   int tq[TQ];
   auto prologue = [&](int s_, int e_) {
-    if (cmode) ncv = compact(s_, e_);
 #pragma unroll
     for (int j = 0; j < TQ; ++j) tq[j] = prim_at(s_, e_, j * THREADS + tid);
 #pragma unroll
@@ -2774,7 +2672,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_co
     // larger ones: warp-cooperative (triangle, pixel) expansion.
     TL_MARK(b, 5);  // tile cleared
     if (!pre) prologue(s, e);
-    const int nround = ((cmode ? ncv : e - s) + THREADS - 1) / THREADS;
+    const int nround = (e - s + THREADS - 1) / THREADS;
     for (int k = 0; k < nround; ++k) {
       const int buf = k % NSTAGE;
       const int t_cur = tq[0];

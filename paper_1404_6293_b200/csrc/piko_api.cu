@@ -104,7 +104,6 @@ struct piko_ctx {
   int4* ovq = nullptr; long long ovq_ctas = 0;  // k_tile queue overflow [ctas][OVQ_CAP][6]
   Control* ctl = nullptr;
   uint2* rect = nullptr;                 // [rec_cap] tile rect per triangle
-  uint32_t* nocov = nullptr;             // [rec_cap / 32 + 1] no-coverage bits (k_setup -> k_tile)
   int tri_chunk = EX_MAX_TRIS;           // triangles per expand chunk (adapted to P/T)
   unsigned long long* st_scan = nullptr; long long st_scan_n = 0;
   unsigned long long* st_rx = nullptr; long long st_rx_chunks = 0;  // [npass][chunks][256]
@@ -188,7 +187,6 @@ struct piko_ctx {
   long long cm_dense_T = -1;                 // triangle count of frames whose count matrix was dense
   long long last_cm_rows = 0;
   // chunk-list AssignBin (NB <= CL_MAX_NB; the default where it applies)
-  int nocov_mode = 0;                       // PIKO_NOCOV=1: no-coverage bits + compacted item lists (slower)
   int early_empty = 1;                      // PIKO_EARLY_EMPTY=0: empty bins after the pair items
   int cl_mode = 0;                          // 0 off (default: slower on c2/c3), 1 on where it applies
   bool cl_off = false;                      // a chunk overflowed CL_WIN: count matrix from now on
@@ -330,7 +328,6 @@ extern "C" piko_ctx* piko_create(int width, int height, int bin_w, int bin_h) {
   if (const char* e = getenv("PIKO_DEFERRED")) ctx->deferred = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_CM")) ctx->cm_mode = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_CL")) ctx->cl_mode = e[0] == '0' ? 0 : 1;
-  if (const char* e = getenv("PIKO_NOCOV")) ctx->nocov_mode = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_EARLY_EMPTY")) ctx->early_empty = e[0] == '0' ? 0 : 1;
   if (const char* e = getenv("PIKO_TILE_GRID")) ctx->tile_items_grid = strcmp(e, "items") == 0;
   if (const char* e = getenv("PIKO_CM_TC_LOG2")) ctx->cm_tc_log2 = atoi(e);
@@ -351,7 +348,7 @@ extern "C" void piko_destroy(piko_ctx* ctx) {
     cudaFree(ctx->p2p_sync);
   }
   void* bufs[] = {ctx->xv, ctx->rec, ctx->keys[0], ctx->keys[1], ctx->vals[0], ctx->vals[1], ctx->bin_count,
-                  ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->fkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->nocov, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
+                  ctx->bin_start, ctx->frag_list, ctx->bin_list, ctx->fkey, ctx->gcov, ctx->arrive, ctx->ctl, ctx->rect, ctx->st_scan, ctx->st_rx, ctx->st_grp, ctx->ccount, ctx->garr, ctx->primid,
                   ctx->cov, ctx->d_verts, ctx->d_idx, ctx->d_rgba, ctx->d_depth, ctx->tile_keys, ctx->def_keys, ctx->cm, ctx->cp, ctx->dice_verts, ctx->dice_idx, ctx->dice_rate, ctx->dice_base, ctx->dice_total,
                   ctx->all_keys, ctx->fp_keys, ctx->ovq, ctx->sc.sink, ctx->bl_keys, ctx->frag_key,
                   ctx->frag_px, ctx->frag_rgba, ctx->cl_ent, ctx->cl_bm, ctx->cl_tot};
@@ -389,13 +386,10 @@ static int ensure_tris(piko_ctx* ctx, long long T) {
     long long cap = std::max<long long>(T, 1024);
     if (ctx->rec) cudaFree(ctx->rec);
     if (ctx->rect) cudaFree(ctx->rect);
-    if (ctx->nocov) cudaFree(ctx->nocov);
     ctx->rec = nullptr;
     ctx->rect = nullptr;
-    ctx->nocov = nullptr;
     CK(cudaMalloc(&ctx->rec, sizeof(int4) * 3 * cap));
     CK(cudaMalloc(&ctx->rect, sizeof(uint2) * cap));
-    CK(cudaMalloc(&ctx->nocov, sizeof(uint32_t) * (cap / 32 + 1)));
     ctx->rec_cap = cap;
     return alloc_rx_status(ctx);
   }
@@ -775,9 +769,6 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
   const bool cm = !clm && use_cm(ctx, T, cm_shift, cm_rows);
   if (cm && ensure_cm(ctx, cm_rows) != PIKO_OK) return PIKO_ECUDA;
   const bool sorted_here = cm || clm;  // no radix passes this frame
-  // no-coverage bits: every work item of a binned grid holds <= FRAG_ROUNDS x
-  // CTA pairs, which k_tile compacts in shared memory (single-bin grids: off)
-  const bool nocov = ctx->nocov_mode && ctx->npass > 0;
   const long long grids[6] = {g1, gx, gp + ntiles, ntiles, clm ? 2 : cm ? 1 : 0, cm ? cm_rows : 0};
   CK(mark(0));
   bool changed = ctx->need_reset;
@@ -816,7 +807,6 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.xv = sep ? ctx->xv : nullptr; a.xv_cap = ctx->xv_cap; a.verts = verts; a.M = M;
     a.idx = idx; a.n_tris = T; a.g = ctx->g;
     a.npass = sorted_here ? 0 : ctx->npass; a.rec = ctx->rec; a.rect = ctx->rect; a.ctl = ctx->ctl;
-    a.nocov = nocov ? ctx->nocov : nullptr;
     a.cm = cm ? ctx->cm : nullptr; a.cm_shift = cm_shift;
     a.frame = ctx->frames++;
     if (clm) {
@@ -893,7 +883,6 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
     a.g = ctx->g; a.npass = ctx->npass; a.rec = ctx->rec; a.bin_start = ctx->bin_start;
     a.bin_prims = ctx->prims_out; a.ctl = ctx->ctl;
-    a.nocov = nocov ? ctx->nocov : nullptr;
     a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
     a.out_cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;
     a.tile_keys = keys_out ? keys_out

@@ -49,13 +49,6 @@ constexpr int LIST_EMPTY = NLIST - 1;
 #define PIKO_FRAG_ROUNDS 4
 #endif
 constexpr int FRAG_ROUNDS = PIKO_FRAG_ROUNDS;  // fragment = FRAG_ROUNDS * threads-per-CTA pairs
-// k_setup tests every sample of a triangle whose sample rect holds at most
-// NOCOV_AREA pixels; one covering none gets its bit in the nocov mask and
-// k_tile drops its pairs from the item's compacted list (the CSR keeps them)
-#ifndef PIKO_NOCOV_AREA
-#define PIKO_NOCOV_AREA 1
-#endif
-constexpr int NOCOV_AREA = PIKO_NOCOV_AREA;
 constexpr int EMPTY_GROUP = 8;   // empty bins per k_tile queue ticket
 constexpr int OVQ_CAP = 1024;
 // Count-matrix AssignBin: used when NB <= CM_MAX_NB and the
@@ -167,8 +160,6 @@ struct SetupArgs {
   int4* rec;                    // [n_tris][3]
   uint2* rect;                  // [n_tris] tile rect {tx0|ty0<<16, tx1|ty1<<16}; empty if culled
   Control* ctl;
-  uint32_t* nocov;              // [ceil(n_tris/32)] bit t: live, sample rect <= NOCOV_AREA px and
-                                //   no sample covered -- its record is not written (null: off)
   // chunk-list AssignBin (null: off): per touched bin b, cl_ent[b][chunk] =
   // {mask of the chunk's 32-triangle groups with a pair in b, pairs}, bit
   // `chunk` of cl_bm[b][cl_nw], cl_tot[b] += pairs
@@ -281,8 +272,6 @@ struct TileArgs {
   const int4* rec;
   int32_t* bin_start;           // written here only when npass == 0 (NB == 1)
   const int32_t* bin_prims;
-  const uint32_t* nocov;        // k_setup's no-coverage bits: each item's pair list is compacted to the
-                                //   triangles that can cover a sample (null: off; needs npass > 0)
   Control* ctl;
   float* out_rgba;              // may be null (keys-only mode)
   float* out_depth;

@@ -699,18 +699,3 @@ def test_dense_count_matrix_switches_to_radix(env, monkeypatch):
     assert got["stats"]["assign_mode"] == 0
     assert_frame_equal(got, oracle_frame(env, s, cov=False), cov=False)
     assert_bins_equal(got, env, s, 16)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("nocov", ["1", "0"])
-@pytest.mark.parametrize("cfg,bw,cov", [("c3", 16, False), ("c2", 8, True), ("c1", 8, True), ("c4", 32, False)])
-def test_nocov_compaction_exact(env, nocov, cfg, bw, cov, monkeypatch):
-    """k_setup's no-coverage bits (tiny triangles that cover no pixel sample:
-    no record, their pairs dropped from k_tile's compacted item lists) leave
-    the frame, the coverage counts and the bin CSR bit-exact, and so does the
-    path without them (PIKO_NOCOV=0)."""
-    monkeypatch.setenv("PIKO_NOCOV", nocov)
-    s = scenes.make(cfg)
-    got = gpu_render(env, s, bw, cov=cov, frames=2)
-    assert_frame_equal(got, oracle_frame(env, s, cov=cov), cov=cov)
-    assert_bins_equal(got, env, s, bw)
