@@ -5,7 +5,7 @@
 # usage: bash tools/refresh_profiles.sh TAG
 TAG=${1:-r2}
 mkdir -p gpurun_out/prof
-IFS=';' read -ra SP <<< "${SPECS:-c3 10 5;c5 10 5}"
+IFS=';' read -ra SP <<< "${SPECS:-c3 8 4;c5 8 4}"
 for spec in "${SP[@]}"; do
   set -- $spec; c=$1; skip=$2; cnt=$3
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv \
