@@ -2437,7 +2437,10 @@ __device__ __forceinline__ void store_pixel(const TileArgs& a, const float L[3],
 }
 
 template <int BW, int BH, int THREADS, bool COV, bool KEYS_ONLY>
-__global__ void __launch_bounds__(THREADS, 768 / THREADS) k_tile(const __grid_constant__ TileArgs a) {
+#ifndef PIKO_TILE_TPSM
+#define PIKO_TILE_TPSM 768  // k_tile threads resident per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(THREADS, PIKO_TILE_TPSM / THREADS) k_tile(const __grid_constant__ TileArgs a) {
   constexpr int NPX = BW * BH;
   constexpr int PPT = (NPX + THREADS - 1) / THREADS;
   extern __shared__ __align__(16) unsigned char smem_raw[];

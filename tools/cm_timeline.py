@@ -35,7 +35,8 @@ h = ctypes.CDLL(lib)
 piko.piko_set_sync(r.ctx, piko.PIKO_SYNC_ASYNC)
 st = torch.cuda.current_stream()
 for k in range(4):
-    flush.fill_(float(k))
+    if not os.environ.get("TL_NOFLUSH"):
+        flush.fill_(float(k))
     if k == 3:  # reset the vertex-start slots (atomicMin/Max) before the measured frame
         z = np.zeros((4, 8192, 8), np.uint64)
         z[0, 8190, 0] = z[0, 8191, 0] = np.uint64(2**63)
@@ -98,6 +99,21 @@ if m.any():
     tm = t[m]
     print(f"   heavy bins phases (median ns): clear {np.median(tm[:,5]-tm[:,0]):.0f}  rounds {np.median(tm[:,6]-tm[:,5]):.0f}"
           f"  wait+sync {np.median(tm[:,7]-tm[:,6]):.0f}  prologue+drain {np.median(tm[:,1]-tm[:,7]):.0f}  writeback {np.median(tm[:,2]-tm[:,1]):.0f}")
+if m.any():  # the same phases for each CTA's first heavy item vs its later ones
+    tm = t[m]
+    first = np.zeros(len(tm), bool)
+    seen = set()
+    for j in np.argsort(tm[:, 0]):
+        c_ = int(tm[j, 4])
+        if c_ not in seen:
+            seen.add(c_)
+            first[j] = True
+    for nm, sel in (("first", first), ("later", ~first)):
+        if sel.any():
+            u = tm[sel]
+            print(f"   heavy {nm:5s} items ({sel.sum()}): pairs {np.median(u[:,3]):.0f} clear {np.median(u[:,5]-u[:,0]):.0f}"
+                  f"  rounds {np.median(u[:,6]-u[:,5]):.0f}  wait+sync {np.median(u[:,7]-u[:,6]):.0f}"
+                  f"  prologue+drain {np.median(u[:,1]-u[:,7]):.0f}  writeback {np.median(u[:,2]-u[:,1]):.0f}")
 cta = t[:, 4]
 per = np.bincount(cta.astype(np.int64))
 print(f"   bins per CTA: min {per[per>0].min()} max {per.max()} CTAs {np.count_nonzero(per)}")
