@@ -2437,6 +2437,9 @@ __device__ __forceinline__ void store_pixel(const TileArgs& a, const float L[3],
 }
 
 template <int BW, int BH, int THREADS, bool COV, bool KEYS_ONLY>
+#ifndef PIKO_EARLY_ITEM2
+#define PIKO_EARLY_ITEM2 0  // 1: k_tile looks the second static item up with the first (no gain)
+#endif
 #ifndef PIKO_TILE_TPSM
 #define PIKO_TILE_TPSM 768  // k_tile threads resident per SM the register budget is sized for
 #endif
@@ -2614,6 +2617,7 @@ __global__ void __launch_bounds__(THREADS, PIKO_TILE_TPSM / THREADS) k_tile(cons
   // thread 0 keeps the next item in registers one item ahead
   int q_bin = -1, q_s = 0, q_e = 0, q_nf = 0, q_fs = -1, q_fj = 0;
   unsigned q_tk = 0;
+  bool have_q = false;  // thread 0: the q_* item is already looked up
   if (tid == 0) {
     // the first two items are static (blockIdx, blockIdx + grid): 2 x grid
     // same-address atomics at kernel start serialise at L2 for ~10 us; later
@@ -2622,6 +2626,12 @@ __global__ void __launch_bounds__(THREADS, PIKO_TILE_TPSM / THREADS) k_tile(cons
     q_tk = blockIdx.x + gridDim.x;
     int b0 = -1, s0 = 0, e0 = 0, nf0 = 0, fs0 = -1, fj0 = 0;
     work_item(t0, b0, s0, e0, nf0, fs0, fj0);
+#if PIKO_EARLY_ITEM2
+    // the second static item's lookups too, so its loads overlap the first's
+    // (at the first item's start every CTA queries the lists at once)
+    work_item(q_tk, q_bin, q_s, q_e, q_nf, q_fs, q_fj);
+    have_q = true;
+#endif
     s_bin = b0; s_rng[0] = s0; s_rng[1] = e0; s_rng[2] = nf0; s_rng[3] = fs0; s_rng[4] = fj0;
   }
   __syncthreads();
@@ -2652,7 +2662,8 @@ __global__ void __launch_bounds__(THREADS, PIKO_TILE_TPSM / THREADS) k_tile(cons
     const int s = s_rng[0], e = s_rng[1], nfrag = s_rng[2], fslot0 = s_rng[3], fidx = s_rng[4];
     TL_MARK(b, 0);
     if (tid == 0) {  // prefetch the next item
-      work_item(q_tk, q_bin, q_s, q_e, q_nf, q_fs, q_fj);
+      if (!have_q) work_item(q_tk, q_bin, q_s, q_e, q_nf, q_fs, q_fj);
+      have_q = false;
       if (q_bin >= 0) q_tk = 2u * gridDim.x + atomicAdd(&a.ctl->tile_next, 1u);
       s_nx[0] = q_bin; s_nx[1] = q_s; s_nx[2] = q_e;
     }
