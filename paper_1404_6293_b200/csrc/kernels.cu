@@ -203,6 +203,22 @@ struct Tri {
   int small;
 };
 
+// Part j (0..2) of triangle t's 48-byte setup record: interleaved (default,
+// [T][3]) or in three planes ([3][stride], PIKO_REC_SOA=1: the parts of
+// consecutive triangles contiguous -- fewer, fuller sectors per warp on runs
+// of consecutive primIDs, yet measured slower: c3 +2, c4 +17, c5 +25 us).
+#ifndef PIKO_REC_SOA
+#define PIKO_REC_SOA 0
+#endif
+__device__ __forceinline__ long long rec_at(long long t, int j, long long stride) {
+#if PIKO_REC_SOA
+  return (long long)j * stride + t;
+#else
+  (void)stride;
+  return 3 * t + j;
+#endif
+}
+
 __device__ __forceinline__ bool xform_corner(const float4 p, const Mat4& M, float hw, float hh,
                                              int& X, int& Y, float& zw, float& rw) {
   const float cx = __fmaf_rn(M.m[0], p.x, __fmaf_rn(M.m[1], p.y, __fmaf_rn(M.m[2], p.z, M.m[3])));
@@ -713,11 +729,10 @@ __global__ void __launch_bounds__(K1_THREADS, PIKO_K1_MINB) k_setup(SetupArgs a)
         const float inv = __frcp_rn(__ll2float_rn(o.area2));
         const float za = __fmul_rn(__fmaf_rn(dz1, dy2, -__fmul_rn(dz2, dy1)), inv);
         const float zb = __fmul_rn(__fmaf_rn(dz2, dx1, -__fmul_rn(dz1, dx2)), inv);
-        int4* r = a.rec + 3 * t;
-        r[0] = make_int4(o.X0, o.Y0, o.X1, o.Y1);
-        r[1] = make_int4(o.X2, o.Y2, __float_as_int(o.zw0), __float_as_int(za));
-        r[2] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16), o.px1 | (o.py1 << 16),
-                         o.small ? REC_SMALL : 0);
+        a.rec[rec_at(t, 0, a.rec_stride)] = make_int4(o.X0, o.Y0, o.X1, o.Y1);
+        a.rec[rec_at(t, 1, a.rec_stride)] = make_int4(o.X2, o.Y2, __float_as_int(o.zw0), __float_as_int(za));
+        a.rec[rec_at(t, 2, a.rec_stride)] = make_int4(__float_as_int(zb), o.px0 | (o.py0 << 16),
+                                                      o.px1 | (o.py1 << 16), o.small ? REC_SMALL : 0);
         // digit histograms of the radix passes over this triangle's pairs
         if (cl && c > 1 && c <= (unsigned)K1_BIG) {  // chunk-list: walked by this thread
           sm1.mrect[k * K1_THREADS + tid] = rr;
@@ -2648,9 +2663,10 @@ __global__ void __launch_bounds__(THREADS, PIKO_TILE_TPSM / THREADS) k_tile(cons
 #pragma unroll
     for (int j = 0; j < NSTAGE - 1; ++j) {
       if (tq[j] >= 0) {
-        const int4* rp = a.rec + 3ll * tq[j];
-        cp_async16(&sm.rec[j][tid][0], rp); cp_async16(&sm.rec[j][tid][1], rp + 1);
-        cp_async16(&sm.rec[j][tid][2], rp + 2);
+        const int tj = tq[j];
+        cp_async16(&sm.rec[j][tid][0], a.rec + rec_at(tj, 0, a.rec_stride));
+        cp_async16(&sm.rec[j][tid][1], a.rec + rec_at(tj, 1, a.rec_stride));
+        cp_async16(&sm.rec[j][tid][2], a.rec + rec_at(tj, 2, a.rec_stride));
       }
       cp_async_commit();
     }
@@ -2694,9 +2710,9 @@ __global__ void __launch_bounds__(THREADS, PIKO_TILE_TPSM / THREADS) k_tile(cons
         const int tn = tq[NSTAGE - 1];
         if (tn >= 0) {
           const int nb = (k + NSTAGE - 1) % NSTAGE;
-          const int4* rp = a.rec + 3ll * tn;
-          cp_async16(&sm.rec[nb][tid][0], rp); cp_async16(&sm.rec[nb][tid][1], rp + 1);
-          cp_async16(&sm.rec[nb][tid][2], rp + 2);
+          cp_async16(&sm.rec[nb][tid][0], a.rec + rec_at(tn, 0, a.rec_stride));
+          cp_async16(&sm.rec[nb][tid][1], a.rec + rec_at(tn, 1, a.rec_stride));
+          cp_async16(&sm.rec[nb][tid][2], a.rec + rec_at(tn, 2, a.rec_stride));
         }
         cp_async_commit();
 #pragma unroll

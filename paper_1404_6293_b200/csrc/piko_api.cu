@@ -806,7 +806,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     SetupArgs a{};
     a.xv = sep ? ctx->xv : nullptr; a.xv_cap = ctx->xv_cap; a.verts = verts; a.M = M;
     a.idx = idx; a.n_tris = T; a.g = ctx->g;
-    a.npass = sorted_here ? 0 : ctx->npass; a.rec = ctx->rec; a.rect = ctx->rect; a.ctl = ctx->ctl;
+    a.npass = sorted_here ? 0 : ctx->npass; a.rec = ctx->rec; a.rec_stride = ctx->rec_cap; a.rect = ctx->rect; a.ctl = ctx->ctl;
     a.cm = cm ? ctx->cm : nullptr; a.cm_shift = cm_shift;
     a.frame = ctx->frames++;
     if (clm) {
@@ -881,7 +881,7 @@ static int enqueue_frame(piko_ctx* ctx, const float* verts, long long V, const i
     a.sc = ctx->sc;
     a.verts = verts; a.xv = sep ? ctx->xv : nullptr; a.M = M; a.idx = idx;
     a.light[0] = L[0]; a.light[1] = L[1]; a.light[2] = L[2];
-    a.g = ctx->g; a.npass = ctx->npass; a.rec = ctx->rec; a.bin_start = ctx->bin_start;
+    a.g = ctx->g; a.npass = ctx->npass; a.rec = ctx->rec; a.rec_stride = ctx->rec_cap; a.bin_start = ctx->bin_start;
     a.bin_prims = ctx->prims_out; a.ctl = ctx->ctl;
     a.out_rgba = rgba; a.out_depth = depth; a.out_primid = ctx->primid;
     a.out_cov = (ctx->debug & PIKO_DEBUG_COVERAGE_COUNT) ? ctx->cov : nullptr;

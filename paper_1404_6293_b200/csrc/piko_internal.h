@@ -157,7 +157,8 @@ struct SetupArgs {
   uint32_t* cm;                 // count-matrix AssignBin: M[n_tris >> cm_shift][NB] (null: radix mode)
   int cm_shift;                 // log2 triangles per count-matrix row
   unsigned long long frame;     // frames enqueued since the control block was reset (host counter)
-  int4* rec;                    // [n_tris][3]
+  int4* rec;                    // 3 x 16 B per triangle (rec_at: [3][rec_stride] or [n_tris][3])
+  long long rec_stride;         // triangles per record plane (the record capacity)
   uint2* rect;                  // [n_tris] tile rect {tx0|ty0<<16, tx1|ty1<<16}; empty if culled
   Control* ctl;
   // chunk-list AssignBin (null: off): per touched bin b, cl_ent[b][chunk] =
@@ -270,6 +271,7 @@ struct TileArgs {
   Grid g;
   int npass;
   const int4* rec;
+  long long rec_stride;
   int32_t* bin_start;           // written here only when npass == 0 (NB == 1)
   const int32_t* bin_prims;
   Control* ctl;
