@@ -1553,6 +1553,9 @@ struct CmSmem {
 // pairs are laid out in pair order through an exclusive scan in that order
 // and ranked stably per bin through dense local digits (<= 256 per ranking
 // window).  Cursors start at CP[row][b] (bin_start + earlier rows).
+#ifndef PIKO_CM_EARLY_OFFSETS
+#define PIKO_CM_EARLY_OFFSETS 1  // k_cm_scatter: first sub-chunk's pair offsets before the dependency wait
+#endif
 __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_constant__ CmArgs a) {
   extern __shared__ __align__(16) unsigned char cm_smem[];
   CmSmem& sm = *reinterpret_cast<CmSmem*>(cm_smem);
@@ -1573,6 +1576,37 @@ __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_const
     const long long t = tbeg + warp * TPW + k * 32 + lane;
     rr[k] = t < tend ? __ldcg(a.rect + t) : make_uint2(1u, 0u);
   }
+  // owned-bin counts of the sub-chunk's triangles and their exclusive prefix
+  // in (warp, k, lane) order: for the first sub-chunk this needs only
+  // k_setup's rects (complete: k_cm_scan passed its own wait before this grid
+  // launched), so it runs before the wait on k_cm_scan
+  unsigned off[TPT], wbase = 0, n = 0;
+  auto pair_offsets = [&]() {  // CTA-uniform call (one barrier)
+    unsigned wrun = 0;
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+      const unsigned c = owned_in_rect(rr[k].x & 0xffff, rr[k].x >> 16, rr[k].y & 0xffff, rr[k].y >> 16, a.g);
+      unsigned inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      off[k] = wrun + inc - c;   // within the warp; the count is off-delta
+      wrun += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    __syncthreads();  // the previous reads of wsum are done
+    if (lane == 0) sm.wsum[warp] = wrun;  // warp totals (wrun is warp-uniform)
+    __syncthreads();
+    wbase = 0; n = 0;
+#pragma unroll
+    for (int w = 0; w < CM_WARPS; ++w) {
+      const unsigned c = sm.wsum[w];
+      wbase += (w < warp) ? c : 0u;
+      n += c;
+    }
+  };
+  if (!sched && PIKO_CM_EARLY_OFFSETS) pair_offsets();
   pdl_wait();   // k_cm_scan's column prefixes and bin totals (bin_start too when NB > RX_CHUNK)
   pdl_trigger();
   CM_MARK(2, blockIdx.x, 1);
@@ -1676,29 +1710,7 @@ __global__ void __launch_bounds__(CM_THREADS, 2) k_cm_scatter(const __grid_const
         rr[k] = t < tend ? __ldcg(a.rect + t) : make_uint2(1u, 0u);
       }
     }
-    // owned-bin counts and their exclusive prefix in (warp, k, lane) order
-    unsigned off[TPT], wrun = 0;
-#pragma unroll
-    for (int k = 0; k < TPT; ++k) {
-      const unsigned c = owned_in_rect(rr[k].x & 0xffff, rr[k].x >> 16, rr[k].y & 0xffff, rr[k].y >> 16, a.g);
-      unsigned inc = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
-      }
-      off[k] = wrun + inc - c;   // within the warp; the count is off-delta
-      wrun += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    if (lane == 0) sm.wsum[warp] = wrun;  // warp totals (wrun is warp-uniform)
-    __syncthreads();
-    unsigned wbase = 0, n = 0;
-#pragma unroll
-    for (int w = 0; w < CM_WARPS; ++w) {
-      const unsigned c = sm.wsum[w];
-      wbase += (w < warp) ? c : 0u;
-      n += c;
-    }
+    if (sub != tbeg || !PIKO_CM_EARLY_OFFSETS) pair_offsets();
     CM_MARK(2, blockIdx.x, 3);
     for (unsigned lo = 0; lo < n; lo += RX_CHUNK) {
       const unsigned m = min((unsigned)RX_CHUNK, n - lo);
