@@ -16,6 +16,10 @@ constexpr int K1_THREADS = 256;                     // triangle-setup CTA
 #endif
 constexpr int K1_TPT = PIKO_K1_TPT;                 // triangles per thread (strided)
 constexpr int K1_CHUNK = K1_THREADS * K1_TPT;       // triangles per CTA
+// the host sizes count-matrix rows from 2^10 = K1_CHUNK triangles and the
+// chunk-list groups from 32 per warp slot; other chunk sizes are not supported
+// (K1_TPT = 1 / 2 builds fail at run time)
+static_assert(K1_CHUNK == 1024, "k_setup handles 1024 triangles per CTA");
 constexpr int EX_MAX_TRIS = 4096;                   // triangles per expand chunk (radix pass 0)
 #ifndef PIKO_RX_THREADS
 #define PIKO_RX_THREADS 256
